@@ -1,0 +1,147 @@
+/*
+ * pslr.h — C-ABI of libpslr.so, the B200-native (sm_100a) hot path of the
+ * PSLR preconditioner (arXiv 2002.00917).
+ *
+ * The reference (pslr 0.1.0, pure Python) has no FFI layer: its seam is the
+ * Python API.  Each entry point below replaces one reference function, cited
+ * as file:line under /root/reference/pkg/src/pslr/.  Plain pointers and sizes
+ * only; no torch types.  Device-side entry points take DEVICE pointers and a
+ * cudaStream_t passed as void*; `_host` variants take host pointers and do the
+ * host<->device copies inside the call.
+ *
+ * Status codes map to the reference's exceptions in the Python binding:
+ *   PSLR_EDIM / PSLR_EINVAL -> ValueError            (schur.py:62-66, preconditioner.py:82-84,
+ *                                                     lowrank.py:101-102, ilu.py:189-191)
+ *   PSLR_ENONFINITE         -> ArithmeticError       (krylov.py:81-82, 122-123)
+ *   PSLR_ESINGULAR          -> CorrectionSingularError (lowrank.py:88-93)
+ *   PSLR_ECUDA / PSLR_ENOMEM-> RuntimeError
+ * pslr_last_error() returns a thread-local message for the last failure.
+ *
+ * Threading: one context per GPU per process; calls on one context are
+ * stream-ordered and must not run concurrently (the context owns its scratch).
+ */
+#ifndef PSLR_H_
+#define PSLR_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define PSLR_OK 0
+#define PSLR_EDIM 1
+#define PSLR_ENONFINITE 2
+#define PSLR_ESINGULAR 3
+#define PSLR_ECUDA 4
+#define PSLR_EINVAL 5
+#define PSLR_ENOMEM 6
+#define PSLR_ENCCL 7
+
+typedef struct pslr_ctx pslr_ctx;
+typedef struct pslr_factors pslr_factors;
+
+/* A CSR matrix in host memory (sorted column indices, no duplicates). */
+typedef struct {
+  int64_t nrows, ncols, nnz;
+  const int64_t* indptr;  /* nrows+1 */
+  const int32_t* indices; /* nnz */
+  const double* data;     /* nnz */
+} pslr_csr;
+
+/* The reordered system and its block factors — the state the reference keeps in
+ * PartitionedSystem (partition.py:33-56) and SchurContext (schur.py:26-38). */
+typedef struct {
+  int64_t n, p, q, s;
+  const int64_t* interior_offsets;  /* s+1: block offsets of B (cumsum of interior_sizes) */
+  const int64_t* interface_offsets; /* s+1: block offsets of C0 (cumsum of interface_sizes) */
+  pslr_csr LB, UB;                  /* BlockILU of B: unit-lower L (diag stored), upper U (ilu.py:141-164) */
+  pslr_csr LC, UC;                  /* BlockILU of C0 */
+  pslr_csr E, F;                    /* p x q, q x p (partition.py:522-525) */
+  pslr_csr C, C0, Cg;               /* q x q: C, its block-diagonal part C0, and C - C0 (schur.py:52-59) */
+  pslr_csr A;                       /* n x n reordered matrix (PartitionedSystem.matrix; cli.py:135) */
+} pslr_system;
+
+typedef struct {
+  int64_t n, p, q, s, rank;
+  int64_t levels_LB, levels_UB, levels_LC, levels_UC;      /* summed over blocks */
+  int64_t maxdepth_LB, maxdepth_UB, maxdepth_LC, maxdepth_UC;
+  int64_t nnz_LB, nnz_UB, nnz_LC, nnz_UC, nnz_E, nnz_F, nnz_C, nnz_C0, nnz_Cg, nnz_A;
+  int64_t device_bytes;                                    /* resident device footprint */
+  int64_t sm_count;
+} pslr_ctx_info_t;
+
+/* ---------------------------------------------------------------- misc */
+const char* pslr_last_error(void);
+int pslr_abi_version(void);
+
+/* ---------------------------------------------------------------- host setup (C++)
+ * Bit-identical restatements of the reference's pure-Python setup loops. */
+
+/* partition.py:72-132 (_bfs_order/_bisect/partition_graph) on the symmetrised
+ * off-diagonal adjacency pattern (partition.py:59-69). assignment: n int64. */
+int pslr_partition_bisect(int64_t n, const int64_t* adj_indptr, const int64_t* adj_indices,
+                          int64_t parts, int64_t* assignment);
+
+/* ilu.py:35-138 (ilut) for every diagonal block, ilu.py:167-184 (factor_blocks).
+ * Input: the block-diagonal matrix (CSR) and nblocks+1 offsets; fill_cap < 0 = None.
+ * Blocks run in parallel on nthreads host threads (<=0: all cores). */
+int pslr_ilut_blocks(int64_t n, const int64_t* indptr, const int32_t* indices, const double* data,
+                     int64_t nblocks, const int64_t* offsets, double droptol, int64_t fill_cap,
+                     int nthreads, pslr_factors** out, int64_t* nnz_L, int64_t* nnz_U,
+                     int64_t* pivot_repairs);
+/* Assembled block-diagonal CSR factors (global indices), as sp.block_diag builds them. */
+int pslr_factors_fetch(const pslr_factors* f, int64_t* Lp, int32_t* Li, double* Lx, int64_t* Up,
+                       int32_t* Ui, double* Ux, int64_t* block_nnz /* 2*nblocks or NULL */,
+                       int64_t* block_repairs /* nblocks or NULL */);
+void pslr_factors_free(pslr_factors* f);
+/* ilu.py:52 row norms (np.sqrt(A.multiply(A).sum(axis=1))), exposed for bit-exact tests. */
+int pslr_row_norms(int64_t n, const int64_t* indptr, const double* data, double* out);
+
+/* ---------------------------------------------------------------- device context */
+/* Uploads the system, level-schedules every triangular factor per block, packs the
+ * device formats. Replaces the state build() hands to the apply (preconditioner.py:120-141). */
+int pslr_ctx_create(pslr_ctx** out, int device, const pslr_system* sys);
+void pslr_ctx_destroy(pslr_ctx* ctx);
+int pslr_ctx_info(const pslr_ctx* ctx, pslr_ctx_info_t* info);
+/* LowRankCorrection (lowrank.py:26-36): V q x r row-major, G r x r row-major, host pointers. */
+int pslr_ctx_set_correction(pslr_ctx* ctx, int64_t r, const double* V, const double* G);
+/* same, V already on the device (q x r row-major), G on the host */
+int pslr_ctx_set_correction_device(pslr_ctx* ctx, int64_t r, const double* V_dev, const double* G);
+
+/* ---------------------------------------------------------------- hot-path operators (device ptrs) */
+int pslr_solve_B(pslr_ctx* ctx, const double* f, double* x, void* stream);        /* schur.py:69-70 */
+int pslr_solve_C0(pslr_ctx* ctx, const double* g, double* y, void* stream);       /* schur.py:73-74 */
+int pslr_apply_S(pslr_ctx* ctx, const double* v, double* out, void* stream);      /* schur.py:77-80 */
+int pslr_apply_Es(pslr_ctx* ctx, const double* v, double* out, void* stream);     /* schur.py:83-86 */
+int pslr_apply_neumann(pslr_ctx* ctx, int64_t m, const double* v, double* out, void* stream); /* schur.py:89-101 */
+int pslr_apply_Err(pslr_ctx* ctx, int64_t m, const double* v, double* out, void* stream);     /* schur.py:104-112 */
+int pslr_apply_correction(pslr_ctx* ctx, const double* y, double* out, void* stream);         /* lowrank.py:98-105 */
+int pslr_apply(pslr_ctx* ctx, int64_t m, const double* b, double* z, void* stream);          /* preconditioner.py:79-93 */
+/* which: 0=A 1=E 2=F 3=C0 4=Cg 5=C ; y = M x  (sparse.py:60-65 / scipy csr @) */
+int pslr_spmv(pslr_ctx* ctx, int which, const double* x, double* y, void* stream);
+/* pslr_apply with a CUDA event after every kernel launch (measurement only): per-launch
+ * milliseconds and kinds (1 correction core, 2 first step, 3 correction+C0, 4 Horner step,
+ * 5 last step); nlaunch = launches issued (up to cap reported). */
+int pslr_apply_profiled(pslr_ctx* ctx, int64_t m, const double* b, double* z, void* stream,
+                        double* launch_ms, int32_t* launch_kind, int64_t cap, int64_t* nlaunch);
+/* Alg. 3.2 with HOST buffers (copies inside): the call a CPU user of P.apply makes. */
+int pslr_apply_host(pslr_ctx* ctx, int64_t m, const double* b_host, double* z_host, void* stream);
+
+/* ---------------------------------------------------------------- Krylov (device) */
+/* lowrank.py:39-73 on op = E_rr(m) (schur.py:104-112), preconditioner.py:133-136.
+ * v0: host start vector (q doubles, NOT normalised — the seeded draw); V_dev: q x rank
+ * row-major output; H: host rank x rank row-major; r_out: achieved rank. */
+int pslr_arnoldi(pslr_ctx* ctx, int64_t m, int64_t rank, const double* v0, double* V_dev,
+                 double* H, int64_t* r_out, void* stream);
+/* krylov.py:35-129 on (A = reordered matrix, M = PSLR apply (precond!=0) or identity).
+ * flexible!=0: FGMRES (Z_j = M v_j stored, x += Z y) — config 3's accelerator.
+ * b, x: device n-vectors. history: host buffer of maxit+1 doubles. */
+int pslr_gmres(pslr_ctx* ctx, int64_t m, const double* b, double* x, double tol, int64_t maxit,
+               int64_t restart, int precond, int flexible, int64_t* iterations, int* converged,
+               double* final_relres, double* history, int64_t* history_len, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PSLR_H_ */
