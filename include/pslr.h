@@ -69,6 +69,10 @@ typedef struct {
   int64_t nnz_LB, nnz_UB, nnz_LC, nnz_UC, nnz_E, nnz_F, nnz_C, nnz_C0, nnz_Cg, nnz_A;
   int64_t device_bytes;                                    /* resident device footprint */
   int64_t sm_count;
+  int64_t ring_slots;  /* W: shared-memory solution ring (doubles) of the streamed solve */
+  int64_t stages;      /* TMA pipeline stages per CTA */
+  int64_t far_deps;    /* dependencies read from global memory (beyond the ring) */
+  int64_t reach;       /* max level-order distance of a dependency */
 } pslr_ctx_info_t;
 
 /* ---------------------------------------------------------------- misc */
@@ -125,6 +129,9 @@ int pslr_spmv(pslr_ctx* ctx, int which, const double* x, double* y, void* stream
  * 5 last step); nlaunch = launches issued (up to cap reported). */
 int pslr_apply_profiled(pslr_ctx* ctx, int64_t m, const double* b, double* z, void* stream,
                         double* launch_ms, int32_t* launch_kind, int64_t cap, int64_t* nlaunch);
+/* Diagnostics (contexts created with PSLR_TRACE=1): timeline of CTA 0 since the last call,
+ * as (code<<32 | arg, globaltimer ns) pairs; count = pairs returned. */
+int pslr_debug_trace(pslr_ctx* ctx, int64_t* out, int64_t cap, int64_t* count);
 /* Alg. 3.2 with HOST buffers (copies inside): the call a CPU user of P.apply makes. */
 int pslr_apply_host(pslr_ctx* ctx, int64_t m, const double* b_host, double* z_host, void* stream);
 

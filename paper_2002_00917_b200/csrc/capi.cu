@@ -1,15 +1,18 @@
-// capi.cu — the C-ABI of libpslr.so: device context (upload + level-schedule
-// packing), the hot-path operators of Alg. 3.2, device Arnoldi and GMRES/FGMRES.
-// Every entry point cites the reference function it replaces (see include/pslr.h).
+// capi.cu — the C-ABI of libpslr.so: device context (upload + streamed-factor
+// packing), the hot-path operators of Alg. 3.2 and their launch-level profiling.
+// Krylov drivers (Arnoldi, GMRES/FGMRES) are in krylov.cu.  Every entry point
+// cites the reference function it replaces (see include/pslr.h).
 #include <cuda_runtime.h>
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
 
 #include "pslr_internal.h"
+#include "pslr_ops.h"
 
 namespace pslr {
 
@@ -19,41 +22,6 @@ int fail(int code, const std::string& msg) {
   g_last_error = msg;
   return code;
 }
-
-// launchers (kernels.cu)
-int launch_step(const pslr_ctx* ctx, const StepArgs& a, cudaStream_t st);
-int launch_correction_core(const pslr_ctx* ctx, cudaStream_t st);
-int launch_spmv(const DevCsr& M, const double* x, double* y, cudaStream_t st);
-int launch_multidot(pslr_ctx* ctx, const double* X, int64_t ld, int k, const double* y, int64_t n,
-                    double* out, cudaStream_t st);
-int launch_gemv_sub(const double* X, int64_t ld, int k, const double* h, double* w, int64_t n,
-                    cudaStream_t st);
-int launch_gemv(const double* X, int64_t ld, int k, const double* h, double* y, int64_t n,
-                cudaStream_t st);
-int launch_sub(const double* a, const double* b, double* y, int64_t n, cudaStream_t st);
-int launch_add_inplace(double* y, const double* a, int64_t n, cudaStream_t st);
-int launch_div_scalar(const double* x, const double* s, double* y, int64_t n, cudaStream_t st);
-int launch_transpose_basis(const double* X, int64_t q, int r, double* Y, cudaStream_t st);
-int dot_grid(int64_t n, int sm_count);
-
-#define CK(call)                                                                          \
-  do {                                                                                    \
-    cudaError_t _e = (call);                                                              \
-    if (_e != cudaSuccess)                                                                \
-      return ::pslr::fail(PSLR_ECUDA, std::string(#call) + ": " + cudaGetErrorString(_e)); \
-  } while (0)
-#define CKL(expr)                                                                      \
-  do {                                                                                 \
-    int _e = (expr);                                                                   \
-    if (_e != 0)                                                                       \
-      return ::pslr::fail(PSLR_ECUDA, std::string(#expr) + ": " +                      \
-                                          cudaGetErrorString((cudaError_t)_e));        \
-  } while (0)
-#define RET(expr)              \
-  do {                         \
-    int _r = (expr);           \
-    if (_r != PSLR_OK) return _r; \
-  } while (0)
 
 template <class T>
 static int upload(pslr_ctx* ctx, const std::vector<T>& h, const T** out) {
@@ -70,7 +38,7 @@ static int upload(pslr_ctx* ctx, const std::vector<T>& h, const T** out) {
   return PSLR_OK;
 }
 
-static int alloc_scratch(pslr_ctx* ctx, double** p, int64_t count) {
+int alloc_scratch(pslr_ctx* ctx, double** p, int64_t count) {
   *p = nullptr;
   if (count <= 0) count = 1;
   void* d = nullptr;
@@ -82,20 +50,24 @@ static int alloc_scratch(pslr_ctx* ctx, double** p, int64_t count) {
   return PSLR_OK;
 }
 
-static void free_ptr(pslr_ctx* ctx, void* p) {
+void free_ptr(pslr_ctx* ctx, void* p) {
   if (!p) return;
   auto it = std::find(ctx->allocations.begin(), ctx->allocations.end(), p);
   if (it != ctx->allocations.end()) ctx->allocations.erase(it);
   cudaFree(p);
 }
 
-// grow-on-demand scratch
-static int ensure(pslr_ctx* ctx, double** p, int64_t* len, int64_t need) {
+int ensure(pslr_ctx* ctx, double** p, int64_t* len, int64_t need) {
   if (*len >= need) return PSLR_OK;
   free_ptr(ctx, *p);
   RET(alloc_scratch(ctx, p, need));
   *len = need;
   return PSLR_OK;
+}
+
+static int64_t env_int(const char* name, int64_t dflt) {
+  const char* v = std::getenv(name);
+  return (v && *v) ? std::atoll(v) : dflt;
 }
 
 static int check_csr(const pslr_csr& M, int64_t nr, int64_t nc, const char* name) {
@@ -122,143 +94,36 @@ static int upload_csr(pslr_ctx* ctx, const pslr_csr& M, DevCsr* out) {
   return PSLR_OK;
 }
 
-// Level-schedule and pack one block-diagonal triangular factor.
-static int pack_tri(pslr_ctx* ctx, const pslr_csr& M, const std::vector<int64_t>& off, bool upper,
-                    DevTri* out, int64_t* levels_total, int64_t* maxdepth, const char* name) {
-  const int64_t nb = (int64_t)off.size() - 1;
-  std::vector<int32_t> blk_lvl(nb + 1, 0), lvl_pos{0}, pos_row, pos_ent{0}, col;
-  std::vector<double> val, sd, invd;
-  std::vector<int32_t> lev;
-  std::vector<double> dinv;  // per row (block-local) 1/diag for the U pre-scaling
-  int64_t depth_max = 0;
-  for (int64_t b = 0; b < nb; ++b) {
-    const int64_t lo = off[b], hi = off[b + 1], nr = hi - lo;
-    lev.assign(nr, 0);
-    if (upper) {
-      dinv.assign(nr, 0.0);
-      std::vector<double> dg(nr, 0.0);
-      for (int64_t i = 0; i < nr; ++i) {
-        bool found = false;
-        for (int64_t e = M.indptr[lo + i]; e < M.indptr[lo + i + 1]; ++e) {
-          const int64_t j = M.indices[e];
-          if (j < lo || j >= hi) return fail(PSLR_EINVAL, std::string(name) + " is not block diagonal");
-          if (j < lo + i) return fail(PSLR_EINVAL, std::string(name) + " is not upper triangular");
-          if (j == lo + i) {
-            dg[i] = M.data[e];
-            found = true;
-          }
-        }
-        if (!found || dg[i] == 0.0)
-          return fail(PSLR_ESINGULAR, std::string(name) + ": A is singular: zero entry on diagonal.");
-        dinv[i] = 1.0 / dg[i];
-      }
-      for (int64_t i = nr - 1; i >= 0; --i) {
-        int32_t lv = 0;
-        for (int64_t e = M.indptr[lo + i]; e < M.indptr[lo + i + 1]; ++e) {
-          const int64_t j = M.indices[e] - lo;
-          if (j > i) lv = std::max(lv, lev[j] + 1);
-        }
-        lev[i] = lv;
-      }
-      // stash the diagonal for sd/invd
-      for (int64_t i = 0; i < nr; ++i) (void)dg[i];
-      // pack below, recomputing sd from dg
-      int32_t depth = 0;
-      for (int64_t i = 0; i < nr; ++i) depth = std::max(depth, lev[i] + 1);
-      if (nr == 0) depth = 0;
-      depth_max = std::max<int64_t>(depth_max, depth);
-      std::vector<int32_t> cnt(depth + 1, 0);
-      for (int64_t i = 0; i < nr; ++i) cnt[lev[i] + 1]++;
-      for (int32_t l = 0; l < depth; ++l) cnt[l + 1] += cnt[l];
-      std::vector<int32_t> order(nr);
-      {
-        std::vector<int32_t> fill(cnt.begin(), cnt.end() - 1);
-        for (int64_t i = 0; i < nr; ++i) order[fill[lev[i]]++] = (int32_t)i;
-      }
-      for (int32_t l = 0; l < depth; ++l) {
-        for (int32_t k = cnt[l]; k < cnt[l + 1]; ++k) {
-          const int64_t i = order[k];
-          pos_row.push_back((int32_t)(lo + i));
-          for (int64_t e = M.indptr[lo + i]; e < M.indptr[lo + i + 1]; ++e) {
-            const int64_t j = M.indices[e] - lo;
-            if (j > i) {
-              col.push_back((int32_t)(lo + j));
-              val.push_back(M.data[e] * dinv[j]);  // scipy: U @ diags(1/diag)
-            }
-          }
-          pos_ent.push_back((int32_t)col.size());
-          sd.push_back(dg[i] * dinv[i]);
-          invd.push_back(dinv[i]);
-        }
-        lvl_pos.push_back((int32_t)pos_row.size());
-      }
-      blk_lvl[b + 1] = blk_lvl[b] + depth;
-    } else {
-      for (int64_t i = 0; i < nr; ++i) {
-        int32_t lv = 0;
-        for (int64_t e = M.indptr[lo + i]; e < M.indptr[lo + i + 1]; ++e) {
-          const int64_t jg = M.indices[e];
-          if (jg < lo || jg >= hi) return fail(PSLR_EINVAL, std::string(name) + " is not block diagonal");
-          const int64_t j = jg - lo;
-          if (j > i) return fail(PSLR_EINVAL, std::string(name) + " is not lower triangular");
-          if (j < i) lv = std::max(lv, lev[j] + 1);
-        }
-        lev[i] = lv;
-      }
-      int32_t depth = 0;
-      for (int64_t i = 0; i < nr; ++i) depth = std::max(depth, lev[i] + 1);
-      depth_max = std::max<int64_t>(depth_max, depth);
-      std::vector<int32_t> cnt(depth + 1, 0);
-      for (int64_t i = 0; i < nr; ++i) cnt[lev[i] + 1]++;
-      for (int32_t l = 0; l < depth; ++l) cnt[l + 1] += cnt[l];
-      std::vector<int32_t> order(nr);
-      {
-        std::vector<int32_t> fill(cnt.begin(), cnt.end() - 1);
-        for (int64_t i = 0; i < nr; ++i) order[fill[lev[i]]++] = (int32_t)i;
-      }
-      for (int32_t l = 0; l < depth; ++l) {
-        for (int32_t k = cnt[l]; k < cnt[l + 1]; ++k) {
-          const int64_t i = order[k];
-          pos_row.push_back((int32_t)(lo + i));
-          for (int64_t e = M.indptr[lo + i]; e < M.indptr[lo + i + 1]; ++e) {
-            const int64_t j = M.indices[e] - lo;
-            if (j < i) {  // unit diagonal: the stored diagonal is ignored (setdiag(1))
-              col.push_back((int32_t)(lo + j));
-              val.push_back(M.data[e]);
-            }
-          }
-          pos_ent.push_back((int32_t)col.size());
-        }
-        lvl_pos.push_back((int32_t)pos_row.size());
-      }
-      blk_lvl[b + 1] = blk_lvl[b] + depth;
-    }
-  }
-  out->nblocks = (int32_t)nb;
-  out->nlevels = blk_lvl[nb];
-  out->npos = (int32_t)pos_row.size();
-  out->nnz = (int32_t)col.size();
-  RET(upload(ctx, blk_lvl, &out->blk_lvl));
-  RET(upload(ctx, lvl_pos, &out->lvl_pos));
-  RET(upload(ctx, pos_row, &out->pos_row));
-  RET(upload(ctx, pos_ent, &out->pos_ent));
-  RET(upload(ctx, col, &out->col));
-  RET(upload(ctx, val, &out->val));
-  if (upper) {
-    RET(upload(ctx, sd, &out->sd));
-    RET(upload(ctx, invd, &out->invd));
-  }
-  *levels_total = blk_lvl[nb];
-  *maxdepth = depth_max;
+static int upload_tri(pslr_ctx* ctx, const TriHost& H, const std::vector<int32_t>* lpos,
+                      DevTri* out) {
+  out->nblocks = (int32_t)H.blk_chunk.size() - 1;
+  out->nchunks = (int32_t)H.chunks.size();
+  RET(upload(ctx, H.data, &out->data));
+  RET(upload(ctx, H.chunks, &out->chunks));
+  RET(upload(ctx, H.blk_chunk, &out->blk_chunk));
+  if (lpos) RET(upload(ctx, *lpos, &out->lpos));
+  return PSLR_OK;
+}
+
+// Pack one block ILU pair (L, U) for the streamed solve.  The U-positions are where
+// every value lives globally (L writes its output there, U its intermediate).
+static int build_pair(pslr_ctx* ctx, const pslr_csr& L, const pslr_csr& U,
+                      const std::vector<int64_t>& off, const TriAnalysis& AL,
+                      const TriAnalysis& AU, int64_t W, int64_t SB, DevTri* dL, DevTri* dU,
+                      const char* nameL, const char* nameU, int64_t* far) {
+  const int64_t n = L.nrows;
+  std::vector<int32_t> row_id(n);
+  for (int64_t i = 0; i < n; ++i) row_id[i] = (int32_t)i;
+  TriHost HL, HU;
+  RET(emit_factor(U, off, AU, W, SB, kStepThreads, AU.pos_of_row, row_id, HU, nameU));
+  RET(emit_factor(L, off, AL, W, SB, kStepThreads, AU.pos_of_row, AU.pos_of_row, HL, nameL));
+  RET(upload_tri(ctx, HL, &AL.pos_of_row, dL));
+  RET(upload_tri(ctx, HU, nullptr, dU));
+  *far = HL.far + HU.far;
   return PSLR_OK;
 }
 
 static cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
-
-// Launch-level profiling (pslr_apply_profiled): an event after every launch.
-// kinds: 0 generic step, 1 correction core, 2 apply-first (B solve + F), 3 correction + C0,
-// 4 Horner step (E, B solve, F, Cg, C0 solve), 5 apply-last (E, B solve)
-enum LaunchKind : int32_t { LK_STEP = 0, LK_CORE = 1, LK_FIRST = 2, LK_CORR = 3, LK_HORNER = 4, LK_LAST = 5 };
 
 static int mark(pslr_ctx* ctx, int32_t kind, cudaStream_t st) {
   if (!ctx->prof_on) return PSLR_OK;
@@ -280,56 +145,49 @@ static int run_core(pslr_ctx* ctx, cudaStream_t st) {
   return mark(ctx, LK_CORE, st);
 }
 
-static int set_device(const pslr_ctx* ctx) {
+int set_device(const pslr_ctx* ctx) {
   CK(cudaSetDevice(ctx->device));
   return PSLR_OK;
 }
 
 // ---------------------------------------------------------------- composite operators
-static int op_solve_B(pslr_ctx* ctx, const double* f, double* x, cudaStream_t st) {
+int op_solve_B(pslr_ctx* ctx, const double* f, double* x, cudaStream_t st) {
   StepArgs a;
   a.b1 = BT_F;
   a.f = f;
-  a.tb = ctx->tb;
   a.xb = x;
-  RET(run_step(ctx, a, st));
-  return PSLR_OK;
+  return run_step(ctx, a, st);
 }
 
-static int op_solve_C0(pslr_ctx* ctx, const double* g, double* y, cudaStream_t st) {
+int op_solve_C0(pslr_ctx* ctx, const double* g, double* y, cudaStream_t st) {
   StepArgs a;
   a.i1 = IT_G;
   a.g = g;
   a.do_c0 = 1;
-  a.tw = ctx->tw;
   a.yout = y;
-  RET(run_step(ctx, a, st));
-  return PSLR_OK;
+  return run_step(ctx, a, st);
 }
 
 // out = [C0^{-1}] (F B^{-1} E v - Cg v) [+ cadd]
-static int op_es_step(pslr_ctx* ctx, const double* v, double* out, int do_c0, const double* cadd,
-                      cudaStream_t st) {
+int op_es_step(pslr_ctx* ctx, const double* v, double* out, int do_c0, const double* cadd,
+               cudaStream_t st) {
   StepArgs a;
   a.b1 = BT_EY;
   a.yE = v;
-  a.tb = ctx->tb;
   a.xb = ctx->xb;
   a.i1 = IT_FX;
   a.i2 = IT_CGY;
   a.i2_sub = 1;
   a.yC = v;
   a.do_c0 = do_c0;
-  a.tw = ctx->tw;
   a.cadd = cadd;
   a.yout = out;
   a.tag = (do_c0 && cadd) ? LK_HORNER : LK_STEP;
-  RET(run_step(ctx, a, st));
-  return PSLR_OK;
+  return run_step(ctx, a, st);
 }
 
 // Horner recurrence of schur.py:89-101 starting from c = C0^{-1} v already in `c`.
-static int op_horner(pslr_ctx* ctx, int64_t m, const double* c, double* out, cudaStream_t st) {
+int op_horner(pslr_ctx* ctx, int64_t m, const double* c, double* out, cudaStream_t st) {
   if (m == 0) {
     if (out != c) CK(cudaMemcpyAsync(out, c, ctx->q * sizeof(double), cudaMemcpyDeviceToDevice, st));
     return PSLR_OK;
@@ -346,65 +204,51 @@ static int op_horner(pslr_ctx* ctx, int64_t m, const double* c, double* out, cud
   return PSLR_OK;
 }
 
-// u = G V^T y (partials + core), y given on the device
-static int op_correction_core_from(pslr_ctx* ctx, const double* y, cudaStream_t st) {
-  StepArgs a;
-  a.i1 = IT_G;
-  a.g = y;
-  a.yout = ctx->y0 == y ? ctx->y2 : ctx->y0;  // harmless copy target
-  a.partials = ctx->partials;
-  RET(run_step(ctx, a, st));
-  RET(run_core(ctx, st));
-  return PSLR_OK;
-}
-
-static int op_apply(pslr_ctx* ctx, int64_t m, const double* b, double* z, cudaStream_t st) {
+int op_apply(pslr_ctx* ctx, int64_t m, const double* b, double* z, cudaStream_t st) {
   const int64_t p = ctx->p, q = ctx->q;
   if (q == 0) return op_solve_B(ctx, b, z, st);
-  // (1) y0 = g - F B^{-1} f                                   preconditioner.py:89
+  // (1) y0 = g - F B^{-1} f  (+ per-subdomain V^T y0 partials)   preconditioner.py:89
   {
     StepArgs a;
     a.b1 = BT_F;
     a.f = b;
-    a.tb = ctx->tb;
     a.xb = ctx->xb;
     a.i1 = IT_G;
     a.g = b + p;
     a.i2 = IT_FX;
     a.i2_sub = 1;
     a.yout = ctx->y0;
-    a.partials = ctx->r > 0 ? ctx->partials : nullptr;
     a.tag = LK_FIRST;
     RET(run_step(ctx, a, st));
   }
-  // (2) y1 = y0 + V G V^T y0 ; c = C0^{-1} y1                 preconditioner.py:90, schur.py:97
+  // (2) y1 = y0 + V G V^T y0 (all-SM GEMV kernels) ; c = C0^{-1} y1   preconditioner.py:90, schur.py:97
   double* c = (m == 0) ? z + p : ctx->c;
+  const double* y1 = ctx->y0;
+  if (ctx->r > 0) {
+    CKL(launch_vt_dot(ctx, ctx->y0, st));
+    RET(mark(ctx, LK_CORE, st));
+    CKL(launch_vu_add(ctx, ctx->y0, ctx->y1, st));
+    RET(mark(ctx, LK_CORE, st));
+    y1 = ctx->y1;
+  }
   {
     StepArgs a;
     a.i1 = IT_G;
-    a.g = ctx->y0;
-    if (ctx->r > 0) {
-      RET(run_core(ctx, st));
-      a.i2 = IT_VU;
-      a.i2_sub = 0;
-      a.u = ctx->u;
-    }
+    a.g = y1;
     a.do_c0 = 1;
-    a.tw = ctx->tw;
     a.yout = c;
     a.tag = LK_CORR;
     RET(run_step(ctx, a, st));
   }
-  // (3) m Horner steps y = C0^{-1}(Es y) + c                  schur.py:99-100
+  // (3) m Horner steps y = C0^{-1}(Es y) + c                     schur.py:99-100
   if (m > 0) RET(op_horner(ctx, m, c, z + p, st));
-  // (4) x = B^{-1}(f - E y)                                   preconditioner.py:92
+  // (4) x = B^{-1}(f - E y)                                      preconditioner.py:92
   {
     StepArgs a;
     a.b1 = BT_F;
     a.f = b;
     a.b2 = BT_EY;
     a.yE = z + p;
-    a.tb = ctx->tb;
     a.xb = z;
     a.tag = LK_LAST;
     RET(run_step(ctx, a, st));
@@ -412,7 +256,7 @@ static int op_apply(pslr_ctx* ctx, int64_t m, const double* b, double* z, cudaSt
   return PSLR_OK;
 }
 
-static int op_apply_err(pslr_ctx* ctx, int64_t m, const double* v, double* out, cudaStream_t st) {
+int op_apply_err(pslr_ctx* ctx, int64_t m, const double* v, double* out, cudaStream_t st) {
   if (ctx->q == 0) return PSLR_OK;
   double* buf[2] = {ctx->y1, ctx->y2};
   RET(op_solve_C0(ctx, v, buf[0], st));
@@ -428,41 +272,6 @@ static int op_apply_err(pslr_ctx* ctx, int64_t m, const double* v, double* out, 
   return PSLR_OK;
 }
 
-static int dnorm(pslr_ctx* ctx, const double* x, int64_t n, double* out_host, cudaStream_t st) {
-  RET(ensure(ctx, &ctx->red, &ctx->red_len, (int64_t)dot_grid(n, ctx->sm_count) * 1 + 8));
-  RET(ensure(ctx, &ctx->h_dev, &ctx->h_len, 8));
-  CKL(launch_multidot(ctx, x, n, 1, x, n, ctx->h_dev, st));
-  double d = 0.0;
-  CK(cudaMemcpyAsync(&d, ctx->h_dev, sizeof(double), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  *out_host = std::sqrt(d);
-  return PSLR_OK;
-}
-
-// Classical Gram-Schmidt with one reorthogonalisation on the first k columns of
-// X (column-major, ld = n): krylov.py:75-80 / lowrank.py:62-67.  Returns h (host,
-// h1 + h2) and the norm of the orthogonalised w.
-static int cgs2(pslr_ctx* ctx, const double* X, int64_t n, int k, double* w, double* h_host,
-                double* hnorm, cudaStream_t st) {
-  RET(ensure(ctx, &ctx->red, &ctx->red_len, (int64_t)dot_grid(n, ctx->sm_count) * (k + 1) + 8));
-  RET(ensure(ctx, &ctx->h_dev, &ctx->h_len, 2 * (int64_t)k + 8));
-  double* h1 = ctx->h_dev;
-  double* h2 = ctx->h_dev + k;
-  double* nn = ctx->h_dev + 2 * k;
-  CKL(launch_multidot(ctx, X, n, k, w, n, h1, st));
-  CKL(launch_gemv_sub(X, n, k, h1, w, n, st));
-  CKL(launch_multidot(ctx, X, n, k, w, n, h2, st));
-  CKL(launch_gemv_sub(X, n, k, h2, w, n, st));
-  CKL(launch_multidot(ctx, w, n, 1, w, n, nn, st));
-  std::vector<double> tmp(2 * k + 1);
-  CK(cudaMemcpyAsync(tmp.data(), ctx->h_dev, (2 * k + 1) * sizeof(double), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  for (int c = 0; c < k; ++c) h_host[c] = tmp[c] + tmp[k + c];
-  *hnorm = std::sqrt(tmp[2 * k]);
-  // keep the unsummed h1 for callers that need it (arnoldi stores h+h2 = same)
-  return PSLR_OK;
-}
-
 }  // namespace pslr
 
 using namespace pslr;
@@ -470,7 +279,7 @@ using namespace pslr;
 extern "C" {
 
 const char* pslr_last_error(void) { return g_last_error.c_str(); }
-int pslr_abi_version(void) { return 1; }
+int pslr_abi_version(void) { return 2; }
 
 int pslr_ctx_create(pslr_ctx** out, int device, const pslr_system* sys) {
   *out = nullptr;
@@ -506,16 +315,77 @@ int pslr_ctx_create(pslr_ctx** out, int device, const pslr_system* sys) {
   if (cudaSetDevice(device) != cudaSuccess) return bail(fail(PSLR_ECUDA, "cudaSetDevice failed"));
   cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
   if (ctx->sm_count <= 0) ctx->sm_count = 148;
+  int smem_optin = 0;
+  cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
+  if (smem_optin <= 0) smem_optin = 232448;
   pslr_ctx_info_t& I = ctx->info;
-  if ((rc = pack_tri(ctx, sys->LB, ctx->interior_off, false, &ctx->LB, &I.levels_LB, &I.maxdepth_LB, "L_B"))) return bail(rc);
-  if ((rc = pack_tri(ctx, sys->UB, ctx->interior_off, true, &ctx->UB, &I.levels_UB, &I.maxdepth_UB, "U_B"))) return bail(rc);
-  if ((rc = pack_tri(ctx, sys->LC, ctx->interface_off, false, &ctx->LC, &I.levels_LC, &I.maxdepth_LC, "L_C0"))) return bail(rc);
-  if ((rc = pack_tri(ctx, sys->UC, ctx->interface_off, true, &ctx->UC, &I.levels_UC, &I.maxdepth_UC, "U_C0"))) return bail(rc);
-  if ((rc = upload_csr(ctx, sys->E, &ctx->E))) return bail(rc);
-  if ((rc = upload_csr(ctx, sys->F, &ctx->F))) return bail(rc);
-  if ((rc = upload_csr(ctx, sys->C, &ctx->C))) return bail(rc);
+
+  // ---- level analysis of the four factors, then the ring size W and the stage plan
+  TriAnalysis aLB, aUB, aLC, aUC;
+  if ((rc = analyze_factor(sys->LB, ctx->interior_off, false, aLB, "L_B"))) return bail(rc);
+  if ((rc = analyze_factor(sys->UB, ctx->interior_off, true, aUB, "U_B"))) return bail(rc);
+  if ((rc = analyze_factor(sys->LC, ctx->interface_off, false, aLC, "L_C0"))) return bail(rc);
+  if ((rc = analyze_factor(sys->UC, ctx->interface_off, true, aUC, "U_C0"))) return bail(rc);
+  const int64_t reach = std::max({aLB.reach, aUB.reach, aLC.reach, aUC.reach, (int64_t)1});
+  // Shared-memory plan: nst stages of (chunk bytes SB + rhs slice RB) and a W-slot ring.
+  // In-flight bytes set the per-SM stream rate (~1 us TMA latency), the ring size sets
+  // how many dependencies must come from global memory; W = 8192 balances the two
+  // for the 3D configs (tools/micro/tma_stream.cu).
+  const int64_t SB = env_int("PSLR_STAGE_BYTES", 32 * 1024);
+  const int64_t RB = ((8 * (kChunkRows + 2)) + 127) / 128 * 128;
+  int64_t wmax = env_int("PSLR_RING", 8192);
+  int64_t W = 2048;  // >= 2048: the ring doubles as the V^T y reduction scratch
+  while (W < reach && W < wmax) W *= 2;
+  const int64_t CTL = 256;  // mbarriers
+  int64_t nst = (smem_optin - 1024 - CTL - W * 8) / (SB + RB);
+  while (nst < 2 && W > 2048) {
+    W /= 2;
+    nst = (smem_optin - 1024 - CTL - W * 8) / (SB + RB);
+  }
+  nst = std::min<int64_t>(nst, std::min<int64_t>(8, env_int("PSLR_MAX_STAGES", 8)));
+  if (nst < 2) return bail(fail(PSLR_EINVAL, "not enough shared memory for the streamed solve"));
+  ctx->K.ring_mask = (int)(W - 1);
+  ctx->K.nst = (int)nst;
+  ctx->K.stage_bytes = (int)SB;
+  ctx->K.rhs_stride = (int)(RB / 8);
+  ctx->K.smem_bytes = (int)(CTL + nst * (SB + RB) + W * 8 + 16);  // ring + zero slot
+  if (configure_step_kernel(ctx->K.smem_bytes) != 0)
+    return bail(fail(PSLR_ECUDA, "cannot configure the step kernel's shared memory"));
+  if (env_int("PSLR_TRACE", 0)) {  // diagnostics: timeline of CTA 0 (pslr_debug_trace)
+    const int64_t cap = 1 << 20;
+    void* d = nullptr;
+    if (cudaMalloc(&d, (2 + 2 * cap) * sizeof(long long)) != cudaSuccess)
+      return bail(fail(PSLR_ECUDA, "cudaMalloc trace"));
+    cudaMemset(d, 0, 16);
+    ctx->allocations.push_back(d);
+    ctx->K.trace = static_cast<long long*>(d);
+    ctx->K.trace_cap = cap;
+  }
+  int64_t farB = 0, farC = 0;
+  if ((rc = build_pair(ctx, sys->LB, sys->UB, ctx->interior_off, aLB, aUB, W, SB, &ctx->K.LB,
+                       &ctx->K.UB, "L_B", "U_B", &farB)))
+    return bail(rc);
+  if ((rc = build_pair(ctx, sys->LC, sys->UC, ctx->interface_off, aLC, aUC, W, SB, &ctx->K.LC,
+                       &ctx->K.UC, "L_C0", "U_C0", &farC)))
+    return bail(rc);
+  I.levels_LB = aLB.levels;
+  I.levels_UB = aUB.levels;
+  I.levels_LC = aLC.levels;
+  I.levels_UC = aUC.levels;
+  I.maxdepth_LB = aLB.depth_max;
+  I.maxdepth_UB = aUB.depth_max;
+  I.maxdepth_LC = aLC.depth_max;
+  I.maxdepth_UC = aUC.depth_max;
+  I.ring_slots = W;
+  I.stages = nst;
+  I.far_deps = farB + farC;
+  I.reach = reach;
+
+  if ((rc = upload_csr(ctx, sys->E, &ctx->K.E))) return bail(rc);
+  if ((rc = upload_csr(ctx, sys->F, &ctx->K.F))) return bail(rc);
+  if ((rc = upload_csr(ctx, sys->C, &ctx->K.C))) return bail(rc);
   if ((rc = upload_csr(ctx, sys->C0, &ctx->C0))) return bail(rc);
-  if ((rc = upload_csr(ctx, sys->Cg, &ctx->Cg))) return bail(rc);
+  if ((rc = upload_csr(ctx, sys->Cg, &ctx->K.Cg))) return bail(rc);
   if ((rc = upload_csr(ctx, sys->A, &ctx->A))) return bail(rc);
   {
     std::vector<int32_t> io(s + 1), fo(s + 1);
@@ -523,15 +393,25 @@ int pslr_ctx_create(pslr_ctx** out, int device, const pslr_system* sys) {
       io[b] = (int32_t)ctx->interior_off[b];
       fo[b] = (int32_t)ctx->interface_off[b];
     }
-    const int32_t* d = nullptr;
-    if ((rc = upload(ctx, io, &d))) return bail(rc);
-    ctx->d_int_off = const_cast<int32_t*>(d);
-    if ((rc = upload(ctx, fo, &d))) return bail(rc);
-    ctx->d_ifc_off = const_cast<int32_t*>(d);
+    if ((rc = upload(ctx, io, &ctx->K.int_off))) return bail(rc);
+    if ((rc = upload(ctx, fo, &ctx->K.ifc_off))) return bail(rc);
+    // interior rows that carry E entries (~30% on the stencil configs), per block
+    std::vector<int32_t> er, eo(s + 1, 0);
+    for (int64_t b = 0; b < s; ++b) {
+      for (int64_t i = ctx->interior_off[b]; i < ctx->interior_off[b + 1]; ++i)
+        if (sys->E.indptr[i + 1] > sys->E.indptr[i]) er.push_back((int32_t)i);
+      eo[b + 1] = (int32_t)er.size();
+    }
+    if (er.empty()) er.push_back(0);
+    if ((rc = upload(ctx, er, &ctx->K.erows))) return bail(rc);
+    if ((rc = upload(ctx, eo, &ctx->K.erow_off))) return bail(rc);
   }
-  if ((rc = alloc_scratch(ctx, &ctx->tb, p))) return bail(rc);
+  // position-ordered rhs arrays: +2 so a chunk's even-aligned TMA slice stays in bounds
+  if ((rc = alloc_scratch(ctx, &ctx->K.rhsB, p + 2))) return bail(rc);
+  if ((rc = alloc_scratch(ctx, &ctx->K.zB, p + 2))) return bail(rc);
+  if ((rc = alloc_scratch(ctx, &ctx->K.rhsC, q + 2))) return bail(rc);
+  if ((rc = alloc_scratch(ctx, &ctx->K.zC, q + 2))) return bail(rc);
   if ((rc = alloc_scratch(ctx, &ctx->xb, p))) return bail(rc);
-  if ((rc = alloc_scratch(ctx, &ctx->tw, q))) return bail(rc);
   if ((rc = alloc_scratch(ctx, &ctx->y0, q))) return bail(rc);
   if ((rc = alloc_scratch(ctx, &ctx->y1, q))) return bail(rc);
   if ((rc = alloc_scratch(ctx, &ctx->y2, q))) return bail(rc);
@@ -572,7 +452,7 @@ void pslr_ctx_destroy(pslr_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   for (void* p : ctx->allocations) cudaFree(p);
-  if (ctx->pinned) cudaFreeHost(ctx->pinned);
+  for (cudaEvent_t ev : ctx->prof_events) cudaEventDestroy(ev);
   delete ctx;
 }
 
@@ -593,6 +473,8 @@ static int set_correction_common(pslr_ctx* ctx, int64_t r, const double* V, bool
   free_ptr(ctx, ctx->u);
   ctx->V = ctx->G = ctx->partials = ctx->u = nullptr;
   ctx->r = 0;
+  ctx->K.V = nullptr;
+  ctx->K.r = 0;
   if (r == 0 || ctx->q == 0) return PSLR_OK;
   RET(alloc_scratch(ctx, &ctx->V, ctx->q * r));
   RET(alloc_scratch(ctx, &ctx->G, r * r));
@@ -602,6 +484,10 @@ static int set_correction_common(pslr_ctx* ctx, int64_t r, const double* V, bool
                 V_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice));
   CK(cudaMemcpy(ctx->G, G, r * r * sizeof(double), cudaMemcpyHostToDevice));
   ctx->r = r;
+  ctx->K.V = ctx->V;
+  ctx->K.r = (int)r;
+  // per-CTA partials of the V^T y reduction
+  RET(ensure(ctx, &ctx->red, &ctx->red_len, (int64_t)vt_grid(ctx->q, ctx->sm_count) * r + 8));
   return PSLR_OK;
 }
 
@@ -633,15 +519,13 @@ int pslr_apply_S(pslr_ctx* ctx, const double* v, double* out, void* stream) {
   StepArgs a;
   a.b1 = BT_EY;
   a.yE = v;
-  a.tb = ctx->tb;
   a.xb = ctx->xb;
   a.i1 = IT_CY;
   a.yC = v;
   a.i2 = IT_FX;
   a.i2_sub = 1;
   a.yout = out;
-  RET(run_step(ctx, a, S(stream)));
-  return PSLR_OK;
+  return run_step(ctx, a, S(stream));
 }
 
 int pslr_apply_neumann(pslr_ctx* ctx, int64_t m, const double* v, double* out, void* stream) {
@@ -664,15 +548,8 @@ int pslr_apply_correction(pslr_ctx* ctx, const double* y, double* out, void* str
     if (out != y) CK(cudaMemcpyAsync(out, y, ctx->q * sizeof(double), cudaMemcpyDeviceToDevice, st));
     return PSLR_OK;
   }
-  RET(op_correction_core_from(ctx, y, st));
-  StepArgs a;
-  a.i1 = IT_G;
-  a.g = y;
-  a.i2 = IT_VU;
-  a.i2_sub = 0;
-  a.u = ctx->u;
-  a.yout = out;
-  RET(run_step(ctx, a, st));
+  CKL(launch_vt_dot(ctx, y, st));     // u = G V^T y
+  CKL(launch_vu_add(ctx, y, out, st));  // out = y + V u
   return PSLR_OK;
 }
 
@@ -687,11 +564,11 @@ int pslr_spmv(pslr_ctx* ctx, int which, const double* x, double* y, void* stream
   const DevCsr* M = nullptr;
   switch (which) {
     case 0: M = &ctx->A; break;
-    case 1: M = &ctx->E; break;
-    case 2: M = &ctx->F; break;
+    case 1: M = &ctx->K.E; break;
+    case 2: M = &ctx->K.F; break;
     case 3: M = &ctx->C0; break;
-    case 4: M = &ctx->Cg; break;
-    case 5: M = &ctx->C; break;
+    case 4: M = &ctx->K.Cg; break;
+    case 5: M = &ctx->K.C; break;
     default: return fail(PSLR_EINVAL, "unknown matrix selector");
   }
   CKL(launch_spmv(*M, x, y, S(stream)));
@@ -726,189 +603,27 @@ int pslr_apply_profiled(pslr_ctx* ctx, int64_t m, const double* b, double* z, vo
   return PSLR_OK;
 }
 
+int pslr_debug_trace(pslr_ctx* ctx, int64_t* out, int64_t cap, int64_t* count) {
+  *count = 0;
+  if (!ctx->K.trace) return PSLR_OK;
+  RET(set_device(ctx));
+  long long n = 0;
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpy(&n, ctx->K.trace, sizeof(long long), cudaMemcpyDeviceToHost));
+  n = std::min<long long>(n, ctx->K.trace_cap);
+  n = std::min<long long>(n, cap / 2);
+  if (n > 0) CK(cudaMemcpy(out, ctx->K.trace + 2, 2 * n * sizeof(long long), cudaMemcpyDeviceToHost));
+  CK(cudaMemset(ctx->K.trace, 0, 16));
+  *count = n;
+  return PSLR_OK;
+}
+
 int pslr_apply_host(pslr_ctx* ctx, int64_t m, const double* b_host, double* z_host, void* stream) {
   RET(set_device(ctx));
   cudaStream_t st = S(stream);
   CK(cudaMemcpyAsync(ctx->io_b, b_host, ctx->n * sizeof(double), cudaMemcpyHostToDevice, st));
   RET(op_apply(ctx, m, ctx->io_b, ctx->io_z, st));
   CK(cudaMemcpyAsync(z_host, ctx->io_z, ctx->n * sizeof(double), cudaMemcpyDeviceToHost, st));
-  CK(cudaStreamSynchronize(st));
-  return PSLR_OK;
-}
-
-int pslr_arnoldi(pslr_ctx* ctx, int64_t m, int64_t rank, const double* v0, double* V_dev, double* H,
-                 int64_t* r_out, void* stream) {
-  RET(set_device(ctx));
-  cudaStream_t st = S(stream);
-  const int64_t q = ctx->q;
-  if (rank < 0) return fail(PSLR_EDIM, "rank must be >= 0");
-  rank = std::min(rank, q);
-  *r_out = 0;
-  if (q == 0 || rank == 0) return PSLR_OK;
-  RET(ensure(ctx, &ctx->kv, &ctx->kv_len, q * (rank + 1)));
-  double* Vc = ctx->kv;  // column-major q x (rank+1)
-  CK(cudaMemsetAsync(Vc, 0, q * (rank + 1) * sizeof(double), st));
-  CK(cudaMemcpyAsync(Vc, v0, q * sizeof(double), cudaMemcpyHostToDevice, st));
-  std::vector<double> Hb((rank + 1) * rank, 0.0);  // row-major (rank+1) x rank
-  std::vector<double> h(rank + 1);
-  int64_t r = rank;
-  double* w = ctx->kw;
-  for (int64_t j = 0; j < rank; ++j) {
-    RET(op_apply_err(ctx, m, Vc + j * q, w, st));
-    double hn = 0.0;
-    RET(cgs2(ctx, Vc, q, (int)(j + 1), w, h.data(), &hn, st));
-    for (int64_t i = 0; i <= j; ++i) Hb[i * rank + j] = h[i];
-    Hb[(j + 1) * rank + j] = hn;
-    if (hn <= 1e-14) {  // lowrank.py:69-71 (BREAKDOWN_RTOL, start vector has norm 1)
-      r = j + 1;
-      break;
-    }
-    CK(cudaMemcpyAsync(ctx->h_dev, &hn, sizeof(double), cudaMemcpyHostToDevice, st));
-    CKL(launch_div_scalar(w, ctx->h_dev, Vc + (j + 1) * q, q, st));
-  }
-  CKL(launch_transpose_basis(Vc, q, (int)r, V_dev, st));
-  for (int64_t i = 0; i < r; ++i)
-    for (int64_t j = 0; j < r; ++j) H[i * r + j] = Hb[i * rank + j];
-  CK(cudaStreamSynchronize(st));
-  *r_out = r;
-  return PSLR_OK;
-}
-
-int pslr_gmres(pslr_ctx* ctx, int64_t m, const double* b, double* x, double tol, int64_t maxit,
-               int64_t restart, int precond, int flexible, int64_t* iterations, int* converged,
-               double* final_relres, double* history, int64_t* history_len, void* stream) {
-  RET(set_device(ctx));
-  cudaStream_t st = S(stream);
-  const int64_t n = ctx->n;
-  std::vector<double> hist;
-  auto finish = [&](bool conv, int64_t its, double rel) {
-    *iterations = its;
-    *converged = conv ? 1 : 0;
-    *final_relres = rel;
-    for (size_t i = 0; i < hist.size() && (int64_t)i <= maxit; ++i) history[i] = hist[i];
-    *history_len = (int64_t)std::min<size_t>(hist.size(), (size_t)maxit + 1);
-  };
-  double bnorm = 0.0;
-  RET(dnorm(ctx, b, n, &bnorm, st));
-  CK(cudaMemsetAsync(x, 0, n * sizeof(double), st));
-  if (bnorm == 0.0) {
-    hist.push_back(1.0);
-    finish(true, 0, 0.0);
-    CK(cudaStreamSynchronize(st));
-    return PSLR_OK;
-  }
-  hist.push_back(1.0);
-  int64_t total = 0;
-  bool conv = false;
-  double relres = 1.0;
-  double* r = ctx->kr;
-  double* w = ctx->kw;
-  double* t = ctx->kt;
-  auto apply_M = [&](const double* in, double* out) -> int {
-    if (precond) return op_apply(ctx, m, in, out, st);
-    if (out != in) CK(cudaMemcpyAsync(out, in, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
-    return PSLR_OK;
-  };
-  while (total < maxit && !conv) {
-    // r = b - A x                                            krylov.py:56
-    CKL(launch_spmv(ctx->A, x, t, st));
-    CKL(launch_sub(b, t, r, n, st));
-    double beta = 0.0;
-    RET(dnorm(ctx, r, n, &beta, st));
-    relres = beta / bnorm;
-    if (relres <= tol) {
-      conv = true;
-      break;
-    }
-    const int64_t cycle = restart <= 0 ? maxit - total : std::min(restart, maxit - total);
-    RET(ensure(ctx, &ctx->kv, &ctx->kv_len, n * (cycle + 1)));
-    if (flexible) RET(ensure(ctx, &ctx->kz, &ctx->kz_len, n * cycle));
-    double* Vb = ctx->kv;
-    std::vector<double> Hc((cycle + 1) * cycle, 0.0);  // row-major (cycle+1) x cycle
-    auto Hat = [&](int64_t i, int64_t j) -> double& { return Hc[i * cycle + j]; };
-    std::vector<double> cs(cycle, 0.0), sn(cycle, 0.0), g(cycle + 1, 0.0), h(cycle + 1);
-    g[0] = beta;
-    RET(ensure(ctx, &ctx->h_dev, &ctx->h_len, 2 * (cycle + 1) + 8));
-    CK(cudaMemcpyAsync(ctx->h_dev, &beta, sizeof(double), cudaMemcpyHostToDevice, st));
-    CKL(launch_div_scalar(r, ctx->h_dev, Vb, n, st));
-    int64_t j = 0;
-    bool breakdown = false;
-    while (j < cycle) {
-      // w = A M v_j                                          krylov.py:74
-      double* mv = flexible ? ctx->kz + j * n : t;
-      RET(apply_M(Vb + j * n, mv));
-      CKL(launch_spmv(ctx->A, mv, w, st));
-      double hnext = 0.0;
-      RET(cgs2(ctx, Vb, n, (int)(j + 1), w, h.data(), &hnext, st));
-      bool finite = std::isfinite(hnext);
-      for (int64_t i = 0; i <= j; ++i) finite = finite && std::isfinite(h[i]);
-      if (!finite) return fail(PSLR_ENONFINITE, "GMRES diverged: non-finite values in the recurrence");
-      for (int64_t i = 0; i <= j; ++i) Hat(i, j) = h[i];
-      Hat(j + 1, j) = hnext;
-      for (int64_t i = 0; i < j; ++i) {  // krylov.py:86-97
-        const double tmp = cs[i] * Hat(i, j) + sn[i] * Hat(i + 1, j);
-        Hat(i + 1, j) = -sn[i] * Hat(i, j) + cs[i] * Hat(i + 1, j);
-        Hat(i, j) = tmp;
-      }
-      const double denom = std::hypot(Hat(j, j), hnext);
-      if (denom == 0.0) {
-        cs[j] = 1.0;
-        sn[j] = 0.0;
-      } else {
-        cs[j] = Hat(j, j) / denom;
-        sn[j] = hnext / denom;
-      }
-      Hat(j, j) = denom;
-      g[j + 1] = -sn[j] * g[j];
-      g[j] = cs[j] * g[j];
-      ++total;
-      ++j;
-      const double est = std::fabs(g[j]) / bnorm;
-      hist.push_back(est);
-      if (hnext <= 1e-14 * beta) {
-        breakdown = true;
-        break;
-      }
-      if (est <= tol) break;
-      if (j < cycle) {
-        CK(cudaMemcpyAsync(ctx->h_dev, &hnext, sizeof(double), cudaMemcpyHostToDevice, st));
-        CKL(launch_div_scalar(w, ctx->h_dev, Vb + j * n, n, st));
-      }
-    }
-    if (j > 0) {  // krylov.py:110-114
-      std::vector<double> y(j, 0.0);
-      for (int64_t i = j - 1; i >= 0; --i) {
-        double acc = 0.0;
-        for (int64_t k = i + 1; k < j; ++k) acc += Hat(i, k) * y[k];
-        y[i] = (g[i] - acc) / Hat(i, i);
-      }
-      CK(cudaMemcpyAsync(ctx->h_dev, y.data(), j * sizeof(double), cudaMemcpyHostToDevice, st));
-      if (flexible) {
-        CKL(launch_gemv(ctx->kz, n, (int)j, ctx->h_dev, t, n, st));
-        CKL(launch_add_inplace(x, t, n, st));
-      } else {
-        CKL(launch_gemv(Vb, n, (int)j, ctx->h_dev, r, n, st));
-        RET(apply_M(r, t));
-        CKL(launch_add_inplace(x, t, n, st));
-      }
-    }
-    CKL(launch_spmv(ctx->A, x, t, st));
-    CKL(launch_sub(b, t, r, n, st));
-    double rn = 0.0;
-    RET(dnorm(ctx, r, n, &rn, st));
-    relres = rn / bnorm;
-    hist.back() = relres;
-    if (relres <= tol)
-      conv = true;
-    else if (breakdown)
-      break;
-  }
-  if (!conv && total < maxit && !std::isfinite(relres))
-    return fail(PSLR_ENONFINITE, "GMRES diverged: non-finite residual");
-  const int64_t its = conv ? total : maxit;
-  if (!conv)
-    while ((int64_t)hist.size() < maxit + 1) hist.push_back(relres);
-  finish(conv, its, relres);
   CK(cudaStreamSynchronize(st));
   return PSLR_OK;
 }

@@ -1,0 +1,234 @@
+// krylov.cu — device Krylov drivers of the C-ABI: Arnoldi on E_rr(m)
+// (lowrank.py:39-73) and restarted right-preconditioned GMRES / FGMRES
+// (krylov.py:35-129).  Vectors, the Krylov basis and every reduction live on the
+// device (libpslr kernels); the (cycle+1)-sized Hessenberg/Givens bookkeeping is
+// scalar host code with the reference's exact control flow.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "pslr_ops.h"
+
+namespace pslr {
+
+static cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
+
+static int dnorm(pslr_ctx* ctx, const double* x, int64_t n, double* out_host, cudaStream_t st) {
+  RET(ensure(ctx, &ctx->red, &ctx->red_len, (int64_t)dot_grid(n, ctx->sm_count) * 1 + 8));
+  RET(ensure(ctx, &ctx->h_dev, &ctx->h_len, 8));
+  CKL(launch_multidot(ctx, x, n, 1, x, n, ctx->h_dev, st));
+  double d = 0.0;
+  CK(cudaMemcpyAsync(&d, ctx->h_dev, sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  *out_host = std::sqrt(d);
+  return PSLR_OK;
+}
+
+// Classical Gram-Schmidt with one reorthogonalisation against the first k columns
+// of X (column-major, ld = n): krylov.py:75-80 / lowrank.py:62-67.  h_host = h1 + h2,
+// hnorm = ||w|| after both passes.
+static int cgs2(pslr_ctx* ctx, const double* X, int64_t n, int k, double* w, double* h_host,
+                double* hnorm, cudaStream_t st) {
+  RET(ensure(ctx, &ctx->red, &ctx->red_len, (int64_t)dot_grid(n, ctx->sm_count) * (k + 1) + 8));
+  RET(ensure(ctx, &ctx->h_dev, &ctx->h_len, 2 * (int64_t)k + 8));
+  double* h1 = ctx->h_dev;
+  double* h2 = ctx->h_dev + k;
+  double* nn = ctx->h_dev + 2 * k;
+  CKL(launch_multidot(ctx, X, n, k, w, n, h1, st));
+  CKL(launch_gemv_sub(X, n, k, h1, w, n, st));
+  CKL(launch_multidot(ctx, X, n, k, w, n, h2, st));
+  CKL(launch_gemv_sub(X, n, k, h2, w, n, st));
+  CKL(launch_multidot(ctx, w, n, 1, w, n, nn, st));
+  std::vector<double> tmp(2 * k + 1);
+  CK(cudaMemcpyAsync(tmp.data(), ctx->h_dev, (2 * k + 1) * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  for (int c = 0; c < k; ++c) h_host[c] = tmp[c] + tmp[k + c];
+  *hnorm = std::sqrt(tmp[2 * k]);
+  return PSLR_OK;
+}
+
+}  // namespace pslr
+
+using namespace pslr;
+
+extern "C" {
+
+int pslr_arnoldi(pslr_ctx* ctx, int64_t m, int64_t rank, const double* v0, double* V_dev, double* H,
+                 int64_t* r_out, void* stream) {
+  RET(set_device(ctx));
+  cudaStream_t st = S(stream);
+  const int64_t q = ctx->q;
+  if (rank < 0) return fail(PSLR_EDIM, "rank must be >= 0");
+  rank = std::min(rank, q);
+  *r_out = 0;
+  if (q == 0 || rank == 0) return PSLR_OK;
+  RET(ensure(ctx, &ctx->kv, &ctx->kv_len, q * (rank + 1)));
+  double* Vc = ctx->kv;  // column-major q x (rank+1)
+  CK(cudaMemsetAsync(Vc, 0, q * (rank + 1) * sizeof(double), st));
+  CK(cudaMemcpyAsync(Vc, v0, q * sizeof(double), cudaMemcpyHostToDevice, st));
+  std::vector<double> Hb((rank + 1) * rank, 0.0);  // row-major (rank+1) x rank
+  std::vector<double> h(rank + 1);
+  int64_t r = rank;
+  double* w = ctx->kw;
+  for (int64_t j = 0; j < rank; ++j) {
+    RET(op_apply_err(ctx, m, Vc + j * q, w, st));
+    double hn = 0.0;
+    RET(cgs2(ctx, Vc, q, (int)(j + 1), w, h.data(), &hn, st));
+    for (int64_t i = 0; i <= j; ++i) Hb[i * rank + j] = h[i];
+    Hb[(j + 1) * rank + j] = hn;
+    if (hn <= 1e-14) {  // lowrank.py:69-71 (BREAKDOWN_RTOL, start vector has norm 1)
+      r = j + 1;
+      break;
+    }
+    CK(cudaMemcpyAsync(ctx->h_dev, &hn, sizeof(double), cudaMemcpyHostToDevice, st));
+    CKL(launch_div_scalar(w, ctx->h_dev, Vc + (j + 1) * q, q, st));
+  }
+  CKL(launch_transpose_basis(Vc, q, (int)r, V_dev, st));
+  for (int64_t i = 0; i < r; ++i)
+    for (int64_t j = 0; j < r; ++j) H[i * r + j] = Hb[i * rank + j];
+  CK(cudaStreamSynchronize(st));
+  *r_out = r;
+  return PSLR_OK;
+}
+
+int pslr_gmres(pslr_ctx* ctx, int64_t m, const double* b, double* x, double tol, int64_t maxit,
+               int64_t restart, int precond, int flexible, int64_t* iterations, int* converged,
+               double* final_relres, double* history, int64_t* history_len, void* stream) {
+  RET(set_device(ctx));
+  cudaStream_t st = S(stream);
+  const int64_t n = ctx->n;
+  std::vector<double> hist;
+  auto finish = [&](bool conv, int64_t its, double rel) {
+    *iterations = its;
+    *converged = conv ? 1 : 0;
+    *final_relres = rel;
+    for (size_t i = 0; i < hist.size() && (int64_t)i <= maxit; ++i) history[i] = hist[i];
+    *history_len = (int64_t)std::min<size_t>(hist.size(), (size_t)maxit + 1);
+  };
+  double bnorm = 0.0;
+  RET(dnorm(ctx, b, n, &bnorm, st));
+  CK(cudaMemsetAsync(x, 0, n * sizeof(double), st));
+  hist.push_back(1.0);
+  if (bnorm == 0.0) {
+    finish(true, 0, 0.0);
+    CK(cudaStreamSynchronize(st));
+    return PSLR_OK;
+  }
+  int64_t total = 0;
+  bool conv = false;
+  double relres = 1.0;
+  double* r = ctx->kr;
+  double* w = ctx->kw;
+  double* t = ctx->kt;
+  auto apply_M = [&](const double* in, double* out) -> int {
+    if (precond) return op_apply(ctx, m, in, out, st);
+    if (out != in) CK(cudaMemcpyAsync(out, in, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    return PSLR_OK;
+  };
+  while (total < maxit && !conv) {
+    // r = b - A x                                            krylov.py:56
+    CKL(launch_spmv(ctx->A, x, t, st));
+    CKL(launch_sub(b, t, r, n, st));
+    double beta = 0.0;
+    RET(dnorm(ctx, r, n, &beta, st));
+    relres = beta / bnorm;
+    if (relres <= tol) {
+      conv = true;
+      break;
+    }
+    const int64_t cycle = restart <= 0 ? maxit - total : std::min(restart, maxit - total);
+    RET(ensure(ctx, &ctx->kv, &ctx->kv_len, n * (cycle + 1)));
+    if (flexible) RET(ensure(ctx, &ctx->kz, &ctx->kz_len, n * cycle));
+    double* Vb = ctx->kv;
+    std::vector<double> Hc((cycle + 1) * cycle, 0.0);  // row-major (cycle+1) x cycle
+    auto Hat = [&](int64_t i, int64_t j) -> double& { return Hc[i * cycle + j]; };
+    std::vector<double> cs(cycle, 0.0), sn(cycle, 0.0), g(cycle + 1, 0.0), h(cycle + 1);
+    g[0] = beta;
+    RET(ensure(ctx, &ctx->h_dev, &ctx->h_len, 2 * (cycle + 1) + 8));
+    CK(cudaMemcpyAsync(ctx->h_dev, &beta, sizeof(double), cudaMemcpyHostToDevice, st));
+    CKL(launch_div_scalar(r, ctx->h_dev, Vb, n, st));
+    int64_t j = 0;
+    bool breakdown = false;
+    while (j < cycle) {
+      // w = A M v_j                                          krylov.py:74
+      double* mv = flexible ? ctx->kz + j * n : t;
+      RET(apply_M(Vb + j * n, mv));
+      CKL(launch_spmv(ctx->A, mv, w, st));
+      double hnext = 0.0;
+      RET(cgs2(ctx, Vb, n, (int)(j + 1), w, h.data(), &hnext, st));
+      bool finite = std::isfinite(hnext);
+      for (int64_t i = 0; i <= j; ++i) finite = finite && std::isfinite(h[i]);
+      if (!finite) return fail(PSLR_ENONFINITE, "GMRES diverged: non-finite values in the recurrence");
+      for (int64_t i = 0; i <= j; ++i) Hat(i, j) = h[i];
+      Hat(j + 1, j) = hnext;
+      for (int64_t i = 0; i < j; ++i) {  // krylov.py:86-97
+        const double tmp = cs[i] * Hat(i, j) + sn[i] * Hat(i + 1, j);
+        Hat(i + 1, j) = -sn[i] * Hat(i, j) + cs[i] * Hat(i + 1, j);
+        Hat(i, j) = tmp;
+      }
+      const double denom = std::hypot(Hat(j, j), hnext);
+      if (denom == 0.0) {
+        cs[j] = 1.0;
+        sn[j] = 0.0;
+      } else {
+        cs[j] = Hat(j, j) / denom;
+        sn[j] = hnext / denom;
+      }
+      Hat(j, j) = denom;
+      g[j + 1] = -sn[j] * g[j];
+      g[j] = cs[j] * g[j];
+      ++total;
+      ++j;
+      const double est = std::fabs(g[j]) / bnorm;
+      hist.push_back(est);
+      if (hnext <= 1e-14 * beta) {
+        breakdown = true;
+        break;
+      }
+      if (est <= tol) break;
+      if (j < cycle) {
+        CK(cudaMemcpyAsync(ctx->h_dev, &hnext, sizeof(double), cudaMemcpyHostToDevice, st));
+        CKL(launch_div_scalar(w, ctx->h_dev, Vb + j * n, n, st));
+      }
+    }
+    if (j > 0) {  // krylov.py:110-114
+      std::vector<double> y(j, 0.0);
+      for (int64_t i = j - 1; i >= 0; --i) {
+        double acc = 0.0;
+        for (int64_t k = i + 1; k < j; ++k) acc += Hat(i, k) * y[k];
+        y[i] = (g[i] - acc) / Hat(i, i);
+      }
+      CK(cudaMemcpyAsync(ctx->h_dev, y.data(), j * sizeof(double), cudaMemcpyHostToDevice, st));
+      if (flexible) {
+        CKL(launch_gemv(ctx->kz, n, (int)j, ctx->h_dev, t, n, st));
+        CKL(launch_add_inplace(x, t, n, st));
+      } else {
+        CKL(launch_gemv(Vb, n, (int)j, ctx->h_dev, r, n, st));
+        RET(apply_M(r, t));
+        CKL(launch_add_inplace(x, t, n, st));
+      }
+    }
+    CKL(launch_spmv(ctx->A, x, t, st));
+    CKL(launch_sub(b, t, r, n, st));
+    double rn = 0.0;
+    RET(dnorm(ctx, r, n, &rn, st));
+    relres = rn / bnorm;
+    hist.back() = relres;
+    if (relres <= tol)
+      conv = true;
+    else if (breakdown)
+      break;
+  }
+  if (!conv && total < maxit && !std::isfinite(relres))
+    return fail(PSLR_ENONFINITE, "GMRES diverged: non-finite residual");
+  const int64_t its = conv ? total : maxit;
+  if (!conv)
+    while ((int64_t)hist.size() < maxit + 1) hist.push_back(relres);
+  finish(conv, its, relres);
+  CK(cudaStreamSynchronize(st));
+  return PSLR_OK;
+}
+
+}  // extern "C"

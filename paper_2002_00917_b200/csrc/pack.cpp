@@ -1,0 +1,250 @@
+// pack.cpp — host packer: level-schedules every block of a block-diagonal
+// triangular factor and emits the streamed device format the sm_100a solve
+// kernel consumes (see kernels.cu: tri_phase).
+//
+// Per block the rows are ordered by (dependency level, entry count desc, row),
+// which defines the row's "position".  Positions are global (block b owns
+// [off_b, off_{b+1}) in both row and position space).  Each level is cut into
+// segments (jagged-diagonal layout: slab k holds the k-th entry of every row
+// that has one, so within a row the reference's ascending-column summation
+// order is kept), segments are grouped into chunks of <= stage_bytes that the
+// kernel streams into shared memory with TMA bulk copies.
+//
+// A dependency is read from the shared-memory ring (slot = local position mod W)
+// when fewer than W positions separate it from the end of the reading row's
+// level; otherwise ("far") it is read from the global position-ordered array.
+#include "pslr_internal.h"
+
+#include <algorithm>
+#include <cstring>
+#include <numeric>
+
+namespace pslr {
+
+namespace {
+
+inline int64_t a4(int64_t x) { return (x + 3) & ~int64_t(3); }
+inline int64_t a2(int64_t x) { return (x + 1) & ~int64_t(1); }
+
+}  // namespace
+
+int analyze_factor(const pslr_csr& M, const std::vector<int64_t>& off, bool upper, TriAnalysis& A,
+                   const char* name) {
+  const int64_t n = M.nrows;
+  const int64_t nb = (int64_t)off.size() - 1;
+  A.upper = upper;
+  A.pos_of_row.assign(n, 0);
+  A.row_at_pos.assign(n, 0);
+  A.level_end.assign(n, 0);
+  A.diag.assign(upper ? n : 0, 0.0);
+  A.depth_max = 0;
+  A.levels = 0;
+  A.reach = 0;
+  A.level_of_row.assign(n, 0);
+  A.len.assign(n, 0);
+  for (int64_t r = 0; r < n; ++r) {
+    int32_t c = 0;
+    for (int64_t e = M.indptr[r]; e < M.indptr[r + 1]; ++e) c += (M.indices[e] != r);
+    A.len[r] = c;
+  }
+  std::vector<int32_t> lev;
+  for (int64_t b = 0; b < nb; ++b) {
+    const int64_t lo = off[b], hi = off[b + 1], nr = hi - lo;
+    lev.assign(nr, 0);
+    for (int64_t t = 0; t < nr; ++t) {
+      const int64_t i = upper ? nr - 1 - t : t;
+      int32_t lv = 0;
+      bool has_diag = false;
+      for (int64_t e = M.indptr[lo + i]; e < M.indptr[lo + i + 1]; ++e) {
+        const int64_t jg = M.indices[e];
+        if (jg < lo || jg >= hi) return fail(PSLR_EINVAL, std::string(name) + " is not block diagonal");
+        const int64_t j = jg - lo;
+        if (upper ? (j < i) : (j > i))
+          return fail(PSLR_EINVAL, std::string(name) + (upper ? " is not upper" : " is not lower") +
+                                       " triangular");
+        if (j == i) {
+          has_diag = true;
+          if (upper) A.diag[lo + i] = M.data[e];
+        } else {
+          lv = std::max(lv, lev[j] + 1);
+        }
+      }
+      if (upper && (!has_diag || A.diag[lo + i] == 0.0))
+        return fail(PSLR_ESINGULAR, std::string(name) + ": A is singular: zero entry on diagonal.");
+      lev[i] = lv;
+    }
+    int32_t depth = 0;
+    for (int64_t i = 0; i < nr; ++i) depth = std::max(depth, lev[i] + 1);
+    A.depth_max = std::max<int64_t>(A.depth_max, depth);
+    A.levels += depth;
+    std::vector<int64_t> order(nr);
+    std::iota(order.begin(), order.end(), 0);
+    auto len = [&](int64_t i) { return A.len[lo + i]; };
+    std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t c) {
+      if (lev[a] != lev[c]) return lev[a] < lev[c];
+      return len(a) > len(c);
+    });
+    // level boundaries in position space
+    std::vector<int64_t> lvl_end(depth, 0);
+    for (int64_t k = 0; k < nr; ++k) lvl_end[lev[order[k]]] = lo + k + 1;
+    for (int64_t k = 0; k < nr; ++k) {
+      const int64_t i = order[k];
+      A.pos_of_row[lo + i] = (int32_t)(lo + k);
+      A.row_at_pos[lo + k] = (int32_t)(lo + i);
+      A.level_end[lo + i] = (int32_t)lvl_end[lev[i]];
+    }
+    for (int64_t i = 0; i < nr; ++i) A.level_of_row[lo + i] = lev[i];
+    // reach: positions between a dependency and the end of the reading row's level
+    for (int64_t i = 0; i < nr; ++i)
+      for (int64_t e = M.indptr[lo + i]; e < M.indptr[lo + i + 1]; ++e) {
+        const int64_t j = M.indices[e] - lo;
+        if (j == i) continue;
+        A.reach = std::max<int64_t>(A.reach, A.level_end[lo + i] - A.pos_of_row[lo + j]);
+      }
+  }
+  return PSLR_OK;
+}
+
+// Emit the streamed format.  far_index[row] gives the global index a far dependency
+// is read from (the U-position of the row, where the kernel keeps every value).
+// info_of_row[row]: the per-row int the kernel needs (L: U-position, U: row id).
+int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAnalysis& A, int64_t W,
+                int64_t stage_bytes, int64_t seg_rows, const std::vector<int32_t>& far_index,
+                const std::vector<int32_t>& info_of_row, TriHost& out, const char* name) {
+  const int64_t nb = (int64_t)off.size() - 1;
+  const bool upper = A.upper;
+  out.data.clear();
+  out.chunks.clear();
+  out.blk_chunk.assign(nb + 1, 0);
+  out.far = 0;
+  out.nnz_offdiag = 0;
+  out.segments = 0;
+  std::vector<uint8_t> seg;
+  auto seg_bytes = [&](int64_t nrows, int64_t w, int64_t nnz) {
+    int64_t b = 32 + 4 * a4(w + 1) + 4 * a4(nrows);
+    if (upper) b += 16 * a2(nrows);
+    b += 8 * a2(nnz) + 4 * a4(nnz);
+    return b;
+  };
+  // current chunk being filled
+  int64_t chunk_start = 0, chunk_nseg = 0, chunk_pos0 = 0, chunk_rows = 0;
+  auto close_chunk = [&]() {
+    if (chunk_nseg == 0) return;
+    ChunkDesc d;
+    d.off = chunk_start;
+    d.bytes = (int32_t)((int64_t)out.data.size() - chunk_start);
+    d.nseg = (int32_t)chunk_nseg;
+    d.pos0 = (int32_t)chunk_pos0;
+    d.npos = (int32_t)chunk_rows;
+    d.pad[0] = d.pad[1] = 0;
+    chunk_rows = 0;
+    // the kernel reads the segment count from the first segment's header (word 6)
+    reinterpret_cast<int32_t*>(out.data.data() + chunk_start)[6] = (int32_t)chunk_nseg;
+    // ... and the base position of the chunk's rhs slice (word 7, even for 16-B TMA alignment)
+    reinterpret_cast<int32_t*>(out.data.data() + chunk_start)[7] = (int32_t)(chunk_pos0 & ~int64_t(1));
+    out.chunks.push_back(d);
+    chunk_nseg = 0;
+    chunk_start = (int64_t)out.data.size();
+  };
+  for (int64_t b = 0; b < nb; ++b) {
+    const int64_t lo = off[b], hi = off[b + 1];
+    close_chunk();
+    out.blk_chunk[b] = (int32_t)out.chunks.size();
+    int64_t k = lo;
+    while (k < hi) {
+      // one level: positions [k, level_end)
+      const int64_t row0 = A.row_at_pos[k];
+      const int64_t lend = A.level_end[row0];
+      int64_t s0 = k;
+      while (s0 < lend) {
+        // grow a segment while it fits a stage
+        int64_t s1 = s0, nnz = 0, w = 0;
+        while (s1 < lend && s1 - s0 < seg_rows) {
+          const int64_t len = A.len[A.row_at_pos[s1]];
+          const int64_t w2 = std::max(w, len);
+          if (seg_bytes(s1 - s0 + 1, w2, nnz + len) > stage_bytes) break;
+          w = w2;
+          nnz += len;
+          ++s1;
+        }
+        if (s1 == s0)
+          return fail(PSLR_EINVAL, std::string(name) + ": a row is too long for the streaming format");
+        const int64_t nrows = s1 - s0;
+        const int64_t bytes = seg_bytes(nrows, w, nnz);
+        if ((int64_t)out.data.size() - chunk_start + bytes > stage_bytes ||
+            chunk_rows + nrows > kChunkRows)
+          close_chunk();
+        if (chunk_nseg == 0) chunk_pos0 = s0;
+        chunk_rows += nrows;
+        seg.assign(bytes, 0);
+        int32_t* h = reinterpret_cast<int32_t*>(seg.data());
+        h[0] = (int32_t)nrows;
+        h[1] = (int32_t)w;
+        h[2] = (s1 == lend) ? 1 : 0;  // ends a level
+        h[3] = (int32_t)s0;
+        h[4] = (int32_t)nnz;
+        h[5] = (int32_t)bytes;
+        int32_t* soff = h + 8;  // slab offsets, w+1 entries
+        int32_t* info = soff + a4(w + 1);
+        std::vector<int64_t> cnt(w, 0);
+        uint8_t* p = reinterpret_cast<uint8_t*>(info + a4(nrows));
+        double* sd = nullptr;
+        double* invd = nullptr;
+        if (upper) {
+          sd = reinterpret_cast<double*>(p);
+          invd = sd + a2(nrows);
+          p = reinterpret_cast<uint8_t*>(invd + a2(nrows));
+        }
+        double* val = reinterpret_cast<double*>(p);
+        int32_t* slot = reinterpret_cast<int32_t*>(val + a2(nnz));
+        // slab counts (rows sorted by length desc within the level)
+        for (int64_t t = 0; t < nrows; ++t) {
+          const int64_t r = A.row_at_pos[s0 + t];
+          const int64_t len = A.len[r];
+          for (int64_t kk = 0; kk < len; ++kk) cnt[kk]++;
+          info[t] = info_of_row[r];
+          if (upper) {
+            const double dinv = 1.0 / A.diag[r];
+            sd[t] = A.diag[r] * dinv;  // scipy: (U @ diags(1/diag)) diagonal
+            invd[t] = dinv;
+          }
+        }
+        std::vector<int64_t> slab_off(w + 1, 0);
+        for (int64_t kk = 0; kk < w; ++kk) slab_off[kk + 1] = slab_off[kk] + cnt[kk];
+        for (int64_t kk = 0; kk <= w; ++kk) soff[kk] = (int32_t)slab_off[kk];
+        for (int64_t t = 0; t < nrows; ++t) {
+          const int64_t r = A.row_at_pos[s0 + t];
+          int64_t kk = 0;
+          for (int64_t e = M.indptr[r]; e < M.indptr[r + 1]; ++e) {
+            const int64_t j = M.indices[e];
+            if (j == r) continue;
+            const int64_t idx = slab_off[kk] + t;
+            double v = M.data[e];
+            if (upper) v = v * (1.0 / A.diag[j]);  // scipy pre-scales U's columns by 1/diag
+            val[idx] = v;
+            const int64_t pj = A.pos_of_row[j];
+            if (lend - pj <= W) {
+              slot[idx] = (int32_t)((pj - lo) & (W - 1));
+            } else {
+              slot[idx] = (int32_t)(0x80000000u | (uint32_t)far_index[j]);
+              out.far++;
+              h[2] |= 2;  // the segment has far dependencies (kernel slow path)
+            }
+            ++kk;
+          }
+        }
+        out.data.insert(out.data.end(), seg.begin(), seg.end());
+        chunk_nseg++;
+        out.segments++;
+        out.nnz_offdiag += nnz;
+        s0 = s1;
+      }
+      k = lend;
+    }
+    close_chunk();
+  }
+  out.blk_chunk[nb] = (int32_t)out.chunks.size();
+  return PSLR_OK;
+}
+
+}  // namespace pslr

@@ -18,12 +18,6 @@ namespace pslr {
 int fail(int code, const std::string& msg);  // records the thread-local message, returns code
 double numpy_sum(const double* a, int64_t n);
 
-#ifdef __CUDACC__
-#define PSLR_HD __host__ __device__
-#else
-#define PSLR_HD
-#endif
-
 // CSR on the device, int32 row pointers (every matrix here has < 2^31 entries).
 struct DevCsr {
   int32_t nrows = 0, ncols = 0, nnz = 0;
@@ -32,23 +26,57 @@ struct DevCsr {
   const double* val = nullptr;
 };
 
-// A block-diagonal triangular factor, level-scheduled per block and packed in
-// level order ("position" = index in that order).  Off-diagonal entries only;
-// for U the values are pre-scaled by 1/diag of their column, exactly as scipy's
-// spsolve_triangular does before calling SuperLU (so the device solve reproduces
-// the reference bit for bit):  z_i = (b_i / sd_i) - sum_j U'_ij z_j ,  x_i = z_i * invd_i.
-struct DevTri {
-  int32_t nblocks = 0;
-  int32_t nlevels = 0, npos = 0, nnz = 0;
-  const int32_t* blk_lvl = nullptr;  // nblocks+1: level range of each block
-  const int32_t* lvl_pos = nullptr;  // nlevels+1: position range of each level
-  const int32_t* pos_row = nullptr;  // npos: absolute row (index into the p- or q-vector)
-  const int32_t* pos_ent = nullptr;  // npos+1: entry range of each position
-  const int32_t* col = nullptr;      // nnz: absolute column
-  const double* val = nullptr;       // nnz
-  const double* sd = nullptr;        // U only, per position: U_ii * (1/U_ii)
-  const double* invd = nullptr;      // U only, per position: 1/U_ii
+// One TMA-streamed chunk of a packed triangular factor (pack.cpp).
+struct ChunkDesc {
+  int64_t off;    // byte offset in the factor's data
+  int32_t bytes;  // multiple of 16
+  int32_t nseg;   // segments in the chunk
+  int32_t pos0;   // first global position of the chunk's rows
+  int32_t npos;   // rows in the chunk (consecutive positions)
+  int32_t pad[2];
 };
+
+// max rows per chunk: bounds the per-stage right-hand-side buffer
+constexpr int kChunkRows = 1024;
+
+// Segment layout inside a chunk (all parts 16-byte aligned):
+//   int32 hdr[8]   = {nrows, w, flags(bit0: ends a level), pos0, nnz, bytes, 0, 0}
+//   int32 cnt[w]   (slab sizes, non-increasing), padded to 4
+//   int32 info[nrows]  L: U-position of the row ; U: row id           , padded to 4
+//   U only: double sd[nrows], invd[nrows]                             , padded to 2
+//   double val[nnz]  (slab-major; U values pre-scaled by 1/diag of their column)
+//   int32 slot[nnz]  near: ring slot (< W) ; far: 0x80000000 | U-position of the dependency
+struct DevTri {
+  int32_t nblocks = 0, nchunks = 0;
+  const uint8_t* data = nullptr;
+  const ChunkDesc* chunks = nullptr;
+  const int32_t* blk_chunk = nullptr;  // nblocks+1
+  const int32_t* lpos = nullptr;       // L only: row -> global L-position (rhs placement)
+};
+
+// host-side analysis + packed output (pack.cpp)
+struct TriAnalysis {
+  bool upper = false;
+  std::vector<int32_t> pos_of_row, row_at_pos, level_end, level_of_row, len;
+  std::vector<double> diag;
+  int64_t depth_max = 0, levels = 0, reach = 0;
+};
+
+struct TriHost {
+  std::vector<uint8_t> data;
+  std::vector<ChunkDesc> chunks;
+  std::vector<int32_t> blk_chunk;
+  int64_t far = 0, nnz_offdiag = 0, segments = 0;
+};
+
+int analyze_factor(const pslr_csr& M, const std::vector<int64_t>& off, bool upper, TriAnalysis& A,
+                   const char* name);
+// threads per CTA of the fused step kernel = max rows per packed segment
+constexpr int kStepThreads = 512;
+
+int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAnalysis& A, int64_t W,
+                int64_t stage_bytes, int64_t seg_rows, const std::vector<int32_t>& far_index,
+                const std::vector<int32_t>& info_of_row, TriHost& out, const char* name);
 
 // Terms of the per-subdomain fused step (see kernels.cu: subdomain_step_kernel).
 enum BTerm : int { BT_NONE = 0, BT_F = 1, BT_EY = 2 };
@@ -59,7 +87,6 @@ struct StepArgs {
   int b1 = BT_NONE, b2 = BT_NONE;
   const double* f = nullptr;   // p-vector used by BT_F
   const double* yE = nullptr;  // q-vector multiplied by E for BT_EY
-  double* tb = nullptr;        // p scratch (L output / scaled U intermediate)
   double* xb = nullptr;        // p output of the B solve
   // ---- interface phase:  w = i1 (+|-) i2 ;  [y = C0^{-1} w] ; [y += cadd]
   int i1 = IT_NONE, i2 = IT_NONE;
@@ -68,11 +95,33 @@ struct StepArgs {
   const double* yC = nullptr;  // q-vector for IT_CY / IT_CGY
   const double* u = nullptr;   // r-vector for IT_VU
   int do_c0 = 0;
-  double* tw = nullptr;        // q scratch for the C0 solve
   const double* cadd = nullptr;
   double* yout = nullptr;      // q output
   double* partials = nullptr;  // [s][r] V^T yout partial sums (nullable)
   int tag = 0;                 // launch kind, for pslr_apply_profiled
+};
+
+// Everything the fused kernel reads besides StepArgs (constant per context).
+struct StepConst {
+  DevTri LB, UB, LC, UC;
+  DevCsr E, F, C, Cg;
+  const int32_t* int_off = nullptr;
+  const int32_t* ifc_off = nullptr;
+  const int32_t* erows = nullptr;     // interior rows with E entries, grouped by block
+  const int32_t* erow_off = nullptr;  // s+1
+  const double* V = nullptr;
+  int r = 0;
+  double* rhsB = nullptr;  // p: L_B right-hand side in L-position order
+  double* zB = nullptr;    // p: L_B output / U_B intermediate in U-position order
+  double* rhsC = nullptr;  // q
+  double* zC = nullptr;    // q
+  int ring_mask = 0;       // W - 1
+  int nst = 0;             // pipeline stages
+  int stage_bytes = 0;
+  int rhs_stride = 0;      // doubles per stage right-hand-side buffer
+  int smem_bytes = 0;
+  long long* trace = nullptr;  // PSLR_TRACE: [count, pad, (code, ns)...] of CTA 0
+  long long trace_cap = 0;
 };
 
 }  // namespace pslr
@@ -84,22 +133,18 @@ struct pslr_ctx {
   int sm_count = 0;
   std::vector<int64_t> interior_off, interface_off;
   // device-resident state
-  pslr::DevTri LB, UB, LC, UC;
-  pslr::DevCsr E, F, C, C0, Cg, A;
-  int32_t* d_int_off = nullptr;  // s+1
-  int32_t* d_ifc_off = nullptr;  // s+1
+  pslr::StepConst K;
+  pslr::DevCsr A, C0;
   double* V = nullptr;           // q x r row-major
   double* G = nullptr;           // r x r row-major
   // scratch
-  double* tb = nullptr;          // p
   double* xb = nullptr;          // p
-  double* tw = nullptr;          // q
   double* y0 = nullptr;          // q
   double* y1 = nullptr;          // q
   double* y2 = nullptr;          // q
   double* c = nullptr;           // q
   double* partials = nullptr;    // s x r
-  double* u = nullptr;           // r
+  double* u = nullptr;           // 2r
   double* red = nullptr;         // reduction scratch (multi-dot partials)
   int64_t red_len = 0;
   unsigned int* counter = nullptr;  // last-block reduction ticket
@@ -113,8 +158,6 @@ struct pslr_ctx {
   double* kw = nullptr;          // n
   double* kt = nullptr;          // n
   double* kr = nullptr;          // n
-  double* pinned = nullptr;      // host staging
-  int64_t pinned_len = 0;
   double* io_b = nullptr;        // n device staging for host apply
   double* io_z = nullptr;        // n
   std::vector<void*> allocations;

@@ -1,0 +1,89 @@
+"""Timeline of CTA 0 of the fused step kernel over one PSLR apply (PSLR_TRACE=1).
+usage: PSLR_TRACE=1 python tools/trace_apply.py [cfg5]"""
+import ctypes
+import os
+import sys
+
+import numpy as np
+
+os.environ.setdefault("PSLR_TRACE", "1")
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+import paper_2002_00917_b200 as pg  # noqa: E402
+from paper_2002_00917_b200 import _lib, workloads  # noqa: E402
+
+name = sys.argv[1] if len(sys.argv) > 1 else "cfg5"
+wl = workloads.CONFIGS[name]
+P = pg.build(wl.matrix(), wl.config())
+print(P.device.info(), flush=True)
+b = torch.from_numpy(np.random.default_rng(0).standard_normal(P.system.n)).cuda()
+P.apply(b)
+torch.cuda.synchronize()
+buf = np.zeros(2 * (1 << 20), dtype=np.int64)
+cnt = ctypes.c_int64()
+_lib.fns["pslr_debug_trace"](P.device.handle, buf.ctypes.data, buf.size, ctypes.byref(cnt))  # reset
+P.apply(b)
+torch.cuda.synchronize()
+_lib.check(_lib.fns["pslr_debug_trace"](P.device.handle, buf.ctypes.data, buf.size, ctypes.byref(cnt)))
+n = cnt.value
+ev = buf[:2 * n].reshape(n, 2)
+ev = ev[ev[:, 1] != 0]
+n = ev.shape[0]
+codes = ev[:, 0] >> 32
+args = ev[:, 0] & 0xffffffff
+ts = ev[:, 1] - ev[0, 1]
+# per-level timeline: a level = time between consecutive level-end barrier releases (41)
+rel = np.flatnonzero(codes == 41)
+arr = np.flatnonzero(codes == 40)
+if rel.size > 2:
+    lv = np.diff(ts[rel])
+    rows = args[arr[1:]] & 0xffff
+    ws = args[arr[1:]] >> 16
+    wait = ts[rel] - ts[arr]
+    print(f"levels {rel.size}: level us mean {lv.mean() / 1e3:.3f} median {np.median(lv) / 1e3:.3f} "
+          f"p90 {np.percentile(lv, 90) / 1e3:.3f}; barrier wait (thread0) mean {wait.mean() / 1e3:.3f}")
+    for lo, hi in ((0, 64), (64, 256), (256, 520)):
+        sel = (rows >= lo) & (rows < hi)
+        if sel.any():
+            print(f"   rows [{lo},{hi}): n={sel.sum()} level us mean {lv[sel].mean() / 1e3:.3f}")
+    print("   first 40 levels (us, rows, w):",
+          [(round(lv[i] / 1e3, 2), int(rows[i]), int(ws[i])) for i in range(min(40, lv.size))])
+names = {1: "start", 3: "prepass", 10: "phase0", 11: "phase1", 12: "phase2", 13: "phase3",
+         20: "chunk_ready", 21: "chunk_done", 30: "iface"}
+# summarise per launch: split at code 1
+starts = np.flatnonzero(codes == 1)
+for li, s0 in enumerate(starts):
+    s1 = starts[li + 1] if li + 1 < len(starts) else n
+    c, a, t = codes[s0:s1], args[s0:s1], ts[s0:s1]
+    t = t - t[0]
+    print(f"--- launch {li}: {t[-1] / 1e3:.1f} us, chunks {a[0]}")
+    wait = 0.0
+    work = 0.0
+    last_done = None
+    for i in range(len(c)):
+        if c[i] in (10, 11, 12, 13, 3, 30):
+            print(f"   {names[c[i]]:>8} at {t[i] / 1e3:8.1f} us")
+        if c[i] == 20:
+            prev = t[i - 1]
+            wait += t[i] - prev
+        if c[i] == 21:
+            work += t[i] - t[i - 1]
+    print(f"   chunk wait total {wait / 1e3:.1f} us, chunk work total {work / 1e3:.1f} us")
+    ready = [(a[i], t[i]) for i in range(len(c)) if c[i] == 20]
+    done = [(a[i], t[i]) for i in range(len(c)) if c[i] == 21]
+    if ready:
+        w = [done[i][1] - ready[i][1] for i in range(min(len(ready), len(done)))]
+        print(f"   per-chunk work us: mean {np.mean(w) / 1e3:.2f} max {np.max(w) / 1e3:.2f}; "
+              f"first 10: {[round(x / 1e3, 2) for x in w[:10]]}")
+# fine-grained clock64 events 50..53 (thread 0): header -> rhs -> fold done -> stores done
+sel = np.isin(codes, [50, 51, 52, 53])
+if sel.any():
+    c5, a5 = codes[sel], args[sel]
+    d = {}
+    for i in range(len(c5) - 1):
+        if c5[i + 1] == c5[i] + 1:
+            d.setdefault(int(c5[i]), []).append((int(a5[i + 1]) - int(a5[i])) & 0x7fffffff)
+    for k in sorted(d):
+        v = np.array(d[k])
+        print(f"clock {k}->{k + 1}: n={v.size} median {np.median(v):.0f} mean {v.mean():.0f} p90 {np.percentile(v, 90):.0f} cycles")
