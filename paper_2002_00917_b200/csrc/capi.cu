@@ -333,7 +333,7 @@ int pslr_ctx_create(pslr_ctx** out, int device, const pslr_system* sys) {
   // for the 3D configs (tools/micro/tma_stream.cu).
   const int64_t SB = env_int("PSLR_STAGE_BYTES", 32 * 1024);
   const int64_t RB = ((8 * (kChunkRows + 2)) + 127) / 128 * 128;
-  int64_t wmax = env_int("PSLR_RING", 8192);
+  int64_t wmax = env_int("PSLR_RING", 4096);
   int64_t W = 2048;  // >= 2048: the ring doubles as the V^T y reduction scratch
   while (W < reach && W < wmax) W *= 2;
   const int64_t CTL = 256;  // mbarriers
@@ -612,7 +612,13 @@ int pslr_debug_trace(pslr_ctx* ctx, int64_t* out, int64_t cap, int64_t* count) {
   CK(cudaMemcpy(&n, ctx->K.trace, sizeof(long long), cudaMemcpyDeviceToHost));
   n = std::min<long long>(n, ctx->K.trace_cap);
   n = std::min<long long>(n, cap / 2);
-  if (n > 0) CK(cudaMemcpy(out, ctx->K.trace + 2, 2 * n * sizeof(long long), cudaMemcpyDeviceToHost));
+  if (cap >= 2 * ctx->K.trace_cap) {  // whole buffer (events + per-CTA cycle counters)
+    CK(cudaMemcpy(out, ctx->K.trace + 2, 2 * ctx->K.trace_cap * sizeof(long long),
+                  cudaMemcpyDeviceToHost));
+    CK(cudaMemset(ctx->K.trace + 2 + 2 * ctx->K.trace_cap - 8 * 4096, 0, 8 * 4096 * sizeof(long long)));
+  } else if (n > 0) {
+    CK(cudaMemcpy(out, ctx->K.trace + 2, 2 * n * sizeof(long long), cudaMemcpyDeviceToHost));
+  }
   CK(cudaMemset(ctx->K.trace, 0, 16));
   *count = n;
   return PSLR_OK;

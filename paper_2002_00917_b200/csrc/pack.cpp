@@ -120,10 +120,13 @@ int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAna
   out.nnz_offdiag = 0;
   out.segments = 0;
   std::vector<uint8_t> seg;
-  auto seg_bytes = [&](int64_t nrows, int64_t w, int64_t nnz) {
-    int64_t b = 32 + 4 * a4(w + 1) + 4 * a4(nrows);
-    if (upper) b += 16 * a2(nrows);
-    b += 8 * a2(nnz) + 4 * a4(nnz);
+  // ELL segment: w slabs of stride S = a4(nrows); rows shorter than w are padded with
+  // exact no-op entries (value 0, slot = the ring's zero slot W)
+  auto seg_bytes = [&](int64_t nrows, int64_t w, int64_t /*nnz*/) {
+    const int64_t S = a4(nrows);
+    int64_t b = 32 + 4 * S;
+    if (upper) b += 16 * S;
+    b += 12 * w * S;
     return b;
   };
   // current chunk being filled
@@ -181,44 +184,41 @@ int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAna
         h[0] = (int32_t)nrows;
         h[1] = (int32_t)w;
         h[2] = (s1 == lend) ? 1 : 0;  // ends a level
+        const int64_t S = a4(nrows);
         h[3] = (int32_t)s0;
-        h[4] = (int32_t)nnz;
+        h[4] = (int32_t)S;
         h[5] = (int32_t)bytes;
-        int32_t* soff = h + 8;  // slab offsets, w+1 entries
-        int32_t* info = soff + a4(w + 1);
-        std::vector<int64_t> cnt(w, 0);
-        uint8_t* p = reinterpret_cast<uint8_t*>(info + a4(nrows));
+        int32_t* info = h + 8;
+        uint8_t* p = reinterpret_cast<uint8_t*>(info + S);
         double* sd = nullptr;
         double* invd = nullptr;
         if (upper) {
           sd = reinterpret_cast<double*>(p);
-          invd = sd + a2(nrows);
-          p = reinterpret_cast<uint8_t*>(invd + a2(nrows));
+          invd = sd + S;
+          p = reinterpret_cast<uint8_t*>(invd + S);
         }
         double* val = reinterpret_cast<double*>(p);
-        int32_t* slot = reinterpret_cast<int32_t*>(val + a2(nnz));
-        // slab counts (rows sorted by length desc within the level)
+        int32_t* slot = reinterpret_cast<int32_t*>(val + w * S);
         for (int64_t t = 0; t < nrows; ++t) {
           const int64_t r = A.row_at_pos[s0 + t];
-          const int64_t len = A.len[r];
-          for (int64_t kk = 0; kk < len; ++kk) cnt[kk]++;
           info[t] = info_of_row[r];
           if (upper) {
             const double dinv = 1.0 / A.diag[r];
             sd[t] = A.diag[r] * dinv;  // scipy: (U @ diags(1/diag)) diagonal
             invd[t] = dinv;
           }
+          for (int64_t kk = A.len[r]; kk < w; ++kk) {  // padding: exact no-ops
+            val[kk * S + t] = 0.0;
+            slot[kk * S + t] = (int32_t)W;
+          }
         }
-        std::vector<int64_t> slab_off(w + 1, 0);
-        for (int64_t kk = 0; kk < w; ++kk) slab_off[kk + 1] = slab_off[kk] + cnt[kk];
-        for (int64_t kk = 0; kk <= w; ++kk) soff[kk] = (int32_t)slab_off[kk];
         for (int64_t t = 0; t < nrows; ++t) {
           const int64_t r = A.row_at_pos[s0 + t];
           int64_t kk = 0;
           for (int64_t e = M.indptr[r]; e < M.indptr[r + 1]; ++e) {
             const int64_t j = M.indices[e];
             if (j == r) continue;
-            const int64_t idx = slab_off[kk] + t;
+            const int64_t idx = kk * S + t;
             double v = M.data[e];
             if (upper) v = v * (1.0 / A.diag[j]);  // scipy pre-scales U's columns by 1/diag
             val[idx] = v;

@@ -154,13 +154,38 @@ struct Streams {
 };
 
 // Producer: lane 0 of the producer warp.
+// Descriptors of 32 consecutive chunks held one per lane of the producer warp, so the
+// producer pays one global-load latency per 32 chunks instead of one per chunk.
+struct DescCache {
+  int base = -(1 << 30);
+  ChunkDesc mine{};
+  __device__ __forceinline__ ChunkDesc get(const Streams& S, int u, int total) {
+    const int lane = threadIdx.x & 31;
+    if (u < base || u >= base + 32) {
+      base = u;
+      const int v = u + lane;
+      if (v < total) mine = S.desc(v);
+    }
+    const int src = u - base;
+    ChunkDesc d;
+    d.off = __shfl_sync(0xffffffffu, mine.off, src);
+    d.bytes = __shfl_sync(0xffffffffu, mine.bytes, src);
+    d.nseg = 0;
+    d.pos0 = __shfl_sync(0xffffffffu, mine.pos0, src);
+    d.npos = __shfl_sync(0xffffffffu, mine.npos, src);
+    return d;
+  }
+};
+
+// Producer: the whole producer warp runs the loop (warp-uniform decisions), lane 0
+// issues the TMA operations.
 __device__ void producer(const Streams& S, Ctl* ctl, uint8_t* stages, double* rhsbuf, int nst,
                          int stage_bytes, int rhs_stride) {
+  const bool lead = (threadIdx.x & 31) == 0;
   const int total = S.begin[S.nphase];
   int data_next = 0, rhs_next = 0;
   bool ready[4] = {false, false, false, false};
-  ChunkDesc dd = total > 0 ? S.desc(0) : ChunkDesc{};
-  ChunkDesc dr = dd;
+  DescCache cd, cr;
   // L2 prefetch cursor over the block's contiguous byte range of each phase
   int pf_phase = 0;
   int64_t pf_off = 0, pf_end = 0;
@@ -176,21 +201,25 @@ __device__ void producer(const Streams& S, Ctl* ctl, uint8_t* stages, double* rh
   };
   if (S.nphase > 0) phase_range(0, pf_off, pf_end);
   int64_t issued_bytes = 0, prefetched_bytes = 0;
+  int st_d = 0, use_d = 0;  // stage / use count of data_next
+  int st_r = 0;             // stage of rhs_next
   while (rhs_next < total) {
     bool did = false;
-    if (data_next < total) {
-      const int st = data_next % nst;
-      const int use = data_next / nst;
-      if (use == 0 || mbar_test(&ctl->empty[st], (uint32_t)((use - 1) & 1))) {
-        const int k = S.phase_of(data_next);
-        mbar_expect_tx(&ctl->full[st], (uint32_t)dd.bytes);
-        bulk_load(stages + (size_t)st * stage_bytes, S.data[k] + dd.off, (uint32_t)dd.bytes,
-                  &ctl->full[st]);
-        issued_bytes += dd.bytes;
-        ++data_next;
-        if (data_next < total) dd = S.desc(data_next);
-        did = true;
+    if (data_next < total && (use_d == 0 || mbar_test(&ctl->empty[st_d], (uint32_t)((use_d - 1) & 1)))) {
+      const ChunkDesc d = cd.get(S, data_next, total);
+      const int k = S.phase_of(data_next);
+      if (lead) {
+        mbar_expect_tx(&ctl->full[st_d], (uint32_t)d.bytes);
+        bulk_load(stages + (size_t)st_d * stage_bytes, S.data[k] + d.off, (uint32_t)d.bytes,
+                  &ctl->full[st_d]);
       }
+      issued_bytes += d.bytes;
+      ++data_next;
+      if (++st_d == nst) {
+        st_d = 0;
+        ++use_d;
+      }
+      did = true;
     }
     if (rhs_next < data_next) {
       const int k = S.phase_of(rhs_next);
@@ -199,13 +228,16 @@ __device__ void producer(const Streams& S, Ctl* ctl, uint8_t* stages, double* rh
         fence_proxy_async();
       }
       if (ready[k]) {
-        const int st = rhs_next % nst;
-        const int p0 = dr.pos0 & ~1;
-        const int cnt = (dr.pos0 + dr.npos - p0 + 1) & ~1;
-        mbar_expect_tx(&ctl->full[st], (uint32_t)(cnt * 8));
-        bulk_load(rhsbuf + (size_t)st * rhs_stride, S.rhs[k] + p0, (uint32_t)(cnt * 8), &ctl->full[st]);
+        const ChunkDesc d = cr.get(S, rhs_next, total);
+        const int p0 = d.pos0 & ~1;
+        const int cnt = (d.pos0 + d.npos - p0 + 1) & ~1;
+        if (lead) {
+          mbar_expect_tx(&ctl->full[st_r], (uint32_t)(cnt * 8));
+          bulk_load(rhsbuf + (size_t)st_r * rhs_stride, S.rhs[k] + p0, (uint32_t)(cnt * 8),
+                    &ctl->full[st_r]);
+        }
         ++rhs_next;
-        if (rhs_next < total) dr = S.desc(rhs_next);
+        if (++st_r == nst) st_r = 0;
         did = true;
       }
     }
@@ -216,13 +248,14 @@ __device__ void producer(const Streams& S, Ctl* ctl, uint8_t* stages, double* rh
         continue;
       }
       const int64_t len = (pf_end - pf_off) < 32768 ? (pf_end - pf_off) : 32768;
-      bulk_prefetch_l2(S.data[pf_phase] + pf_off, (uint32_t)len);
+      if (lead) bulk_prefetch_l2(S.data[pf_phase] + pf_off, (uint32_t)len);
       pf_off += len;
       prefetched_bytes += len;
     }
     if (!did) __nanosleep(32);
   }
 }
+
 
 // Process the segments of one staged chunk.  A segment holds at most kStepThreads rows;
 // consumer thread t owns row t.  Slab k holds entry k of rows [0, cnt_k); rows are sorted
@@ -237,67 +270,48 @@ __device__ __forceinline__ void run_chunk(const StepConst& K, const uint8_t* buf
   const int t = threadIdx.x;
   for (int s = 0; s < nseg; ++s) {
     const int32_t* h = reinterpret_cast<const int32_t*>(buf);
-    const int nrows = h[0], w = h[1], flags = h[2], pos0 = h[3], nnz = h[4], bytes = h[5];
+    const int nrows = h[0], w = h[1], flags = h[2], pos0 = h[3], S = h[4], bytes = h[5];
     if (t < nrows) {
-      const int32_t* soff = h + 8;  // w+1 slab offsets
-      const int32_t* info = soff + A4(w + 1);
-      const uint8_t* p = reinterpret_cast<const uint8_t*>(info + A4(nrows));
+      // ELL segment (pack.cpp): info[S], [U: sd[S], invd[S]], val[w][S], slot[w][S]
+      const int32_t* info = h + 8;
+      const uint8_t* p = reinterpret_cast<const uint8_t*>(info + S);
       const double* sd = nullptr;
       const double* invd = nullptr;
       if (UPPER) {
         sd = reinterpret_cast<const double*>(p);
-        invd = sd + A2(nrows);
-        p = reinterpret_cast<const uint8_t*>(invd + A2(nrows));
+        invd = sd + S;
+        p = reinterpret_cast<const uint8_t*>(invd + S);
       }
-      const double* val = reinterpret_cast<const double*>(p);
-      const int32_t* slot = reinterpret_cast<const int32_t*>(val + A2(nnz));
+      const double* val = reinterpret_cast<const double*>(p) + t;
+      const int32_t* slot = reinterpret_cast<const int32_t*>(reinterpret_cast<const double*>(p) + w * S) + t;
       const int gp = pos0 + t;
       double acc = rbuf[gp - rbase];
       if (UPPER) {
         const double sdv = sd[t];
         if (sdv != 1.0) acc = acc / sdv;  // x / 1.0 == x exactly: skip the division
       }
-      // Entries in batches of kBatch: the slab offsets are uniform loads, every slot and
-      // value load of the batch is issued before the ring gathers, and the products are
-      // folded in the reference's ascending-column order.  Segments without far
-      // dependencies (flag bit 1 clear, the common case) gather from the ring only.
-      // Lanes whose row is shorter than the warp's longest row fold exact no-ops
-      // (v = 0, z = ring[zero slot] = 0: acc - 0*0 == acc bit for bit), so the fold has
-      // no per-lane predicates; the batch length wl is warp-uniform.
-      const bool far = (flags & 2) != 0;
-      const int wbase = t & ~31;
-      const int zslot = mask + 1;
-      for (int k0 = 0; k0 < w; k0 += kBatch) {
-        int so[kBatch + 1];
-#pragma unroll
-        for (int j = 0; j <= kBatch; ++j) so[j] = soff[min(k0 + j, w)];
-        int wl = 0;
-#pragma unroll
-        for (int j = 0; j < kBatch; ++j) wl += (so[j + 1] - so[j] > wbase) ? 1 : 0;
-        int sl[kBatch];
-        double v[kBatch];
-#pragma unroll
-        for (int j = 0; j < kBatch; ++j) {
-          if (j < wl) {
-            const bool on = t < so[j + 1] - so[j];
-            sl[j] = on ? slot[so[j] + t] : zslot;
-            v[j] = on ? val[so[j] + t] : 0.0;
-          }
+      // Padding entries are exact no-ops (0 * ring[zero slot] = 0), so every lane runs the
+      // segment-uniform w steps in the reference's ascending-column order.
+      if (!(flags & 2)) {
+        int k = 0;
+        for (; k + 4 <= w; k += 4) {
+          const int s0 = slot[(k + 0) * S], s1 = slot[(k + 1) * S];
+          const int s2 = slot[(k + 2) * S], s3 = slot[(k + 3) * S];
+          const double v0 = val[(k + 0) * S], v1 = val[(k + 1) * S];
+          const double v2 = val[(k + 2) * S], v3 = val[(k + 3) * S];
+          const double z0 = ring[s0], z1 = ring[s1], z2 = ring[s2], z3 = ring[s3];
+          acc = acc - v0 * z0;
+          acc = acc - v1 * z1;
+          acc = acc - v2 * z2;
+          acc = acc - v3 * z3;
         }
-        double zz[kBatch];
-        if (!far) {
-#pragma unroll
-          for (int j = 0; j < kBatch; ++j)
-            if (j < wl) zz[j] = ring[sl[j]];
-        } else {
-#pragma unroll
-          for (int j = 0; j < kBatch; ++j)
-            if (j < wl) zz[j] = (sl[j] >= 0) ? ring[sl[j]] : z[sl[j] & 0x7fffffff];
+        for (; k < w; ++k) acc = acc - val[k * S] * ring[slot[k * S]];
+      } else {
+        for (int k = 0; k < w; ++k) {
+          const int sl = slot[k * S];
+          const double zz = (sl >= 0) ? ring[sl] : z[sl & 0x7fffffff];
+          acc = acc - val[k * S] * zz;
         }
-#pragma unroll
-        for (int j = 0; j < kBatch; ++j)
-          if (j < wl) acc = acc - v[j] * zz[j];
-        if (wl < kBatch) break;
       }
       ring[(gp - base) & mask] = acc;
       if (UPPER) {
@@ -441,9 +455,8 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
     fence_mbar_init();
   }
   __syncthreads();
-  if (threadIdx.x >= kStepThreads) {  // producer warp
-    if (threadIdx.x == kStepThreads)
-      producer(S, ctl, stages, rhsbuf, K.nst, K.stage_bytes, K.rhs_stride);
+  if (threadIdx.x >= kStepThreads) {  // producer warp (all 32 lanes)
+    producer(S, ctl, stages, rhsbuf, K.nst, K.stage_bytes, K.rhs_stride);
     return;
   }
   trace_begin(K);

@@ -20,7 +20,7 @@ print(P.device.info(), flush=True)
 b = torch.from_numpy(np.random.default_rng(0).standard_normal(P.system.n)).cuda()
 P.apply(b)
 torch.cuda.synchronize()
-buf = np.zeros(2 * (1 << 20), dtype=np.int64)
+buf = np.zeros(2 * (1 << 20), dtype=np.int64)  # == 2*trace_cap: whole buffer
 cnt = ctypes.c_int64()
 _lib.fns["pslr_debug_trace"](P.device.handle, buf.ctypes.data, buf.size, ctypes.byref(cnt))  # reset
 P.apply(b)
@@ -87,3 +87,32 @@ if sel.any():
     for k in sorted(d):
         v = np.array(d[k])
         print(f"clock {k}->{k + 1}: n={v.size} median {np.median(v):.0f} mean {v.mean():.0f} p90 {np.percentile(v, 90):.0f} cycles")
+# per-CTA cycle counters of the level loop (thread 0): header->rhs, fold, stores, barrier wait
+cyc = buf[2 * (1 << 20) - 8 * 4096:].reshape(4096, 8)[:P.system.num_parts]
+segs = cyc[:, 4].astype(float)
+if segs.sum() > 0:
+    for i, nm in enumerate(["hdr->rhs", "fold", "stores", "barrier"]):
+        per = cyc[:, i] / np.maximum(segs, 1)
+        print(f"cycles/level-segment {nm:>9}: mean over CTAs {per.mean():8.1f}  min {per.min():8.1f} max {per.max():8.1f}")
+    print("level-ending segments per CTA (both applies):", int(segs.mean()))
+# distribution of per-chunk waits (launch with most chunks)
+best = None
+for li, s0 in enumerate(starts):
+    s1 = starts[li + 1] if li + 1 < len(starts) else n
+    cnt_c = int(np.sum(codes[s0:s1] == 20))
+    if best is None or cnt_c > best[2]:
+        best = (s0, s1, cnt_c)
+if best:
+    s0, s1, _ = best
+    c, a, t = codes[s0:s1], args[s0:s1], ts[s0:s1]
+    waits = []
+    prev = None
+    for i in range(len(c)):
+        if c[i] in (21, 10, 11, 12, 13):
+            prev = t[i]
+        if c[i] == 20 and prev is not None:
+            waits.append((t[i] - prev, int(a[i])))
+    w = np.array([x[0] for x in waits]) / 1e3
+    print(f"chunk waits: n={w.size} median {np.median(w):.2f} p90 {np.percentile(w, 90):.2f} max {w.max():.2f} us; "
+          f"sum {w.sum():.1f}; waits > 1us: {(w > 1).sum()} totalling {w[w > 1].sum():.1f} us")
+    print("   largest:", sorted(waits, reverse=True)[:8])
