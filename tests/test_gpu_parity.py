@@ -179,7 +179,7 @@ def test_gmres_cfg1_fails_at_maxit_like_reference():
     # E_rr(3) has spectral radius ~778 on cfg1: rounding differences in the
     # BLAS-ordered correction and CGS2 reductions grow along the cycle.  Bit-identical for
     # the first ~7 estimates, ~5e-3 relative by the end of the first cycle (measured).
-    assert np.max(np.abs(h[:8] - hr[:8]) / hr[:8]) <= 1e-9
+    assert np.max(np.abs(h[:7] - hr[:7]) / hr[:7]) <= 1e-10
     assert np.max(np.abs(h - hr) / hr) <= 2e-2
 
 
