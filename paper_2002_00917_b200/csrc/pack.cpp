@@ -134,12 +134,11 @@ int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAna
   auto close_chunk = [&]() {
     if (chunk_nseg == 0) return;
     ChunkDesc d;
-    d.off = chunk_start;
-    d.bytes = (int32_t)((int64_t)out.data.size() - chunk_start);
-    d.nseg = (int32_t)chunk_nseg;
-    d.pos0 = (int32_t)chunk_pos0;
-    d.npos = (int32_t)chunk_rows;
-    d.pad[0] = d.pad[1] = 0;
+    d.off16 = (uint32_t)(chunk_start / 16);
+    d.bytes = (uint32_t)((int64_t)out.data.size() - chunk_start);
+    const int64_t p0 = chunk_pos0 & ~int64_t(1);
+    d.rpos = (int32_t)p0;
+    d.rbytes = (uint32_t)(((chunk_pos0 + chunk_rows - p0 + 1) & ~int64_t(1)) * 8);
     chunk_rows = 0;
     // the kernel reads the segment count from the first segment's header (word 6)
     reinterpret_cast<int32_t*>(out.data.data() + chunk_start)[6] = (int32_t)chunk_nseg;
@@ -160,9 +159,12 @@ int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAna
       const int64_t lend = A.level_end[row0];
       int64_t s0 = k;
       while (s0 < lend) {
+        // Segments of one level run side by side: the segment's rows go to consumer
+        // threads [tb, tb + nrows), tb = rows of the level emitted before, mod seg_rows.
+        const int64_t tb = (s0 - k) % seg_rows;
         // grow a segment while it fits a stage
         int64_t s1 = s0, nnz = 0, w = 0;
-        while (s1 < lend && s1 - s0 < seg_rows) {
+        while (s1 < lend && s1 - s0 < seg_rows - tb) {
           const int64_t len = A.len[A.row_at_pos[s1]];
           const int64_t w2 = std::max(w, len);
           if (seg_bytes(s1 - s0 + 1, w2, nnz + len) > stage_bytes) break;
@@ -183,7 +185,7 @@ int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAna
         int32_t* h = reinterpret_cast<int32_t*>(seg.data());
         h[0] = (int32_t)nrows;
         h[1] = (int32_t)w;
-        h[2] = (s1 == lend) ? 1 : 0;  // ends a level
+        h[2] = ((s1 == lend) ? 1 : 0) | (int32_t)(tb << 8);  // bit0: ends a level; tb
         const int64_t S = a4(nrows);
         h[3] = (int32_t)s0;
         h[4] = (int32_t)S;
@@ -244,6 +246,8 @@ int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAna
     close_chunk();
   }
   out.blk_chunk[nb] = (int32_t)out.chunks.size();
+  if ((uint64_t)out.data.size() / 16 > 0xffffffffull)
+    return fail(PSLR_EINVAL, std::string(name) + ": packed factor exceeds 64 GiB");
   return PSLR_OK;
 }
 

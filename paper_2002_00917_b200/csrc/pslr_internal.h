@@ -26,26 +26,26 @@ struct DevCsr {
   const double* val = nullptr;
 };
 
-// One TMA-streamed chunk of a packed triangular factor (pack.cpp).
-struct ChunkDesc {
-  int64_t off;    // byte offset in the factor's data
-  int32_t bytes;  // multiple of 16
-  int32_t nseg;   // segments in the chunk
-  int32_t pos0;   // first global position of the chunk's rows
-  int32_t npos;   // rows in the chunk (consecutive positions)
-  int32_t pad[2];
+// One TMA-streamed chunk of a packed triangular factor (pack.cpp): the two bulk copies
+// the producer issues for it, precomputed so the producer loop does no arithmetic.
+struct alignas(16) ChunkDesc {
+  uint32_t off16;   // byte offset in the factor's data / 16
+  uint32_t bytes;   // packed bytes (multiple of 16)
+  int32_t rpos;     // first position of the chunk's rhs slice (even: 16-B aligned)
+  uint32_t rbytes;  // rhs slice bytes (multiple of 16)
 };
 
 // max rows per chunk: bounds the per-stage right-hand-side buffer
 constexpr int kChunkRows = 1024;
 
 // Segment layout inside a chunk (all parts 16-byte aligned):
-//   int32 hdr[8]   = {nrows, w, flags(bit0: ends a level), pos0, nnz, bytes, 0, 0}
-//   int32 cnt[w]   (slab sizes, non-increasing), padded to 4
-//   int32 info[nrows]  L: U-position of the row ; U: row id           , padded to 4
-//   U only: double sd[nrows], invd[nrows]                             , padded to 2
-//   double val[nnz]  (slab-major; U values pre-scaled by 1/diag of their column)
-//   int32 slot[nnz]  near: ring slot (< W) ; far: 0x80000000 | U-position of the dependency
+//   int32 hdr[8]   = {nrows, w, flags, pos0, S, bytes, nseg (first seg), rbase (first seg)}
+//                    flags: bit0 ends a level, bit1 has far deps, bits 8.. first consumer thread
+//   S = nrows rounded up to 4; ELL with w slabs (rows shorter than w padded with no-ops)
+//   int32 info[S]   L: U-position of the row ; U: row id
+//   U only: double sd[S], invd[S]
+//   double val[w][S]  (slab-major; U values pre-scaled by 1/diag of their column)
+//   int32 slot[w][S]  near: ring slot (<= W, W = zero slot) ; far: 0x80000000 | U-position
 struct DevTri {
   int32_t nblocks = 0, nchunks = 0;
   const uint8_t* data = nullptr;
@@ -122,6 +122,7 @@ struct StepConst {
   int smem_bytes = 0;
   long long* trace = nullptr;  // PSLR_TRACE: [count, pad, (code, ns)...] of CTA 0
   long long trace_cap = 0;
+  int dbg = 0;  // PSLR_DBG diagnostics knobs (timing experiments only; results are wrong when set)
 };
 
 }  // namespace pslr

@@ -107,6 +107,7 @@ __device__ __forceinline__ double spmv_row_rw(const DevCsr& M, int row, const do
 // Thread 0 of CTA 0 reserves a window with one atomic per launch, then stores plainly.
 __shared__ long long* g_trace_ptr;
 __shared__ int g_trace_n;
+
 constexpr int kTraceWindow = 1 << 15;
 
 __device__ __forceinline__ void trace_begin(const StepConst& K) {
@@ -132,6 +133,7 @@ struct Ctl {
   uint64_t full[8];       // data + rhs landed (2 arrivals + tx bytes)
   uint64_t empty[8];      // all consumer warps done with the stage (kConsumerWarps arrivals)
   uint64_t rhs_ready[4];  // phase k's rhs array is final (1 arrival)
+  int2 rrec[8];           // per stage: rhs slice (first position, bytes) of the staged chunk
 };
 
 // The chunks of up to four factor streams of this CTA's block form one sequence.
@@ -141,200 +143,243 @@ struct Streams {
   const uint8_t* data[4];
   const ChunkDesc* chunks[4];  // this block's first chunk of the phase
   const double* rhs[4];        // position-ordered right-hand-side array of each phase
-
-  __device__ __forceinline__ int phase_of(int u) const {
-    int k = 0;
-    while (k + 1 < nphase && u >= begin[k + 1]) ++k;
-    return k;
-  }
-  __device__ __forceinline__ ChunkDesc desc(int u) const {
-    const int k = phase_of(u);
-    return chunks[k][u - begin[k]];
-  }
 };
 
-// Producer: lane 0 of the producer warp.
-// Descriptors of 32 consecutive chunks held one per lane of the producer warp, so the
-// producer pays one global-load latency per 32 chunks instead of one per chunk.
-struct DescCache {
-  int base = -(1 << 30);
-  ChunkDesc mine{};
-  __device__ __forceinline__ ChunkDesc get(const Streams& S, int u, int total) {
-    const int lane = threadIdx.x & 31;
-    if (u < base || u >= base + 32) {
-      base = u;
-      const int v = u + lane;
-      if (v < total) mine = S.desc(v);
-    }
-    const int src = u - base;
-    ChunkDesc d;
-    d.off = __shfl_sync(0xffffffffu, mine.off, src);
-    d.bytes = __shfl_sync(0xffffffffu, mine.bytes, src);
-    d.nseg = 0;
-    d.pos0 = __shfl_sync(0xffffffffu, mine.pos0, src);
-    d.npos = __shfl_sync(0xffffffffu, mine.npos, src);
-    return d;
-  }
-};
+__device__ __forceinline__ ChunkDesc load_desc(const ChunkDesc* p) {
+  const uint4 v = __ldg(reinterpret_cast<const uint4*>(p));
+  ChunkDesc d;
+  d.off16 = v.x;
+  d.bytes = v.y;
+  d.rpos = (int32_t)v.z;
+  d.rbytes = v.w;
+  return d;
+}
 
-// Producer: the whole producer warp runs the loop (warp-uniform decisions), lane 0
-// issues the TMA operations.
+// Producer: one thread (lane 0 of the producer warp).  The loop is latency-bound on a
+// single thread, so everything per chunk is precomputed (ChunkDesc) and the next
+// descriptor load is in flight while the producer waits for a free stage.
+//   data cursor: chunk d_u goes to stage d_u % nst once the consumers released it;
+//   rhs cursor:  chunk r_u < d_u gets its rhs slice once its phase's rhs is final;
+//   L2 cursor:   bulk prefetch kL2Ahead bytes beyond the issued data.
 __device__ void producer(const Streams& S, Ctl* ctl, uint8_t* stages, double* rhsbuf, int nst,
-                         int stage_bytes, int rhs_stride) {
-  const bool lead = (threadIdx.x & 31) == 0;
-  const int total = S.begin[S.nphase];
-  int data_next = 0, rhs_next = 0;
-  bool ready[4] = {false, false, false, false};
-  DescCache cd, cr;
-  // L2 prefetch cursor over the block's contiguous byte range of each phase
-  int pf_phase = 0;
-  int64_t pf_off = 0, pf_end = 0;
-  auto phase_range = [&](int k, int64_t& lo, int64_t& hi) {
+                         int stage_bytes, int rhs_stride, int dbg, long long* g_dbg_out) {
+  if ((threadIdx.x & 31) != 0) return;
+  const int np = S.nphase;
+  const int total = S.begin[np];
+  if (total == 0) return;
+  const int64_t l2ahead = (dbg & 64) ? 0 : kL2Ahead;
+  // data cursor
+  int d_u = 0, d_k = 0;
+  while (S.begin[d_k + 1] == 0) ++d_k;
+  int d_end = S.begin[d_k + 1], d_base = 0;
+  const uint8_t* d_data = S.data[d_k];
+  const ChunkDesc* d_ops = S.chunks[d_k];
+  ChunkDesc dop = load_desc(d_ops);
+  int st_d = 0, use_d = 0;
+  // rhs cursor
+  int r_u = 0, r_k = d_k, r_end = d_end, st_r = 0;
+  const double* r_rhs = S.rhs[r_k];
+  uint32_t ready = 0;
+  // L2 cursor over the byte ranges of the phases (chunks of a phase are contiguous)
+  int pf_k = d_k;
+  int64_t pf_off = 0, pf_hi = 0, issued = 0, prefetched = 0;
+  auto pf_range = [&](int k) {
     const int n = S.begin[k + 1] - S.begin[k];
-    if (n <= 0) {
-      lo = hi = 0;
+    if (n == 0) {
+      pf_off = pf_hi = 0;
       return;
     }
-    const ChunkDesc a = S.chunks[k][0], z = S.chunks[k][n - 1];
-    lo = a.off;
-    hi = z.off + z.bytes;
+    const ChunkDesc a = load_desc(S.chunks[k]), z = load_desc(S.chunks[k] + n - 1);
+    pf_off = (int64_t)a.off16 * 16;
+    pf_hi = (int64_t)z.off16 * 16 + z.bytes;
   };
-  if (S.nphase > 0) phase_range(0, pf_off, pf_end);
-  int64_t issued_bytes = 0, prefetched_bytes = 0;
-  int st_d = 0, use_d = 0;  // stage / use count of data_next
-  int st_r = 0;             // stage of rhs_next
-  while (rhs_next < total) {
+  pf_range(pf_k);
+  long long c_idle = 0, n_it = 0;
+  const long long c_all = clock64();
+  while (r_u < total) {
     bool did = false;
-    if (data_next < total && (use_d == 0 || mbar_test(&ctl->empty[st_d], (uint32_t)((use_d - 1) & 1)))) {
-      const ChunkDesc d = cd.get(S, data_next, total);
-      const int k = S.phase_of(data_next);
-      if (lead) {
-        mbar_expect_tx(&ctl->full[st_d], (uint32_t)d.bytes);
-        bulk_load(stages + (size_t)st_d * stage_bytes, S.data[k] + d.off, (uint32_t)d.bytes,
-                  &ctl->full[st_d]);
-      }
-      issued_bytes += d.bytes;
-      ++data_next;
+    ++n_it;
+    const long long c_it = clock64();
+    if (d_u < total && (use_d == 0 || mbar_test(&ctl->empty[st_d], (uint32_t)((use_d - 1) & 1)))) {
+      mbar_expect_tx(&ctl->full[st_d], dop.bytes);
+      bulk_load(stages + (size_t)st_d * stage_bytes, d_data + (size_t)dop.off16 * 16, dop.bytes,
+                &ctl->full[st_d]);
+      ctl->rrec[st_d] = make_int2(dop.rpos, (int)dop.rbytes);
+      issued += dop.bytes;
       if (++st_d == nst) {
         st_d = 0;
         ++use_d;
       }
+      if (++d_u < total) {
+        while (d_u >= d_end) {
+          ++d_k;
+          d_base = S.begin[d_k];
+          d_end = S.begin[d_k + 1];
+          d_data = S.data[d_k];
+          d_ops = S.chunks[d_k];
+        }
+        dop = load_desc(d_ops + (d_u - d_base));
+      }
       did = true;
     }
-    if (rhs_next < data_next) {
-      const int k = S.phase_of(rhs_next);
-      if (!ready[k] && mbar_test(&ctl->rhs_ready[k], 0)) {
-        ready[k] = true;
+    if (r_u < d_u) {
+      while (r_u >= r_end) {
+        ++r_k;
+        r_end = S.begin[r_k + 1];
+        r_rhs = S.rhs[r_k];
+      }
+      if (!(ready & (1u << r_k)) && mbar_test(&ctl->rhs_ready[r_k], 0)) {
+        ready |= 1u << r_k;
         fence_proxy_async();
       }
-      if (ready[k]) {
-        const ChunkDesc d = cr.get(S, rhs_next, total);
-        const int p0 = d.pos0 & ~1;
-        const int cnt = (d.pos0 + d.npos - p0 + 1) & ~1;
-        if (lead) {
-          mbar_expect_tx(&ctl->full[st_r], (uint32_t)(cnt * 8));
-          bulk_load(rhsbuf + (size_t)st_r * rhs_stride, S.rhs[k] + p0, (uint32_t)(cnt * 8),
-                    &ctl->full[st_r]);
+      if (ready & (1u << r_k)) {
+        const int2 rr = ctl->rrec[st_r];
+        if (dbg & 512) {
+          mbar_arrive(&ctl->full[st_r]);  // diagnostics: no rhs copy
+        } else {
+          mbar_expect_tx(&ctl->full[st_r], (uint32_t)rr.y);
+          bulk_load(rhsbuf + (size_t)st_r * rhs_stride, r_rhs + rr.x, (uint32_t)rr.y, &ctl->full[st_r]);
         }
-        ++rhs_next;
+        ++r_u;
         if (++st_r == nst) st_r = 0;
         did = true;
       }
     }
-    // keep ~kL2Ahead bytes of the stream prefetched into L2 beyond the issued chunks
-    while (pf_phase < S.nphase && prefetched_bytes < issued_bytes + kL2Ahead) {
-      if (pf_off >= pf_end) {
-        if (++pf_phase < S.nphase) phase_range(pf_phase, pf_off, pf_end);
+    while (prefetched < issued + l2ahead && pf_k < np) {
+      if (pf_off >= pf_hi) {
+        if (++pf_k < np) pf_range(pf_k);
         continue;
       }
-      const int64_t len = (pf_end - pf_off) < 32768 ? (pf_end - pf_off) : 32768;
-      if (lead) bulk_prefetch_l2(S.data[pf_phase] + pf_off, (uint32_t)len);
+      const int64_t len = (pf_hi - pf_off) < 32768 ? (pf_hi - pf_off) : 32768;
+      bulk_prefetch_l2(S.data[pf_k] + pf_off, (uint32_t)len);
       pf_off += len;
-      prefetched_bytes += len;
+      prefetched += len;
     }
-    if (!did) __nanosleep(32);
+    if (!did) {
+      if (dbg & 16) __nanosleep(200);
+      else if (dbg & 32) __nanosleep(1000);
+      else if (!(dbg & 128)) __nanosleep(20);
+      c_idle += clock64() - c_it;
+    }
+  }
+  if (g_dbg_out) {
+    atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg_out + 5), (unsigned long long)c_idle);
+    atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg_out + 7), (unsigned long long)(clock64() - c_all));
+    atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg_out + 4), (unsigned long long)n_it);
   }
 }
 
+// ---------------------------------------------------------------------------------------
+// Consumer side: the level loop.
+//
+// A level's critical path is latency: gather the dependencies from the ring, the
+// sequential DADD chain, store, barrier.  Everything that does not depend on the
+// previous level - the next segment's header, the row's slots, its right-hand side
+// (already divided by sd) and the U epilogue operands - is loaded for segment s+1 before
+// segment s is computed, so after each barrier a thread only issues its ring gathers
+// (with the value loads alongside) and runs the chain.
+//
+// Segment layout (pack.cpp): hdr {nrows, w, flags, pos0, S, bytes, nseg, rbase},
+// info[S], [U: sd[S], invd[S]], val[w][S], slot[w][S].  Consumer thread tb + t owns row t
+// (tb = flags >> 8), so the segments of one level run side by side.
+constexpr int kPre = 8;  // dependencies whose slots are prefetched (the rest: after the barrier)
 
-// Process the segments of one staged chunk.  A segment holds at most kStepThreads rows;
-// consumer thread t owns row t.  Slab k holds entry k of rows [0, cnt_k); rows are sorted
-// by length, so a warp stops at the first slab its leading row does not reach.
+struct Row {
+  int bytes, flags, w, S;
+  bool active;
+  int gp;              // global position of the row
+  int info;            // L: U-position (z index) ; U: row id (xout index)
+  double acc;          // rhs (U: already divided by sd)
+  double invd, cadd;   // U epilogue
+  const double* val;   // &val[0][t]
+  int sl[kPre];
+};
+
 template <bool UPPER>
-__device__ __forceinline__ void run_chunk(const StepConst& K, const uint8_t* buf,
-                                          const double* rbuf, double* ring, int mask, int base,
-                                          double* z, double* xout, const double* __restrict__ cadd) {
-  const int32_t* h0 = reinterpret_cast<const int32_t*>(buf);
-  const int nseg = h0[6];
-  const int rbase = h0[7];
-  const int t = threadIdx.x;
-  for (int s = 0; s < nseg; ++s) {
-    const int32_t* h = reinterpret_cast<const int32_t*>(buf);
-    const int nrows = h[0], w = h[1], flags = h[2], pos0 = h[3], S = h[4], bytes = h[5];
-    if (t < nrows) {
-      // ELL segment (pack.cpp): info[S], [U: sd[S], invd[S]], val[w][S], slot[w][S]
-      const int32_t* info = h + 8;
-      const uint8_t* p = reinterpret_cast<const uint8_t*>(info + S);
-      const double* sd = nullptr;
-      const double* invd = nullptr;
-      if (UPPER) {
-        sd = reinterpret_cast<const double*>(p);
-        invd = sd + S;
-        p = reinterpret_cast<const uint8_t*>(invd + S);
-      }
-      const double* val = reinterpret_cast<const double*>(p) + t;
-      const int32_t* slot = reinterpret_cast<const int32_t*>(reinterpret_cast<const double*>(p) + w * S) + t;
-      const int gp = pos0 + t;
-      double acc = rbuf[gp - rbase];
-      if (UPPER) {
-        const double sdv = sd[t];
-        if (sdv != 1.0) acc = acc / sdv;  // x / 1.0 == x exactly: skip the division
-      }
-      // Padding entries are exact no-ops (0 * ring[zero slot] = 0), so every lane runs the
-      // segment-uniform w steps in the reference's ascending-column order.
-      if (!(flags & 2)) {
-        int k = 0;
-        for (; k + 4 <= w; k += 4) {
-          const int s0 = slot[(k + 0) * S], s1 = slot[(k + 1) * S];
-          const int s2 = slot[(k + 2) * S], s3 = slot[(k + 3) * S];
-          const double v0 = val[(k + 0) * S], v1 = val[(k + 1) * S];
-          const double v2 = val[(k + 2) * S], v3 = val[(k + 3) * S];
-          const double z0 = ring[s0], z1 = ring[s1], z2 = ring[s2], z3 = ring[s3];
-          acc = acc - v0 * z0;
-          acc = acc - v1 * z1;
-          acc = acc - v2 * z2;
-          acc = acc - v3 * z3;
-        }
-        for (; k < w; ++k) acc = acc - val[k * S] * ring[slot[k * S]];
-      } else {
-        for (int k = 0; k < w; ++k) {
-          const int sl = slot[k * S];
-          const double zz = (sl >= 0) ? ring[sl] : z[sl & 0x7fffffff];
-          acc = acc - val[k * S] * zz;
-        }
-      }
-      ring[(gp - base) & mask] = acc;
-      if (UPPER) {
-        z[gp] = acc;
-        const int row = info[t];
-        double x = acc * invd[t];
-        if (cadd) x = x + __ldg(cadd + row);
-        xout[row] = x;
-      } else {
-        z[info[t]] = acc;
-      }
-    }
-    if (flags & 1) {
-      trace_ev(K, 40, nrows | (w << 16));
-      consumer_sync();
-      trace_ev(K, 41, 0);
-    }
-    buf += bytes;
+__device__ __forceinline__ void load_row(const uint8_t* seg, const double* rbuf, int rbase, int zslot,
+                                         const double* __restrict__ cadd, Row& r) {
+  const int4 h0 = *reinterpret_cast<const int4*>(seg);       // nrows, w, flags, pos0
+  const int2 h1 = *reinterpret_cast<const int2*>(seg + 16);  // S, bytes
+  r.w = h0.y;
+  r.flags = h0.z;
+  r.S = h1.x;
+  r.bytes = h1.y;
+  const int t = (int)threadIdx.x - (h0.z >> 8);
+  r.active = (unsigned)t < (unsigned)h0.x;
+  if (!r.active) return;
+  const int S = h1.x, w = h0.y;
+  const int32_t* info = reinterpret_cast<const int32_t*>(seg + 32);
+  const uint8_t* p = reinterpret_cast<const uint8_t*>(info + S);
+  r.gp = h0.w + t;
+  r.info = info[t];
+  double acc = rbuf[r.gp - rbase];
+  if (UPPER) {
+    const double* sd = reinterpret_cast<const double*>(p);
+    const double sdv = sd[t];
+    if (sdv != 1.0) acc = acc / sdv;  // x / 1.0 == x exactly: skip the division
+    r.invd = sd[S + t];
+    r.cadd = cadd ? __ldg(cadd + r.info) : 0.0;
+    p += 16 * (size_t)S;
   }
+  r.acc = acc;
+  r.val = reinterpret_cast<const double*>(p) + t;
+  const int32_t* slot = reinterpret_cast<const int32_t*>(p + 8 * (size_t)w * S) + t;
+#pragma unroll
+  for (int k = 0; k < kPre; ++k) r.sl[k] = (k < w) ? slot[k * S] : zslot;
+}
+
+// acc -= val_k * z_k for the row, in the reference's ascending-column order.  Entries
+// k >= w of the prefetched block read the zero slot with value 0: exact no-ops, so only
+// the chain length depends on w (segment-uniform branches).
+template <bool FAR>
+__device__ __forceinline__ double fold_row(const Row& r, const double* ring, const double* z, int zslot) {
+  const int S = r.S, w = r.w;
+  double acc = r.acc;
+  double zz[kPre], vv[kPre];
+#pragma unroll
+  for (int k = 0; k < kPre; ++k) {
+    const int sl = r.sl[k];
+    zz[k] = FAR ? ((sl >= 0) ? ring[sl] : z[sl & 0x7fffffff]) : ring[sl];
+    vv[k] = (k < w) ? r.val[k * S] : 0.0;
+  }
+  acc = acc - vv[0] * zz[0];
+  if (w > 1) {
+    acc = acc - vv[1] * zz[1];
+    if (w > 2) {
+      acc = acc - vv[2] * zz[2];
+      acc = acc - vv[3] * zz[3];
+      if (w > 4) {
+        acc = acc - vv[4] * zz[4];
+        acc = acc - vv[5] * zz[5];
+        acc = acc - vv[6] * zz[6];
+        acc = acc - vv[7] * zz[7];
+      }
+    }
+  }
+  if (w > kPre) {  // long rows: the rest straight from the staged segment
+    const int t = (int)threadIdx.x - (r.flags >> 8);
+    const int32_t* slot = reinterpret_cast<const int32_t*>(r.val - t + (size_t)w * S) + t;
+    for (int k = kPre; k < w; k += 4) {
+      int s4[4];
+      double v4[4], z4[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        s4[j] = (k + j < w) ? slot[(k + j) * S] : zslot;
+        v4[j] = (k + j < w) ? r.val[(k + j) * S] : 0.0;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j)
+        z4[j] = FAR ? ((s4[j] >= 0) ? ring[s4[j]] : z[s4[j] & 0x7fffffff]) : ring[s4[j]];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) acc = acc - v4[j] * z4[j];
+    }
+  }
+  return acc;
 }
 
 // Consumer side of one triangular phase.  Callers arrive right after a consumer barrier
-// that follows the last write of the phase's rhs array.
+// that follows the last write of the phase's rhs array; the phase ends with the barrier
+// of its last level.
 template <bool UPPER>
 __device__ void tri_phase(const StepConst& K, const Streams& S, Ctl* ctl, uint8_t* stages,
                           double* rhsbuf, int k, double* ring, int base, double* z, double* xout,
@@ -345,24 +390,66 @@ __device__ void tri_phase(const StepConst& K, const Streams& S, Ctl* ctl, uint8_
     fence_proxy_async();
     mbar_arrive(&ctl->rhs_ready[k]);
   }
-  const int nst = K.nst;
+  const int u0 = S.begin[k], u1 = S.begin[k + 1];
+  if (u0 == u1) return;
+  const int nst = K.nst, mask = K.ring_mask, zslot = K.ring_mask + 1;
   const int lane = threadIdx.x & 31;
-  int st = S.begin[k] % nst;
-  uint32_t par = (uint32_t)((S.begin[k] / nst) & 1);
-  for (int u = S.begin[k]; u < S.begin[k + 1]; ++u) {
-    mbar_wait(&ctl->full[st], par);
-    trace_ev(K, 20, u);
-    run_chunk<UPPER>(K, stages + (size_t)st * K.stage_bytes, rhsbuf + (size_t)st * K.rhs_stride, ring,
-                     K.ring_mask, base, z, xout, cadd);
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&ctl->empty[st]);
-    trace_ev(K, 21, u);
-    if (++st == nst) {
-      st = 0;
-      par ^= 1u;
+  int u = u0, st = u0 % nst;
+  uint32_t par = (uint32_t)((u0 / nst) & 1);
+  mbar_wait(&ctl->full[st], par);
+  const uint8_t* seg = stages + (size_t)st * K.stage_bytes;
+  const double* rbuf = rhsbuf + (size_t)st * K.rhs_stride;
+  int nseg = reinterpret_cast<const int32_t*>(seg)[6];
+  int rbase = reinterpret_cast<const int32_t*>(seg)[7];
+  int si = 0;
+  Row cur;
+  load_row<UPPER>(seg, rbuf, rbase, zslot, cadd, cur);
+  while (true) {
+    // locate + prefetch the next segment (next chunk: wait for it, it is normally staged)
+    const uint8_t* nseg_ptr = seg + cur.bytes;
+    const int cur_st = st;
+    bool chunk_done = false, more = true;
+    if (++si == nseg) {
+      chunk_done = true;
+      if (++u == u1) {
+        more = false;
+      } else {
+        if (++st == nst) {
+          st = 0;
+          par ^= 1u;
+        }
+        mbar_wait(&ctl->full[st], par);
+        nseg_ptr = stages + (size_t)st * K.stage_bytes;
+        rbuf = rhsbuf + (size_t)st * K.rhs_stride;
+        nseg = reinterpret_cast<const int32_t*>(nseg_ptr)[6];
+        rbase = reinterpret_cast<const int32_t*>(nseg_ptr)[7];
+        si = 0;
+      }
     }
+    Row nxt;
+    if (more) load_row<UPPER>(nseg_ptr, rbuf, rbase, zslot, cadd, nxt);
+    if (cur.active) {
+      const double acc = (cur.flags & 2) ? fold_row<true>(cur, ring, z, zslot)
+                                         : fold_row<false>(cur, ring, z, zslot);
+      ring[(cur.gp - base) & mask] = acc;
+      if (UPPER) {
+        z[cur.gp] = acc;
+        double x = acc * cur.invd;
+        if (cadd) x = x + cur.cadd;
+        xout[cur.info] = x;
+      } else {
+        z[cur.info] = acc;
+      }
+    }
+    if (chunk_done) {  // the staged chunk is no longer read by this warp
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&ctl->empty[cur_st]);
+    }
+    if (cur.flags & 1) consumer_sync();
+    if (!more) break;
+    cur = nxt;
+    seg = nseg_ptr;
   }
-  consumer_sync();
 }
 
 // Four SpMV rows at once (independent gathers in flight): s[j] = sum_e M_ij x_j in CSR
@@ -427,24 +514,29 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
   double* rhsbuf = reinterpret_cast<double*>(stages + (size_t)K.nst * K.stage_bytes);
   double* ring = rhsbuf + (size_t)K.nst * K.rhs_stride;
 
-  Streams S;
-  S.nphase = 0;
-  S.begin[0] = 0;
-  auto add_phase = [&](const DevTri& T, const double* rhs) {
-    const int c0 = T.blk_chunk[b], c1 = T.blk_chunk[b + 1];
-    S.data[S.nphase] = T.data;
-    S.chunks[S.nphase] = T.chunks + c0;
-    S.rhs[S.nphase] = rhs;
-    S.begin[S.nphase + 1] = S.begin[S.nphase] + (c1 - c0);
-    S.nphase++;
-  };
-  if (do_b) {
-    add_phase(K.LB, K.rhsB);
-    add_phase(K.UB, K.zB);
-  }
-  if (do_c) {
-    add_phase(K.LC, K.rhsC);
-    add_phase(K.UC, K.zC);
+  // The stream table lives in shared memory: dynamically indexed per-thread arrays would
+  // spill to local memory, which misses the small L1 left beside 229 KB of shared memory.
+  __shared__ Streams s_streams;
+  Streams& S = s_streams;
+  if (threadIdx.x == 0) {
+    S.nphase = 0;
+    S.begin[0] = 0;
+    auto add_phase = [&](const DevTri& T, const double* rhs) {
+      const int c0 = T.blk_chunk[b], c1 = T.blk_chunk[b + 1];
+      S.data[S.nphase] = T.data;
+      S.chunks[S.nphase] = T.chunks + c0;
+      S.rhs[S.nphase] = rhs;
+      S.begin[S.nphase + 1] = S.begin[S.nphase] + (c1 - c0);
+      S.nphase++;
+    };
+    if (do_b) {
+      add_phase(K.LB, K.rhsB);
+      add_phase(K.UB, K.zB);
+    }
+    if (do_c) {
+      add_phase(K.LC, K.rhsC);
+      add_phase(K.UC, K.zC);
+    }
   }
   if (threadIdx.x == 0) {
     for (int s = 0; s < K.nst; ++s) {
@@ -456,7 +548,9 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
   }
   __syncthreads();
   if (threadIdx.x >= kStepThreads) {  // producer warp (all 32 lanes)
-    producer(S, ctl, stages, rhsbuf, K.nst, K.stage_bytes, K.rhs_stride);
+    producer(S, ctl, stages, rhsbuf, K.nst, K.stage_bytes, K.rhs_stride, K.dbg,
+             (K.trace && K.trace_cap >= (1 << 20)) ? K.trace + 2 + 2 * K.trace_cap - 8 * 4096 + b * 8
+                                                   : nullptr);
     return;
   }
   trace_begin(K);

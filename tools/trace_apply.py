@@ -116,3 +116,28 @@ if best:
     print(f"chunk waits: n={w.size} median {np.median(w):.2f} p90 {np.percentile(w, 90):.2f} max {w.max():.2f} us; "
           f"sum {w.sum():.1f}; waits > 1us: {(w > 1).sum()} totalling {w[w > 1].sum():.1f} us")
     print("   largest:", sorted(waits, reverse=True)[:8])
+# producer counters (the producer thread): idle cycles, total cycles, iterations
+if segs.sum() > 0 or cyc[:, 7].sum() > 0:
+    tot = cyc[:, 7].astype(float)
+    print(f"producer: total cycles/CTA {tot.mean():.0f}, idle {cyc[:, 5].mean() / max(tot.mean(), 1):.2%}, "
+          f"iterations/CTA {cyc[:, 4].mean():.0f}")
+
+# PSLR_PROBE build: thread-0 cycle totals of the level loop's parts (rows 2048+b)
+pr = buf[2 * (1 << 20) - 8 * 4096:].reshape(4096, 8)[2048:2048 + P.system.num_parts].astype(float)
+if pr.sum() > 0:
+    names_p = ["loop+hdr", "rhs(+div)", "fold", "stores", "->barrier", "barrier", "chunk tail", "chunk wait"]
+    tot = pr.sum(axis=1).mean()
+    print(f"probe (thread 0, both applies, mean over CTAs): total {tot:.0f} cycles")
+    for i, nm in enumerate(names_p):
+        print(f"   {nm:>10}: {pr[:, i].mean():12.0f} cycles ({pr[:, i].mean() / tot:6.1%})")
+lat = buf[2 * (1 << 20) - 8 * 4096:].reshape(4096, 8)[3072:3072 + P.system.num_parts].astype(float)
+if lat[:, 2].sum() > 0:
+    n_ = lat[:, 2].sum()
+    print(f"latency probes: dependent LDS {lat[:, 0].sum() / n_ / 16:.1f} cycles, dependent DADD {lat[:, 1].sum() / n_ / 16:.1f} cycles (n={n_:.0f})")
+if lat[:, 3].sum() > 0:
+    m = lat.mean(axis=0)
+    print(f"thread 0 per CTA: rows {m[3]:.0f}, entries {m[4]:.0f} (w/row {m[4] / max(m[3], 1):.1f}), levels {m[5]:.0f}, segments {m[6]:.0f}")
+    if pr.sum() > 0:
+        pm = pr.mean(axis=0)
+        print(f"   fold cycles/row {pm[2] / m[3]:.0f}, per entry {pm[2] / max(m[4], 1):.1f}; rhs cycles/row {pm[1] / m[3]:.0f}; "
+              f"stores/row {pm[3] / m[3]:.0f}; hdr/segment {pm[0] / m[6]:.0f}; barrier/level {pm[5] / m[5]:.0f}")
