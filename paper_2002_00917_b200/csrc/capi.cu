@@ -337,10 +337,10 @@ int pslr_ctx_create(pslr_ctx** out, int device, const pslr_system* sys) {
   int64_t W = 2048;  // >= 2048: the ring doubles as the V^T y reduction scratch
   while (W < reach && W < wmax) W *= 2;
   const int64_t CTL = 256;  // mbarriers
-  int64_t nst = (smem_optin - 1024 - CTL - W * 8) / (SB + RB);
+  int64_t nst = (smem_optin - 1024 - CTL - W * 8 - 128) / (SB + RB);
   while (nst < 2 && W > 2048) {
     W /= 2;
-    nst = (smem_optin - 1024 - CTL - W * 8) / (SB + RB);
+    nst = (smem_optin - 1024 - CTL - W * 8 - 128) / (SB + RB);
   }
   nst = std::min<int64_t>(nst, std::min<int64_t>(8, env_int("PSLR_MAX_STAGES", 8)));
   if (nst < 2) return bail(fail(PSLR_EINVAL, "not enough shared memory for the streamed solve"));
@@ -348,7 +348,7 @@ int pslr_ctx_create(pslr_ctx** out, int device, const pslr_system* sys) {
   ctx->K.nst = (int)nst;
   ctx->K.stage_bytes = (int)SB;
   ctx->K.rhs_stride = (int)(RB / 8);
-  ctx->K.smem_bytes = (int)(CTL + nst * (SB + RB) + W * 8 + 16);  // ring + zero slot
+  ctx->K.smem_bytes = (int)(CTL + W * 8 + 128 + nst * (SB + RB));  // ring + zero slot (padded)
   if (configure_step_kernel(ctx->K.smem_bytes) != 0)
     return bail(fail(PSLR_ECUDA, "cannot configure the step kernel's shared memory"));
   ctx->K.dbg = (int)env_int("PSLR_DBG", 0);

@@ -120,13 +120,16 @@ int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAna
   out.nnz_offdiag = 0;
   out.segments = 0;
   std::vector<uint8_t> seg;
-  // ELL segment: w slabs of stride S = a4(nrows); rows shorter than w are padded with
-  // exact no-op entries (value 0, slot = the ring's zero slot W)
+  // ELL segment, S = a4(nrows) row slots, G = ceil(w/4) groups of 4 entries per row:
+  // slots int32[G][S][4] (one 16-B load per row and group), values double[G][2][S][2]
+  // (two conflict-free 16-B loads).  Entries past a row's length are exact no-ops
+  // (value 0, slot = the ring's zero slot W).
+  // U rows also carry sd (scipy's scaled diagonal), rcp = RN(1/sd) and invd = 1/diag.
   auto seg_bytes = [&](int64_t nrows, int64_t w, int64_t /*nnz*/) {
-    const int64_t S = a4(nrows);
+    const int64_t S = a4(nrows), G = std::max<int64_t>(1, (w + 3) / 4);
     int64_t b = 32 + 4 * S;
-    if (upper) b += 16 * S;
-    b += 12 * w * S;
+    if (upper) b += 24 * S;
+    b += 48 * G * S;
     return b;
   };
   // current chunk being filled
@@ -193,25 +196,34 @@ int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAna
         int32_t* info = h + 8;
         uint8_t* p = reinterpret_cast<uint8_t*>(info + S);
         double* sd = nullptr;
+        double* rcp = nullptr;
         double* invd = nullptr;
         if (upper) {
           sd = reinterpret_cast<double*>(p);
-          invd = sd + S;
+          rcp = sd + S;
+          invd = rcp + S;
           p = reinterpret_cast<uint8_t*>(invd + S);
         }
-        double* val = reinterpret_cast<double*>(p);
-        int32_t* slot = reinterpret_cast<int32_t*>(val + w * S);
+        const int64_t G = std::max<int64_t>(1, (w + 3) / 4);
+        int32_t* slot = reinterpret_cast<int32_t*>(p);
+        double* val = reinterpret_cast<double*>(p + 16 * G * S);
+        auto slot_at = [&](int64_t t, int64_t kk) -> int32_t& { return slot[((kk >> 2) * S + t) * 4 + (kk & 3)]; };
+        auto val_at = [&](int64_t t, int64_t kk) -> double& {
+          return val[(((kk >> 2) * 2 + ((kk >> 1) & 1)) * S + t) * 2 + (kk & 1)];
+        };
+        for (int64_t t = 0; t < S; ++t)
+          for (int64_t kk = 0; kk < 4 * G; ++kk) {  // padding (incl. rows nrows..S-1): exact no-ops
+            val_at(t, kk) = 0.0;
+            slot_at(t, kk) = (int32_t)W;
+          }
         for (int64_t t = 0; t < nrows; ++t) {
           const int64_t r = A.row_at_pos[s0 + t];
           info[t] = info_of_row[r];
           if (upper) {
             const double dinv = 1.0 / A.diag[r];
             sd[t] = A.diag[r] * dinv;  // scipy: (U @ diags(1/diag)) diagonal
+            rcp[t] = 1.0 / sd[t];
             invd[t] = dinv;
-          }
-          for (int64_t kk = A.len[r]; kk < w; ++kk) {  // padding: exact no-ops
-            val[kk * S + t] = 0.0;
-            slot[kk * S + t] = (int32_t)W;
           }
         }
         for (int64_t t = 0; t < nrows; ++t) {
@@ -220,15 +232,14 @@ int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAna
           for (int64_t e = M.indptr[r]; e < M.indptr[r + 1]; ++e) {
             const int64_t j = M.indices[e];
             if (j == r) continue;
-            const int64_t idx = kk * S + t;
             double v = M.data[e];
             if (upper) v = v * (1.0 / A.diag[j]);  // scipy pre-scales U's columns by 1/diag
-            val[idx] = v;
+            val_at(t, kk) = v;
             const int64_t pj = A.pos_of_row[j];
             if (lend - pj <= W) {
-              slot[idx] = (int32_t)((pj - lo) & (W - 1));
+              slot_at(t, kk) = (int32_t)((pj - lo) & (W - 1));
             } else {
-              slot[idx] = (int32_t)(0x80000000u | (uint32_t)far_index[j]);
+              slot_at(t, kk) = (int32_t)(0x80000000u | (uint32_t)far_index[j]);
               out.far++;
               h[2] |= 2;  // the segment has far dependencies (kernel slow path)
             }

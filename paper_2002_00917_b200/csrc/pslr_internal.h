@@ -41,11 +41,11 @@ constexpr int kChunkRows = 1024;
 // Segment layout inside a chunk (all parts 16-byte aligned):
 //   int32 hdr[8]   = {nrows, w, flags, pos0, S, bytes, nseg (first seg), rbase (first seg)}
 //                    flags: bit0 ends a level, bit1 has far deps, bits 8.. first consumer thread
-//   S = nrows rounded up to 4; ELL with w slabs (rows shorter than w padded with no-ops)
+//   S = nrows rounded up to 4; G = max(1, ceil(w/4)) groups of 4 entries (no-op padding)
 //   int32 info[S]   L: U-position of the row ; U: row id
-//   U only: double sd[S], invd[S]
-//   double val[w][S]  (slab-major; U values pre-scaled by 1/diag of their column)
-//   int32 slot[w][S]  near: ring slot (<= W, W = zero slot) ; far: 0x80000000 | U-position
+//   U only: double sd[S], rcp[S] = RN(1/sd), invd[S]
+//   int32 slot[G][S][4]     near: ring slot (<= W, W = zero slot) ; far: 0x80000000 | U-position
+//   double val[G][2][S][2]  (U values pre-scaled by 1/diag of their column)
 struct DevTri {
   int32_t nblocks = 0, nchunks = 0;
   const uint8_t* data = nullptr;

@@ -103,15 +103,20 @@ __device__ __forceinline__ double spmv_row_rw(const DevCsr& M, int row, const do
   return s;
 }
 
-// Optional timeline of one CTA (PSLR_TRACE=1): (code<<32|arg, %globaltimer ns) pairs.
-// Thread 0 of CTA 0 reserves a window with one atomic per launch, then stores plainly.
+// Optional timeline of one CTA: (code<<32|arg, %globaltimer ns) pairs, recorded only by a
+// trace build (make EXTRA=-DPSLR_TRACE_BUILD=1) run with PSLR_TRACE=1; in the normal build
+// trace_ev compiles to nothing (even a predicated-off check costs the level loop ~10
+// instructions per call).  Thread 0 of CTA 0 reserves a window with one atomic per launch.
+#ifndef PSLR_TRACE_BUILD
+#define PSLR_TRACE_BUILD 0
+#endif
 __shared__ long long* g_trace_ptr;
 __shared__ int g_trace_n;
 
 constexpr int kTraceWindow = 1 << 15;
 
 __device__ __forceinline__ void trace_begin(const StepConst& K) {
-  if (K.trace && blockIdx.x == 0 && threadIdx.x == 0) {
+  if (PSLR_TRACE_BUILD && K.trace && blockIdx.x == 0 && threadIdx.x == 0) {
     const unsigned long long i =
         atomicAdd(reinterpret_cast<unsigned long long*>(K.trace), (unsigned long long)kTraceWindow);
     g_trace_ptr = (i + kTraceWindow <= (unsigned long long)K.trace_cap) ? K.trace + 2 + 2 * i : nullptr;
@@ -119,7 +124,8 @@ __device__ __forceinline__ void trace_begin(const StepConst& K) {
   }
 }
 __device__ __forceinline__ void trace_ev(const StepConst& K, int code, int arg) {
-  if (K.trace && blockIdx.x == 0 && threadIdx.x == 0 && g_trace_ptr && g_trace_n < kTraceWindow) {
+  if (PSLR_TRACE_BUILD && K.trace && blockIdx.x == 0 && threadIdx.x == 0 && g_trace_ptr &&
+      g_trace_n < kTraceWindow) {
     unsigned long long ns;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
     g_trace_ptr[2 * g_trace_n] = ((long long)code << 32) | (unsigned)arg;
@@ -274,107 +280,195 @@ __device__ void producer(const Streams& S, Ctl* ctl, uint8_t* stages, double* rh
 //
 // A level's critical path is latency: gather the dependencies from the ring, the
 // sequential DADD chain, store, barrier.  Everything that does not depend on the
-// previous level - the next segment's header, the row's slots, its right-hand side
-// (already divided by sd) and the U epilogue operands - is loaded for segment s+1 before
-// segment s is computed, so after each barrier a thread only issues its ring gathers
-// (with the value loads alongside) and runs the chain.
+// previous level is loaded one segment ahead: the next segment's header, the row's
+// slots (two groups), its first four values, rhs, U's sd / rcp / invd / cadd.  The step
+// is written as straight-line code (no per-row branches: inactive lanes compute on row
+// 0 of the segment and skip the stores) so the compiler can interleave the next
+// segment's loads and address arithmetic with the current row's gathers and chain.
 //
 // Segment layout (pack.cpp): hdr {nrows, w, flags, pos0, S, bytes, nseg, rbase},
-// info[S], [U: sd[S], invd[S]], val[w][S], slot[w][S].  Consumer thread tb + t owns row t
-// (tb = flags >> 8), so the segments of one level run side by side.
-constexpr int kPre = 8;  // dependencies whose slots are prefetched (the rest: after the barrier)
-
+// info[S], [U: sd[S], rcp[S], invd[S]], slot int4[G][S], val double2[G][2][S]; consumer
+// thread tb + t owns row t (tb = flags >> 8), so the segments of one level run side by side.
 struct Row {
-  int bytes, flags, w, S;
-  bool active;
-  int gp;              // global position of the row
-  int info;            // L: U-position (z index) ; U: row id (xout index)
-  double acc;          // rhs (U: already divided by sd)
-  double invd, cadd;   // U epilogue
-  const double* val;   // &val[0][t]
-  int sl[kPre];
+  const uint8_t* slots;  // &slot[0][t]
+  int bytes, flags, G, S;
+  bool wact;             // the warp owns rows of this segment (warp-uniform)
+  bool active;           // this lane owns a row
+  int ridx;              // ring slot of the row
+  int zidx;              // z index: L: U-position ; U: position
+  int xidx;              // U: xout index (row id)
+  double rhs;            // raw right-hand side
+  double sd, rcp, invd, cadd;  // U only
+  int4 s0, s1;           // slot groups 0 and 1 (zero slot when absent)
+  double2 va, vb;        // group-0 values
 };
 
 template <bool UPPER>
-__device__ __forceinline__ void load_row(const uint8_t* seg, const double* rbuf, int rbase, int zslot,
+__device__ __forceinline__ void load_row(const uint8_t* seg, const int4 h0, const int2 h1, const double* rbuf,
+                                         int rbase, int base, int mask, int zslot,
                                          const double* __restrict__ cadd, Row& r) {
-  const int4 h0 = *reinterpret_cast<const int4*>(seg);       // nrows, w, flags, pos0
-  const int2 h1 = *reinterpret_cast<const int2*>(seg + 16);  // S, bytes
-  r.w = h0.y;
+  const int S = h1.x;
+  const int G = max(1, (h0.y + 3) >> 2);
   r.flags = h0.z;
-  r.S = h1.x;
+  r.S = S;
+  r.G = G;
   r.bytes = h1.y;
-  const int t = (int)threadIdx.x - (h0.z >> 8);
+  // warps owning no row of the segment skip it entirely (the four schedulers are shared
+  // by all 16 consumer warps, so idle warps must not spend issue slots)
+  const int tb = h0.z >> 8, w0 = (int)threadIdx.x & ~31;
+  r.wact = w0 < tb + h0.x && w0 + 32 > tb;
+  if (!r.wact) return;
+  int t = (int)threadIdx.x - tb;
   r.active = (unsigned)t < (unsigned)h0.x;
-  if (!r.active) return;
-  const int S = h1.x, w = h0.y;
+  t = r.active ? t : 0;  // inactive lanes read row 0 (in bounds); their results are not stored
   const int32_t* info = reinterpret_cast<const int32_t*>(seg + 32);
-  const uint8_t* p = reinterpret_cast<const uint8_t*>(info + S);
-  r.gp = h0.w + t;
-  r.info = info[t];
-  double acc = rbuf[r.gp - rbase];
+  const uint8_t* p = seg + 32 + 4 * S;
+  const int gp = h0.w + t;
+  r.ridx = (gp - base) & mask;
+  r.rhs = rbuf[gp - rbase];
+  const int inf = info[t];
   if (UPPER) {
-    const double* sd = reinterpret_cast<const double*>(p);
-    const double sdv = sd[t];
-    if (sdv != 1.0) acc = acc / sdv;  // x / 1.0 == x exactly: skip the division
-    r.invd = sd[S + t];
-    r.cadd = cadd ? __ldg(cadd + r.info) : 0.0;
-    p += 16 * (size_t)S;
+    const double* d = reinterpret_cast<const double*>(p);
+    r.sd = d[t];
+    r.rcp = d[S + t];
+    r.invd = d[2 * S + t];
+    r.zidx = gp;
+    r.xidx = inf;
+    r.cadd = (cadd && r.active) ? __ldg(cadd + inf) : 0.0;
+    p += 24 * S;
+  } else {
+    r.zidx = inf;
   }
-  r.acc = acc;
-  r.val = reinterpret_cast<const double*>(p) + t;
-  const int32_t* slot = reinterpret_cast<const int32_t*>(p + 8 * (size_t)w * S) + t;
-#pragma unroll
-  for (int k = 0; k < kPre; ++k) r.sl[k] = (k < w) ? slot[k * S] : zslot;
+  r.slots = p + 16 * t;
+  r.s0 = *reinterpret_cast<const int4*>(r.slots);
+  r.s1 = (G > 1) ? *reinterpret_cast<const int4*>(r.slots + 16 * S) : make_int4(zslot, zslot, zslot, zslot);
+  const uint8_t* v = p + 16 * G * S + 16 * t;
+  r.va = *reinterpret_cast<const double2*>(v);
+  r.vb = *reinterpret_cast<const double2*>(v + 16 * S);
 }
 
-// acc -= val_k * z_k for the row, in the reference's ascending-column order.  Entries
-// k >= w of the prefetched block read the zero slot with value 0: exact no-ops, so only
-// the chain length depends on w (segment-uniform branches).
+// dependency value: near -> ring slot, far (sign bit) -> global position-ordered array
 template <bool FAR>
-__device__ __forceinline__ double fold_row(const Row& r, const double* ring, const double* z, int zslot) {
-  const int S = r.S, w = r.w;
-  double acc = r.acc;
-  double zz[kPre], vv[kPre];
-#pragma unroll
-  for (int k = 0; k < kPre; ++k) {
-    const int sl = r.sl[k];
-    zz[k] = FAR ? ((sl >= 0) ? ring[sl] : z[sl & 0x7fffffff]) : ring[sl];
-    vv[k] = (k < w) ? r.val[k * S] : 0.0;
+__device__ __forceinline__ double gather(const double* ring, const double* z, int sl) {
+  return FAR ? ((sl >= 0) ? ring[sl] : z[sl & 0x7fffffff]) : ring[sl];
+}
+
+// acc -= val_k * z_k over the row's groups in the reference's ascending-column order
+// (padding entries: 0 * 0); group 0's slots and values are in registers.
+template <bool FAR>
+__device__ __forceinline__ double fold_row(double acc, const Row& r, const double* ring, const double* z) {
+  {
+    const double z0 = gather<FAR>(ring, z, r.s0.x), z1 = gather<FAR>(ring, z, r.s0.y);
+    const double z2 = gather<FAR>(ring, z, r.s0.z), z3 = gather<FAR>(ring, z, r.s0.w);
+    acc = acc - r.va.x * z0;
+    acc = acc - r.va.y * z1;
+    acc = acc - r.vb.x * z2;
+    acc = acc - r.vb.y * z3;
   }
-  acc = acc - vv[0] * zz[0];
-  if (w > 1) {
-    acc = acc - vv[1] * zz[1];
-    if (w > 2) {
-      acc = acc - vv[2] * zz[2];
-      acc = acc - vv[3] * zz[3];
-      if (w > 4) {
-        acc = acc - vv[4] * zz[4];
-        acc = acc - vv[5] * zz[5];
-        acc = acc - vv[6] * zz[6];
-        acc = acc - vv[7] * zz[7];
-      }
-    }
-  }
-  if (w > kPre) {  // long rows: the rest straight from the staged segment
-    const int t = (int)threadIdx.x - (r.flags >> 8);
-    const int32_t* slot = reinterpret_cast<const int32_t*>(r.val - t + (size_t)w * S) + t;
-    for (int k = kPre; k < w; k += 4) {
-      int s4[4];
-      double v4[4], z4[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        s4[j] = (k + j < w) ? slot[(k + j) * S] : zslot;
-        v4[j] = (k + j < w) ? r.val[(k + j) * S] : 0.0;
-      }
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        z4[j] = FAR ? ((s4[j] >= 0) ? ring[s4[j]] : z[s4[j] & 0x7fffffff]) : ring[s4[j]];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) acc = acc - v4[j] * z4[j];
+  if (r.G > 1) {
+    const uint8_t* v = r.slots + 16 * r.G * r.S + 32 * r.S;  // group 1 values
+    const double2 va = *reinterpret_cast<const double2*>(v);
+    const double2 vb = *reinterpret_cast<const double2*>(v + 16 * r.S);
+    const double z0 = gather<FAR>(ring, z, r.s1.x), z1 = gather<FAR>(ring, z, r.s1.y);
+    const double z2 = gather<FAR>(ring, z, r.s1.z), z3 = gather<FAR>(ring, z, r.s1.w);
+    acc = acc - va.x * z0;
+    acc = acc - va.y * z1;
+    acc = acc - vb.x * z2;
+    acc = acc - vb.y * z3;
+    for (int g = 2; g < r.G; ++g) {  // long rows: the rest straight from the staged segment
+      const int4 sg = *reinterpret_cast<const int4*>(r.slots + 16 * g * r.S);
+      const uint8_t* w = r.slots + 16 * r.G * r.S + 32 * g * r.S;
+      const double2 wa = *reinterpret_cast<const double2*>(w);
+      const double2 wb = *reinterpret_cast<const double2*>(w + 16 * r.S);
+      const double y0 = gather<FAR>(ring, z, sg.x), y1 = gather<FAR>(ring, z, sg.y);
+      const double y2 = gather<FAR>(ring, z, sg.z), y3 = gather<FAR>(ring, z, sg.w);
+      acc = acc - wa.x * y0;
+      acc = acc - wa.y * y1;
+      acc = acc - wb.x * y2;
+      acc = acc - wb.y * y3;
     }
   }
   return acc;
+}
+
+struct Cursor {
+  int u, u1, st, nst, si, nseg, rbase;
+  uint32_t par;
+  const uint8_t* seg;
+  const double* rbuf;
+};
+
+template <bool UPPER>
+__device__ __forceinline__ bool level_step(const StepConst& K, Ctl* ctl, uint8_t* stages, double* rhsbuf,
+                                           Cursor& c, Row& cur, const double* ring_c,
+                                           double* ring, int base, double* z, double* xout,
+                                           const double* cadd) {
+  const int mask = K.ring_mask, zslot = K.ring_mask + 1;
+  // C: locate the next segment (next chunk: wait for it; it is normally staged already)
+  //    and issue its header loads, so they are in flight while this row is computed
+  const uint8_t* nseg_ptr = c.seg + cur.bytes;
+  const int cur_st = c.st;
+  bool chunk_done = false, more = true;
+  if (++c.si == c.nseg) {
+    chunk_done = true;
+    if (++c.u == c.u1) {
+      more = false;
+    } else {
+      if (++c.st == c.nst) {
+        c.st = 0;
+        c.par ^= 1u;
+      }
+      mbar_wait(&ctl->full[c.st], c.par);
+      trace_ev(K, 20, c.u);
+      nseg_ptr = stages + (size_t)c.st * K.stage_bytes;
+      c.rbuf = rhsbuf + (size_t)c.st * K.rhs_stride;
+      c.nseg = reinterpret_cast<const int32_t*>(nseg_ptr)[6];
+      c.rbase = reinterpret_cast<const int32_t*>(nseg_ptr)[7];
+      c.si = 0;
+    }
+  }
+  int4 nh0 = make_int4(0, 0, 0, 0);
+  int2 nh1 = make_int2(0, 0);
+  if (more) {
+    nh0 = *reinterpret_cast<const int4*>(nseg_ptr);
+    nh1 = *reinterpret_cast<const int2*>(nseg_ptr + 16);
+  }
+  if (cur.wact) {
+    // B: U rows start from rhs / sd.  rcp = RN(1/sd): q0 = RN(x rcp) is within an ulp of
+    // x/sd and one fma-corrected step gives RN(x/sd) (Markstein); sd == 1 keeps x as is.
+    double acc = cur.rhs;
+    if (UPPER) {
+      const double q0 = acc * cur.rcp;
+      const double q = fma(fma(-q0, cur.sd, acc), cur.rcp, q0);
+      acc = (cur.sd == 1.0) ? acc : q;
+    }
+    // A + D: gathers and the chain
+    acc = (cur.flags & 2) ? fold_row<true>(acc, cur, ring_c, z) : fold_row<false>(acc, cur, ring_c, z);
+    // F: publish the row
+    if (cur.active) {
+      ring[cur.ridx] = acc;
+      z[cur.zidx] = acc;
+      if (UPPER) {
+        double x = acc * cur.invd;
+        if (cadd) x = x + cur.cadd;
+        xout[cur.xidx] = x;
+      }
+    }
+  }
+  const int cur_flags = cur.flags;
+  // E: the next segment's row, loaded in place (everything it needs before its gathers)
+  if (more) load_row<UPPER>(nseg_ptr, nh0, nh1, c.rbuf, c.rbase, base, mask, zslot, cadd, cur);
+  c.seg = nseg_ptr;
+  if (chunk_done) {  // the staged chunk is no longer read by this warp
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) mbar_arrive(&ctl->empty[cur_st]);
+  }
+  if (cur_flags & 1) {
+    trace_ev(K, 40, 0);
+    consumer_sync();
+    trace_ev(K, 41, 0);
+  }
+  return more;
 }
 
 // Consumer side of one triangular phase.  Callers arrive right after a consumer barrier
@@ -390,65 +484,25 @@ __device__ void tri_phase(const StepConst& K, const Streams& S, Ctl* ctl, uint8_
     fence_proxy_async();
     mbar_arrive(&ctl->rhs_ready[k]);
   }
-  const int u0 = S.begin[k], u1 = S.begin[k + 1];
-  if (u0 == u1) return;
-  const int nst = K.nst, mask = K.ring_mask, zslot = K.ring_mask + 1;
-  const int lane = threadIdx.x & 31;
-  int u = u0, st = u0 % nst;
-  uint32_t par = (uint32_t)((u0 / nst) & 1);
-  mbar_wait(&ctl->full[st], par);
-  const uint8_t* seg = stages + (size_t)st * K.stage_bytes;
-  const double* rbuf = rhsbuf + (size_t)st * K.rhs_stride;
-  int nseg = reinterpret_cast<const int32_t*>(seg)[6];
-  int rbase = reinterpret_cast<const int32_t*>(seg)[7];
-  int si = 0;
-  Row cur;
-  load_row<UPPER>(seg, rbuf, rbase, zslot, cadd, cur);
-  while (true) {
-    // locate + prefetch the next segment (next chunk: wait for it, it is normally staged)
-    const uint8_t* nseg_ptr = seg + cur.bytes;
-    const int cur_st = st;
-    bool chunk_done = false, more = true;
-    if (++si == nseg) {
-      chunk_done = true;
-      if (++u == u1) {
-        more = false;
-      } else {
-        if (++st == nst) {
-          st = 0;
-          par ^= 1u;
-        }
-        mbar_wait(&ctl->full[st], par);
-        nseg_ptr = stages + (size_t)st * K.stage_bytes;
-        rbuf = rhsbuf + (size_t)st * K.rhs_stride;
-        nseg = reinterpret_cast<const int32_t*>(nseg_ptr)[6];
-        rbase = reinterpret_cast<const int32_t*>(nseg_ptr)[7];
-        si = 0;
-      }
-    }
-    Row nxt;
-    if (more) load_row<UPPER>(nseg_ptr, rbuf, rbase, zslot, cadd, nxt);
-    if (cur.active) {
-      const double acc = (cur.flags & 2) ? fold_row<true>(cur, ring, z, zslot)
-                                         : fold_row<false>(cur, ring, z, zslot);
-      ring[(cur.gp - base) & mask] = acc;
-      if (UPPER) {
-        z[cur.gp] = acc;
-        double x = acc * cur.invd;
-        if (cadd) x = x + cur.cadd;
-        xout[cur.info] = x;
-      } else {
-        z[cur.info] = acc;
-      }
-    }
-    if (chunk_done) {  // the staged chunk is no longer read by this warp
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&ctl->empty[cur_st]);
-    }
-    if (cur.flags & 1) consumer_sync();
-    if (!more) break;
-    cur = nxt;
-    seg = nseg_ptr;
+  Cursor c;
+  c.u = S.begin[k];
+  c.u1 = S.begin[k + 1];
+  if (c.u == c.u1) return;
+  c.nst = K.nst;
+  c.st = c.u % c.nst;
+  c.par = (uint32_t)((c.u / c.nst) & 1);
+  mbar_wait(&ctl->full[c.st], c.par);
+  trace_ev(K, 20, c.u);
+  c.seg = stages + (size_t)c.st * K.stage_bytes;
+  c.rbuf = rhsbuf + (size_t)c.st * K.rhs_stride;
+  c.nseg = reinterpret_cast<const int32_t*>(c.seg)[6];
+  c.rbase = reinterpret_cast<const int32_t*>(c.seg)[7];
+  c.si = 0;
+  Row row;
+  load_row<UPPER>(c.seg, *reinterpret_cast<const int4*>(c.seg), *reinterpret_cast<const int2*>(c.seg + 16),
+                  c.rbuf, c.rbase, base, K.ring_mask, K.ring_mask + 1, cadd, row);
+  const double* ring_c = ring;
+  while (level_step<UPPER>(K, ctl, stages, rhsbuf, c, row, ring_c, ring, base, z, xout, cadd)) {
   }
 }
 
@@ -510,9 +564,11 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
   const bool do_c = do_i && a.do_c0;
 
   Ctl* ctl = reinterpret_cast<Ctl*>(smem);
-  uint8_t* stages = smem + 256;
+  // [Ctl 256 B][ring: W slots + zero slot, padded to 128 B][nst stages][nst rhs slices]
+  // The ring sits at a constant offset, so a gather is one address op on its slot.
+  double* ring = reinterpret_cast<double*>(smem + 256);
+  uint8_t* stages = smem + 256 + (size_t)(K.ring_mask + 1) * 8 + 128;
   double* rhsbuf = reinterpret_cast<double*>(stages + (size_t)K.nst * K.stage_bytes);
-  double* ring = rhsbuf + (size_t)K.nst * K.rhs_stride;
 
   // The stream table lives in shared memory: dynamically indexed per-thread arrays would
   // spill to local memory, which misses the small L1 left beside 229 KB of shared memory.

@@ -38,8 +38,8 @@ rel = np.flatnonzero(codes == 41)
 arr = np.flatnonzero(codes == 40)
 if rel.size > 2:
     lv = np.diff(ts[rel])
-    rows = args[arr[1:]] & 0xffff
-    ws = args[arr[1:]] >> 16
+    rows = np.zeros(arr.size - 1, dtype=np.int64)
+    ws = args[arr[1:]]
     wait = ts[rel] - ts[arr]
     print(f"levels {rel.size}: level us mean {lv.mean() / 1e3:.3f} median {np.median(lv) / 1e3:.3f} "
           f"p90 {np.percentile(lv, 90) / 1e3:.3f}; barrier wait (thread0) mean {wait.mean() / 1e3:.3f}")
@@ -102,7 +102,7 @@ for li, s0 in enumerate(starts):
     cnt_c = int(np.sum(codes[s0:s1] == 20))
     if best is None or cnt_c > best[2]:
         best = (s0, s1, cnt_c)
-if best:
+if best and best[2] > 0:
     s0, s1, _ = best
     c, a, t = codes[s0:s1], args[s0:s1], ts[s0:s1]
     waits = []
