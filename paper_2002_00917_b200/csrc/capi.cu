@@ -94,14 +94,16 @@ static int upload_csr(pslr_ctx* ctx, const pslr_csr& M, DevCsr* out) {
   return PSLR_OK;
 }
 
-static int upload_tri(pslr_ctx* ctx, const TriHost& H, const std::vector<int32_t>* lpos,
-                      DevTri* out) {
+static int upload_tri(pslr_ctx* ctx, const TriHost& H, const TriAnalysis* AL, DevTri* out) {
   out->nblocks = (int32_t)H.blk_chunk.size() - 1;
   out->nchunks = (int32_t)H.chunks.size();
   RET(upload(ctx, H.data, &out->data));
   RET(upload(ctx, H.chunks, &out->chunks));
   RET(upload(ctx, H.blk_chunk, &out->blk_chunk));
-  if (lpos) RET(upload(ctx, *lpos, &out->lpos));
+  if (AL) {
+    RET(upload(ctx, AL->pos_of_row, &out->lpos));
+    RET(upload(ctx, AL->row_at_pos, &out->lrow));
+  }
   return PSLR_OK;
 }
 
@@ -117,7 +119,7 @@ static int build_pair(pslr_ctx* ctx, const pslr_csr& L, const pslr_csr& U,
   TriHost HL, HU;
   RET(emit_factor(U, off, AU, W, SB, kStepThreads, AU.pos_of_row, row_id, HU, nameU));
   RET(emit_factor(L, off, AL, W, SB, kStepThreads, AU.pos_of_row, AU.pos_of_row, HL, nameL));
-  RET(upload_tri(ctx, HL, &AL.pos_of_row, dL));
+  RET(upload_tri(ctx, HL, &AL, dL));
   RET(upload_tri(ctx, HU, nullptr, dU));
   *far = HL.far + HU.far;
   return PSLR_OK;

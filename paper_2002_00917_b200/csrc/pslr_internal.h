@@ -52,6 +52,7 @@ struct DevTri {
   const ChunkDesc* chunks = nullptr;
   const int32_t* blk_chunk = nullptr;  // nblocks+1
   const int32_t* lpos = nullptr;       // L only: row -> global L-position (rhs placement)
+  const int32_t* lrow = nullptr;       // L only: global L-position -> row
 };
 
 // host-side analysis + packed output (pack.cpp)

@@ -418,6 +418,7 @@ __device__ __forceinline__ bool level_step(const StepConst& K, Ctl* ctl, uint8_t
         c.st = 0;
         c.par ^= 1u;
       }
+      trace_ev(K, 19, c.u);
       mbar_wait(&ctl->full[c.st], c.par);
       trace_ev(K, 20, c.u);
       nseg_ptr = stages + (size_t)c.st * K.stage_bytes;
@@ -618,20 +619,26 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
 
   if (do_b) {
     const int r0 = K.int_off[b], r1 = K.int_off[b + 1];
-    // pass 1: every row gets b1's f term (or 0); independent loads, 4 rows in flight
-    for (int row0 = r0 + tid; row0 < r1; row0 += 4 * kStepThreads) {
-      double v[4];
-      int pos[4];
+    // pass 1: rhs = f scattered to the L-positions (stores do not stall, so scatter
+    // beats a gather here), or a coalesced zero fill
+    if (a.b1 == BT_F) {
+      constexpr int kIn = 8;  // independent loads in flight per thread
+      for (int row0 = r0 + tid; row0 < r1; row0 += kIn * kStepThreads) {
+        double v[kIn];
+        int pos[kIn];
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const int row = row0 + j * kStepThreads;
-        const bool ok = row < r1;
-        v[j] = (ok && a.b1 == BT_F) ? __ldg(a.f + row) : 0.0;
-        pos[j] = ok ? __ldg(K.LB.lpos + row) : 0;
+        for (int j = 0; j < kIn; ++j) {
+          const int row = row0 + j * kStepThreads;
+          const bool ok = row < r1;
+          v[j] = ok ? __ldg(a.f + row) : 0.0;
+          pos[j] = ok ? __ldg(K.LB.lpos + row) : 0;
+        }
+#pragma unroll
+        for (int j = 0; j < kIn; ++j)
+          if (row0 + j * kStepThreads < r1) K.rhsB[pos[j]] = v[j];
       }
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (row0 + j * kStepThreads < r1) K.rhsB[pos[j]] = v[j];
+    } else {
+      for (int p = r0 + tid; p < r1; p += kStepThreads) K.rhsB[p] = 0.0;
     }
     // pass 2: rows with E entries get the E y term: f - E y, or E y alone
     if (a.b1 == BT_EY || a.b2 == BT_EY) {
