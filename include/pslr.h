@@ -73,6 +73,7 @@ typedef struct {
   int64_t stages;      /* TMA pipeline stages per CTA */
   int64_t far_deps;    /* dependencies read from global memory (beyond the ring) */
   int64_t reach;       /* max level-order distance of a dependency */
+  int64_t nghost;      /* sharded contexts: ghost interface values after the local q (see below) */
 } pslr_ctx_info_t;
 
 /* ---------------------------------------------------------------- misc */
@@ -134,6 +135,26 @@ int pslr_apply_profiled(pslr_ctx* ctx, int64_t m, const double* b, double* z, vo
 int pslr_debug_trace(pslr_ctx* ctx, int64_t* out, int64_t cap, int64_t* count);
 /* Alg. 3.2 with HOST buffers (copies inside): the call a CPU user of P.apply makes. */
 int pslr_apply_host(pslr_ctx* ctx, int64_t m, const double* b_host, double* z_host, void* stream);
+
+/* ---------------------------------------------------------------- sharded apply (multi-GPU)
+ * rank g owns a contiguous range of subdomains; B, C0, E, F are local.
+ * A context is SHARDED when its C, Cg (q rows) and A (n rows) carry nghost extra
+ * columns: interface values owned by other ranks ("ghosts"), which every interface
+ * vector the Horner steps read stores after its q local values ("extended" vectors,
+ * q + nghost).  The apply (preconditioner.py:79-93) is split where ranks exchange data;
+ * the caller (paper_2002_00917_b200/shard.py) runs the exchanges between the calls:
+ *   first  : y0 = g - F B^{-1} f ; s = V^T y0 over the local rows   -> allreduce(s)
+ *   mid    : y1 = y0 + V G s ; c = C0^{-1} y1  (c extended)         -> halo(c)
+ *   horner : out = C0^{-1}(E_s y) + c  (y extended), m times        -> halo(out) between
+ *   last   : z = [B^{-1}(f - E y) ; y]
+ * The fused single-context calls above require nghost == 0. */
+int pslr_apply_first(pslr_ctx* ctx, const double* b, double* y0, double* s, void* stream);
+int pslr_apply_mid(pslr_ctx* ctx, const double* y0, const double* s, double* c, void* stream);
+int pslr_apply_horner(pslr_ctx* ctx, const double* y, const double* c, double* out, void* stream);
+int pslr_apply_last(pslr_ctx* ctx, const double* b, const double* y, double* z, void* stream);
+/* out = C0^{-1}? (F B^{-1} E v - Cg v) with v extended: one E_rr / Arnoldi operator step
+ * (schur.py:83-86, 104-112); do_c0 selects the C0 solve. */
+int pslr_apply_es_step(pslr_ctx* ctx, const double* v, double* out, int do_c0, void* stream);
 
 /* ---------------------------------------------------------------- Krylov (device) */
 /* lowrank.py:39-73 on op = E_rr(m) (schur.py:104-112), preconditioner.py:133-136.

@@ -51,7 +51,7 @@ class CtxInfo(ctypes.Structure):
         "levels_LB", "levels_UB", "levels_LC", "levels_UC",
         "maxdepth_LB", "maxdepth_UB", "maxdepth_LC", "maxdepth_UC",
         "nnz_LB", "nnz_UB", "nnz_LC", "nnz_UC", "nnz_E", "nnz_F", "nnz_C", "nnz_C0", "nnz_Cg",
-        "nnz_A", "device_bytes", "sm_count", "ring_slots", "stages", "far_deps", "reach")]
+        "nnz_A", "device_bytes", "sm_count", "ring_slots", "stages", "far_deps", "reach", "nghost")]
 
 
 def _sig(name, res, *args):
@@ -87,6 +87,11 @@ EXPORTS = {
     "pslr_apply": (c_int, P, c_i64, P, P, P),
     "pslr_spmv": (c_int, P, c_int, P, P, P),
     "pslr_apply_host": (c_int, P, c_i64, P, P, P),
+    "pslr_apply_first": (c_int, P, P, P, P, P),
+    "pslr_apply_mid": (c_int, P, P, P, P, P),
+    "pslr_apply_horner": (c_int, P, P, P, P, P),
+    "pslr_apply_last": (c_int, P, P, P, P, P),
+    "pslr_apply_es_step": (c_int, P, P, P, c_int, P),
     "pslr_apply_profiled": (c_int, P, c_i64, P, P, P, P, P, c_i64, ctypes.POINTER(c_i64)),
     "pslr_debug_trace": (c_int, P, P, c_i64, ctypes.POINTER(c_i64)),
     "pslr_arnoldi": (c_int, P, c_i64, c_i64, P, P, P, ctypes.POINTER(c_i64), P),

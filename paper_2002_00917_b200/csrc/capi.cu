@@ -127,6 +127,13 @@ static int build_pair(pslr_ctx* ctx, const pslr_csr& L, const pslr_csr& U,
 
 static cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
 
+// the fused single-context operators read Cg through internal q-vectors without ghosts
+static int unsharded(const pslr_ctx* ctx) {
+  if (ctx->nghost)
+    return fail(PSLR_EINVAL, "sharded context: use the split apply (pslr_apply_first/mid/horner/last)");
+  return PSLR_OK;
+}
+
 static int mark(pslr_ctx* ctx, int32_t kind, cudaStream_t st) {
   if (!ctx->prof_on) return PSLR_OK;
   cudaEvent_t ev;
@@ -294,10 +301,13 @@ int pslr_ctx_create(pslr_ctx** out, int device, const pslr_system* sys) {
   RET(check_csr(sys->UC, q, q, "U_C0"));
   RET(check_csr(sys->E, p, q, "E"));
   RET(check_csr(sys->F, q, p, "F"));
-  RET(check_csr(sys->C, q, q, "C"));
+  // sharded contexts: C, Cg and A carry the same nghost ghost columns (include/pslr.h)
+  const int64_t nghost = sys->Cg.ncols - q;
+  if (nghost < 0) return fail(PSLR_EDIM, "Cg has the wrong shape");
+  RET(check_csr(sys->C, q, q + nghost, "C"));
   RET(check_csr(sys->C0, q, q, "C0"));
-  RET(check_csr(sys->Cg, q, q, "Cg"));
-  RET(check_csr(sys->A, n, n, "A"));
+  RET(check_csr(sys->Cg, q, q + nghost, "Cg"));
+  RET(check_csr(sys->A, n, n + nghost, "A"));
   if (sys->interior_offsets[0] != 0 || sys->interior_offsets[s] != p ||
       sys->interface_offsets[0] != 0 || sys->interface_offsets[s] != q)
     return fail(PSLR_EDIM, "block offsets do not tile the system");
@@ -307,6 +317,7 @@ int pslr_ctx_create(pslr_ctx** out, int device, const pslr_system* sys) {
   ctx->p = p;
   ctx->q = q;
   ctx->s = s;
+  ctx->nghost = nghost;
   ctx->interior_off.assign(sys->interior_offsets, sys->interior_offsets + s + 1);
   ctx->interface_off.assign(sys->interface_offsets, sys->interface_offsets + s + 1);
   int rc = PSLR_OK;
@@ -446,6 +457,7 @@ int pslr_ctx_create(pslr_ctx** out, int device, const pslr_system* sys) {
   I.nnz_Cg = sys->Cg.nnz;
   I.nnz_A = sys->A.nnz;
   I.sm_count = ctx->sm_count;
+  I.nghost = nghost;
   if (cudaDeviceSynchronize() != cudaSuccess) return bail(fail(PSLR_ECUDA, "upload failed"));
   *out = ctx;
   return PSLR_OK;
@@ -513,11 +525,13 @@ int pslr_solve_C0(pslr_ctx* ctx, const double* g, double* y, void* stream) {
 }
 
 int pslr_apply_Es(pslr_ctx* ctx, const double* v, double* out, void* stream) {
+  RET(unsharded(ctx));
   RET(set_device(ctx));
   return op_es_step(ctx, v, out, 0, nullptr, S(stream));
 }
 
 int pslr_apply_S(pslr_ctx* ctx, const double* v, double* out, void* stream) {
+  RET(unsharded(ctx));
   RET(set_device(ctx));
   StepArgs a;
   a.b1 = BT_EY;
@@ -532,6 +546,7 @@ int pslr_apply_S(pslr_ctx* ctx, const double* v, double* out, void* stream) {
 }
 
 int pslr_apply_neumann(pslr_ctx* ctx, int64_t m, const double* v, double* out, void* stream) {
+  RET(unsharded(ctx));
   if (m < 0) return fail(PSLR_EDIM, "series degree m must be >= 0");
   RET(set_device(ctx));
   RET(op_solve_C0(ctx, v, ctx->c, S(stream)));
@@ -539,6 +554,7 @@ int pslr_apply_neumann(pslr_ctx* ctx, int64_t m, const double* v, double* out, v
 }
 
 int pslr_apply_Err(pslr_ctx* ctx, int64_t m, const double* v, double* out, void* stream) {
+  RET(unsharded(ctx));
   if (m < 0) return fail(PSLR_EDIM, "series degree m must be >= 0");
   RET(set_device(ctx));
   return op_apply_err(ctx, m, v, out, S(stream));
@@ -557,9 +573,77 @@ int pslr_apply_correction(pslr_ctx* ctx, const double* y, double* out, void* str
 }
 
 int pslr_apply(pslr_ctx* ctx, int64_t m, const double* b, double* z, void* stream) {
+  RET(unsharded(ctx));
   if (m < 0) return fail(PSLR_EDIM, "series degree m must be >= 0");
   RET(set_device(ctx));
   return op_apply(ctx, m, b, z, S(stream));
+}
+
+// ---------------------------------------------------------------- sharded apply
+int pslr_apply_first(pslr_ctx* ctx, const double* b, double* y0, double* s, void* stream) {
+  RET(set_device(ctx));
+  cudaStream_t st = S(stream);
+  if (ctx->q == 0) return PSLR_OK;
+  StepArgs a;
+  a.b1 = BT_F;
+  a.f = b;
+  a.xb = ctx->xb;
+  a.i1 = IT_G;
+  a.g = b + ctx->p;
+  a.i2 = IT_FX;
+  a.i2_sub = 1;
+  a.yout = y0;
+  a.tag = LK_FIRST;
+  RET(run_step(ctx, a, st));
+  if (ctx->r > 0) CKL(launch_vt_local(ctx, y0, s, st));
+  return PSLR_OK;
+}
+
+int pslr_apply_mid(pslr_ctx* ctx, const double* y0, const double* s, double* c, void* stream) {
+  RET(set_device(ctx));
+  cudaStream_t st = S(stream);
+  if (ctx->q == 0) return PSLR_OK;
+  const double* y1 = y0;
+  if (ctx->r > 0) {
+    CKL(launch_gs(ctx, s, st));
+    CKL(launch_vu_add(ctx, y0, ctx->y1, st));
+    y1 = ctx->y1;
+  }
+  StepArgs a;
+  a.i1 = IT_G;
+  a.g = y1;
+  a.do_c0 = 1;
+  a.yout = c;
+  a.tag = LK_CORR;
+  return run_step(ctx, a, st);
+}
+
+int pslr_apply_horner(pslr_ctx* ctx, const double* y, const double* c, double* out, void* stream) {
+  RET(set_device(ctx));
+  if (ctx->q == 0) return PSLR_OK;
+  return op_es_step(ctx, y, out, 1, c, S(stream));
+}
+
+int pslr_apply_es_step(pslr_ctx* ctx, const double* v, double* out, int do_c0, void* stream) {
+  RET(set_device(ctx));
+  if (ctx->q == 0) return PSLR_OK;
+  return op_es_step(ctx, v, out, do_c0 ? 1 : 0, nullptr, S(stream));
+}
+
+int pslr_apply_last(pslr_ctx* ctx, const double* b, const double* y, double* z, void* stream) {
+  RET(set_device(ctx));
+  cudaStream_t st = S(stream);
+  if (ctx->q > 0 && z + ctx->p != y)
+    CK(cudaMemcpyAsync(z + ctx->p, y, ctx->q * sizeof(double), cudaMemcpyDeviceToDevice, st));
+  if (ctx->q == 0) return op_solve_B(ctx, b, z, st);
+  StepArgs a;
+  a.b1 = BT_F;
+  a.f = b;
+  a.b2 = BT_EY;
+  a.yE = y;
+  a.xb = z;
+  a.tag = LK_LAST;
+  return run_step(ctx, a, st);
 }
 
 int pslr_spmv(pslr_ctx* ctx, int which, const double* x, double* y, void* stream) {

@@ -83,13 +83,24 @@ vt_dot_kernel(const double* __restrict__ V, const double* __restrict__ y, int64_
     h[c] = s;
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < r; i += kVtThreads) {
-    double s = 0.0;
-    const double* gi = G + (int64_t)i * r;
-    for (int c = 0; c < r; ++c) s = s + gi[c] * ((volatile double*)h)[c];
-    hu[i] = s;
-  }
+  if (G)  // sharded contexts stop at h: the ranks sum it before G is applied
+    for (int i = threadIdx.x; i < r; i += kVtThreads) {
+      double s = 0.0;
+      const double* gi = G + (int64_t)i * r;
+      for (int c = 0; c < r; ++c) s = s + gi[c] * ((volatile double*)h)[c];
+      hu[i] = s;
+    }
   if (threadIdx.x == 0) *counter = 0u;
+}
+
+// u = G s (one CTA): the correction core after the ranks' V^T y partial sums are reduced
+__global__ void gs_kernel(const double* __restrict__ G, const double* __restrict__ s, double* u, int r) {
+  for (int i = threadIdx.x; i < r; i += blockDim.x) {
+    double acc = 0.0;
+    const double* gi = G + (int64_t)i * r;
+    for (int c = 0; c < r; ++c) acc = acc + gi[c] * s[c];
+    u[i] = acc;
+  }
 }
 
 // out = y + V u (one warp per row, lanes on columns, fixed shuffle-tree reduction)
@@ -227,6 +238,20 @@ int vt_grid(int64_t q, int sm_count) {
   if (g > cap) g = cap;
   if (g < 1) g = 1;
   return (int)g;
+}
+
+// s = V^T y over this context's rows (sharded contexts; h lands in ctx->u[r..2r) first)
+int launch_vt_local(pslr_ctx* ctx, const double* y, double* s, cudaStream_t st) {
+  const int g = vt_grid(ctx->q, ctx->sm_count);
+  vt_dot_kernel<<<g, kVtThreads, 0, st>>>(ctx->V, y, ctx->q, (int)ctx->r, nullptr, ctx->red, ctx->u,
+                                          ctx->counter);
+  if (cudaGetLastError() != cudaSuccess) return 1;
+  return (int)cudaMemcpyAsync(s, ctx->u + ctx->r, ctx->r * sizeof(double), cudaMemcpyDeviceToDevice, st);
+}
+
+int launch_gs(pslr_ctx* ctx, const double* s, cudaStream_t st) {
+  gs_kernel<<<1, 128, 0, st>>>(ctx->G, s, ctx->u, (int)ctx->r);
+  return (int)cudaGetLastError();
 }
 
 // u = G V^T y  (writes ctx->u[0..r), h in ctx->u[r..2r))

@@ -58,6 +58,7 @@ extern "C" {
 int pslr_arnoldi(pslr_ctx* ctx, int64_t m, int64_t rank, const double* v0, double* V_dev, double* H,
                  int64_t* r_out, void* stream) {
   RET(set_device(ctx));
+  if (ctx->nghost) return fail(PSLR_EINVAL, "sharded context: run the Krylov loop in shard.py");
   cudaStream_t st = S(stream);
   const int64_t q = ctx->q;
   if (rank < 0) return fail(PSLR_EDIM, "rank must be >= 0");
@@ -97,6 +98,7 @@ int pslr_gmres(pslr_ctx* ctx, int64_t m, const double* b, double* x, double tol,
                int64_t restart, int precond, int flexible, int64_t* iterations, int* converged,
                double* final_relres, double* history, int64_t* history_len, void* stream) {
   RET(set_device(ctx));
+  if (ctx->nghost) return fail(PSLR_EINVAL, "sharded context: run the Krylov loop in shard.py");
   cudaStream_t st = S(stream);
   const int64_t n = ctx->n;
   std::vector<double> hist;

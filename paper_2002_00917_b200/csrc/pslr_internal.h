@@ -132,6 +132,7 @@ struct StepConst {
 struct pslr_ctx {
   int device = 0;
   int64_t n = 0, p = 0, q = 0, s = 0, r = 0;
+  int64_t nghost = 0;  // sharded contexts: ghost interface columns of C, Cg and A
   int sm_count = 0;
   std::vector<int64_t> interior_off, interface_off;
   // device-resident state

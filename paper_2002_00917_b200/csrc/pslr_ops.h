@@ -51,6 +51,8 @@ int launch_transpose_basis(const double* X, int64_t q, int r, double* Y, cudaStr
 int dot_grid(int64_t n, int sm_count);
 int vt_grid(int64_t q, int sm_count);
 int launch_vt_dot(pslr_ctx* ctx, const double* y, cudaStream_t st);
+int launch_vt_local(pslr_ctx* ctx, const double* y, double* s, cudaStream_t st);
+int launch_gs(pslr_ctx* ctx, const double* s, cudaStream_t st);
 int launch_vu_add(const pslr_ctx* ctx, const double* y, double* out, cudaStream_t st);
 
 // capi.cu

@@ -391,6 +391,18 @@ __device__ __forceinline__ double fold_row(double acc, const Row& r, const doubl
   return acc;
 }
 
+// trace builds: thread 0's cycles in the parts of the level loop (rows 2048 + b of the
+// trace buffer's counter area): chunk waits, fold, publish + next-row loads, barrier
+struct Probe {
+  long long t, wait, fold, pub, bar, steps, levels, chunks;
+};
+__device__ __forceinline__ long long probe_clock(bool on, double dep) {
+  // the compare consumes dep, so the clock is read after the value is available
+  if (!on) return 0;
+  if (dep == -1.2345e-300) asm volatile("trap;");
+  return clock64();
+}
+
 struct Cursor {
   int u, u1, st, nst, si, nseg, rbase;
   uint32_t par;
@@ -402,8 +414,10 @@ template <bool UPPER>
 __device__ __forceinline__ bool level_step(const StepConst& K, Ctl* ctl, uint8_t* stages, double* rhsbuf,
                                            Cursor& c, Row& cur, const double* ring_c,
                                            double* ring, int base, double* z, double* xout,
-                                           const double* cadd) {
+                                           const double* cadd, Probe& pr) {
   const int mask = K.ring_mask, zslot = K.ring_mask + 1;
+  const bool prb = PSLR_TRACE_BUILD && K.trace && threadIdx.x == 0;
+  long long tc0 = probe_clock(prb, 0.0), twait = 0;
   // C: locate the next segment (next chunk: wait for it; it is normally staged already)
   //    and issue its header loads, so they are in flight while this row is computed
   const uint8_t* nseg_ptr = c.seg + cur.bytes;
@@ -419,7 +433,9 @@ __device__ __forceinline__ bool level_step(const StepConst& K, Ctl* ctl, uint8_t
         c.par ^= 1u;
       }
       trace_ev(K, 19, c.u);
+      const long long tw0 = probe_clock(prb, 0.0);
       mbar_wait(&ctl->full[c.st], c.par);
+      twait = probe_clock(prb, 0.0) - tw0;
       trace_ev(K, 20, c.u);
       nseg_ptr = stages + (size_t)c.st * K.stage_bytes;
       c.rbuf = rhsbuf + (size_t)c.st * K.rhs_stride;
@@ -445,6 +461,11 @@ __device__ __forceinline__ bool level_step(const StepConst& K, Ctl* ctl, uint8_t
     }
     // A + D: gathers and the chain
     acc = (cur.flags & 2) ? fold_row<true>(acc, cur, ring_c, z) : fold_row<false>(acc, cur, ring_c, z);
+    if (prb) {
+      const long long t1 = probe_clock(prb, acc);
+      pr.fold += t1 - tc0 - twait;
+      tc0 = t1 - twait;
+    }
     // F: publish the row
     if (cur.active) {
       ring[cur.ridx] = acc;
@@ -464,10 +485,22 @@ __device__ __forceinline__ bool level_step(const StepConst& K, Ctl* ctl, uint8_t
     __syncwarp();
     if ((threadIdx.x & 31) == 0) mbar_arrive(&ctl->empty[cur_st]);
   }
+  long long tb0 = 0;
+  if (prb) {
+    tb0 = probe_clock(prb, 0.0);
+    pr.pub += tb0 - tc0 - twait;
+    pr.wait += twait;
+    pr.steps += 1;
+    pr.chunks += chunk_done;
+  }
   if (cur_flags & 1) {
     trace_ev(K, 40, 0);
     consumer_sync();
     trace_ev(K, 41, 0);
+    if (prb) {
+      pr.bar += probe_clock(prb, 0.0) - tb0;
+      pr.levels += 1;
+    }
   }
   return more;
 }
@@ -503,7 +536,19 @@ __device__ void tri_phase(const StepConst& K, const Streams& S, Ctl* ctl, uint8_
   load_row<UPPER>(c.seg, *reinterpret_cast<const int4*>(c.seg), *reinterpret_cast<const int2*>(c.seg + 16),
                   c.rbuf, c.rbase, base, K.ring_mask, K.ring_mask + 1, cadd, row);
   const double* ring_c = ring;
-  while (level_step<UPPER>(K, ctl, stages, rhsbuf, c, row, ring_c, ring, base, z, xout, cadd)) {
+  Probe pr{};
+  while (level_step<UPPER>(K, ctl, stages, rhsbuf, c, row, ring_c, ring, base, z, xout, cadd, pr)) {
+  }
+  if (PSLR_TRACE_BUILD && K.trace && threadIdx.x == 0 && K.trace_cap >= (1 << 20) && blockIdx.x < 2048) {
+    unsigned long long* o = reinterpret_cast<unsigned long long*>(K.trace + 2 + 2 * K.trace_cap - 8 * 4096 +
+                                                                  (2048 + blockIdx.x) * 8);
+    atomicAdd(o + 0, (unsigned long long)pr.wait);
+    atomicAdd(o + 1, (unsigned long long)pr.fold);
+    atomicAdd(o + 2, (unsigned long long)pr.pub);
+    atomicAdd(o + 3, (unsigned long long)pr.bar);
+    atomicAdd(o + 4, (unsigned long long)pr.steps);
+    atomicAdd(o + 5, (unsigned long long)pr.levels);
+    atomicAdd(o + 6, (unsigned long long)pr.chunks);
   }
 }
 

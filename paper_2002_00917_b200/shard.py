@@ -1,0 +1,404 @@
+"""Multi-GPU sharding of the PSLR apply: one process per GPU, each rank owns a
+contiguous range of subdomains.
+
+The reference is single-process (pslr/preconditioner.py); this module is the sharded form
+of its apply (preconditioner.py:79-93), Arnoldi (lowrank.py:39-73) and GMRES
+(krylov.py:35-129).  Everything block-diagonal in Eq. 2.2 - the B and C0 solves, E, F - is
+rank-local.  Ranks exchange data at exactly three kinds of points:
+
+  * halo   - C_g couples interface values of different subdomains.  Each rank stores the
+             remote interface values its C_g rows read as *ghosts* after its q local values
+             ("extended" interface vectors); `Halo.exchange` refreshes them with one batch of
+             point-to-point sends/receives before every operator step that reads C_g
+             (m per apply, m+1 per Arnoldi operator, one per GMRES A-SpMV).
+  * allreduce(r) - the low-rank correction's V^T y.
+  * allreduce(k) - inner products of Arnoldi / GMRES (CGS2 projections, norms).
+
+Subdomain ids from the depth-first bisection are contiguous subtrees (partition.py:103-116),
+so a contiguous id range is a compact region of the mesh and the halo is small.
+
+The orchestration is backend-agnostic: `ShardedPreconditioner` drives a local-operator
+backend (`DeviceShardOps`: the split C-ABI apply pslr_apply_first/mid/horner/last on the
+rank's GPU) through `torch.distributed` collectives (NCCL on GPUs; gloo in the CPU tests,
+which plug in an oracle backend).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+import scipy.sparse as sp
+
+from .ilu import factor_blocks
+from .lowrank import BREAKDOWN_RTOL, LowRankCorrection, _start_vector, build_correction
+from .partition import PartitionedSystem
+from .sparse import canonical
+
+
+# ---------------------------------------------------------------------------- plan
+def subdomain_range(s: int, world: int, rank: int) -> tuple[int, int]:
+    """Rank `rank` owns subdomain ids [lo, hi): contiguous, balanced by count."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank / world size")
+    if s < world:
+        raise ValueError(f"{s} subdomains cannot be sharded over {world} ranks")
+    return rank * s // world, (rank + 1) * s // world
+
+
+@dataclass
+class ShardPlan:
+    rank: int
+    world: int
+    sub_lo: int
+    sub_hi: int
+    int_lo: int            # global interior rows [int_lo, int_hi) of [0, p)
+    int_hi: int
+    ifc_lo: int            # global interface indices [ifc_lo, ifc_hi) of [0, q)
+    ifc_hi: int
+    ghosts: np.ndarray     # global interface indices of the ghosts, grouped by owner rank
+    recv_counts: np.ndarray  # ghosts received from each rank (contiguous, in rank order)
+    send_idx: list         # per rank: local interface indices this rank sends to it
+    local: PartitionedSystem = field(repr=False)  # C and matrix carry the ghost columns
+    C0: sp.csr_matrix = field(repr=False, default=None)
+    Cg: sp.csr_matrix = field(repr=False, default=None)
+
+    @property
+    def q_loc(self) -> int:
+        return self.ifc_hi - self.ifc_lo
+
+    @property
+    def nghost(self) -> int:
+        return int(self.ghosts.size)
+
+    @property
+    def n_loc(self) -> int:
+        return self.local.n
+
+
+def _ranges(ps: PartitionedSystem, world: int):
+    io = np.concatenate([[0], np.cumsum(ps.interior_sizes)]).astype(np.int64)
+    fo = np.concatenate([[0], np.cumsum(ps.interface_sizes)]).astype(np.int64)
+    out = []
+    for r in range(world):
+        lo, hi = subdomain_range(ps.num_parts, world, r)
+        out.append((lo, hi, int(io[lo]), int(io[hi]), int(fo[lo]), int(fo[hi])))
+    return out
+
+
+def _remote_cols(C: sp.csr_matrix, f0: int, f1: int) -> np.ndarray:
+    """Interface columns outside [f0, f1) read by interface rows [f0, f1) of C (sorted)."""
+    blk = C[f0:f1]
+    cols = np.unique(blk.indices)
+    return cols[(cols < f0) | (cols >= f1)].astype(np.int64)
+
+
+def plan_shard(ps: PartitionedSystem, world: int, rank: int) -> ShardPlan:
+    """Local system of `rank` and its halo pattern.  Every rank derives every rank's ghost
+    set from the (replicated) global system, so no collective is needed to set up."""
+    if not hasattr(ps, "num_parts"):  # the oracle's System names it `s`
+        ps = PartitionedSystem(matrix=ps.matrix, perm=ps.perm, num_parts=ps.s, p=ps.p, q=ps.q,
+                               interior_sizes=ps.interior_sizes, interface_sizes=ps.interface_sizes,
+                               B=ps.B, E=ps.E, F=ps.F, C=ps.C)
+    rg = _ranges(ps, world)
+    sub_lo, sub_hi, i0, i1, f0, f1 = rg[rank]
+    owner_of_ifc = np.empty(ps.q, dtype=np.int64)
+    for r, (_, _, _, _, a, b) in enumerate(rg):
+        owner_of_ifc[a:b] = r
+    C = canonical(ps.C)
+    ghosts = _remote_cols(C, f0, f1)
+    ghosts = ghosts[np.lexsort((ghosts, owner_of_ifc[ghosts]))]  # by owner, then index
+    recv_counts = np.bincount(owner_of_ifc[ghosts], minlength=world).astype(np.int64)
+    send_idx = []
+    for r, (_, _, _, _, a, b) in enumerate(rg):
+        if r == rank:
+            send_idx.append(np.zeros(0, dtype=np.int64))
+            continue
+        theirs = _remote_cols(C, a, b)
+        mine = theirs[(theirs >= f0) & (theirs < f1)]  # sorted = their ghost order for me
+        send_idx.append((mine - f0).astype(np.int64))
+    p_loc, q_loc = i1 - i0, f1 - f0
+    # local column map of the reordered matrix: interiors, interfaces, ghosts
+    ncol = np.full(ps.n, -1, dtype=np.int64)
+    ncol[i0:i1] = np.arange(p_loc)
+    ncol[ps.p + f0:ps.p + f1] = p_loc + np.arange(q_loc)
+    ncol[ps.p + ghosts] = p_loc + q_loc + np.arange(ghosts.size)
+    A = canonical(ps.matrix)
+    rows = np.concatenate([np.arange(i0, i1), ps.p + np.arange(f0, f1)])
+    Ar = canonical(A[rows])
+    if np.any(ncol[Ar.indices] < 0):
+        raise ValueError("the reordered matrix couples rows outside the subdomain + halo pattern")
+    n_loc = p_loc + q_loc
+    # Entries keep the global column order inside every row (ghost indices are not sorted
+    # against local ones): it is the reference's summation order (scipy csr_matvec), so the
+    # rank-local SpMVs of the ghost-carrying matrices stay bit-identical to the global ones.
+    A_loc = _ordered_csr(Ar.data, ncol[Ar.indices], Ar.indptr, (n_loc, n_loc + ghosts.size))
+    local = PartitionedSystem(
+        matrix=A_loc, perm=None, num_parts=sub_hi - sub_lo, p=p_loc, q=q_loc,
+        interior_sizes=np.asarray(ps.interior_sizes[sub_lo:sub_hi], dtype=np.int64),
+        interface_sizes=np.asarray(ps.interface_sizes[sub_lo:sub_hi], dtype=np.int64),
+        B=_block(A_loc, 0, p_loc, 0, p_loc),
+        E=_block(A_loc, 0, p_loc, p_loc, n_loc),
+        F=_block(A_loc, p_loc, n_loc, 0, p_loc),
+        C=_block(A_loc, p_loc, n_loc, p_loc, n_loc + ghosts.size),  # q_loc x (q_loc + nghost)
+    )
+    C0, Cg = split_interface(local.C, local.interface_sizes)
+    return ShardPlan(rank=rank, world=world, sub_lo=sub_lo, sub_hi=sub_hi, int_lo=i0, int_hi=i1,
+                     ifc_lo=f0, ifc_hi=f1, ghosts=ghosts, recv_counts=recv_counts, send_idx=send_idx,
+                     local=local, C0=C0, Cg=Cg)
+
+
+def _ordered_csr(data, indices, indptr, shape) -> sp.csr_matrix:
+    """CSR taken as given: entries stay in their order within each row (no sorting)."""
+    M = sp.csr_matrix((np.asarray(data, dtype=np.float64), np.asarray(indices, dtype=np.int32),
+                       np.asarray(indptr, dtype=np.int64)), shape=shape)
+    M.has_sorted_indices = False  # never let scipy reorder the summation order
+    return M
+
+
+def _select(M: sp.csr_matrix, r0: int, r1: int, keep_fn, col_fn, ncols: int) -> sp.csr_matrix:
+    """Rows [r0, r1) of M, the entries keep_fn(cols) selects, columns mapped by col_fn,
+    in their original order."""
+    ip = M.indptr
+    lo, hi = ip[r0], ip[r1]
+    cols = M.indices[lo:hi]
+    rows = np.repeat(np.arange(r1 - r0), np.diff(ip[r0:r1 + 1]))
+    k = keep_fn(cols, rows)
+    counts = np.bincount(rows[k], minlength=r1 - r0)
+    indptr = np.concatenate([[0], np.cumsum(counts)]).astype(np.int64)
+    return _ordered_csr(M.data[lo:hi][k], col_fn(cols[k]), indptr, (r1 - r0, ncols))
+
+
+def _block(M, r0, r1, c0, c1):
+    return _select(M, r0, r1, lambda c, r: (c >= c0) & (c < c1), lambda c: c - c0, c1 - c0)
+
+
+def split_interface(C: sp.csr_matrix, sizes) -> tuple[sp.csr_matrix, sp.csr_matrix]:
+    """C0 = block-diagonal part over the local interface blocks (q x q), Cg = C - C0 keeping
+    the ghost columns (schur.py:41-59 on the extended column space), entry order kept."""
+    q = C.shape[0]
+    block_of = np.repeat(np.arange(len(sizes)), sizes)
+
+    def same(cols, rows):
+        inb = cols < q
+        out = np.zeros(cols.size, dtype=bool)
+        out[inb] = block_of[rows[inb]] == block_of[cols[inb]]
+        return out
+
+    C0 = _select(C, 0, q, same, lambda c: c, q)
+    Cg = _select(C, 0, q, lambda c, r: ~same(c, r), lambda c: c, C.shape[1])
+    return C0, Cg
+
+
+# ---------------------------------------------------------------------------- communication
+class Halo:
+    """Ghost exchange + reductions over a torch.distributed process group."""
+
+    def __init__(self, plan: ShardPlan, device, group=None):
+        import torch
+        import torch.distributed as dist
+        self.t, self.dist, self.group = torch, dist, group
+        self.plan = plan
+        self.q = plan.q_loc
+        self.peers_send = [(r, torch.as_tensor(ix, device=device)) for r, ix in enumerate(plan.send_idx)
+                           if ix.size]
+        off = np.concatenate([[0], np.cumsum(plan.recv_counts)])
+        self.peers_recv = [(r, int(off[r]), int(plan.recv_counts[r])) for r in range(plan.world)
+                           if plan.recv_counts[r]]
+
+    def _peer(self, r):
+        return r if self.group is None else self.dist.get_global_rank(self.group, r)
+
+    def exchange(self, v_ext):
+        """Fill v_ext[q:] (the ghosts) with the owners' current values of v_ext[:q]."""
+        if not self.peers_send and not self.peers_recv:
+            return v_ext
+        ops, bufs = [], []
+        for r, ix in self.peers_send:
+            buf = v_ext[:self.q].index_select(0, ix)
+            bufs.append(buf)
+            ops.append(self.dist.P2POp(self.dist.isend, buf, self._peer(r), self.group))
+        for r, off, cnt in self.peers_recv:
+            ops.append(self.dist.P2POp(self.dist.irecv, v_ext[self.q + off:self.q + off + cnt],
+                                       self._peer(r), self.group))
+        for w in self.dist.batch_isend_irecv(ops):
+            w.wait()
+        return v_ext
+
+    def allreduce(self, x):
+        if self.plan.world > 1:
+            self.dist.all_reduce(x, group=self.group)
+        return x
+
+    def dot(self, a, b):
+        d = (a * b).sum().reshape(1)
+        return self.allreduce(d)
+
+
+# ---------------------------------------------------------------------------- device backend
+class DeviceShardOps:
+    """Rank-local operators of the split apply on this rank's GPU (libpslr.so)."""
+
+    def __init__(self, plan: ShardPlan, droptol=1e-2, fill_cap=None, device=None):
+        from .device import DeviceContext, require_cuda
+        t = require_cuda()
+        ps = plan.local
+        self.plan = plan
+        self.b_ilu = factor_blocks(ps.B, ps.interior_sizes, droptol=droptol, fill_cap=fill_cap)
+        self.c0_ilu = factor_blocks(plan.C0, ps.interface_sizes, droptol=droptol, fill_cap=fill_cap)
+        self.dev = DeviceContext(ps, self.b_ilu, self.c0_ilu, plan.C0, plan.Cg, device=device)
+        self.t = t
+        self.device = self.dev.dev
+        self.n, self.p, self.q, self.ng = ps.n, ps.p, ps.q, plan.nghost
+        self.r = 0
+
+    def _call(self, name, *args):
+        from . import _lib
+        _lib.check(_lib.fns[name](self.dev.handle, *args, self.dev.stream()))
+
+    def vec(self, n):
+        return self.t.empty(n, dtype=self.t.float64, device=self.device)
+
+    def zeros(self, n):
+        return self.t.zeros(n, dtype=self.t.float64, device=self.device)
+
+    def set_correction(self, V_loc, G):
+        self.dev.set_correction(V_loc, G)
+        self.r = int(G.shape[0])
+
+    def first(self, b):
+        y0 = self.vec(self.q)
+        s = self.zeros(max(self.r, 1))
+        self._call("pslr_apply_first", b.data_ptr(), y0.data_ptr(), s.data_ptr())
+        return y0, s[:self.r]
+
+    def mid(self, y0, s):
+        c = self.zeros(self.q + self.ng)
+        sp_ = s if self.r else self.zeros(1)
+        self._call("pslr_apply_mid", y0.data_ptr(), sp_.data_ptr(), c.data_ptr())
+        return c
+
+    def horner(self, y_ext, c):
+        out = self.zeros(self.q + self.ng)
+        self._call("pslr_apply_horner", y_ext.data_ptr(), c.data_ptr(), out.data_ptr())
+        return out
+
+    def last(self, b, y):
+        z = self.vec(self.n)
+        self._call("pslr_apply_last", b.data_ptr(), y.data_ptr(), z.data_ptr())
+        return z
+
+    def solve_C0(self, g):
+        out = self.zeros(self.q + self.ng)
+        self._call("pslr_solve_C0", g.data_ptr(), out.data_ptr())
+        return out
+
+    def es_step(self, v_ext, do_c0):
+        out = self.zeros(self.q + self.ng)
+        from . import _lib
+        _lib.check(_lib.fns["pslr_apply_es_step"](self.dev.handle, v_ext.data_ptr(), out.data_ptr(),
+                                                  int(do_c0), self.dev.stream()))
+        return out
+
+    def spmv_A(self, x_ext):
+        y = self.vec(self.n)
+        from . import _lib
+        _lib.check(_lib.fns["pslr_spmv"](self.dev.handle, 0, x_ext.data_ptr(), y.data_ptr(),
+                                         self.dev.stream()))
+        return y
+
+
+# ---------------------------------------------------------------------------- sharded algorithms
+def sharded_arnoldi(ops, halo: Halo, q_global: int, ifc_lo: int, m: int, rank: int, seed: int = 0):
+    """lowrank.py:39-73 on E_rr(m) (schur.py:104-112) with the rank's rows of V: CGS2
+    projections and norms are allreduced, every operator step refreshes the ghosts first.
+    Returns (V_loc q_loc x r, H r x r numpy (identical on every rank), r)."""
+    t = halo.t
+    q = ops.q
+    rank = min(int(rank), q_global)
+    if rank == 0:
+        return ops.zeros(q * 0).reshape(q, 0), np.zeros((0, 0)), 0
+    v0 = _start_vector(q_global, seed)[ifc_lo:ifc_lo + q]  # the rank's rows of the global draw
+    V = t.zeros((rank + 1, q), dtype=t.float64, device=ops.device)  # rows = basis vectors
+    V[0] = t.as_tensor(np.ascontiguousarray(v0), device=ops.device)
+    Hbar = np.zeros((rank + 1, rank))
+    r = rank
+
+    def op(v):
+        src = ops.solve_C0(v)
+        for k in range(1, m + 2):
+            halo.exchange(src)
+            src = ops.es_step(src, do_c0=(k != m + 1))
+        return src[:q]
+
+    for j in range(rank):
+        w = op(V[j].clone())
+        Vj = V[:j + 1]
+        h = halo.allreduce(Vj @ w)
+        w = w - h @ Vj
+        h2 = halo.allreduce(Vj @ w)
+        w = w - h2 @ Vj
+        hh = (h + h2).cpu().numpy()
+        Hbar[:j + 1, j] = hh
+        nrm = float(halo.dot(w, w).sqrt().item())
+        Hbar[j + 1, j] = nrm
+        if nrm <= BREAKDOWN_RTOL:
+            r = j + 1
+            break
+        V[j + 1] = w / nrm
+    return V[:r].T.contiguous(), np.ascontiguousarray(Hbar[:r, :r]), r
+
+
+class ShardedPreconditioner:
+    """The PSLR apply on the rank's rows (preconditioner.py:79-93): b_loc = [f_loc; g_loc]
+    in the rank's local order (interiors, then interfaces)."""
+
+    def __init__(self, plan: ShardPlan, ops, halo: Halo, series_degree: int, correction=None):
+        self.plan, self.ops, self.halo = plan, ops, halo
+        self.series_degree = int(series_degree)
+        self.correction = correction
+
+    def apply(self, b):
+        ops, halo, m = self.ops, self.halo, self.series_degree
+        if b.shape[0] != ops.n:
+            raise ValueError(f"vector has length {b.shape[0]}, local system has {ops.n}")
+        if ops.q == 0 and self.plan.world == 1:
+            return ops.last(b, ops.zeros(0))
+        y0, s = ops.first(b)
+        if ops.r:
+            halo.allreduce(s)
+        c = ops.mid(y0, s)
+        y = c
+        if m > 0:
+            halo.exchange(c)
+            for k in range(m):
+                out = ops.horner(y, c)
+                if k < m - 1:
+                    halo.exchange(out)
+                y = out
+        return ops.last(b, y[:ops.q].contiguous())
+
+
+def build_sharded(ps: PartitionedSystem, cfg, group=None, device=None):
+    """Rank-local part of build() (preconditioner.py:120-141) for the calling rank of the
+    default (or given) process group."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
+    rank = dist.get_rank(group) if dist.is_initialized() else 0
+    plan = plan_shard(ps, world, rank)
+    ops = DeviceShardOps(plan, droptol=cfg.droptol, fill_cap=cfg.fill_cap, device=device)
+    halo = Halo(plan, ops.device, group)
+    Vl, H, r = sharded_arnoldi(ops, halo, ps.q, plan.ifc_lo, cfg.series_degree,
+                               min(cfg.rank, ps.q), seed=cfg.seed)
+    corr = build_correction(np.zeros((0, r)), H) if r else LowRankCorrection(
+        V=np.zeros((0, 0)), H=H, G=np.zeros((0, 0)), rank=0)
+    if r:
+        ops.set_correction(Vl, corr.G)
+    return ShardedPreconditioner(plan, ops, halo, cfg.series_degree, corr)
+
+
+def local_rows(plan: ShardPlan, p_global: int) -> np.ndarray:
+    """Global (reordered) row indices of the rank's local vector, in local order."""
+    return np.concatenate([np.arange(plan.int_lo, plan.int_hi),
+                           p_global + np.arange(plan.ifc_lo, plan.ifc_hi)]).astype(np.int64)

@@ -1,0 +1,115 @@
+"""GPU: the split apply of a sharded context (pslr_apply_first/mid/horner/last with ghost
+columns) against the fused single-context apply.  The ranks of a 2- and 4-way sharding run
+in lockstep in this one process on one GPU; their halo exchanges are host-ordered copies
+between the ranks' tensors (no kernel waits on another rank's kernel).  The process-group
+form of the same orchestration is covered on CPU by tests/test_shard.py (gloo).
+
+Bars: bit-exact with the correction off (every rank-local operation is the single-context
+operation on the same rows); 1e-12 relative with rank r > 0 (V^T y sums per rank, then
+across ranks)."""
+import numpy as np
+import pytest
+
+from conftest import have_cuda
+
+pytestmark = [pytest.mark.gpu, pytest.mark.skipif(not have_cuda(), reason="needs a CUDA device")]
+
+
+class LocalHalo:
+    """Ghost refresh for ranks living in one process (host-ordered device copies)."""
+
+    def __init__(self, plans, device):
+        import torch
+        self.t = torch
+        self.plans = plans
+        self.recv_off = [np.concatenate([[0], np.cumsum(p.recv_counts)]) for p in plans]
+        self.send = [[torch.as_tensor(ix, device=device) for ix in p.send_idx] for p in plans]
+
+    def exchange(self, vecs):
+        for h, ph in enumerate(self.plans):
+            for r, pr in enumerate(self.plans):
+                if r == h or not ph.recv_counts[r]:
+                    continue
+                a, b = self.recv_off[h][r], self.recv_off[h][r + 1]
+                vals = vecs[r][:pr.q_loc].index_select(0, self.send[r][h])
+                vecs[h][ph.q_loc + a:ph.q_loc + b] = vals
+
+
+def _lockstep_apply(plans, ops, halo, b, p_global, m):
+    import torch
+    from paper_2002_00917_b200 import shard
+    bl = [b[torch.as_tensor(shard.local_rows(pl, p_global), device=b.device)].contiguous() for pl in plans]
+    first = [o.first(x) for o, x in zip(ops, bl)]
+    s = sum(f[1] for f in first) if ops[0].r else None
+    c = [o.mid(f[0], s.clone() if s is not None else f[1]) for o, f in zip(ops, first)]
+    y = c
+    if m > 0:
+        halo.exchange(c)
+        for k in range(m):
+            out = [o.horner(yy, cc) for o, yy, cc in zip(ops, y, c)]
+            if k < m - 1:
+                halo.exchange(out)
+            y = out
+    z = torch.empty_like(b)
+    for pl, o, x, yy in zip(plans, ops, bl, y):
+        z[torch.as_tensor(shard.local_rows(pl, p_global), device=b.device)] = o.last(x, yy[:o.q].contiguous())
+    return z
+
+
+@pytest.mark.parametrize("world", [1, 2, 4])
+@pytest.mark.parametrize("with_corr", [False, True])
+def test_split_apply_matches_fused(world, with_corr):
+    import torch
+    import paper_2002_00917_b200 as pg
+    from paper_2002_00917_b200 import shard, workloads
+    A = workloads.laplacian3d(14, 14, 14, 0.5)
+    m = 3
+    cfg = pg.PslrConfig(num_subdomains=8, series_degree=m, rank=8 if with_corr else 0, droptol=1e-2, seed=0)
+    P = pg.build(A, cfg)
+    ps = P.system
+    plans = [shard.plan_shard(ps, world, r) for r in range(world)]
+    ops = [shard.DeviceShardOps(pl) for pl in plans]
+    if with_corr:
+        V, G = np.asarray(P.correction.V), P.correction.G
+        for pl, o in zip(plans, ops):
+            o.set_correction(torch.as_tensor(np.ascontiguousarray(V[pl.ifc_lo:pl.ifc_hi]), device="cuda"), G)
+    halo = LocalHalo(plans, "cuda")
+    b = torch.as_tensor(np.random.default_rng(5).standard_normal(ps.n), device="cuda")
+    z = _lockstep_apply(plans, ops, halo, b, ps.p, m).cpu().numpy()
+    z_ref = P.apply(b).cpu().numpy()
+    if with_corr:
+        assert np.linalg.norm(z - z_ref) <= 1e-12 * np.linalg.norm(z_ref)
+    else:
+        np.testing.assert_array_equal(z, z_ref)
+    if world > 1:
+        assert sum(pl.nghost for pl in plans) > 0  # the halo was exercised
+
+
+def test_sharded_arnoldi_matches_build():
+    """sharded_arnoldi over a 1-rank 'process group' of the local halo type == the device
+    Arnoldi of build() (same operator, CGS2 order; sums differ only in rounding)."""
+    import torch
+    import paper_2002_00917_b200 as pg
+    from paper_2002_00917_b200 import shard, workloads
+    A = workloads.laplacian3d(12, 12, 12, 0.5)
+    cfg = pg.PslrConfig(num_subdomains=4, series_degree=3, rank=6, droptol=1e-2, seed=0)
+    P = pg.build(A, cfg)
+    plan = shard.plan_shard(P.system, 1, 0)
+    ops = shard.DeviceShardOps(plan)
+
+    class OneRank:
+        t = torch
+
+        def exchange(self, v):
+            return v
+
+        def allreduce(self, x):
+            return x
+
+        def dot(self, a, b):
+            return (a * b).sum().reshape(1)
+
+    V, H, r = shard.sharded_arnoldi(ops, OneRank(), P.system.q, 0, 3, 6, seed=0)
+    assert r == P.correction.rank
+    assert np.allclose(H, P.correction.H, rtol=1e-9, atol=1e-12)
+    assert np.allclose(V.cpu().numpy(), np.asarray(P.correction.V), rtol=1e-8, atol=1e-10)
