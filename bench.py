@@ -5,7 +5,8 @@ Workload (N=1): BASELINE config 5, the preconditioner-apply sweep — a 128^3 bl
 3D 7-point Laplacian (diagonal 6, shift 0.5), 32 subdomains, m=3, rank 64, fp64, applied
 to seeded N(0,1) vectors (8 pre-generated, cycled).  One step = one PSLR apply
 (Alg. 3.2, preconditioner.py:79-93) of one vector.  Under torchrun each rank applies its
-own 128^3 block (weak scaling, replicas in round 1).
+own 128^3 slab of ONE coupled global problem (grid 128 x 128 x 128N, s = 32N; subdomain
+sharding with NCCL halo exchanges, weak scaling; see run_sharded and DESIGN.md §Multi-GPU).
 
   value   : algorithmic GB/s over all ranks = N * bytes_apply * K / max-over-ranks time
   e2e     : same metric through the C-ABI host-buffer call (pslr_apply_host: pinned H2D
@@ -22,6 +23,9 @@ import os
 _NCPU = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
 for _v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
     os.environ.setdefault(_v, str(_NCPU))
+# the JSON line must be the only stdout output: NCCL's own log lines go to stderr
+os.environ.setdefault("NCCL_DEBUG", "WARN")
+os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
 
 import argparse  # noqa: E402
 import json  # noqa: E402
@@ -49,6 +53,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=100)
     ap.add_argument("--cpu-applies", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--sharded", action="store_true",
+                    help="run the sharded (multi-GPU) path even at N=1 (testing the NCCL path)")
     return ap.parse_args()
 
 
@@ -196,6 +202,118 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def run_sharded(args, rank, world, local):
+    """N > 1: config 5 as one coupled problem sharded over the ranks:
+    the 128 x 128 x (128 N) grid, s = 32 N subdomains, rank g owns subdomains
+    [32 g, 32 (g+1)) (a 128^3 slab).  Per apply: m halo exchanges for C_g and one
+    r-double allreduce (NCCL), everything else rank-local.  Weak scaling: per-GPU work is
+    one 128^3 slab at every N."""
+    import torch
+    import torch.distributed as dist
+    from paper_2002_00917_b200 import shard, workloads
+    from paper_2002_00917_b200.partition import classify_and_reorder, partition_graph
+
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dist.barrier()
+    base = workloads.CONFIGS[args.config]
+    nx, ny, nz = base.grid
+    t0 = time.perf_counter()
+    A = workloads.laplacian3d(nx, ny, nz * world, base.shift)
+    s_glob = base.s * world
+    spec = partition_graph(A, s_glob, seed=0)
+    ps = classify_and_reorder(A, spec)
+    cfg = __import__("paper_2002_00917_b200").PslrConfig(num_subdomains=s_glob, series_degree=base.m,
+                                                         rank=base.rank, droptol=1e-2, seed=0)
+    P = shard.build_sharded(ps, cfg, device=local)
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t0
+    plan, ops = P.plan, P.ops
+    info = ops.dev.info()
+    m, r = base.m, int(P.correction.rank)
+    bytes_local = algorithmic_bytes(info, m, r, plan.n_loc)
+    tb = torch.tensor([float(bytes_local)], device="cuda", dtype=torch.float64)
+    dist.all_reduce(tb)
+    bytes_apply = float(tb.item())
+    rows = torch.as_tensor(shard.local_rows(plan, ps.p), device="cuda")
+    rng = np.random.default_rng(0)
+    vecs = []
+    for _ in range(8):
+        g = torch.as_tensor(rng.standard_normal(ps.n), device="cuda")
+        vecs.append(g[rows].contiguous())
+    stream = torch.cuda.current_stream()
+    for k in range(max(3, args.warmup)):
+        P.apply(vecs[k % 8])
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for k in range(args.steps):
+        P.apply(vecs[k % 8])
+    e1.record(stream)
+    torch.cuda.synchronize()
+    dist.barrier()
+    ms = e0.elapsed_time(e1)
+    clk = clocks.stop()
+    tt = torch.tensor([ms], device="cuda", dtype=torch.float64)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    ms = float(tt.item())
+    value = bytes_apply * args.steps / (ms / 1e3) / 1e9
+    # e2e: host (pinned) b -> device, sharded apply, z -> host, every step
+    bh = vecs[0].cpu().pin_memory()
+    zh = torch.empty_like(bh).pin_memory()
+    for _ in range(3):
+        zh.copy_(P.apply(bh.to("cuda", non_blocking=True)), non_blocking=True)
+    dist.barrier()
+    torch.cuda.synchronize()
+    e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e2.record(stream)
+    for _ in range(args.e2e_steps):
+        bd = bh.to("cuda", non_blocking=True)
+        zh.copy_(P.apply(bd), non_blocking=True)
+    e3.record(stream)
+    torch.cuda.synchronize()
+    ms_e2e = e2.elapsed_time(e3)
+    tt = torch.tensor([ms_e2e], device="cuda", dtype=torch.float64)
+    dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+    ms_e2e = float(tt.item())
+    peak, peak_src = hbm_peak()
+    per_gpu = bytes_local / (ms / args.steps / 1e3) / 1e9
+    nghost = torch.tensor([float(plan.nghost)], device="cuda", dtype=torch.float64)
+    dist.all_reduce(nghost, op=dist.ReduceOp.MAX)
+    if rank == 0:
+        line = {
+            "metric": "PSLR apply GB/s", "value": value, "unit": "GB/s", "n_gpus": world,
+            "steps": args.steps, "warmup": max(3, args.warmup), "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": f"{base.name} sharded: 3D 7-point Laplacian {nx}x{ny}x{nz * world} "
+                                   f"shift {base.shift}, s={s_glob} ({base.s} per GPU), m={m}, rank={r}; "
+                                   "one step = one PSLR apply of the global system",
+                       "n": int(ps.n), "n_per_gpu_rank0": int(plan.n_loc),
+                       "bytes_per_apply": int(bytes_apply),
+                       "parallelism": f"subdomain sharding x{world} (NCCL: {m} halo exchanges + 1 "
+                                      f"allreduce({r}) per apply; max ghosts/rank {int(nghost.item())})",
+                       "l2": "no flush: each apply streams %.2f GB per GPU (> 126 MB L2)" % (bytes_local / 1e9),
+                       "build_s": round(build_s, 2)},
+            "roofline": {"bound": "hbm", "kernel": "whole sharded apply on rank 0 (all launches + halo)",
+                         "achieved": per_gpu, "peak": peak, "unit": "GB/s", "frac": per_gpu / peak,
+                         "traffic": None, "peak_source": peak_src},
+            "cpu_baseline": None,
+            "e2e": {"value": bytes_apply * args.e2e_steps / (ms_e2e / 1e3) / 1e9, "unit": "GB/s",
+                    "h2d_bytes_per_step": 8 * int(plan.n_loc), "d2h_bytes_per_step": 8 * int(plan.n_loc),
+                    "ms_per_step": ms_e2e / args.e2e_steps},
+            "gpu_launches": (m + 6) * args.steps,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    dist.destroy_process_group()
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
@@ -206,6 +324,13 @@ def main():
             run_reference(args)
         return
 
+    if world > 1 or args.sharded:
+        if world == 1:
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29533")
+            os.environ.setdefault("RANK", "0")
+            os.environ.setdefault("WORLD_SIZE", "1")
+        return run_sharded(args, rank, world, local)
     import torch
     import paper_2002_00917_b200 as pg
     from paper_2002_00917_b200 import _lib
