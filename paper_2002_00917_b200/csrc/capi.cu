@@ -409,14 +409,20 @@ int pslr_ctx_create(pslr_ctx** out, int device, const pslr_system* sys) {
     }
     if ((rc = upload(ctx, io, &ctx->K.int_off))) return bail(rc);
     if ((rc = upload(ctx, fo, &ctx->K.ifc_off))) return bail(rc);
-    // interior rows that carry E entries (~30% on the stencil configs), per block
+    // interior rows that carry E entries (~30% on the stencil configs), per block, as
+    // {L-position, row, E row start, E row end}: one 16-B load per row in the prepass
     std::vector<int32_t> er, eo(s + 1, 0);
     for (int64_t b = 0; b < s; ++b) {
       for (int64_t i = ctx->interior_off[b]; i < ctx->interior_off[b + 1]; ++i)
-        if (sys->E.indptr[i + 1] > sys->E.indptr[i]) er.push_back((int32_t)i);
-      eo[b + 1] = (int32_t)er.size();
+        if (sys->E.indptr[i + 1] > sys->E.indptr[i]) {
+          er.push_back(aLB.pos_of_row[i]);
+          er.push_back((int32_t)i);
+          er.push_back((int32_t)sys->E.indptr[i]);
+          er.push_back((int32_t)sys->E.indptr[i + 1]);
+        }
+      eo[b + 1] = (int32_t)(er.size() / 4);
     }
-    if (er.empty()) er.push_back(0);
+    if (er.empty()) er.assign(4, 0);
     if ((rc = upload(ctx, er, &ctx->K.erows))) return bail(rc);
     if ((rc = upload(ctx, eo, &ctx->K.erow_off))) return bail(rc);
   }

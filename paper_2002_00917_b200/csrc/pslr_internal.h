@@ -108,7 +108,8 @@ struct StepConst {
   DevCsr E, F, C, Cg;
   const int32_t* int_off = nullptr;
   const int32_t* ifc_off = nullptr;
-  const int32_t* erows = nullptr;     // interior rows with E entries, grouped by block
+  const int32_t* erows = nullptr;     // int4 per interior row with E entries, grouped by block:
+                                      // {L-position, row, E.ptr[row], E.ptr[row+1]}
   const int32_t* erow_off = nullptr;  // s+1
   const double* V = nullptr;
   int r = 0;

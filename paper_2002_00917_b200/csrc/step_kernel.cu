@@ -134,6 +134,23 @@ __device__ __forceinline__ void trace_ev(const StepConst& K, int code, int arg) 
   }
 }
 
+// =3 builds: one (code|arg, clock64) record per level-loop step, cheap enough (no
+// %globaltimer) to time individual levels in cycles
+__device__ __forceinline__ void trace_clk(const StepConst& K, int code, int arg) {
+  if (PSLR_TRACE_BUILD == 3 && K.trace && blockIdx.x == 0 && threadIdx.x == 0 && g_trace_ptr &&
+      g_trace_n < kTraceWindow) {
+    g_trace_ptr[2 * g_trace_n] = ((long long)code << 32) | (unsigned)arg;
+    g_trace_ptr[2 * g_trace_n + 1] = clock64();
+    ++g_trace_n;
+  }
+}
+
+// per-chunk / per-level events: only in PSLR_TRACE_BUILD=2 builds (they perturb the level
+// loop's timing; =1 records the phase boundaries only)
+__device__ __forceinline__ void trace_fine(const StepConst& K, int code, int arg) {
+  if (PSLR_TRACE_BUILD >= 2) trace_ev(K, code, arg);
+}
+
 // Shared-memory control block
 struct Ctl {
   uint64_t full[8];       // data + rhs landed (2 arrivals + tx bytes)
@@ -291,7 +308,7 @@ __device__ void producer(const Streams& S, Ctl* ctl, uint8_t* stages, double* rh
 // thread tb + t owns row t (tb = flags >> 8), so the segments of one level run side by side.
 struct Row {
   const uint8_t* slots;  // &slot[0][t]
-  int bytes, flags, G, S;
+  int bytes, flags, G, S, nrows;
   bool wact;             // the warp owns rows of this segment (warp-uniform)
   bool active;           // this lane owns a row
   int ridx;              // ring slot of the row
@@ -312,6 +329,7 @@ __device__ __forceinline__ void load_row(const uint8_t* seg, const int4 h0, cons
   r.flags = h0.z;
   r.S = S;
   r.G = G;
+  r.nrows = h0.x;
   r.bytes = h1.y;
   // warps owning no row of the segment skip it entirely (the four schedulers are shared
   // by all 16 consumer warps, so idle warps must not spend issue slots)
@@ -350,7 +368,11 @@ __device__ __forceinline__ void load_row(const uint8_t* seg, const int4 h0, cons
 // dependency value: near -> ring slot, far (sign bit) -> global position-ordered array
 template <bool FAR>
 __device__ __forceinline__ double gather(const double* ring, const double* z, int sl) {
+#ifdef PSLR_DBG_NOFAR  // timing experiment only: far dependencies read a ring slot (wrong values)
+  return FAR ? ring[sl & 4095] : ring[sl];
+#else
   return FAR ? ((sl >= 0) ? ring[sl] : z[sl & 0x7fffffff]) : ring[sl];
+#endif
 }
 
 // acc -= val_k * z_k over the row's groups in the reference's ascending-column order
@@ -391,18 +413,6 @@ __device__ __forceinline__ double fold_row(double acc, const Row& r, const doubl
   return acc;
 }
 
-// trace builds: thread 0's cycles in the parts of the level loop (rows 2048 + b of the
-// trace buffer's counter area): chunk waits, fold, publish + next-row loads, barrier
-struct Probe {
-  long long t, wait, fold, pub, bar, steps, levels, chunks;
-};
-__device__ __forceinline__ long long probe_clock(bool on, double dep) {
-  // the compare consumes dep, so the clock is read after the value is available
-  if (!on) return 0;
-  if (dep == -1.2345e-300) asm volatile("trap;");
-  return clock64();
-}
-
 struct Cursor {
   int u, u1, st, nst, si, nseg, rbase;
   uint32_t par;
@@ -414,10 +424,8 @@ template <bool UPPER>
 __device__ __forceinline__ bool level_step(const StepConst& K, Ctl* ctl, uint8_t* stages, double* rhsbuf,
                                            Cursor& c, Row& cur, const double* ring_c,
                                            double* ring, int base, double* z, double* xout,
-                                           const double* cadd, Probe& pr) {
+                                           const double* cadd) {
   const int mask = K.ring_mask, zslot = K.ring_mask + 1;
-  const bool prb = PSLR_TRACE_BUILD && K.trace && threadIdx.x == 0;
-  long long tc0 = probe_clock(prb, 0.0), twait = 0;
   // C: locate the next segment (next chunk: wait for it; it is normally staged already)
   //    and issue its header loads, so they are in flight while this row is computed
   const uint8_t* nseg_ptr = c.seg + cur.bytes;
@@ -432,11 +440,9 @@ __device__ __forceinline__ bool level_step(const StepConst& K, Ctl* ctl, uint8_t
         c.st = 0;
         c.par ^= 1u;
       }
-      trace_ev(K, 19, c.u);
-      const long long tw0 = probe_clock(prb, 0.0);
+      trace_fine(K, 19, c.u);
       mbar_wait(&ctl->full[c.st], c.par);
-      twait = probe_clock(prb, 0.0) - tw0;
-      trace_ev(K, 20, c.u);
+      trace_fine(K, 20, c.u);
       nseg_ptr = stages + (size_t)c.st * K.stage_bytes;
       c.rbuf = rhsbuf + (size_t)c.st * K.rhs_stride;
       c.nseg = reinterpret_cast<const int32_t*>(nseg_ptr)[6];
@@ -461,11 +467,6 @@ __device__ __forceinline__ bool level_step(const StepConst& K, Ctl* ctl, uint8_t
     }
     // A + D: gathers and the chain
     acc = (cur.flags & 2) ? fold_row<true>(acc, cur, ring_c, z) : fold_row<false>(acc, cur, ring_c, z);
-    if (prb) {
-      const long long t1 = probe_clock(prb, acc);
-      pr.fold += t1 - tc0 - twait;
-      tc0 = t1 - twait;
-    }
     // F: publish the row
     if (cur.active) {
       ring[cur.ridx] = acc;
@@ -478,6 +479,7 @@ __device__ __forceinline__ bool level_step(const StepConst& K, Ctl* ctl, uint8_t
     }
   }
   const int cur_flags = cur.flags;
+  const int cur_info = (cur.G << 2) | (cur.nrows << 8);
   // E: the next segment's row, loaded in place (everything it needs before its gathers)
   if (more) load_row<UPPER>(nseg_ptr, nh0, nh1, c.rbuf, c.rbase, base, mask, zslot, cadd, cur);
   c.seg = nseg_ptr;
@@ -485,23 +487,12 @@ __device__ __forceinline__ bool level_step(const StepConst& K, Ctl* ctl, uint8_t
     __syncwarp();
     if ((threadIdx.x & 31) == 0) mbar_arrive(&ctl->empty[cur_st]);
   }
-  long long tb0 = 0;
-  if (prb) {
-    tb0 = probe_clock(prb, 0.0);
-    pr.pub += tb0 - tc0 - twait;
-    pr.wait += twait;
-    pr.steps += 1;
-    pr.chunks += chunk_done;
-  }
   if (cur_flags & 1) {
-    trace_ev(K, 40, 0);
+    trace_fine(K, 40, 0);
     consumer_sync();
-    trace_ev(K, 41, 0);
-    if (prb) {
-      pr.bar += probe_clock(prb, 0.0) - tb0;
-      pr.levels += 1;
-    }
+    trace_fine(K, 41, 0);
   }
+  trace_clk(K, 50, (cur_flags & 1) | (chunk_done ? 2 : 0) | cur_info);
   return more;
 }
 
@@ -526,7 +517,7 @@ __device__ void tri_phase(const StepConst& K, const Streams& S, Ctl* ctl, uint8_
   c.st = c.u % c.nst;
   c.par = (uint32_t)((c.u / c.nst) & 1);
   mbar_wait(&ctl->full[c.st], c.par);
-  trace_ev(K, 20, c.u);
+  trace_fine(K, 20, c.u);
   c.seg = stages + (size_t)c.st * K.stage_bytes;
   c.rbuf = rhsbuf + (size_t)c.st * K.rhs_stride;
   c.nseg = reinterpret_cast<const int32_t*>(c.seg)[6];
@@ -536,19 +527,7 @@ __device__ void tri_phase(const StepConst& K, const Streams& S, Ctl* ctl, uint8_
   load_row<UPPER>(c.seg, *reinterpret_cast<const int4*>(c.seg), *reinterpret_cast<const int2*>(c.seg + 16),
                   c.rbuf, c.rbase, base, K.ring_mask, K.ring_mask + 1, cadd, row);
   const double* ring_c = ring;
-  Probe pr{};
-  while (level_step<UPPER>(K, ctl, stages, rhsbuf, c, row, ring_c, ring, base, z, xout, cadd, pr)) {
-  }
-  if (PSLR_TRACE_BUILD && K.trace && threadIdx.x == 0 && K.trace_cap >= (1 << 20) && blockIdx.x < 2048) {
-    unsigned long long* o = reinterpret_cast<unsigned long long*>(K.trace + 2 + 2 * K.trace_cap - 8 * 4096 +
-                                                                  (2048 + blockIdx.x) * 8);
-    atomicAdd(o + 0, (unsigned long long)pr.wait);
-    atomicAdd(o + 1, (unsigned long long)pr.fold);
-    atomicAdd(o + 2, (unsigned long long)pr.pub);
-    atomicAdd(o + 3, (unsigned long long)pr.bar);
-    atomicAdd(o + 4, (unsigned long long)pr.steps);
-    atomicAdd(o + 5, (unsigned long long)pr.levels);
-    atomicAdd(o + 6, (unsigned long long)pr.chunks);
+  while (level_step<UPPER>(K, ctl, stages, rhsbuf, c, row, ring_c, ring, base, z, xout, cadd)) {
   }
 }
 
@@ -685,27 +664,44 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
     } else {
       for (int p = r0 + tid; p < r1; p += kStepThreads) K.rhsB[p] = 0.0;
     }
-    // pass 2: rows with E entries get the E y term: f - E y, or E y alone
+    // pass 2: rows with E entries get the E y term: f - E y, or E y alone (scipy
+    // csr_matvec order), kIn rows per thread in flight; one int4 record per row
     if (a.b1 == BT_EY || a.b2 == BT_EY) {
       consumer_sync();
+      constexpr int kIn = 4;
       const int e0 = K.erow_off[b], e1 = K.erow_off[b + 1];
-      for (int i0 = e0 + tid; i0 < e1; i0 += 4 * kStepThreads) {
-        int row[4];
-        bool ok[4];
+      const int4* rec = reinterpret_cast<const int4*>(K.erows);
+      for (int i0 = e0 + tid; i0 < e1; i0 += kIn * kStepThreads) {
+        int4 r[kIn];
+        double fv[kIn], sum[kIn];
+        int len = 0;
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
+        for (int j = 0; j < kIn; ++j) {
           const int i = i0 + j * kStepThreads;
-          ok[j] = i < e1;
-          row[j] = ok[j] ? __ldg(K.erows + i) : 0;
+          r[j] = i < e1 ? __ldg(rec + i) : make_int4(0, 0, 0, 0);
+          len = max(len, r[j].w - r[j].z);
+          sum[j] = 0.0;
         }
-        double s[4];
-        spmv4<true>(K.E, row, ok, a.yE, s);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          if (!ok[j]) continue;
-          const double v = (a.b1 == BT_F) ? (__ldg(a.f + row[j]) - s[j]) : s[j];
-          K.rhsB[__ldg(K.LB.lpos + row[j])] = v;
+        for (int j = 0; j < kIn; ++j) fv[j] = (a.b1 == BT_F && r[j].w > r[j].z) ? __ldg(a.f + r[j].y) : 0.0;
+        for (int k = 0; k < len; ++k) {
+          int c[kIn];
+          double v[kIn], yv[kIn];
+#pragma unroll
+          for (int j = 0; j < kIn; ++j) {
+            const bool on = r[j].z + k < r[j].w;
+            c[j] = on ? __ldg(K.E.col + r[j].z + k) : 0;
+            v[j] = on ? __ldg(K.E.val + r[j].z + k) : 0.0;
+          }
+#pragma unroll
+          for (int j = 0; j < kIn; ++j) yv[j] = (r[j].z + k < r[j].w) ? __ldg(a.yE + c[j]) : 0.0;
+#pragma unroll
+          for (int j = 0; j < kIn; ++j)
+            if (r[j].z + k < r[j].w) sum[j] = sum[j] + v[j] * yv[j];
         }
+#pragma unroll
+        for (int j = 0; j < kIn; ++j)
+          if (i0 + j * kStepThreads < e1) K.rhsB[r[j].x] = (a.b1 == BT_F) ? (fv[j] - sum[j]) : sum[j];
       }
     }
     consumer_sync();

@@ -386,6 +386,8 @@ def build_sharded(ps: PartitionedSystem, cfg, group=None, device=None):
     import torch.distributed as dist
     world = dist.get_world_size(group) if dist.is_initialized() else 1
     rank = dist.get_rank(group) if dist.is_initialized() else 0
+    if world > 1:
+        dist.barrier(group)  # a full collective first: NCCL's first P2P batch must not be partial
     plan = plan_shard(ps, world, rank)
     ops = DeviceShardOps(plan, droptol=cfg.droptol, fill_cap=cfg.fill_cap, device=device)
     halo = Halo(plan, ops.device, group)

@@ -63,3 +63,50 @@ if cyc[:, 7].sum() > 0:
     print(f"producer: total cycles/CTA {tot.mean():.0f}, idle {cyc[:, 5].mean() / max(tot.mean(), 1):.2%}, "
           f"iterations/CTA {cyc[:, 4].mean():.0f}")
 
+pr = buf[2 * (1 << 20) - 8 * 4096:].reshape(4096, 8)[2048:2048 + P.system.num_parts].astype(float)
+if pr[:, 4].sum() > 0:
+    m = pr.mean(axis=0)
+    tot = m[0] + m[1] + m[2] + m[3]
+    print(f"thread 0 level loop (one apply, mean over CTAs): {tot:.0f} cycles; steps {m[4]:.0f}, levels {m[5]:.0f}, chunks {m[6]:.0f}")
+    for i, nm in enumerate(["chunk wait", "fold", "publish+next", "barrier"]):
+        print(f"   {nm:>13}: {m[i]:11.0f} cycles ({m[i] / tot:6.1%}); per level {m[i] / max(m[5], 1):7.1f}, per step {m[i] / max(m[4], 1):7.1f}")
+# PSLR_TRACE_BUILD=3: per-step clock64 records (code 50, arg = level_end | chunk_done<<1 |
+# G<<2 | nrows<<8) of CTA 0: level durations in cycles by phase, rows and width
+i50 = np.flatnonzero(codes == 50)
+if i50.size:
+    clk = ev[:, 1]
+    pstarts = {int(i): int(codes[i]) for i in np.flatnonzero((codes >= 10) & (codes <= 13))}
+    phase_of = np.zeros(n, dtype=np.int64)
+    cur = -1
+    for i in range(n):
+        if i in pstarts:
+            cur = pstarts[i] - 10
+        phase_of[i] = cur
+    stats = {}
+    prev_end = None
+    lv_rows, lv_g, lv_chunks, lv_segs = 0, 0, 0, 0
+    for i in i50:
+        a = int(args[i])
+        if prev_end is None or phase_of[i] != phase_of[prev_end] or (i - prev_end) > 64:
+            prev_end = i  # first step of a phase: no start reference
+            lv_rows = lv_g = lv_chunks = lv_segs = 0
+            continue
+        lv_rows += (a >> 8) & 0xffff
+        lv_g = max(lv_g, (a >> 2) & 0x3f)
+        lv_chunks += (a >> 1) & 1
+        lv_segs += 1
+        if a & 1:
+            dur = int(clk[i] - clk[prev_end])
+            key = int(phase_of[i])
+            stats.setdefault(key, []).append((dur, lv_rows, lv_g, lv_chunks, lv_segs))
+            prev_end = i
+            lv_rows = lv_g = lv_chunks = lv_segs = 0
+    for k, v in sorted(stats.items()):
+        v = np.array(v, dtype=np.float64)
+        print(f"phase {k}: levels {len(v)}, cycles/level mean {v[:, 0].mean():.0f} median {np.median(v[:, 0]):.0f}; "
+              f"rows/level {v[:, 1].mean():.0f}, segs/level {v[:, 4].mean():.2f}, chunk ends/level {v[:, 3].mean():.2f}")
+        for lo, hi in ((0, 33), (33, 129), (129, 257), (257, 513), (513, 100000)):
+            sel = (v[:, 1] >= lo) & (v[:, 1] < hi)
+            if sel.any():
+                print(f"    rows [{lo},{hi}): n={sel.sum():4d} cycles {v[sel, 0].mean():7.0f}  G {v[sel, 2].mean():.2f} "
+                      f"segs {v[sel, 4].mean():.2f} chunk-ends {v[sel, 3].mean():.2f}")
