@@ -404,3 +404,102 @@ def local_rows(plan: ShardPlan, p_global: int) -> np.ndarray:
     """Global (reordered) row indices of the rank's local vector, in local order."""
     return np.concatenate([np.arange(plan.int_lo, plan.int_hi),
                            p_global + np.arange(plan.ifc_lo, plan.ifc_hi)]).astype(np.int64)
+
+
+def sharded_gmres(P: ShardedPreconditioner, b, tol=1e-8, maxit=500, restart=0, precond=True,
+                  flexible=False):
+    """krylov.py:35-129 on the rank's rows: right-preconditioned restarted GMRES, CGS2 +
+    Givens, true residual at every cycle boundary (FGMRES stores Z_j = M v_j, the config 3
+    accelerator).  Vectors stay on the rank's device; per iteration one sharded apply, one
+    A-SpMV with a halo refresh, two allreduced CGS2 projections and an allreduced norm.
+    The Givens/least-squares scalars are replicated host numpy, as in the reference.
+    Returns (x_loc, converged, iterations, final_relres, history)."""
+    ops, halo = P.ops, P.halo
+    t = halo.t
+    n, p, q = ops.n, ops.p, ops.q
+    x_ext = ops.zeros(n + ops.ng)
+
+    def matvec(v):
+        x_ext[:n] = v
+        halo.exchange(x_ext[p:])
+        return ops.spmv_A(x_ext)
+
+    M = P.apply if precond else (lambda v: v)
+
+    def norm(v):
+        return float(halo.dot(v, v).sqrt().item())
+
+    bn = norm(b)
+    if bn == 0.0:
+        return ops.zeros(n), True, 0, 0.0, [1.0]
+    x = ops.zeros(n)
+    hist, total, conv, rel = [1.0], 0, False, 1.0
+    while total < maxit and not conv:
+        r = b - matvec(x)
+        beta = norm(r)
+        rel = beta / bn
+        if rel <= tol:
+            conv = True
+            break
+        cyc = maxit - total if restart <= 0 else min(restart, maxit - total)
+        V = t.zeros((cyc + 1, n), dtype=t.float64, device=ops.device)
+        Z = t.zeros((cyc, n), dtype=t.float64, device=ops.device) if flexible else None
+        Hc = np.zeros((cyc + 1, cyc))
+        cs, sn, g = np.zeros(cyc), np.zeros(cyc), np.zeros(cyc + 1)
+        g[0] = beta
+        V[0] = r / beta
+        j, brk = 0, False
+        while j < cyc:
+            zj = M(V[j].contiguous())
+            if flexible:
+                Z[j] = zj
+            w = matvec(zj)
+            Vj = V[:j + 1]
+            h = halo.allreduce(Vj @ w)
+            w = w - h @ Vj
+            h2 = halo.allreduce(Vj @ w)
+            w = w - h2 @ Vj
+            h = (h + h2).cpu().numpy()
+            hn = norm(w)
+            if not (np.all(np.isfinite(h)) and np.isfinite(hn)):
+                raise ArithmeticError("GMRES diverged: non-finite values in the recurrence")
+            Hc[:j + 1, j] = h
+            Hc[j + 1, j] = hn
+            for i in range(j):
+                tt = cs[i] * Hc[i, j] + sn[i] * Hc[i + 1, j]
+                Hc[i + 1, j] = -sn[i] * Hc[i, j] + cs[i] * Hc[i + 1, j]
+                Hc[i, j] = tt
+            d = np.hypot(Hc[j, j], hn)
+            cs[j], sn[j] = (1.0, 0.0) if d == 0.0 else (Hc[j, j] / d, hn / d)
+            Hc[j, j] = d
+            g[j + 1] = -sn[j] * g[j]
+            g[j] = cs[j] * g[j]
+            total += 1
+            j += 1
+            est = abs(g[j]) / bn
+            hist.append(est)
+            if hn <= 1e-14 * beta:
+                brk = True
+                break
+            if est <= tol:
+                break
+            if j < cyc:
+                V[j] = w / hn
+        if j > 0:
+            y = np.zeros(j)
+            for i in range(j - 1, -1, -1):
+                y[i] = (g[i] - Hc[i, i + 1:j] @ y[i + 1:j]) / Hc[i, i]
+            yt = t.as_tensor(y, device=ops.device)
+            x = x + (yt @ Z[:j] if flexible else M((yt @ V[:j]).contiguous()))
+        rel = norm(b - matvec(x)) / bn
+        hist[-1] = rel
+        if rel <= tol:
+            conv = True
+        elif brk:
+            break
+    if not conv and total < maxit and not np.isfinite(rel):
+        raise ArithmeticError("GMRES diverged: non-finite residual")
+    its = total if conv else maxit
+    if not conv:
+        hist.extend([rel] * (maxit + 1 - len(hist)))
+    return x, conv, its, rel, hist

@@ -113,3 +113,32 @@ def test_sharded_arnoldi_matches_build():
     assert r == P.correction.rank
     assert np.allclose(H, P.correction.H, rtol=1e-9, atol=1e-12)
     assert np.allclose(V.cpu().numpy(), np.asarray(P.correction.V), rtol=1e-8, atol=1e-10)
+
+
+@pytest.mark.parametrize("flexible", [False, True])
+def test_sharded_gmres_one_rank_matches_device_gmres(flexible):
+    """shard.sharded_gmres on a one-rank sharding (device ops, no process group needed)
+    == the fused device GMRES / FGMRES (pslr_gmres): iterations within +-2, histories
+    to 1e-6 (reduction order differs)."""
+    import torch
+    import paper_2002_00917_b200 as pg
+    from paper_2002_00917_b200 import shard, workloads
+    from paper_2002_00917_b200.krylov import gmres_device
+    A = workloads.laplacian3d(16, 16, 16, 0.5)
+    m = 3
+    cfg = pg.PslrConfig(num_subdomains=8, series_degree=m, rank=8, droptol=1e-2, seed=0)
+    P = pg.build(A, cfg)
+    ps = P.system
+    b = ps.matrix @ np.random.default_rng(0).standard_normal(ps.n)
+    x_ref, rep = gmres_device(P, b, tol=1e-8, maxit=80, restart=20, flexible=flexible)
+    plan = shard.plan_shard(ps, 1, 0)
+    ops = shard.DeviceShardOps(plan)
+    ops.set_correction(torch.as_tensor(np.ascontiguousarray(P.correction.V), device="cuda"), P.correction.G)
+    halo = shard.Halo(plan, "cuda")
+    SP = shard.ShardedPreconditioner(plan, ops, halo, m)
+    x, conv, its, rel, hist = shard.sharded_gmres(SP, torch.as_tensor(b, device="cuda"), tol=1e-8,
+                                                  maxit=80, restart=20, flexible=flexible)
+    assert abs(its - rep.iterations) <= 2
+    k = min(len(hist), len(rep.history))
+    assert np.allclose(np.asarray(hist[:k]), np.asarray(rep.history[:k]), rtol=1e-6, atol=1e-14)
+    assert conv == rep.converged

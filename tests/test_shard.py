@@ -112,6 +112,9 @@ class OracleShardOps:
         e = self._es(v_ext)
         return self._ext(O.block_solve(self.c0, e) if do_c0 else e)
 
+    def spmv_A(self, x_ext):
+        return self._t(self.plan.local.matrix @ x_ext.numpy())
+
 
 def _worker(rank, world, port, n, s, m, r, out):
     import torch.distributed as dist
@@ -165,3 +168,59 @@ def test_sharded_apply_matches_single_process(tmp_path, world, n, s):
         Vs[d["ifc"]] = d["V"]
     assert np.allclose(Vs, V, rtol=1e-9, atol=1e-11)
     assert np.max(np.abs(z - z_ref)) <= 1e-10 * np.max(np.abs(z_ref))
+
+
+def _gmres_worker(rank, world, port, n, s, m, r, out):
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ps = _system(n, s)
+        plan = shard.plan_shard(ps, world, rank)
+        ops = OracleShardOps(plan)
+        halo = shard.Halo(plan, "cpu")
+        Vl, H, rr = shard.sharded_arnoldi(ops, halo, ps.q, plan.ifc_lo, m, r, seed=0)
+        ops.set_correction(Vl.numpy(), O.build_correction(np.zeros((0, rr)), H).G)
+        P = shard.ShardedPreconditioner(plan, ops, halo, m)
+        xs = np.random.default_rng(0).standard_normal(ps.n)
+        b = ps.matrix @ xs
+        rows = shard.local_rows(plan, ps.p)
+        res = {}
+        for flex in (False, True):
+            x, conv, its, rel, hist = shard.sharded_gmres(P, torch.as_tensor(b[rows]), tol=1e-8,
+                                                          maxit=60, restart=10, flexible=flex)
+            res[f"x{int(flex)}"] = x.numpy()
+            res[f"its{int(flex)}"] = its
+            res[f"hist{int(flex)}"] = np.asarray(hist)
+        np.savez(os.path.join(out, f"g{rank}.npz"), rows=rows, **res)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_sharded_gmres_matches_single_process(tmp_path):
+    """GMRES / FGMRES over a gloo world of 2 == the oracle's krylov.py:35-129 (its within
+    +-2, residual histories to 1e-6 relative: only reduction order differs)."""
+    import torch.multiprocessing as mp
+    world, n, s, m, r = 2, 10, 4, 3, 6
+    mp.spawn(_gmres_worker, args=(world, _free_port(), n, s, m, r, str(tmp_path)), nprocs=world, join=True)
+    ps = _system(n, s)
+    ctx = O.schur_context(ps)
+    V, H, rr = O.arnoldi(lambda v: O.apply_Err(ctx, m, v), ps.q, r, seed=0)
+    P = O.Preconditioner(ps, ctx, m, O.build_correction(V, H))
+    xs = np.random.default_rng(0).standard_normal(ps.n)
+    b = ps.matrix @ xs
+    x_ref, rep = O.gmres(lambda v: ps.matrix @ v, P.apply, b, tol=1e-8, maxit=60, restart=10)
+    d = [np.load(tmp_path / f"g{k}.npz") for k in range(world)]
+    for flex in (0, 1):
+        assert abs(int(d[0][f"its{flex}"]) - rep.iterations) <= 2
+        assert int(d[0][f"its{flex}"]) == int(d[1][f"its{flex}"])
+        h = d[0][f"hist{flex}"]
+        k = min(len(h), len(rep.history))
+        assert np.allclose(h[:k], rep.history[:k], rtol=1e-6, atol=1e-14)
+        x = np.zeros(ps.n)
+        for dk in d:
+            x[dk["rows"]] = dk[f"x{flex}"]
+        rel = np.linalg.norm(ps.matrix @ x - b) / np.linalg.norm(b)
+        assert abs(rel - rep.final_relres) <= 1e-3 * rep.final_relres + 1e-12
