@@ -15,7 +15,8 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libpslr.so")
+# PSLR_LIB: an alternative build of the same library (timing experiments, tools/)
+LIB_PATH = os.environ.get("PSLR_LIB") or os.path.join(_HERE, "lib", "libpslr.so")
 
 PSLR_OK, PSLR_EDIM, PSLR_ENONFINITE, PSLR_ESINGULAR, PSLR_ECUDA, PSLR_EINVAL, PSLR_ENOMEM, \
     PSLR_ENCCL = range(8)

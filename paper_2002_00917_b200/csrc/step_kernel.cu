@@ -456,7 +456,11 @@ __device__ __forceinline__ bool level_step(const StepConst& K, Ctl* ctl, uint8_t
     nh0 = *reinterpret_cast<const int4*>(nseg_ptr);
     nh1 = *reinterpret_cast<const int2*>(nseg_ptr + 16);
   }
+#ifdef PSLR_X_NOFOLD  // timing experiments (tools/knobs.sh): results are wrong
+  if (false) {
+#else
   if (cur.wact) {
+#endif
     // B: U rows start from rhs / sd.  rcp = RN(1/sd): q0 = RN(x rcp) is within an ulp of
     // x/sd and one fma-corrected step gives RN(x/sd) (Markstein); sd == 1 keeps x as is.
     double acc = cur.rhs;
@@ -470,18 +474,30 @@ __device__ __forceinline__ bool level_step(const StepConst& K, Ctl* ctl, uint8_t
     // F: publish the row
     if (cur.active) {
       ring[cur.ridx] = acc;
+#ifndef PSLR_X_NOSTG
       z[cur.zidx] = acc;
+#endif
       if (UPPER) {
         double x = acc * cur.invd;
         if (cadd) x = x + cur.cadd;
+#ifndef PSLR_X_NOSTG
         xout[cur.xidx] = x;
+#endif
       }
     }
   }
   const int cur_flags = cur.flags;
   const int cur_info = (cur.G << 2) | (cur.nrows << 8);
   // E: the next segment's row, loaded in place (everything it needs before its gathers)
+#ifdef PSLR_X_NOLOAD
+  if (more) {
+    cur.bytes = nh1.y;
+    cur.flags = nh0.z;
+    cur.wact = ((int)threadIdx.x & ~31) < (nh0.z >> 8) + nh0.x && ((int)threadIdx.x & ~31) + 32 > (nh0.z >> 8);
+  }
+#else
   if (more) load_row<UPPER>(nseg_ptr, nh0, nh1, c.rbuf, c.rbase, base, mask, zslot, cadd, cur);
+#endif
   c.seg = nseg_ptr;
   if (chunk_done) {  // the staged chunk is no longer read by this warp
     __syncwarp();
@@ -489,7 +505,9 @@ __device__ __forceinline__ bool level_step(const StepConst& K, Ctl* ctl, uint8_t
   }
   if (cur_flags & 1) {
     trace_fine(K, 40, 0);
+#ifndef PSLR_X_NOBAR
     consumer_sync();
+#endif
     trace_fine(K, 41, 0);
   }
   trace_clk(K, 50, (cur_flags & 1) | (chunk_done ? 2 : 0) | cur_info);
