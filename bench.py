@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=100)
     ap.add_argument("--cpu-applies", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--gmres-maxit", type=int, default=500,
+                    help="N=1: also time one device GMRES solve (SURVEY §8d time-to-solution); 0 = skip")
     ap.add_argument("--sharded", action="store_true",
                     help="run the sharded (multi-GPU) path even at N=1 (testing the NCCL path)")
     return ap.parse_args()
@@ -438,6 +440,27 @@ def main():
         ms_e2e = float(tt.item())
     e2e_value = world * bytes_apply * args.e2e_steps / (ms_e2e / 1e3) / 1e9
 
+    # GMRES time-to-solution: b = A x*, x* seeded; the device solve with the
+    # reference's control flow (krylov.py:35-129); bytes per iteration j of a cycle =
+    # apply + A-SpMV + CGS2 (4 passes over j+1 basis vectors) + 16 n
+    solve = None
+    if args.gmres_maxit > 0:
+        from paper_2002_00917_b200.krylov import gmres_device
+        xs = np.random.default_rng(0).standard_normal(n)
+        bg = torch.from_numpy(P.system.matrix @ xs).cuda()
+        torch.cuda.synchronize()
+        rs = wl.restart if wl.restart > 0 else 50  # cfg5 names no solver: GMRES(50)
+        xg, rep = gmres_device(P, bg, tol=wl.tol, maxit=args.gmres_maxit, restart=rs,
+                               flexible=wl.flexible)
+        torch.cuda.synchronize()
+        spmv_b = 12 * info["nnz_A"] + 16 * n
+        gb = sum(bytes_apply + spmv_b + 8 * n * ((k % rs) + 1) * 4 + 16 * n for k in range(rep.iterations))
+        solve = {"solver": "FGMRES" if wl.flexible else "GMRES", "restart": rs, "tol": wl.tol,
+                 "maxit": args.gmres_maxit, "iterations": rep.iterations, "converged": rep.converged,
+                 "final_relres": rep.final_relres, "time_s": rep.time_s,
+                 "ms_per_iteration": rep.time_s * 1e3 / max(rep.iterations, 1),
+                 "GB_per_s": gb / rep.time_s / 1e9 if rep.time_s > 0 else None}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         V, H, G = P.correction.V, P.correction.H, P.correction.G
@@ -470,6 +493,7 @@ def main():
             "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": 8 * n,
                     "d2h_bytes_per_step": 8 * n, "ms_per_step": ms_e2e / args.e2e_steps},
             "gpu_launches": launches_per_apply * args.steps,
+            "solve": solve,
             "clocks": clk,
             "levels": {k: info[k] for k in ("maxdepth_LB", "maxdepth_UB", "maxdepth_LC", "maxdepth_UC")},
         }
