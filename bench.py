@@ -404,7 +404,7 @@ def main():
             per_kind.setdefault(int(lkind[i]), []).append(float(lms[i]))
     launches_per_apply = int(nl.value)
     kind_names = {1: "correction_core", 2: "first_step", 3: "correction_c0", 4: "horner_step",
-                  5: "last_step", 0: "step"}
+                  5: "last_step", 6: "permute_f", 0: "step"}
     launch_ms = {kind_names.get(k, str(k)): float(np.mean(v)) for k, v in per_kind.items()}
     horner_ms = launch_ms.get("horner_step")
     peak, peak_src = hbm_peak()

@@ -127,7 +127,7 @@ int pslr_apply(pslr_ctx* ctx, int64_t m, const double* b, double* z, void* strea
 int pslr_spmv(pslr_ctx* ctx, int which, const double* x, double* y, void* stream);
 /* pslr_apply with a CUDA event after every kernel launch (measurement only): per-launch
  * milliseconds and kinds (1 correction core, 2 first step, 3 correction+C0, 4 Horner step,
- * 5 last step); nlaunch = launches issued (up to cap reported). */
+ * 5 last step, 6 permute of f); nlaunch = launches issued (up to cap reported). */
 int pslr_apply_profiled(pslr_ctx* ctx, int64_t m, const double* b, double* z, void* stream,
                         double* launch_ms, int32_t* launch_kind, int64_t cap, int64_t* nlaunch);
 /* Diagnostics (contexts created with PSLR_TRACE=1): timeline of CTA 0 since the last call,
@@ -146,7 +146,7 @@ int pslr_apply_host(pslr_ctx* ctx, int64_t m, const double* b_host, double* z_ho
  *   first  : y0 = g - F B^{-1} f ; s = V^T y0 over the local rows   -> allreduce(s)
  *   mid    : y1 = y0 + V G s ; c = C0^{-1} y1  (c extended)         -> halo(c)
  *   horner : out = C0^{-1}(E_s y) + c  (y extended), m times        -> halo(out) between
- *   last   : z = [B^{-1}(f - E y) ; y]
+ *   last   : z = [B^{-1}(f - E y) ; y]   (same b as the preceding first: f is kept permuted)
  * The fused single-context calls above require nghost == 0. */
 int pslr_apply_first(pslr_ctx* ctx, const double* b, double* y0, double* s, void* stream);
 int pslr_apply_mid(pslr_ctx* ctx, const double* y0, const double* s, double* c, void* stream);

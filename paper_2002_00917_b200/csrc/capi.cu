@@ -216,11 +216,17 @@ int op_horner(pslr_ctx* ctx, int64_t m, const double* c, double* out, cudaStream
 int op_apply(pslr_ctx* ctx, int64_t m, const double* b, double* z, cudaStream_t st) {
   const int64_t p = ctx->p, q = ctx->q;
   if (q == 0) return op_solve_B(ctx, b, z, st);
+  // (0) f in L-position order, shared by the first and the last step
+  if (p > 0) {
+    CKL(launch_permute_f(ctx, b, st));
+    RET(mark(ctx, LK_PERMUTE, st));
+  }
   // (1) y0 = g - F B^{-1} f  (+ per-subdomain V^T y0 partials)   preconditioner.py:89
   {
     StepArgs a;
     a.b1 = BT_F;
     a.f = b;
+    a.fL = ctx->fL;
     a.xb = ctx->xb;
     a.i1 = IT_G;
     a.g = b + p;
@@ -256,6 +262,7 @@ int op_apply(pslr_ctx* ctx, int64_t m, const double* b, double* z, cudaStream_t 
     StepArgs a;
     a.b1 = BT_F;
     a.f = b;
+    a.fL = ctx->fL;  // last reader of fL: its E rows become f - E y in place
     a.b2 = BT_EY;
     a.yE = z + p;
     a.xb = z;
@@ -432,6 +439,7 @@ int pslr_ctx_create(pslr_ctx** out, int device, const pslr_system* sys) {
   if ((rc = alloc_scratch(ctx, &ctx->K.rhsC, q + 2))) return bail(rc);
   if ((rc = alloc_scratch(ctx, &ctx->K.zC, q + 2))) return bail(rc);
   if ((rc = alloc_scratch(ctx, &ctx->xb, p))) return bail(rc);
+  if ((rc = alloc_scratch(ctx, &ctx->fL, p + 2))) return bail(rc);
   if ((rc = alloc_scratch(ctx, &ctx->y0, q))) return bail(rc);
   if ((rc = alloc_scratch(ctx, &ctx->y1, q))) return bail(rc);
   if ((rc = alloc_scratch(ctx, &ctx->y2, q))) return bail(rc);
@@ -590,9 +598,11 @@ int pslr_apply_first(pslr_ctx* ctx, const double* b, double* y0, double* s, void
   RET(set_device(ctx));
   cudaStream_t st = S(stream);
   if (ctx->q == 0) return PSLR_OK;
+  if (ctx->p > 0) CKL(launch_permute_f(ctx, b, st));  // kept for pslr_apply_last
   StepArgs a;
   a.b1 = BT_F;
   a.f = b;
+  a.fL = ctx->fL;
   a.xb = ctx->xb;
   a.i1 = IT_G;
   a.g = b + ctx->p;
@@ -645,6 +655,7 @@ int pslr_apply_last(pslr_ctx* ctx, const double* b, const double* y, double* z, 
   StepArgs a;
   a.b1 = BT_F;
   a.f = b;
+  a.fL = ctx->fL;  // permuted by pslr_apply_first of the same b
   a.b2 = BT_EY;
   a.yE = y;
   a.xb = z;

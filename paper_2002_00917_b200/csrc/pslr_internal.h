@@ -87,6 +87,8 @@ struct StepArgs {
   // ---- interior (B) phase:  rhs = b1 [(-) b2];  xb = B^{-1} rhs
   int b1 = BT_NONE, b2 = BT_NONE;
   const double* f = nullptr;   // p-vector used by BT_F
+  double* fL = nullptr;        // f already in L-position order (permute_f): the L phase reads
+                               // it as its right-hand side; E y rows are folded into it
   const double* yE = nullptr;  // q-vector multiplied by E for BT_EY
   double* xb = nullptr;        // p output of the B solve
   // ---- interface phase:  w = i1 (+|-) i2 ;  [y = C0^{-1} w] ; [y += cadd]
@@ -143,6 +145,7 @@ struct pslr_ctx {
   double* G = nullptr;           // r x r row-major
   // scratch
   double* xb = nullptr;          // p
+  double* fL = nullptr;          // p+2: f in L-position order, per apply
   double* y0 = nullptr;          // q
   double* y1 = nullptr;          // q
   double* y2 = nullptr;          // q

@@ -31,7 +31,9 @@ namespace pslr {
 // Launch kinds recorded by pslr_apply_profiled: 0 generic step, 1 correction core,
 // 2 apply-first (B solve + F), 3 correction + C0, 4 Horner step (E, B solve, F, Cg,
 // C0 solve), 5 apply-last (E, B solve).
-enum LaunchKind : int32_t { LK_STEP = 0, LK_CORE = 1, LK_FIRST = 2, LK_CORR = 3, LK_HORNER = 4, LK_LAST = 5 };
+enum LaunchKind : int32_t {
+  LK_STEP = 0, LK_CORE = 1, LK_FIRST = 2, LK_CORR = 3, LK_HORNER = 4, LK_LAST = 5, LK_PERMUTE = 6
+};
 
 // kernels.cu
 int configure_step_kernel(int smem_bytes);
@@ -53,6 +55,7 @@ int vt_grid(int64_t q, int sm_count);
 int launch_vt_dot(pslr_ctx* ctx, const double* y, cudaStream_t st);
 int launch_vt_local(pslr_ctx* ctx, const double* y, double* s, cudaStream_t st);
 int launch_gs(pslr_ctx* ctx, const double* s, cudaStream_t st);
+int launch_permute_f(const pslr_ctx* ctx, const double* f, cudaStream_t st);
 int launch_vu_add(const pslr_ctx* ctx, const double* y, double* out, cudaStream_t st);
 
 // capi.cu

@@ -629,7 +629,7 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
       S.nphase++;
     };
     if (do_b) {
-      add_phase(K.LB, K.rhsB);
+      add_phase(K.LB, a.fL ? a.fL : K.rhsB);
       add_phase(K.UB, K.zB);
     }
     if (do_c) {
@@ -662,8 +662,11 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
   if (do_b) {
     const int r0 = K.int_off[b], r1 = K.int_off[b + 1];
     // pass 1: rhs = f scattered to the L-positions (stores do not stall, so scatter
-    // beats a gather here), or a coalesced zero fill
-    if (a.b1 == BT_F) {
+    // beats a gather here), or a coalesced zero fill.  With a.fL the all-SM permute_f
+    // kernel has done it: the L phase reads fL and only the E rows are rewritten.
+    double* rhs = a.fL ? a.fL : K.rhsB;
+    if (a.fL) {
+    } else if (a.b1 == BT_F) {
       constexpr int kIn = 8;  // independent loads in flight per thread
       for (int row0 = r0 + tid; row0 < r1; row0 += kIn * kStepThreads) {
         double v[kIn];
@@ -685,7 +688,7 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
     // pass 2: rows with E entries get the E y term: f - E y, or E y alone (scipy
     // csr_matvec order), kIn rows per thread in flight; one int4 record per row
     if (a.b1 == BT_EY || a.b2 == BT_EY) {
-      consumer_sync();
+      if (!a.fL) consumer_sync();
       constexpr int kIn = 4;
       const int e0 = K.erow_off[b], e1 = K.erow_off[b + 1];
       const int4* rec = reinterpret_cast<const int4*>(K.erows);
@@ -701,7 +704,8 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
           sum[j] = 0.0;
         }
 #pragma unroll
-        for (int j = 0; j < kIn; ++j) fv[j] = (a.b1 == BT_F && r[j].w > r[j].z) ? __ldg(a.f + r[j].y) : 0.0;
+        for (int j = 0; j < kIn; ++j)
+          fv[j] = (a.b1 == BT_F && r[j].w > r[j].z) ? (a.fL ? a.fL[r[j].x] : __ldg(a.f + r[j].y)) : 0.0;
         for (int k = 0; k < len; ++k) {
           int c[kIn];
           double v[kIn], yv[kIn];
@@ -719,7 +723,7 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
         }
 #pragma unroll
         for (int j = 0; j < kIn; ++j)
-          if (i0 + j * kStepThreads < e1) K.rhsB[r[j].x] = (a.b1 == BT_F) ? (fv[j] - sum[j]) : sum[j];
+          if (i0 + j * kStepThreads < e1) rhs[r[j].x] = (a.b1 == BT_F) ? (fv[j] - sum[j]) : sum[j];
       }
     }
     consumer_sync();
