@@ -120,18 +120,18 @@ __global__ void vu_add_kernel(const double* __restrict__ V, const double* __rest
   }
 }
 
-// fL[lpos[i]] = f[i]: the L solve's right-hand side in position order, all SMs (scattered
-// stores spread over 148 SMs instead of one CTA per subdomain)
-__global__ void permute_f_kernel(const int32_t* __restrict__ lpos, const double* __restrict__ f,
+// fL[pos] = f[row at pos]: the L solve's right-hand side in position order, on all SMs
+__global__ void permute_f_kernel(const int32_t* __restrict__ lrow, const double* __restrict__ f,
                                  double* __restrict__ fL, int64_t p) {
+  // gather form: coalesced stores, the random reads of f (15 MB at cfg5) hit L2
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p; i += (int64_t)gridDim.x * blockDim.x)
-    fL[__ldg(lpos + i)] = __ldg(f + i);
+    fL[i] = __ldg(f + __ldg(lrow + i));
 }
 
 int launch_permute_f(const pslr_ctx* ctx, const double* f, cudaStream_t st) {
   if (ctx->p == 0) return 0;
   const int blocks = 4 * ctx->sm_count;
-  permute_f_kernel<<<blocks, 512, 0, st>>>(ctx->K.LB.lpos, f, ctx->fL, ctx->p);
+  permute_f_kernel<<<blocks, 512, 0, st>>>(ctx->K.LB.lrow, f, ctx->fL, ctx->p);
   return (int)cudaGetLastError();
 }
 
