@@ -435,6 +435,7 @@ int pslr_ctx_create(pslr_ctx** out, int device, const pslr_system* sys) {
   }
   // position-ordered rhs arrays: +2 so a chunk's even-aligned TMA slice stays in bounds
   if ((rc = alloc_scratch(ctx, &ctx->K.rhsB, p + 2))) return bail(rc);
+  if ((rc = alloc_scratch(ctx, &ctx->K.rhsE, p + 2))) return bail(rc);  // zeroed
   if ((rc = alloc_scratch(ctx, &ctx->K.zB, p + 2))) return bail(rc);
   if ((rc = alloc_scratch(ctx, &ctx->K.rhsC, q + 2))) return bail(rc);
   if ((rc = alloc_scratch(ctx, &ctx->K.zC, q + 2))) return bail(rc);

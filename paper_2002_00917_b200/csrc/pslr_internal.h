@@ -116,6 +116,8 @@ struct StepConst {
   const double* V = nullptr;
   int r = 0;
   double* rhsB = nullptr;  // p: L_B right-hand side in L-position order
+  double* rhsE = nullptr;  // p: right-hand side E y alone: only the E rows are ever written,
+                           //    every other position stays 0 from the allocation
   double* zB = nullptr;    // p: L_B output / U_B intermediate in U-position order
   double* rhsC = nullptr;  // q
   double* zC = nullptr;    // q

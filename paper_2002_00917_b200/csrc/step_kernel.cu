@@ -629,7 +629,7 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
       S.nphase++;
     };
     if (do_b) {
-      add_phase(K.LB, a.fL ? a.fL : K.rhsB);
+      add_phase(K.LB, a.fL ? a.fL : (a.b1 == BT_EY && a.b2 == BT_NONE) ? K.rhsE : K.rhsB);
       add_phase(K.UB, K.zB);
     }
     if (do_c) {
@@ -664,8 +664,10 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
     // pass 1: rhs = f scattered to the L-positions (stores do not stall, so scatter
     // beats a gather here), or a coalesced zero fill.  With a.fL the all-SM permute_f
     // kernel has done it: the L phase reads fL and only the E rows are rewritten.
-    double* rhs = a.fL ? a.fL : K.rhsB;
-    if (a.fL) {
+    const bool ey_only = a.b1 == BT_EY && a.b2 == BT_NONE;
+    double* rhs = a.fL ? a.fL : ey_only ? K.rhsE : K.rhsB;
+    if (a.fL || ey_only) {
+      // fL holds f already; rhsE's non-E positions are permanently 0
     } else if (a.b1 == BT_F) {
       constexpr int kIn = 8;  // independent loads in flight per thread
       for (int row0 = r0 + tid; row0 < r1; row0 += kIn * kStepThreads) {
@@ -688,7 +690,7 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
     // pass 2: rows with E entries get the E y term: f - E y, or E y alone (scipy
     // csr_matvec order), kIn rows per thread in flight; one int4 record per row
     if (a.b1 == BT_EY || a.b2 == BT_EY) {
-      if (!a.fL) consumer_sync();
+      if (!a.fL && !ey_only) consumer_sync();
       constexpr int kIn = 4;
       const int e0 = K.erow_off[b], e1 = K.erow_off[b + 1];
       const int4* rec = reinterpret_cast<const int4*>(K.erows);
