@@ -110,3 +110,12 @@ if i50.size:
             if sel.any():
                 print(f"    rows [{lo},{hi}): n={sel.sum():4d} cycles {v[sel, 0].mean():7.0f}  G {v[sel, 2].mean():.2f} "
                       f"segs {v[sel, 4].mean():.2f} chunk-ends {v[sel, 3].mean():.2f}")
+i51 = np.flatnonzero(codes == 51)
+if i51.size:
+    w = args[i51].astype(np.int64)
+    print(f"chunk transitions (CTA 0, trace build 3): n={w.size}, wait cycles mean {w.mean():.0f} median "
+          f"{np.median(w):.0f} p90 {np.percentile(w, 90):.0f}; > 200 cycles: {(w > 200).mean():.1%}, "
+          f"sum {w.sum() / 1.965e3:.1f} us")
+    for k in sorted(set(phase_of[i51].tolist())):
+        sel = phase_of[i51] == k
+        print(f"   phase {k}: n={sel.sum()}, mean {w[sel].mean():.0f}, sum {w[sel].sum() / 1.965e3:.1f} us")
