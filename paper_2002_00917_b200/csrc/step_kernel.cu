@@ -441,7 +441,13 @@ __device__ __forceinline__ bool level_step(const StepConst& K, Ctl* ctl, uint8_t
         c.par ^= 1u;
       }
       trace_fine(K, 19, c.u);
+#if PSLR_TRACE_BUILD == 3
+      const long long tw0 = clock64();
       mbar_wait(&ctl->full[c.st], c.par);
+      trace_clk(K, 51, (int)(clock64() - tw0));
+#else
+      mbar_wait(&ctl->full[c.st], c.par);
+#endif
       trace_fine(K, 20, c.u);
       nseg_ptr = stages + (size_t)c.st * K.stage_bytes;
       c.rbuf = rhsbuf + (size_t)c.st * K.rhs_stride;
