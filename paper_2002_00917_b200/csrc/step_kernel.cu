@@ -658,6 +658,11 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
                                                    : nullptr);
     return;
   }
+  // Programmatic dependent launch: this grid may start while the previous kernel of the
+  // stream finishes (setup above and the producer's factor stream do not depend on it);
+  // consumers wait here for its completion before reading any vector it produced or
+  // writing any buffer it may still read.  A no-op for ordinary launches.
+  asm volatile("griddepcontrol.wait;" ::: "memory");
   trace_begin(K);
   trace_ev(K, 1, S.begin[S.nphase]);
   if (threadIdx.x == 0) ring[K.ring_mask + 1] = 0.0;  // the zero slot (visible after the next barrier)
@@ -784,8 +789,20 @@ int configure_step_kernel(int smem_bytes) {
 
 int launch_step(const pslr_ctx* ctx, const StepArgs& a, cudaStream_t st) {
   if (ctx->s == 0) return 0;
-  subdomain_step_kernel<<<(unsigned)ctx->s, kBlockThreads, ctx->K.smem_bytes, st>>>(a, ctx->K);
-  return (int)cudaGetLastError();
+  // programmatic stream serialization: the step kernel's CTAs (one per subdomain, far
+  // fewer than the 148 SMs) launch and stage their first factor chunks while the
+  // previous kernel drains; griddepcontrol.wait orders the data accesses
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)ctx->s);
+  cfg.blockDim = dim3(kBlockThreads);
+  cfg.dynamicSmemBytes = (size_t)ctx->K.smem_bytes;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = ctx->pdl ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return (int)cudaLaunchKernelEx(&cfg, subdomain_step_kernel, a, ctx->K);
 }
 
 }  // namespace pslr
