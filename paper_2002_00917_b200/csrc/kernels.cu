@@ -52,7 +52,28 @@ vt_dot_kernel(const double* __restrict__ V, const double* __restrict__ y, int64_
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = kVtThreads / 32;
   for (int c0 = 0; c0 < r; c0 += 128) {
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    for (int64_t row = (int64_t)blockIdx.x * nw + warp; row < q; row += (int64_t)gridDim.x * nw) {
+    const int64_t stride = (int64_t)gridDim.x * nw;
+    int64_t row = (int64_t)blockIdx.x * nw + warp;
+    // four rows per iteration: their loads are independent and in flight together
+    for (; row + 3 * stride < q; row += 4 * stride) {
+      double yv[4], vv[4][4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        yv[u] = __ldg(y + row + u * stride);
+        const double* vr = V + (row + u * stride) * r;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int c = c0 + lane + 32 * k;
+          vv[u][k] = (c < r) ? __ldg(vr + c) : 0.0;
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (c0 + lane + 32 * k < r) acc[k] = acc[k] + vv[u][k] * yv[u];
+    }
+    for (; row < q; row += stride) {
       const double yv = __ldg(y + row);
       const double* vr = V + row * r;
 #pragma unroll
@@ -109,8 +130,29 @@ __global__ void vu_add_kernel(const double* __restrict__ V, const double* __rest
                               int r) {
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
-  for (int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); row < q;
-       row += nwarps) {
+  int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r <= 64) {  // two columns per lane, four rows in flight per warp
+    const double u0 = lane < r ? __ldg(u + lane) : 0.0, u1 = lane + 32 < r ? __ldg(u + lane + 32) : 0.0;
+    for (; row + 3 * nwarps < q; row += 4 * nwarps) {
+      double s[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const double* vr = V + (row + k * nwarps) * r;
+        const double a = lane < r ? __ldg(vr + lane) : 0.0;
+        const double b = lane + 32 < r ? __ldg(vr + lane + 32) : 0.0;
+        s[k] = (lane < r ? a * u0 : 0.0);
+        s[k] = s[k] + (lane + 32 < r ? b * u1 : 0.0);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) s[k] = s[k] + __shfl_xor_sync(0xffffffffu, s[k], o);
+      if (lane == 0)
+#pragma unroll
+        for (int k = 0; k < 4; ++k) out[row + k * nwarps] = __ldg(y + row + k * nwarps) + s[k];
+    }
+  }
+  for (; row < q; row += nwarps) {
     const double* vr = V + row * r;
     double s = 0.0;
     for (int c = lane; c < r; c += 32) s = s + __ldg(vr + c) * __ldg(u + c);
