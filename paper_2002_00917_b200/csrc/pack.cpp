@@ -121,17 +121,41 @@ int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAna
   out.segments = 0;
   std::vector<uint8_t> seg;
   // ELL segment, S = a4(nrows) row slots, G = ceil(w/4) groups of 4 entries per row:
-  // slots int32[G][S][4] (one 16-B load per row and group), values double[G][2][S][2]
-  // (two conflict-free 16-B loads).  Entries past a row's length are exact no-ops
-  // (value 0, slot = the ring's zero slot W).
-  // U rows also carry sd (scipy's scaled diagonal), rcp = RN(1/sd) and invd = 1/diag.
-  auto seg_bytes = [&](int64_t nrows, int64_t w, int64_t /*nnz*/) {
+  //   hdr int32[12] {nrows, w, flags, pos0, S, bytes, nseg, rbase, far_off, 0, 0, 0}
+  //   info int32[S]     L: U-position ; U: row id, bit 31 set when sd = 1 - 2^-53
+  //   U: invd f64[S], and only for flags bit 2 ("explicit sd"): sd f64[S], rcp f64[S]
+  //   slot u16[G][S][4] near: ring slot (< W), W = zero slot; far: 0x8000 | far-list index
+  //   val  f64[G][2][S][2]
+  //   far  int32[a4(nfar)] U-positions of the segment's far dependencies
+  // Entries past a row's length are exact no-ops (value 0, slot W).  scipy's scaled
+  // diagonal sd = d * (1/d) is 1 or 1 - 2^-53 for every diagonal met so far; the flag bit
+  // carries it (rcp = RN(1/sd) is then a constant), other values switch the segment to
+  // explicit sd / rcp arrays.
+  constexpr double kSdLow = 0x1.fffffffffffffp-1;  // 1 - 2^-53
+  auto seg_bytes = [&](int64_t nrows, int64_t w, int64_t nfar, bool explicit_sd) {
     const int64_t S = a4(nrows), G = std::max<int64_t>(1, (w + 3) / 4);
-    int64_t b = 32 + 4 * S;
-    if (upper) b += 24 * S;
-    b += 48 * G * S;
+    int64_t b = 48 + 4 * S;
+    if (upper) b += (explicit_sd ? 24 : 8) * S;
+    b += 40 * G * S;
+    b += 4 * a4(nfar);
     return b;
   };
+  auto sd_of = [&](int64_t r) { return A.diag[r] * (1.0 / A.diag[r]); };
+  auto sd_plain = [&](int64_t r) {
+    const double v = sd_of(r);
+    return v == 1.0 || (v == kSdLow && 1.0 / v == 0x1.0000000000001p+0);
+  };
+  // far dependencies of the row at position s1 within a level ending at lend
+  auto row_far = [&](int64_t s1, int64_t lend) {
+    const int64_t r = A.row_at_pos[s1];
+    int64_t f = 0;
+    for (int64_t e = M.indptr[r]; e < M.indptr[r + 1]; ++e) {
+      const int64_t j = M.indices[e];
+      if (j != r && lend - A.pos_of_row[j] > W) ++f;
+    }
+    return f;
+  };
+  if (W >= 0x8000) return fail(PSLR_EINVAL, std::string(name) + ": ring too large for 16-bit slots");
   // current chunk being filled
   int64_t chunk_start = 0, chunk_nseg = 0, chunk_pos0 = 0, chunk_rows = 0;
   auto close_chunk = [&]() {
@@ -166,19 +190,24 @@ int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAna
         // threads [tb, tb + nrows), tb = rows of the level emitted before, mod seg_rows.
         const int64_t tb = (s0 - k) % seg_rows;
         // grow a segment while it fits a stage
-        int64_t s1 = s0, nnz = 0, w = 0;
+        int64_t s1 = s0, nnz = 0, w = 0, nfar = 0;
+        bool expl = false;
         while (s1 < lend && s1 - s0 < seg_rows - tb) {
           const int64_t len = A.len[A.row_at_pos[s1]];
           const int64_t w2 = std::max(w, len);
-          if (seg_bytes(s1 - s0 + 1, w2, nnz + len) > stage_bytes) break;
+          const int64_t f2 = nfar + row_far(s1, lend);
+          const bool e2 = expl || (upper && !sd_plain(A.row_at_pos[s1]));
+          if (seg_bytes(s1 - s0 + 1, w2, f2, e2) > stage_bytes || f2 >= 0x8000) break;
           w = w2;
           nnz += len;
+          nfar = f2;
+          expl = e2;
           ++s1;
         }
         if (s1 == s0)
           return fail(PSLR_EINVAL, std::string(name) + ": a row is too long for the streaming format");
         const int64_t nrows = s1 - s0;
-        const int64_t bytes = seg_bytes(nrows, w, nnz);
+        const int64_t bytes = seg_bytes(nrows, w, nfar, expl);
         if ((int64_t)out.data.size() - chunk_start + bytes > stage_bytes ||
             chunk_rows + nrows > kChunkRows)
           close_chunk();
@@ -188,44 +217,55 @@ int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAna
         int32_t* h = reinterpret_cast<int32_t*>(seg.data());
         h[0] = (int32_t)nrows;
         h[1] = (int32_t)w;
-        h[2] = ((s1 == lend) ? 1 : 0) | (int32_t)(tb << 8);  // bit0: ends a level; tb
+        h[2] = ((s1 == lend) ? 1 : 0) | (expl ? 4 : 0) | (int32_t)(tb << 8);  // bit0 level end, bit2 explicit sd
         const int64_t S = a4(nrows);
+        const int64_t G = std::max<int64_t>(1, (w + 3) / 4);
         h[3] = (int32_t)s0;
         h[4] = (int32_t)S;
         h[5] = (int32_t)bytes;
-        int32_t* info = h + 8;
+        int32_t* info = h + 12;
         uint8_t* p = reinterpret_cast<uint8_t*>(info + S);
+        double* invd = nullptr;
         double* sd = nullptr;
         double* rcp = nullptr;
-        double* invd = nullptr;
         if (upper) {
-          sd = reinterpret_cast<double*>(p);
-          rcp = sd + S;
-          invd = rcp + S;
-          p = reinterpret_cast<uint8_t*>(invd + S);
+          invd = reinterpret_cast<double*>(p);
+          p += 8 * S;
+          if (expl) {
+            sd = reinterpret_cast<double*>(p);
+            rcp = sd + S;
+            p += 16 * S;
+          }
         }
-        const int64_t G = std::max<int64_t>(1, (w + 3) / 4);
-        int32_t* slot = reinterpret_cast<int32_t*>(p);
-        double* val = reinterpret_cast<double*>(p + 16 * G * S);
-        auto slot_at = [&](int64_t t, int64_t kk) -> int32_t& { return slot[((kk >> 2) * S + t) * 4 + (kk & 3)]; };
+        uint16_t* slot = reinterpret_cast<uint16_t*>(p);
+        double* val = reinterpret_cast<double*>(p + 8 * G * S);
+        int32_t* far = reinterpret_cast<int32_t*>(p + 40 * G * S);
+        h[8] = (int32_t)(reinterpret_cast<uint8_t*>(far) - seg.data());
+        auto slot_at = [&](int64_t t, int64_t kk) -> uint16_t& { return slot[((kk >> 2) * S + t) * 4 + (kk & 3)]; };
         auto val_at = [&](int64_t t, int64_t kk) -> double& {
           return val[(((kk >> 2) * 2 + ((kk >> 1) & 1)) * S + t) * 2 + (kk & 1)];
         };
         for (int64_t t = 0; t < S; ++t)
           for (int64_t kk = 0; kk < 4 * G; ++kk) {  // padding (incl. rows nrows..S-1): exact no-ops
             val_at(t, kk) = 0.0;
-            slot_at(t, kk) = (int32_t)W;
+            slot_at(t, kk) = (uint16_t)W;
           }
         for (int64_t t = 0; t < nrows; ++t) {
           const int64_t r = A.row_at_pos[s0 + t];
           info[t] = info_of_row[r];
           if (upper) {
             const double dinv = 1.0 / A.diag[r];
-            sd[t] = A.diag[r] * dinv;  // scipy: (U @ diags(1/diag)) diagonal
-            rcp[t] = 1.0 / sd[t];
+            const double sdv = A.diag[r] * dinv;  // scipy: (U @ diags(1/diag)) diagonal
             invd[t] = dinv;
+            if (expl) {
+              sd[t] = sdv;
+              rcp[t] = 1.0 / sdv;
+            } else if (sdv != 1.0) {
+              info[t] = (int32_t)((uint32_t)info[t] | 0x80000000u);
+            }
           }
         }
+        int64_t nf = 0;
         for (int64_t t = 0; t < nrows; ++t) {
           const int64_t r = A.row_at_pos[s0 + t];
           int64_t kk = 0;
@@ -237,11 +277,13 @@ int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAna
             val_at(t, kk) = v;
             const int64_t pj = A.pos_of_row[j];
             if (lend - pj <= W) {
-              slot_at(t, kk) = (int32_t)((pj - lo) & (W - 1));
+              slot_at(t, kk) = (uint16_t)((pj - lo) & (W - 1));
             } else {
-              slot_at(t, kk) = (int32_t)(0x80000000u | (uint32_t)far_index[j]);
+              far[nf] = far_index[j];
+              slot_at(t, kk) = (uint16_t)(0x8000 | nf);
+              ++nf;
               out.far++;
-              h[2] |= 2;  // the segment has far dependencies (kernel slow path)
+              h[2] |= 2;  // the segment has far dependencies (kernel gather variant)
             }
             ++kk;
           }

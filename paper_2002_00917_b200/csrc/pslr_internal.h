@@ -38,14 +38,16 @@ struct alignas(16) ChunkDesc {
 // max rows per chunk: bounds the per-stage right-hand-side buffer
 constexpr int kChunkRows = 1024;
 
-// Segment layout inside a chunk (all parts 16-byte aligned):
-//   int32 hdr[8]   = {nrows, w, flags, pos0, S, bytes, nseg (first seg), rbase (first seg)}
-//                    flags: bit0 ends a level, bit1 has far deps, bits 8.. first consumer thread
+// Segment layout inside a chunk (all parts 16-byte aligned; pack.cpp emit_factor):
+//   int32 hdr[12] = {nrows, w, flags, pos0, S, bytes, nseg (first seg), rbase (first seg),
+//                    far_off, 0, 0, 0}; flags: bit0 ends a level, bit1 has far deps,
+//                    bit2 explicit sd/rcp, bits 8.. first consumer thread
 //   S = nrows rounded up to 4; G = max(1, ceil(w/4)) groups of 4 entries (no-op padding)
-//   int32 info[S]   L: U-position of the row ; U: row id
-//   U only: double sd[S], rcp[S] = RN(1/sd), invd[S]
-//   int32 slot[G][S][4]     near: ring slot (<= W, W = zero slot) ; far: 0x80000000 | U-position
+//   int32 info[S]   L: U-position of the row ; U: row id | sd flag (bit 31: sd = 1 - 2^-53)
+//   U only: double invd[S] [, sd[S], rcp[S] if flags bit2]
+//   uint16 slot[G][S][4]    near: ring slot (<= W, W = zero slot) ; far: 0x8000 | far index
 //   double val[G][2][S][2]  (U values pre-scaled by 1/diag of their column)
+//   int32 far[a4(nfar)]     U-positions of the far dependencies
 struct DevTri {
   int32_t nblocks = 0, nchunks = 0;
   const uint8_t* data = nullptr;

@@ -307,21 +307,31 @@ __device__ void producer(const Streams& S, Ctl* ctl, uint8_t* stages, double* rh
 // info[S], [U: sd[S], rcp[S], invd[S]], slot int4[G][S], val double2[G][2][S]; consumer
 // thread tb + t owns row t (tb = flags >> 8), so the segments of one level run side by side.
 struct Row {
-  const uint8_t* slots;  // &slot[0][t]
+  const uint8_t* slots;  // &slot[0][t]  (4 x u16 per row and group)
+  const uint8_t* vals;   // &val[0][0][t]
+  const int32_t* far;    // the segment's far list (U-positions)
   int bytes, flags, G, S, nrows;
   bool wact;             // the warp owns rows of this segment (warp-uniform)
   bool active;           // this lane owns a row
   int ridx;              // ring slot of the row
   int zidx;              // z index: L: U-position ; U: position
   int xidx;              // U: xout index (row id)
-  double rhs;            // raw right-hand side
-  double sd, rcp, invd, cadd;  // U only
-  int4 s0, s1;           // slot groups 0 and 1 (zero slot when absent)
+  double acc;            // right-hand side (U: already divided by sd)
+  double invd, cadd;     // U epilogue
+  uint2 s0, s1;          // slot groups 0 and 1 (zero slot when absent)
   double2 va, vb;        // group-0 values
 };
 
+// U rows start from rhs / sd.  rcp = RN(1/sd): q0 = RN(x rcp) is within an ulp of x/sd
+// and one fma-corrected step gives RN(x/sd) (Markstein); sd == 1 keeps x as is.
+__device__ __forceinline__ double div_sd(double x, double sd, double rcp) {
+  const double q0 = x * rcp;
+  const double q = fma(fma(-q0, sd, x), rcp, q0);
+  return (sd == 1.0) ? x : q;
+}
+
 template <bool UPPER>
-__device__ __forceinline__ void load_row(const uint8_t* seg, const int4 h0, const int2 h1, const double* rbuf,
+__device__ __forceinline__ void load_row(const uint8_t* seg, const int4 h0, const int4 h1, const double* rbuf,
                                          int rbase, int base, int mask, int zslot,
                                          const double* __restrict__ cadd, Row& r) {
   const int S = h1.x;
@@ -332,82 +342,81 @@ __device__ __forceinline__ void load_row(const uint8_t* seg, const int4 h0, cons
   r.nrows = h0.x;
   r.bytes = h1.y;
   // warps owning no row of the segment skip it entirely (the four schedulers are shared
-  // by all 16 consumer warps, so idle warps must not spend issue slots)
+  // by all consumer warps, so idle warps must not spend issue slots)
   const int tb = h0.z >> 8, w0 = (int)threadIdx.x & ~31;
   r.wact = w0 < tb + h0.x && w0 + 32 > tb;
   if (!r.wact) return;
   int t = (int)threadIdx.x - tb;
   r.active = (unsigned)t < (unsigned)h0.x;
   t = r.active ? t : 0;  // inactive lanes read row 0 (in bounds); their results are not stored
-  const int32_t* info = reinterpret_cast<const int32_t*>(seg + 32);
-  const uint8_t* p = seg + 32 + 4 * S;
+  const int32_t* info = reinterpret_cast<const int32_t*>(seg + 48);
+  const uint8_t* p = seg + 48 + 4 * S;
   const int gp = h0.w + t;
   r.ridx = (gp - base) & mask;
-  r.rhs = rbuf[gp - rbase];
+  double x = rbuf[gp - rbase];
   const int inf = info[t];
   if (UPPER) {
     const double* d = reinterpret_cast<const double*>(p);
-    r.sd = d[t];
-    r.rcp = d[S + t];
-    r.invd = d[2 * S + t];
+    r.invd = d[t];
+    if (h0.z & 4) {  // explicit sd / rcp arrays
+      x = div_sd(x, d[S + t], d[2 * S + t]);
+      p += 24 * S;
+    } else {         // info bit 31: sd = 1 - 2^-53 (rcp = 1 + 2^-52), else sd = 1
+      if (inf < 0) x = div_sd(x, 0x1.fffffffffffffp-1, 0x1.0000000000001p+0);
+      p += 8 * S;
+    }
+    const int row = inf & 0x7fffffff;
     r.zidx = gp;
-    r.xidx = inf;
-    r.cadd = (cadd && r.active) ? __ldg(cadd + inf) : 0.0;
-    p += 24 * S;
+    r.xidx = row;
+    r.cadd = (cadd && r.active) ? __ldg(cadd + row) : 0.0;
   } else {
     r.zidx = inf;
   }
-  r.slots = p + 16 * t;
-  r.s0 = *reinterpret_cast<const int4*>(r.slots);
-  r.s1 = (G > 1) ? *reinterpret_cast<const int4*>(r.slots + 16 * S) : make_int4(zslot, zslot, zslot, zslot);
-  const uint8_t* v = p + 16 * G * S + 16 * t;
-  r.va = *reinterpret_cast<const double2*>(v);
-  r.vb = *reinterpret_cast<const double2*>(v + 16 * S);
+  r.acc = x;
+  r.slots = p + 8 * t;
+  r.s0 = *reinterpret_cast<const uint2*>(r.slots);
+  const unsigned z2 = (unsigned)zslot | ((unsigned)zslot << 16);
+  r.s1 = (G > 1) ? *reinterpret_cast<const uint2*>(r.slots + 8 * S) : make_uint2(z2, z2);
+  r.vals = p + 8 * G * S + 16 * t;
+  r.va = *reinterpret_cast<const double2*>(r.vals);
+  r.vb = *reinterpret_cast<const double2*>(r.vals + 16 * S);
+  r.far = reinterpret_cast<const int32_t*>(seg + h1.z);
 }
 
-// dependency value: near -> ring slot, far (sign bit) -> global position-ordered array
+// dependency value: near -> ring slot, far (bit 15) -> the segment's far list -> global
+// position-ordered array
 template <bool FAR>
-__device__ __forceinline__ double gather(const double* ring, const double* z, int sl) {
-#ifdef PSLR_DBG_NOFAR  // timing experiment only: far dependencies read a ring slot (wrong values)
-  return FAR ? ring[sl & 4095] : ring[sl];
-#else
-  return FAR ? ((sl >= 0) ? ring[sl] : z[sl & 0x7fffffff]) : ring[sl];
-#endif
+__device__ __forceinline__ double gather(const double* ring, const double* z, const int32_t* far,
+                                         unsigned sl) {
+  return (FAR && (sl & 0x8000u)) ? z[far[sl & 0x7fffu]] : ring[sl];
+}
+
+template <bool FAR>
+__device__ __forceinline__ double fold4(double acc, uint2 s, double2 va, double2 vb, const double* ring,
+                                        const double* z, const int32_t* far) {
+  const double z0 = gather<FAR>(ring, z, far, s.x & 0xffffu), z1 = gather<FAR>(ring, z, far, s.x >> 16);
+  const double z2 = gather<FAR>(ring, z, far, s.y & 0xffffu), z3 = gather<FAR>(ring, z, far, s.y >> 16);
+  acc = acc - va.x * z0;
+  acc = acc - va.y * z1;
+  acc = acc - vb.x * z2;
+  acc = acc - vb.y * z3;
+  return acc;
 }
 
 // acc -= val_k * z_k over the row's groups in the reference's ascending-column order
 // (padding entries: 0 * 0); group 0's slots and values are in registers.
 template <bool FAR>
 __device__ __forceinline__ double fold_row(double acc, const Row& r, const double* ring, const double* z) {
-  {
-    const double z0 = gather<FAR>(ring, z, r.s0.x), z1 = gather<FAR>(ring, z, r.s0.y);
-    const double z2 = gather<FAR>(ring, z, r.s0.z), z3 = gather<FAR>(ring, z, r.s0.w);
-    acc = acc - r.va.x * z0;
-    acc = acc - r.va.y * z1;
-    acc = acc - r.vb.x * z2;
-    acc = acc - r.vb.y * z3;
-  }
+  acc = fold4<FAR>(acc, r.s0, r.va, r.vb, ring, z, r.far);
   if (r.G > 1) {
-    const uint8_t* v = r.slots + 16 * r.G * r.S + 32 * r.S;  // group 1 values
-    const double2 va = *reinterpret_cast<const double2*>(v);
-    const double2 vb = *reinterpret_cast<const double2*>(v + 16 * r.S);
-    const double z0 = gather<FAR>(ring, z, r.s1.x), z1 = gather<FAR>(ring, z, r.s1.y);
-    const double z2 = gather<FAR>(ring, z, r.s1.z), z3 = gather<FAR>(ring, z, r.s1.w);
-    acc = acc - va.x * z0;
-    acc = acc - va.y * z1;
-    acc = acc - vb.x * z2;
-    acc = acc - vb.y * z3;
+    const uint8_t* v = r.vals + 32 * r.S;  // group 1 values
+    acc = fold4<FAR>(acc, r.s1, *reinterpret_cast<const double2*>(v),
+                     *reinterpret_cast<const double2*>(v + 16 * r.S), ring, z, r.far);
     for (int g = 2; g < r.G; ++g) {  // long rows: the rest straight from the staged segment
-      const int4 sg = *reinterpret_cast<const int4*>(r.slots + 16 * g * r.S);
-      const uint8_t* w = r.slots + 16 * r.G * r.S + 32 * g * r.S;
-      const double2 wa = *reinterpret_cast<const double2*>(w);
-      const double2 wb = *reinterpret_cast<const double2*>(w + 16 * r.S);
-      const double y0 = gather<FAR>(ring, z, sg.x), y1 = gather<FAR>(ring, z, sg.y);
-      const double y2 = gather<FAR>(ring, z, sg.z), y3 = gather<FAR>(ring, z, sg.w);
-      acc = acc - wa.x * y0;
-      acc = acc - wa.y * y1;
-      acc = acc - wb.x * y2;
-      acc = acc - wb.y * y3;
+      const uint2 sg = *reinterpret_cast<const uint2*>(r.slots + 8 * g * r.S);
+      const uint8_t* w = r.vals + 32 * g * r.S;
+      acc = fold4<FAR>(acc, sg, *reinterpret_cast<const double2*>(w),
+                       *reinterpret_cast<const double2*>(w + 16 * r.S), ring, z, r.far);
     }
   }
   return acc;
@@ -456,25 +465,18 @@ __device__ __forceinline__ bool level_step(const StepConst& K, Ctl* ctl, uint8_t
       c.si = 0;
     }
   }
-  int4 nh0 = make_int4(0, 0, 0, 0);
-  int2 nh1 = make_int2(0, 0);
+  int4 nh0 = make_int4(0, 0, 0, 0), nh1 = make_int4(0, 0, 0, 0);
   if (more) {
     nh0 = *reinterpret_cast<const int4*>(nseg_ptr);
-    nh1 = *reinterpret_cast<const int2*>(nseg_ptr + 16);
+    nh1 = make_int4(reinterpret_cast<const int32_t*>(nseg_ptr)[4], reinterpret_cast<const int32_t*>(nseg_ptr)[5],
+                    reinterpret_cast<const int32_t*>(nseg_ptr)[8], 0);  // S, bytes, far_off
   }
 #ifdef PSLR_X_NOFOLD  // timing experiments (tools/knobs.sh): results are wrong
   if (false) {
 #else
   if (cur.wact) {
 #endif
-    // B: U rows start from rhs / sd.  rcp = RN(1/sd): q0 = RN(x rcp) is within an ulp of
-    // x/sd and one fma-corrected step gives RN(x/sd) (Markstein); sd == 1 keeps x as is.
-    double acc = cur.rhs;
-    if (UPPER) {
-      const double q0 = acc * cur.rcp;
-      const double q = fma(fma(-q0, cur.sd, acc), cur.rcp, q0);
-      acc = (cur.sd == 1.0) ? acc : q;
-    }
+    double acc = cur.acc;
     // A + D: gathers and the chain
     acc = (cur.flags & 2) ? fold_row<true>(acc, cur, ring_c, z) : fold_row<false>(acc, cur, ring_c, z);
     // F: publish the row
@@ -548,8 +550,11 @@ __device__ void tri_phase(const StepConst& K, const Streams& S, Ctl* ctl, uint8_
   c.rbase = reinterpret_cast<const int32_t*>(c.seg)[7];
   c.si = 0;
   Row row;
-  load_row<UPPER>(c.seg, *reinterpret_cast<const int4*>(c.seg), *reinterpret_cast<const int2*>(c.seg + 16),
-                  c.rbuf, c.rbase, base, K.ring_mask, K.ring_mask + 1, cadd, row);
+  {
+    const int32_t* h = reinterpret_cast<const int32_t*>(c.seg);
+    load_row<UPPER>(c.seg, *reinterpret_cast<const int4*>(c.seg), make_int4(h[4], h[5], h[8], 0), c.rbuf,
+                    c.rbase, base, K.ring_mask, K.ring_mask + 1, cadd, row);
+  }
   const double* ring_c = ring;
   while (level_step<UPPER>(K, ctl, stages, rhsbuf, c, row, ring_c, ring, base, z, xout, cadd)) {
   }
