@@ -16,6 +16,7 @@
 #include "pslr_internal.h"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <numeric>
 
@@ -141,9 +142,10 @@ int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAna
     return b;
   };
   auto sd_of = [&](int64_t r) { return A.diag[r] * (1.0 / A.diag[r]); };
+  const bool force_explicit = std::getenv("PSLR_EXPLICIT_SD") != nullptr;  // tests: general layout
   auto sd_plain = [&](int64_t r) {
     const double v = sd_of(r);
-    return v == 1.0 || (v == kSdLow && 1.0 / v == 0x1.0000000000001p+0);
+    return !force_explicit && (v == 1.0 || (v == kSdLow && 1.0 / v == 0x1.0000000000001p+0));
   };
   // far dependencies of the row at position s1 within a level ending at lend
   auto row_far = [&](int64_t s1, int64_t lend) {

@@ -246,3 +246,19 @@ def test_full_size_apply_matches_oracle(cfg):
     np.testing.assert_array_equal(z1, P.apply(b))
     b2 = rng.standard_normal(ps.n)
     assert _rel(P.apply(2.0 * b + b2), 2.0 * z1 + P.apply(b2)) <= 1e-10
+
+
+def test_explicit_sd_layout_bitexact(monkeypatch):
+    """The general U-segment layout (explicit sd / rcp arrays, used when a scaled diagonal
+    is neither 1 nor 1 - 2^-53) gives the same bits as the flag layout."""
+    import paper_2002_00917_b200 as pg
+    name = "lap3d6_s4_dt1e-2"
+    meta = G["apply"][name]
+    d = load_npz(f"apply_{name}.npz")
+    A = csr_from(d, "A")
+    cfg = pg.PslrConfig(num_subdomains=meta["s"], series_degree=meta["m"], rank=meta["rank"],
+                        droptol=meta["droptol"], seed=meta["seed"])
+    monkeypatch.setenv("PSLR_EXPLICIT_SD", "1")
+    P = pg.build(A, cfg)
+    np.testing.assert_array_equal(pg.solve_B(P.ctx, d["f"]), d["solve_B"])
+    np.testing.assert_array_equal(pg.apply_neumann(P.ctx, meta["m"], d["v"]), d["apply_neumann"])
