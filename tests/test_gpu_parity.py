@@ -262,3 +262,61 @@ def test_explicit_sd_layout_bitexact(monkeypatch):
     P = pg.build(A, cfg)
     np.testing.assert_array_equal(pg.solve_B(P.ctx, d["f"]), d["solve_B"])
     np.testing.assert_array_equal(pg.apply_neumann(P.ctx, meta["m"], d["v"]), d["apply_neumann"])
+
+
+def _oracle_ctx(P):
+    from oracle import pslr_oracle as O
+    ps = P.system
+    return O.Context(O.System(ps.matrix, O.Perm(ps.perm.forward, ps.perm.inverse), ps.num_parts,
+                              ps.p, ps.q, ps.interior_sizes, ps.interface_sizes, ps.B, ps.E, ps.F, ps.C),
+                     O.BlockFactors([], P.ctx.b_ilu.offsets, P.ctx.b_ilu.L, P.ctx.b_ilu.U),
+                     O.BlockFactors([], P.ctx.c0_ilu.offsets, P.ctx.c0_ilu.L, P.ctx.c0_ilu.U),
+                     P.ctx.C0, P.ctx.Cg)
+
+
+@pytest.mark.parametrize("m", [0, 1, 5, 8])
+def test_series_degree_edge_cases(m):
+    """Alg. 3.2 at series degrees other than the configs' 3/5 (m = 0: no Horner step):
+    the apply against the oracle with the same factors and correction (1e-10), and the
+    correction-free operators bit-exact (preconditioner.py:79-93, schur.py:89-112)."""
+    import paper_2002_00917_b200 as pg
+    from oracle import pslr_oracle as O
+    P, meta, d, A = _build("lap3d6_s4_dt1e-2")
+    octx = _oracle_ctx(P)
+    corr = P.correction
+    OP = O.Preconditioner(octx.system, octx, m, O.Correction(np.asarray(corr.V), corr.H, corr.G, corr.rank))
+    b = np.random.default_rng(7).standard_normal(P.system.n)
+    P.device.ensure_correction(corr)
+    z = P.device.vec_op("pslr_apply", b, P.system.n, P.system.n, m)
+    assert _rel(z, OP.apply(b)) <= 1e-10
+    v = np.random.default_rng(8).standard_normal(P.system.q)
+    np.testing.assert_array_equal(pg.apply_neumann(P.ctx, m, v), O.apply_neumann(octx, m, v))
+    np.testing.assert_array_equal(pg.apply_Err(P.ctx, m, v), O.apply_Err(octx, m, v))
+
+
+def test_rank_zero_apply_bitexact():
+    """rank = 0 (no low-rank correction, lowrank.py:98-105 identity): every step of the
+    apply is a correction-free operator, so it is bit-exact with the oracle."""
+    import paper_2002_00917_b200 as pg
+    from oracle import pslr_oracle as O
+    meta = G["apply"]["lap3d6_s4_dt1e-2"]
+    d = load_npz("apply_lap3d6_s4_dt1e-2.npz")
+    A = csr_from(d, "A")
+    P = pg.build(A, pg.PslrConfig(num_subdomains=meta["s"], series_degree=meta["m"], rank=0,
+                                  droptol=meta["droptol"], seed=meta["seed"]))
+    assert P.correction.rank == 0
+    octx = _oracle_ctx(P)
+    OP = O.Preconditioner(octx.system, octx, meta["m"], O.Correction(np.zeros((P.system.q, 0)),
+                                                                      np.zeros((0, 0)), np.zeros((0, 0)), 0))
+    b = np.random.default_rng(9).standard_normal(P.system.n)
+    np.testing.assert_array_equal(P.apply(b), OP.apply(b))
+
+
+def test_gmres_nonfinite_raises():
+    """krylov.py:81-82: a non-finite recurrence raises ArithmeticError on the device path too."""
+    import paper_2002_00917_b200 as pg
+    P, meta, d, A = _build("lap3d6_s4_dt1e-2")
+    b = np.random.default_rng(0).standard_normal(P.system.n)
+    b[3] = np.nan
+    with pytest.raises(ArithmeticError):
+        pg.gmres(P.matvec, P.apply, b, tol=1e-8, maxit=20)
