@@ -158,6 +158,19 @@ int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAna
     return f;
   };
   if (W >= 0x8000) return fail(PSLR_EINVAL, std::string(name) + ": ring too large for 16-bit slots");
+  // U rows whose value some later row reads as a far dependency: only they need their
+  // value in the global position-ordered array (info bit 30); the others stay in the ring
+  std::vector<uint8_t> far_target;
+  if (upper) {
+    far_target.assign(M.nrows, 0);
+    for (int64_t r = 0; r < M.nrows; ++r) {
+      const int64_t lend_r = A.level_end[r];
+      for (int64_t e = M.indptr[r]; e < M.indptr[r + 1]; ++e) {
+        const int64_t j = M.indices[e];
+        if (j != r && lend_r - A.pos_of_row[j] > W) far_target[j] = 1;
+      }
+    }
+  }
   // current chunk being filled
   int64_t chunk_start = 0, chunk_nseg = 0, chunk_pos0 = 0, chunk_rows = 0;
   auto close_chunk = [&]() {
@@ -265,6 +278,7 @@ int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAna
             } else if (sdv != 1.0) {
               info[t] = (int32_t)((uint32_t)info[t] | 0x80000000u);
             }
+            if (far_target[r]) info[t] = (int32_t)((uint32_t)info[t] | 0x40000000u);
           }
         }
         int64_t nf = 0;

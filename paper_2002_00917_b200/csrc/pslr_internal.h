@@ -43,7 +43,8 @@ constexpr int kChunkRows = 1024;
 //                    far_off, 0, 0, 0}; flags: bit0 ends a level, bit1 has far deps,
 //                    bit2 explicit sd/rcp, bits 8.. first consumer thread
 //   S = nrows rounded up to 4; G = max(1, ceil(w/4)) groups of 4 entries (no-op padding)
-//   int32 info[S]   L: U-position of the row ; U: row id | sd flag (bit 31: sd = 1 - 2^-53)
+//   int32 info[S]   L: U-position of the row ; U: row id | bit 31: sd = 1 - 2^-53
+//                   | bit 30: the row is a far dependency (its value also goes to global z)
 //   U only: double invd[S] [, sd[S], rcp[S] if flags bit2]
 //   uint16 slot[G][S][4]    near: ring slot (<= W, W = zero slot) ; far: 0x8000 | far index
 //   double val[G][2][S][2]  (U values pre-scaled by 1/diag of their column)

@@ -365,8 +365,8 @@ __device__ __forceinline__ void load_row(const uint8_t* seg, const int4 h0, cons
       if (inf < 0) x = div_sd(x, 0x1.fffffffffffffp-1, 0x1.0000000000001p+0);
       p += 8 * S;
     }
-    const int row = inf & 0x7fffffff;
-    r.zidx = gp;
+    const int row = inf & 0x3fffffff;
+    r.zidx = (inf & 0x40000000) ? gp : -1;  // only far-dependency targets go to global z
     r.xidx = row;
     r.cadd = (cadd && r.active) ? __ldg(cadd + row) : 0.0;
   } else {
@@ -483,12 +483,14 @@ __device__ __forceinline__ bool level_step(const StepConst& K, Ctl* ctl, uint8_t
     if (cur.active) {
       ring[cur.ridx] = acc;
 #ifndef PSLR_X_NOSTG
-      z[cur.zidx] = acc;
+      if (!UPPER || cur.zidx >= 0) z[cur.zidx] = acc;
 #endif
       if (UPPER) {
         double x = acc * cur.invd;
         if (cadd) x = x + cur.cadd;
-#ifndef PSLR_X_NOSTG
+#ifdef PSLR_X_XPOS  // timing experiment: x stored in position order (wrong layout)
+        xout[cur.zidx - base + K.int_off[blockIdx.x]] = x;
+#elif !defined(PSLR_X_NOSTG)
         xout[cur.xidx] = x;
 #endif
       }

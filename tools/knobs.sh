@@ -1,11 +1,14 @@
 #!/bin/bash
 # Build timing-experiment variants of libpslr.so (csrc knobs PSLR_X_*) into lib_variants/
 # and run tools/level_floor.py + a short bench against each (on the GPU box).
+#   build: tools/knobs.sh build "base" "NOSTG" "XPOS" ...   run: tools/knobs.sh
 set -e
 cd "$(dirname "$0")/.."
 mkdir -p lib_variants
 if [ "$1" == "build" ]; then
-  for v in base NOFOLD NOLOAD NOBAR NOSTG "NOLOAD NOSTG" "NOFOLD NOLOAD NOSTG"; do
+  shift
+  rm -f lib_variants/*.so
+  for v in "$@"; do
     name=$(echo $v | tr ' ' '_')
     defs=""; for k in $v; do [ "$k" != base ] && defs="$defs -DPSLR_X_$k"; done
     touch paper_2002_00917_b200/csrc/step_kernel.cu
@@ -17,11 +20,10 @@ if [ "$1" == "build" ]; then
 fi
 for f in lib_variants/libpslr_*.so; do
   n=$(basename $f .so)
-  PSLR_LIB=$PWD/$f timeout 120 python tools/level_floor.py 64000 32 2>/dev/null | sed "s/^/$n floor: /"
-  PSLR_LIB=$PWD/$f timeout 300 python bench.py --steps 50 --warmup 3 --no-cpu-baseline --e2e-steps 3 2>/dev/null | python3 -c "
+  PSLR_LIB=$PWD/$f timeout 300 python bench.py --steps 200 --warmup 3 --no-cpu-baseline --e2e-steps 3 --gmres-maxit 0 2>/dev/null | python3 -c "
 import json,sys
 for l in sys.stdin:
     try: d=json.loads(l)
     except: continue
-    print('$n bench: ms/apply %.3f' % d['ms_per_step'], {k: round(v,3) for k,v in d['roofline']['launch_ms'].items()})"
+    print('$n bench: ms/apply %.4f' % d['ms_per_step'], {k: round(v,3) for k,v in d['roofline']['launch_ms'].items()})"
 done
