@@ -145,6 +145,16 @@ __device__ __forceinline__ void trace_clk(const StepConst& K, int code, int arg)
   }
 }
 
+// trace builds: every CTA stamps its phase boundaries (slot 0 start, 1 prepass done,
+// 2..5 phase k start, 6 end) into rows 1024 + b of the counter area (last launch wins)
+__device__ __forceinline__ void trace_cta(const StepConst& K, int slot) {
+  if (PSLR_TRACE_BUILD && K.trace && threadIdx.x == 0 && K.trace_cap >= (1 << 20) && blockIdx.x < 1024) {
+    unsigned long long ns;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
+    K.trace[2 + 2 * K.trace_cap - 8 * 4096 + (1024 + blockIdx.x) * 8 + slot] = (long long)ns;
+  }
+}
+
 // per-chunk / per-level events: only in PSLR_TRACE_BUILD=2 builds (they perturb the level
 // loop's timing; =1 records the phase boundaries only)
 __device__ __forceinline__ void trace_fine(const StepConst& K, int code, int arg) {
@@ -532,6 +542,7 @@ __device__ void tri_phase(const StepConst& K, const Streams& S, Ctl* ctl, uint8_
                           double* rhsbuf, int k, double* ring, int base, double* z, double* xout,
                           const double* cadd) {
   trace_ev(K, 10 + k, 0);
+  trace_cta(K, 2 + k);
   if (threadIdx.x == 0) {
     __threadfence();
     fence_proxy_async();
@@ -672,6 +683,7 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
   asm volatile("griddepcontrol.wait;" ::: "memory");
   trace_begin(K);
   trace_ev(K, 1, S.begin[S.nphase]);
+  trace_cta(K, 0);
   if (threadIdx.x == 0) ring[K.ring_mask + 1] = 0.0;  // the zero slot (visible after the next barrier)
   const int ph_LB = 0, ph_UB = 1;
   const int ph_LC = do_b ? 2 : 0, ph_UC = do_b ? 3 : 1;
@@ -748,6 +760,7 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
     }
     consumer_sync();
     trace_ev(K, 3, 0);
+    trace_cta(K, 1);
     tri_phase<false>(K, S, ctl, stages, rhsbuf, ph_LB, ring, r0, K.zB, nullptr, nullptr);
     tri_phase<true>(K, S, ctl, stages, rhsbuf, ph_UB, ring, r0, K.zB, a.xb, nullptr);
   }
@@ -787,6 +800,7 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
       tri_phase<true>(K, S, ctl, stages, rhsbuf, ph_UC, ring, r0, K.zC, a.yout, a.cadd);
     }
   }
+  trace_cta(K, 6);
 }
 
 int configure_step_kernel(int smem_bytes) {

@@ -119,3 +119,19 @@ if i51.size:
     for k in sorted(set(phase_of[i51].tolist())):
         sel = phase_of[i51] == k
         print(f"   phase {k}: n={sel.sum()}, mean {w[sel].mean():.0f}, sum {w[sel].sum() / 1.965e3:.1f} us")
+# per-CTA phase stamps of the LAST launch traced (trace builds): which block is critical
+cs = buf[2 * (1 << 20) - 8 * 4096:].reshape(4096, 8)[1024:1024 + P.system.num_parts].astype(np.float64)
+if cs[:, 0].sum() > 0:
+    t0 = cs[:, 0].min()
+    end = (cs[:, 6] - t0) / 1e3
+    names_s = ["start", "prepass", "L_B", "U_B", "L_C0", "U_C0", "end"]
+    print("last launch, per CTA (us from the first CTA start): end min %.1f median %.1f max %.1f (CTA %d)"
+          % (end.min(), np.median(end), end.max(), int(end.argmax())))
+    order = np.argsort(-end)[:6]
+    for b in order:
+        row = cs[b]
+        seg = []
+        marks = [(i, row[i]) for i in range(7) if row[i] > 0]
+        for (i, tv), (j, tn) in zip(marks, marks[1:]):
+            seg.append(f"{names_s[i]} {(tn - tv) / 1e3:.1f}")
+        print(f"   CTA {b:3d}: start {(row[0] - t0) / 1e3:6.1f} end {(row[6] - t0) / 1e3:6.1f}  |  " + ", ".join(seg))
