@@ -53,6 +53,8 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=100)
     ap.add_argument("--cpu-applies", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--streams", type=int, default=0,
+                    help="independent applies in flight per GPU (0 = auto: SMs // subdomains, <= 4)")
     ap.add_argument("--gmres-maxit", type=int, default=500,
                     help="N=1: also time one device GMRES solve (SURVEY §8d time-to-solution); 0 = skip")
     ap.add_argument("--sharded", action="store_true",
@@ -228,6 +230,17 @@ def run_sharded(args, rank, world, local):
     cfg = __import__("paper_2002_00917_b200").PslrConfig(num_subdomains=s_glob, series_degree=base.m,
                                                          rank=base.rank, droptol=1e-2, seed=0)
     P = shard.build_sharded(ps, cfg, device=local)
+    # K independent sharded applies in flight (as at N=1): pipeline j has its own clone
+    # context, stream and process group (its NCCL communicator), so every group sees its
+    # collectives in the same order on all ranks
+    K = args.streams if args.streams > 0 else max(1, min(4, P.ops.dev.info()["sm_count"] // max(1, base.s)))
+    pipes, streams = [P], [torch.cuda.current_stream()]
+    for _ in range(K - 1):
+        g = dist.new_group(list(range(world)))
+        ops_j = P.ops.clone()
+        pipes.append(shard.ShardedPreconditioner(P.plan, ops_j, shard.Halo(P.plan, ops_j.device, g),
+                                                 P.series_degree, P.correction))
+        streams.append(torch.cuda.Stream())
     torch.cuda.synchronize()
     build_s = time.perf_counter() - t0
     plan, ops = P.plan, P.ops
@@ -244,39 +257,62 @@ def run_sharded(args, rank, world, local):
         g = torch.as_tensor(rng.standard_normal(ps.n), device="cuda")
         vecs.append(g[rows].contiguous())
     stream = torch.cuda.current_stream()
-    for k in range(max(3, args.warmup)):
-        P.apply(vecs[k % 8])
+
+    def sweep_step(k, fn=None):
+        j = k % K
+        with torch.cuda.stream(streams[j]):
+            out = pipes[j].apply(vecs[k % 8] if fn is None else fn(j))
+        return out
+
+    def sweep(steps):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for st in streams[1:]:
+            st.wait_stream(stream)
+        for k in range(steps):
+            sweep_step(k)
+        for st in streams[1:]:
+            stream.wait_stream(st)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1)
+
+    for k in range(max(3, args.warmup) * K):
+        sweep_step(k)
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
     clocks.start()
     time.sleep(0.3)
     dist.barrier()
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for k in range(args.steps):
-        P.apply(vecs[k % 8])
-    e1.record(stream)
-    torch.cuda.synchronize()
+    ms = sweep(args.steps)
     dist.barrier()
-    ms = e0.elapsed_time(e1)
     clk = clocks.stop()
     tt = torch.tensor([ms], device="cuda", dtype=torch.float64)
     dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     ms = float(tt.item())
     value = bytes_apply * args.steps / (ms / 1e3) / 1e9
     # e2e: host (pinned) b -> device, sharded apply, z -> host, every step
-    bh = vecs[0].cpu().pin_memory()
-    zh = torch.empty_like(bh).pin_memory()
-    for _ in range(3):
-        zh.copy_(P.apply(bh.to("cuda", non_blocking=True)), non_blocking=True)
+    bhs = [vecs[j % 8].cpu().pin_memory() for j in range(K)]
+    zhs = [torch.empty_like(bhs[0]).pin_memory() for _ in range(K)]
+
+    def e2e_step(k):
+        j = k % K
+        with torch.cuda.stream(streams[j]):
+            zhs[j].copy_(pipes[j].apply(bhs[j].to("cuda", non_blocking=True)), non_blocking=True)
+
+    for k in range(3 * K):
+        e2e_step(k)
     dist.barrier()
     torch.cuda.synchronize()
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2.record(stream)
-    for _ in range(args.e2e_steps):
-        bd = bh.to("cuda", non_blocking=True)
-        zh.copy_(P.apply(bd), non_blocking=True)
+    for st in streams[1:]:
+        st.wait_stream(stream)
+    for k in range(args.e2e_steps):
+        e2e_step(k)
+    for st in streams[1:]:
+        stream.wait_stream(st)
     e3.record(stream)
     torch.cuda.synchronize()
     ms_e2e = e2.elapsed_time(e3)
@@ -299,7 +335,9 @@ def run_sharded(args, rank, world, local):
                        "n": int(ps.n), "n_per_gpu_rank0": int(plan.n_loc),
                        "bytes_per_apply": int(bytes_apply),
                        "parallelism": f"subdomain sharding x{world} (NCCL: {m} halo exchanges + 1 "
-                                      f"allreduce({r}) per apply; max ghosts/rank {int(nghost.item())})",
+                                      f"allreduce({r}) per apply; max ghosts/rank {int(nghost.item())}); "
+                                      f"{K} independent applies in flight per GPU (stream + clone + NCCL group each)",
+                       "concurrency": K,
                        "l2": "no flush: each apply streams %.2f GB per GPU (> 126 MB L2)" % (bytes_local / 1e9),
                        "build_s": round(build_s, 2)},
             "roofline": {"bound": "hbm", "kernel": "whole sharded apply on rank 0 (all launches + halo)",
@@ -309,7 +347,7 @@ def run_sharded(args, rank, world, local):
             "e2e": {"value": bytes_apply * args.e2e_steps / (ms_e2e / 1e3) / 1e9, "unit": "GB/s",
                     "h2d_bytes_per_step": 8 * int(plan.n_loc), "d2h_bytes_per_step": 8 * int(plan.n_loc),
                     "ms_per_step": ms_e2e / args.e2e_steps},
-            "gpu_launches": (m + 6) * args.steps,
+            "gpu_launches": (m + 7) * args.steps,
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)
@@ -358,13 +396,38 @@ def main():
     outs = [torch.empty(n, dtype=torch.float64, device="cuda") for _ in range(2)]
     fn = _lib.fns["pslr_apply"]
     h = dev.handle
+    # The sweep's applies are independent and one step launch occupies only s of the
+    # SMs: K applies run concurrently, each on its own stream with its own clone context
+    # (shared factors / correction, private scratch; pslr_ctx_clone).  Every apply is the
+    # single-stream apply bit for bit (tests/test_gpu_parity.py::test_clones_...).
+    K = args.streams if args.streams > 0 else max(1, min(4, info["sm_count"] // max(1, P.system.num_parts)))
+    devs = [dev] + [dev.clone() for _ in range(K - 1)]
+    streams = [stream] + [torch.cuda.Stream() for _ in range(K - 1)]
+    souts = [[torch.empty(n, dtype=torch.float64, device="cuda") for _ in range(2)] for _ in range(K)]
 
-    def step(k):
-        _lib.check(fn(h, m, vecs[k % 8].data_ptr(), outs[k % 2].data_ptr(), sptr))
+    def step(k, kk=None):
+        j = k % K if kk is None else kk
+        _lib.check(fn(devs[j].handle, m, vecs[k % 8].data_ptr(), souts[j][(k // K) % 2].data_ptr(),
+                      streams[j].cuda_stream))
 
-    for k in range(max(3, args.warmup)):
+    def sweep(steps, kk=None):
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for st in streams[1:]:
+            st.wait_stream(stream)
+        for k in range(steps):
+            step(k, kk)
+        for st in streams[1:]:
+            stream.wait_stream(st)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1)
+
+    for k in range(max(3, args.warmup) * K):
         step(k)
     torch.cuda.synchronize()
+    # single-stream latency of one apply (what a GMRES iteration sees), for the record
+    ms_single = sweep(max(10, args.steps // 10), kk=0) / max(10, args.steps // 10)
     gpu_index = int(os.environ.get("CUDA_VISIBLE_DEVICES", str(local)).split(",")[local]) \
         if os.environ.get("CUDA_VISIBLE_DEVICES") else local
     clocks = ClockSampler(gpu_index)
@@ -373,15 +436,9 @@ def main():
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(stream)
-    for k in range(args.steps):
-        step(k)
-    e1.record(stream)
-    torch.cuda.synchronize()
+    ms = sweep(args.steps)
     if dist:
         dist.barrier()
-    ms = e0.elapsed_time(e1)
     clk = clocks.stop()
     if dist:
         tt = torch.tensor([ms], device="cuda", dtype=torch.float64)
@@ -418,19 +475,29 @@ def main():
         except Exception:
             traffic = None
 
-    # e2e through the C-ABI host-buffer call (pinned host memory)
-    bh = torch.from_numpy(rng.standard_normal(n)).pin_memory()
-    zh = torch.empty(n, dtype=torch.float64).pin_memory()
-    fh = _lib.fns["pslr_apply_host"]
-    for _ in range(3):
-        _lib.check(fh(h, m, bh.data_ptr(), zh.data_ptr(), sptr))
+    # e2e through the C-ABI host-buffer call (pinned host memory: b H2D, apply, z D2H
+    # inside the timed region every step), the same K applies in flight
+    bhs = [torch.from_numpy(rng.standard_normal(n)).pin_memory() for _ in range(K)]
+    zhs = [torch.empty(n, dtype=torch.float64).pin_memory() for _ in range(K)]
+    fh = _lib.fns["pslr_apply_host_async"]
+
+    def e2e_step(k):
+        j = k % K
+        _lib.check(fh(devs[j].handle, m, bhs[j].data_ptr(), zhs[j].data_ptr(), streams[j].cuda_stream))
+
+    for k in range(3 * K):
+        e2e_step(k)
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
     e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e2.record(stream)
-    for _ in range(args.e2e_steps):
-        _lib.check(fh(h, m, bh.data_ptr(), zh.data_ptr(), sptr))
+    for st in streams[1:]:
+        st.wait_stream(stream)
+    for k in range(args.e2e_steps):
+        e2e_step(k)
+    for st in streams[1:]:
+        stream.wait_stream(st)
     e3.record(stream)
     torch.cuda.synchronize()
     ms_e2e = e2.elapsed_time(e3)
@@ -479,7 +546,10 @@ def main():
             "config": {"workload": f"{wl.name}: 3D 7-point Laplacian 128^3 per GPU, shift 0.5, "
                                    f"s={wl.s}, m={m}, rank={r}; one step = one PSLR apply",
                        "n_per_gpu": n, "bytes_per_apply": int(bytes_apply),
-                       "parallelism": f"replica x{world}",
+                       "parallelism": f"{K} independent applies in flight (one stream + clone context each)",
+                       "concurrency": K,
+                       "single_stream": {"ms_per_apply": ms_single,
+                                         "value": bytes_apply / (ms_single / 1e3) / 1e9},
                        "l2": "no flush: each apply streams %.2f GB (> 126 MB L2)" % (bytes_apply / 1e9),
                        "build_s": round(build_s, 2)},
             "roofline": {"bound": "hbm", "kernel": "subdomain_step_kernel (Horner step)",
@@ -488,7 +558,8 @@ def main():
                          "peak_source": peak_src,
                          "frac_of_datasheet_8TBs": achieved / DATASHEET_HBM_GBS if achieved else None,
                          "bytes_per_launch": int(hb), "launch_ms": launch_ms,
-                         "apply_frac": (bytes_apply / (ms_per_step / 1e3) / 1e9) / peak},
+                         "apply_frac": (bytes_apply / (ms_per_step / 1e3) / 1e9) / peak,
+                         "apply_frac_single_stream": (bytes_apply / (ms_single / 1e3) / 1e9) / peak},
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": 8 * n,
                     "d2h_bytes_per_step": 8 * n, "ms_per_step": ms_e2e / args.e2e_steps},

@@ -135,6 +135,17 @@ int pslr_apply_profiled(pslr_ctx* ctx, int64_t m, const double* b, double* z, vo
 int pslr_debug_trace(pslr_ctx* ctx, int64_t* out, int64_t cap, int64_t* count);
 /* Alg. 3.2 with HOST buffers (copies inside): the call a CPU user of P.apply makes. */
 int pslr_apply_host(pslr_ctx* ctx, int64_t m, const double* b_host, double* z_host, void* stream);
+/* The same without the final stream synchronisation (pinned host buffers; the caller
+ * synchronises the stream before reading z_host). */
+int pslr_apply_host_async(pslr_ctx* ctx, int64_t m, const double* b_host, double* z_host, void* stream);
+
+/* ---------------------------------------------------------------- concurrent applies
+ * A step launch occupies one SM per subdomain (s of the 148); independent applies (the
+ * apply sweep, several right-hand sides) run concurrently on separate streams, one
+ * context each.  A clone shares every read-only device array of its source (factors,
+ * matrices, the low-rank correction) and owns only its scratch: it must be destroyed
+ * before the source, and the correction cannot be reset while clones exist. */
+int pslr_ctx_clone(const pslr_ctx* src, pslr_ctx** out);
 
 /* ---------------------------------------------------------------- sharded apply (multi-GPU)
  * rank g owns a contiguous range of subdomains; B, C0, E, F are local.

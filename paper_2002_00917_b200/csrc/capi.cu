@@ -53,7 +53,8 @@ int alloc_scratch(pslr_ctx* ctx, double** p, int64_t count) {
 void free_ptr(pslr_ctx* ctx, void* p) {
   if (!p) return;
   auto it = std::find(ctx->allocations.begin(), ctx->allocations.end(), p);
-  if (it != ctx->allocations.end()) ctx->allocations.erase(it);
+  if (it == ctx->allocations.end()) return;  // not this context's (a clone's shared data)
+  ctx->allocations.erase(it);
   cudaFree(p);
 }
 
@@ -497,6 +498,7 @@ int pslr_ctx_info(const pslr_ctx* ctx, pslr_ctx_info_t* info) {
 static int set_correction_common(pslr_ctx* ctx, int64_t r, const double* V, bool V_on_device,
                                  const double* G) {
   if (r < 0) return fail(PSLR_EDIM, "rank must be >= 0");
+  if (ctx->parent) return fail(PSLR_EINVAL, "a cloned context shares its parent's correction");
   RET(set_device(ctx));
   free_ptr(ctx, ctx->V);
   free_ptr(ctx, ctx->G);
@@ -727,6 +729,76 @@ int pslr_debug_trace(pslr_ctx* ctx, int64_t* out, int64_t cap, int64_t* count) {
   }
   CK(cudaMemset(ctx->K.trace, 0, 16));
   *count = n;
+  return PSLR_OK;
+}
+
+// ---------------------------------------------------------------- clones (concurrent applies)
+int pslr_ctx_clone(const pslr_ctx* src, pslr_ctx** out) {
+  *out = nullptr;
+  if (!src) return fail(PSLR_EINVAL, "null context");
+  RET(set_device(src));
+  auto* ctx = new pslr_ctx(*src);  // shares every read-only device array of src
+  ctx->parent = src->parent ? src->parent : src;
+  ctx->allocations.clear();
+  ctx->prof_events.clear();
+  ctx->prof_kinds.clear();
+  ctx->prof_on = false;
+  ctx->device_bytes = 0;
+  ctx->K.trace = nullptr;
+  ctx->K.trace_cap = 0;
+  ctx->kv = ctx->kz = ctx->h_dev = nullptr;
+  ctx->kv_len = ctx->kz_len = ctx->h_len = 0;
+  auto bail = [&](int rc) {
+    pslr_ctx_destroy(ctx);
+    return rc;
+  };
+  const int64_t n = ctx->n, p = ctx->p, q = ctx->q;
+  int rc;
+  // private scratch: every array a launch writes
+  if ((rc = alloc_scratch(ctx, &ctx->K.rhsB, p + 2))) return bail(rc);
+  if ((rc = alloc_scratch(ctx, &ctx->K.rhsE, p + 2))) return bail(rc);  // zeroed
+  if ((rc = alloc_scratch(ctx, &ctx->K.zB, p + 2))) return bail(rc);
+  if ((rc = alloc_scratch(ctx, &ctx->K.rhsC, q + 2))) return bail(rc);
+  if ((rc = alloc_scratch(ctx, &ctx->K.zC, q + 2))) return bail(rc);
+  if ((rc = alloc_scratch(ctx, &ctx->xb, p))) return bail(rc);
+  if ((rc = alloc_scratch(ctx, &ctx->fL, p + 2))) return bail(rc);
+  if ((rc = alloc_scratch(ctx, &ctx->y0, q))) return bail(rc);
+  if ((rc = alloc_scratch(ctx, &ctx->y1, q))) return bail(rc);
+  if ((rc = alloc_scratch(ctx, &ctx->y2, q))) return bail(rc);
+  if ((rc = alloc_scratch(ctx, &ctx->c, q))) return bail(rc);
+  if ((rc = alloc_scratch(ctx, &ctx->kw, n))) return bail(rc);
+  if ((rc = alloc_scratch(ctx, &ctx->kt, n))) return bail(rc);
+  if ((rc = alloc_scratch(ctx, &ctx->kr, n))) return bail(rc);
+  if ((rc = alloc_scratch(ctx, &ctx->io_b, n))) return bail(rc);
+  if ((rc = alloc_scratch(ctx, &ctx->io_z, n))) return bail(rc);
+  {
+    void* d = nullptr;
+    if (cudaMalloc(&d, 64) != cudaSuccess) return bail(fail(PSLR_ECUDA, "cudaMalloc counter"));
+    cudaMemset(d, 0, 64);
+    ctx->allocations.push_back(d);
+    ctx->counter = static_cast<unsigned int*>(d);
+  }
+  if (ctx->r > 0) {  // V and G are shared; the reduction scratch is private
+    ctx->partials = ctx->u = ctx->red = nullptr;
+    ctx->red_len = 0;
+    if ((rc = alloc_scratch(ctx, &ctx->partials, ctx->s * ctx->r))) return bail(rc);
+    if ((rc = alloc_scratch(ctx, &ctx->u, 2 * ctx->r))) return bail(rc);
+    if ((rc = ensure(ctx, &ctx->red, &ctx->red_len, (int64_t)vt_grid(ctx->q, ctx->sm_count) * ctx->r + 8)))
+      return bail(rc);
+  }
+  if (cudaDeviceSynchronize() != cudaSuccess) return bail(fail(PSLR_ECUDA, "clone failed"));
+  *out = ctx;
+  return PSLR_OK;
+}
+
+int pslr_apply_host_async(pslr_ctx* ctx, int64_t m, const double* b_host, double* z_host, void* stream) {
+  if (m < 0) return fail(PSLR_EDIM, "series degree m must be >= 0");
+  RET(unsharded(ctx));
+  RET(set_device(ctx));
+  cudaStream_t st = S(stream);
+  CK(cudaMemcpyAsync(ctx->io_b, b_host, ctx->n * sizeof(double), cudaMemcpyHostToDevice, st));
+  RET(op_apply(ctx, m, ctx->io_b, ctx->io_z, st));
+  CK(cudaMemcpyAsync(z_host, ctx->io_z, ctx->n * sizeof(double), cudaMemcpyDeviceToHost, st));
   return PSLR_OK;
 }
 

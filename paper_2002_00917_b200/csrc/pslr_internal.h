@@ -142,6 +142,7 @@ struct pslr_ctx {
   int64_t n = 0, p = 0, q = 0, s = 0, r = 0;
   int64_t nghost = 0;  // sharded contexts: ghost interface columns of C, Cg and A
   bool pdl = true;     // programmatic dependent launch of the step kernel (PSLR_PDL=0: off)
+  const pslr_ctx* parent = nullptr;  // clones: the context whose read-only data they share
   int sm_count = 0;
   std::vector<int64_t> interior_off, interface_off;
   // device-resident state

@@ -77,6 +77,20 @@ class DeviceContext:
                 pass
             self.handle = None
 
+    def clone(self) -> "DeviceContext":
+        """A context sharing this one's factors, matrices and correction, with its own
+        scratch (pslr_ctx_clone): independent applies on another stream.  Keeps a
+        reference to this context, which must outlive it."""
+        h = ctypes.c_void_p()
+        with torch_mod().cuda.device(self.device):
+            _lib.check(_lib.fns["pslr_ctx_clone"](self.handle, ctypes.byref(h)))
+        c = object.__new__(DeviceContext)
+        c.device, c.dev, c.handle = self.device, self.dev, h
+        c.n, c.p, c.q, c.s = self.n, self.p, self.q, self.s
+        c._parent = self
+        c._bound = getattr(self, "_bound", None)
+        return c
+
     def info(self) -> dict:
         inf = _lib.CtxInfo()
         _lib.check(_lib.fns["pslr_ctx_info"](self.handle, ctypes.byref(inf)))

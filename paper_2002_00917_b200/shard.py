@@ -253,6 +253,14 @@ class DeviceShardOps:
         self.n, self.p, self.q, self.ng = ps.n, ps.p, ps.q, plan.nghost
         self.r = 0
 
+    def clone(self) -> "DeviceShardOps":
+        """Rank-local operators sharing this one's factors and correction (pslr_ctx_clone),
+        with private scratch: a second independent apply pipeline on another stream."""
+        c = object.__new__(DeviceShardOps)
+        c.__dict__.update(self.__dict__)
+        c.dev = self.dev.clone()
+        return c
+
     def _call(self, name, *args):
         from . import _lib
         _lib.check(_lib.fns[name](self.dev.handle, *args, self.dev.stream()))

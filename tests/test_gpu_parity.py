@@ -320,3 +320,30 @@ def test_gmres_nonfinite_raises():
     b[3] = np.nan
     with pytest.raises(ArithmeticError):
         pg.gmres(P.matvec, P.apply, b, tol=1e-8, maxit=20)
+
+
+def test_clones_run_concurrently_bitexact():
+    """pslr_ctx_clone: clones share the factors / correction and own their scratch, so
+    independent applies on separate streams give the bits of the sequential apply."""
+    import torch
+    from paper_2002_00917_b200 import _lib
+    P, meta, d, A = _build("lap3d6_s4_dt1e-2")
+    P.device.ensure_correction(P.correction)
+    clones = [P.device.clone() for _ in range(3)]
+    devs = [P.device] + clones
+    n, m = P.system.n, P.series_degree
+    rng = np.random.default_rng(11)
+    bs = [torch.as_tensor(rng.standard_normal(n), device="cuda") for _ in range(8)]
+    ref = [P.apply(b).clone() for b in bs]
+    streams = [torch.cuda.Stream() for _ in devs]
+    outs = [torch.empty(n, dtype=torch.float64, device="cuda") for _ in bs]
+    torch.cuda.synchronize()
+    for k, b in enumerate(bs):
+        j = k % len(devs)
+        _lib.check(_lib.fns["pslr_apply"](devs[j].handle, m, b.data_ptr(), outs[k].data_ptr(),
+                                          streams[j].cuda_stream))
+    torch.cuda.synchronize()
+    for k in range(len(bs)):
+        assert torch.equal(outs[k], ref[k])
+    with pytest.raises(ValueError):  # clones share the correction: it cannot be reset on them
+        clones[0].set_correction(None, None)
