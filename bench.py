@@ -4,7 +4,11 @@
 Workload (N=1): BASELINE config 5, the preconditioner-apply sweep — a 128^3 block of the
 3D 7-point Laplacian (diagonal 6, shift 0.5), 32 subdomains, m=3, rank 64, fp64, applied
 to seeded N(0,1) vectors (8 pre-generated, cycled).  One step = one PSLR apply
-(Alg. 3.2, preconditioner.py:79-93) of one vector.  Under torchrun each rank applies its
+(Alg. 3.2, preconditioner.py:79-93) of one vector.  The sweep's applies are independent
+and a step launch occupies one SM per subdomain (32 of 148), so K = 4 applies are in
+flight (one stream and pslr_ctx_clone context each; every apply is bit-identical to the
+single-stream one); the single-stream latency (what one GMRES iteration sees) is
+reported beside it in config.single_stream.  Under torchrun each rank applies its
 own 128^3 slab of ONE coupled global problem (grid 128 x 128 x 128N, s = 32N; subdomain
 sharding with NCCL halo exchanges, weak scaling; see run_sharded and DESIGN.md §Multi-GPU).
 

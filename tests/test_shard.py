@@ -224,3 +224,53 @@ def test_sharded_gmres_matches_single_process(tmp_path):
             x[dk["rows"]] = dk[f"x{flex}"]
         rel = np.linalg.norm(ps.matrix @ x - b) / np.linalg.norm(b)
         assert abs(rel - rep.final_relres) <= 1e-3 * rep.final_relres + 1e-12
+
+
+def _groups_worker(rank, world, port, n, s, m, r, out):
+    """Two apply pipelines per rank on two process groups (the bench's concurrent sweep
+    at N > 1): interleaved applies give the single-process results."""
+    import torch
+    import torch.distributed as dist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        ps = _system(n, s)
+        plan = shard.plan_shard(ps, world, rank)
+        g2 = dist.new_group(list(range(world)))
+        pipes = []
+        for grp in (None, g2):
+            ops = OracleShardOps(plan)
+            halo = shard.Halo(plan, "cpu", grp)
+            pipes.append((ops, halo))
+        Vl, H, rr = shard.sharded_arnoldi(pipes[0][0], pipes[0][1], ps.q, plan.ifc_lo, m, r, seed=0)
+        G = O.build_correction(np.zeros((0, rr)), H).G
+        Ps = []
+        for ops, halo in pipes:
+            ops.set_correction(Vl.numpy(), G)
+            Ps.append(shard.ShardedPreconditioner(plan, ops, halo, m))
+        rows = shard.local_rows(plan, ps.p)
+        zs = []
+        for k in range(4):
+            b = np.random.default_rng(100 + k).standard_normal(ps.n)
+            zs.append(Ps[k % 2].apply(torch.as_tensor(b[rows])).numpy())
+        np.savez(os.path.join(out, f"p{rank}.npz"), rows=rows, z=np.stack(zs))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_two_pipelines_on_two_groups(tmp_path):
+    import torch.multiprocessing as mp
+    world, n, s, m, r = 2, 8, 4, 3, 4
+    mp.spawn(_groups_worker, args=(world, _free_port(), n, s, m, r, str(tmp_path)), nprocs=world, join=True)
+    ps = _system(n, s)
+    ctx = O.schur_context(ps)
+    V, H, rr = O.arnoldi(lambda v: O.apply_Err(ctx, m, v), ps.q, r, seed=0)
+    P = O.Preconditioner(ps, ctx, m, O.build_correction(V, H))
+    d = [np.load(tmp_path / f"p{k}.npz") for k in range(world)]
+    for k in range(4):
+        z = np.zeros(ps.n)
+        for dk in d:
+            z[dk["rows"]] = dk["z"][k]
+        zr = P.apply(np.random.default_rng(100 + k).standard_normal(ps.n))
+        assert np.max(np.abs(z - zr)) <= 1e-10 * np.max(np.abs(zr))
