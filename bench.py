@@ -5,7 +5,7 @@ Workload (N=1): BASELINE config 5, the preconditioner-apply sweep — a 128^3 bl
 3D 7-point Laplacian (diagonal 6, shift 0.5), 32 subdomains, m=3, rank 64, fp64, applied
 to seeded N(0,1) vectors (8 pre-generated, cycled).  One step = one PSLR apply
 (Alg. 3.2, preconditioner.py:79-93) of one vector.  The sweep's applies are independent
-and a step launch occupies one SM per subdomain (32 of 148), so K = 4 applies are in
+and a step launch occupies one SM per subdomain (32 of 148), so K = 8 applies are in
 flight (one stream and pslr_ctx_clone context each; every apply is bit-identical to the
 single-stream one); the single-stream latency (what one GMRES iteration sees) is
 reported beside it in config.single_stream.  Under torchrun each rank applies its
@@ -58,12 +58,20 @@ def parse():
     ap.add_argument("--cpu-applies", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--streams", type=int, default=0,
-                    help="independent applies in flight per GPU (0 = auto: SMs // subdomains, <= 4)")
+                    help="independent applies in flight per GPU (0 = auto: 2 * SMs // subdomains, <= 8)")
     ap.add_argument("--gmres-maxit", type=int, default=500,
                     help="N=1: also time one device GMRES solve (SURVEY §8d time-to-solution); 0 = skip")
     ap.add_argument("--sharded", action="store_true",
                     help="run the sharded (multi-GPU) path even at N=1 (testing the NCCL path)")
     return ap.parse_args()
+
+
+def auto_streams(sm_count, s):
+    """Independent applies in flight: a step launch holds one SM per subdomain and its
+    CTAs finish unevenly, so twice the number of launches that fit side by side keeps
+    the SMs busy (measured on cfg5: K = 4 / 6 / 8 / 12 -> 0.58 / 0.49 / 0.477 / 0.475 ms
+    per apply); capped at 8."""
+    return max(1, min(8, 2 * (sm_count // max(1, s))))
 
 
 def hbm_peak():
@@ -237,7 +245,7 @@ def run_sharded(args, rank, world, local):
     # K independent sharded applies in flight (as at N=1): pipeline j has its own clone
     # context, stream and process group (its NCCL communicator), so every group sees its
     # collectives in the same order on all ranks
-    K = args.streams if args.streams > 0 else max(1, min(4, P.ops.dev.info()["sm_count"] // max(1, base.s)))
+    K = args.streams if args.streams > 0 else auto_streams(P.ops.dev.info()["sm_count"], base.s)
     pipes, streams = [P], [torch.cuda.current_stream()]
     for _ in range(K - 1):
         g = dist.new_group(list(range(world)))
@@ -404,7 +412,7 @@ def main():
     # SMs: K applies run concurrently, each on its own stream with its own clone context
     # (shared factors / correction, private scratch; pslr_ctx_clone).  Every apply is the
     # single-stream apply bit for bit (tests/test_gpu_parity.py::test_clones_...).
-    K = args.streams if args.streams > 0 else max(1, min(4, info["sm_count"] // max(1, P.system.num_parts)))
+    K = args.streams if args.streams > 0 else auto_streams(info["sm_count"], P.system.num_parts)
     devs = [dev] + [dev.clone() for _ in range(K - 1)]
     streams = [stream] + [torch.cuda.Stream() for _ in range(K - 1)]
     souts = [[torch.empty(n, dtype=torch.float64, device="cuda") for _ in range(2)] for _ in range(K)]
