@@ -372,7 +372,6 @@ int pslr_ctx_create(pslr_ctx** out, int device, const pslr_system* sys) {
   ctx->K.smem_bytes = (int)(CTL + W * 8 + 128 + nst * (SB + RB));  // ring + zero slot (padded)
   if (configure_step_kernel(ctx->K.smem_bytes) != 0)
     return bail(fail(PSLR_ECUDA, "cannot configure the step kernel's shared memory"));
-  ctx->K.dbg = (int)env_int("PSLR_DBG", 0);
   ctx->pdl = env_int("PSLR_PDL", 1) != 0;
   if (env_int("PSLR_TRACE", 0)) {  // diagnostics: timeline of CTA 0 (pslr_debug_trace)
     const int64_t cap = 1 << 20;

@@ -131,7 +131,6 @@ struct StepConst {
   int smem_bytes = 0;
   long long* trace = nullptr;  // PSLR_TRACE: [count, pad, (code, ns)...] of CTA 0
   long long trace_cap = 0;
-  int dbg = 0;  // PSLR_DBG diagnostics knobs (timing experiments only; results are wrong when set)
 };
 
 }  // namespace pslr

@@ -195,12 +195,12 @@ __device__ __forceinline__ ChunkDesc load_desc(const ChunkDesc* p) {
 //   rhs cursor:  chunk r_u < d_u gets its rhs slice once its phase's rhs is final;
 //   L2 cursor:   bulk prefetch kL2Ahead bytes beyond the issued data.
 __device__ void producer(const Streams& S, Ctl* ctl, uint8_t* stages, double* rhsbuf, int nst,
-                         int stage_bytes, int rhs_stride, int dbg, long long* g_dbg_out) {
+                         int stage_bytes, int rhs_stride, long long* g_dbg_out) {
   if ((threadIdx.x & 31) != 0) return;
   const int np = S.nphase;
   const int total = S.begin[np];
   if (total == 0) return;
-  const int64_t l2ahead = (dbg & 64) ? 0 : kL2Ahead;
+  const int64_t l2ahead = kL2Ahead;
   // data cursor
   int d_u = 0, d_k = 0;
   while (S.begin[d_k + 1] == 0) ++d_k;
@@ -267,12 +267,8 @@ __device__ void producer(const Streams& S, Ctl* ctl, uint8_t* stages, double* rh
       }
       if (ready & (1u << r_k)) {
         const int2 rr = ctl->rrec[st_r];
-        if (dbg & 512) {
-          mbar_arrive(&ctl->full[st_r]);  // diagnostics: no rhs copy
-        } else {
-          mbar_expect_tx(&ctl->full[st_r], (uint32_t)rr.y);
-          bulk_load(rhsbuf + (size_t)st_r * rhs_stride, r_rhs + rr.x, (uint32_t)rr.y, &ctl->full[st_r]);
-        }
+        mbar_expect_tx(&ctl->full[st_r], (uint32_t)rr.y);
+        bulk_load(rhsbuf + (size_t)st_r * rhs_stride, r_rhs + rr.x, (uint32_t)rr.y, &ctl->full[st_r]);
         ++r_u;
         if (++st_r == nst) st_r = 0;
         did = true;
@@ -289,9 +285,7 @@ __device__ void producer(const Streams& S, Ctl* ctl, uint8_t* stages, double* rh
       prefetched += len;
     }
     if (!did) {
-      if (dbg & 16) __nanosleep(200);
-      else if (dbg & 32) __nanosleep(1000);
-      else if (!(dbg & 128)) __nanosleep(20);
+      __nanosleep(20);
       c_idle += clock64() - c_it;
     }
   }
@@ -481,43 +475,25 @@ __device__ __forceinline__ bool level_step(const StepConst& K, Ctl* ctl, uint8_t
     nh1 = make_int4(reinterpret_cast<const int32_t*>(nseg_ptr)[4], reinterpret_cast<const int32_t*>(nseg_ptr)[5],
                     reinterpret_cast<const int32_t*>(nseg_ptr)[8], 0);  // S, bytes, far_off
   }
-#ifdef PSLR_X_NOFOLD  // timing experiments (tools/knobs.sh): results are wrong
-  if (false) {
-#else
   if (cur.wact) {
-#endif
     double acc = cur.acc;
     // A + D: gathers and the chain
     acc = (cur.flags & 2) ? fold_row<true>(acc, cur, ring_c, z) : fold_row<false>(acc, cur, ring_c, z);
     // F: publish the row
     if (cur.active) {
       ring[cur.ridx] = acc;
-#ifndef PSLR_X_NOSTG
       if (!UPPER || cur.zidx >= 0) z[cur.zidx] = acc;
-#endif
       if (UPPER) {
         double x = acc * cur.invd;
         if (cadd) x = x + cur.cadd;
-#ifdef PSLR_X_XPOS  // timing experiment: x stored in position order (wrong layout)
-        xout[cur.zidx - base + K.int_off[blockIdx.x]] = x;
-#elif !defined(PSLR_X_NOSTG)
         xout[cur.xidx] = x;
-#endif
       }
     }
   }
   const int cur_flags = cur.flags;
   const int cur_info = (cur.G << 2) | (cur.nrows << 8);
   // E: the next segment's row, loaded in place (everything it needs before its gathers)
-#ifdef PSLR_X_NOLOAD
-  if (more) {
-    cur.bytes = nh1.y;
-    cur.flags = nh0.z;
-    cur.wact = ((int)threadIdx.x & ~31) < (nh0.z >> 8) + nh0.x && ((int)threadIdx.x & ~31) + 32 > (nh0.z >> 8);
-  }
-#else
   if (more) load_row<UPPER>(nseg_ptr, nh0, nh1, c.rbuf, c.rbase, base, mask, zslot, cadd, cur);
-#endif
   c.seg = nseg_ptr;
   if (chunk_done) {  // the staged chunk is no longer read by this warp
     __syncwarp();
@@ -525,9 +501,7 @@ __device__ __forceinline__ bool level_step(const StepConst& K, Ctl* ctl, uint8_t
   }
   if (cur_flags & 1) {
     trace_fine(K, 40, 0);
-#ifndef PSLR_X_NOBAR
     consumer_sync();
-#endif
     trace_fine(K, 41, 0);
   }
   trace_clk(K, 50, (cur_flags & 1) | (chunk_done ? 2 : 0) | cur_info);
@@ -671,7 +645,7 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
   }
   __syncthreads();
   if (threadIdx.x >= kStepThreads) {  // producer warp (all 32 lanes)
-    producer(S, ctl, stages, rhsbuf, K.nst, K.stage_bytes, K.rhs_stride, K.dbg,
+    producer(S, ctl, stages, rhsbuf, K.nst, K.stage_bytes, K.rhs_stride,
              (K.trace && K.trace_cap >= (1 << 20)) ? K.trace + 2 + 2 * K.trace_cap - 8 * 4096 + b * 8
                                                    : nullptr);
     return;
