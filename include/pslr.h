@@ -139,6 +139,12 @@ int pslr_apply_host(pslr_ctx* ctx, int64_t m, const double* b_host, double* z_ho
  * synchronises the stream before reading z_host). */
 int pslr_apply_host_async(pslr_ctx* ctx, int64_t m, const double* b_host, double* z_host, void* stream);
 
+/* Alg. 3.2 for nv vectors (b, z: nv n-vectors, vector-major, device pointers): pairs of
+ * vectors share one launch sequence (each launch streams the factors once for both and
+ * interleaves their two dependency chains); every vector's result is the single-vector
+ * pslr_apply bit for bit. */
+int pslr_apply_multi(pslr_ctx* ctx, int64_t m, int64_t nv, const double* b, double* z, void* stream);
+
 /* ---------------------------------------------------------------- concurrent applies
  * A step launch occupies one SM per subdomain (s of the 148); independent applies (the
  * apply sweep, several right-hand sides) run concurrently on separate streams, one

@@ -145,8 +145,8 @@ static int mark(pslr_ctx* ctx, int32_t kind, cudaStream_t st) {
   return PSLR_OK;
 }
 
-static int run_step(pslr_ctx* ctx, const StepArgs& a, cudaStream_t st) {
-  CKL(launch_step(ctx, a, st));
+static int run_step(pslr_ctx* ctx, const StepArgs& a, cudaStream_t st, int nv = 1) {
+  CKL(launch_step(ctx, a, st, nv));
   return mark(ctx, a.tag, st);
 }
 
@@ -273,6 +273,118 @@ int op_apply(pslr_ctx* ctx, int64_t m, const double* b, double* z, cudaStream_t 
   return PSLR_OK;
 }
 
+// ---------------------------------------------------------------- two right-hand sides
+// Step constants and interleaved scratch for NV = 2 launches: the ring and the rhs slices
+// double, the factor stages stay (fewer of them fit), the factors are shared with NV = 1.
+static int ensure_nv2(pslr_ctx* ctx) {
+  if (ctx->nv2_ready) return PSLR_OK;
+  const int64_t p = ctx->p, q = ctx->q;
+  StepConst K2 = ctx->K;
+  const int64_t W = (int64_t)ctx->K.ring_mask + 1, SB = ctx->K.stage_bytes, CTL = 256;
+  const int64_t RB2 = ((16 * (kChunkRows + 2)) + 127) / 128 * 128;
+  int64_t nst = (ctx->smem_optin - 1024 - CTL - W * 16 - 128) / (SB + RB2);
+  nst = std::min<int64_t>(nst, 8);
+  if (nst < 2) return fail(PSLR_EINVAL, "not enough shared memory for two right-hand sides per launch");
+  K2.nst = (int)nst;
+  K2.rhs_stride = (int)(RB2 / 8);
+  K2.smem_bytes = (int)(CTL + W * 16 + 128 + nst * (SB + RB2));
+  if (configure_step_kernel(2, K2.smem_bytes) != 0)
+    return fail(PSLR_ECUDA, "cannot configure the two-vector step kernel's shared memory");
+  RET(alloc_scratch(ctx, &K2.rhsB, 2 * (p + 2)));
+  RET(alloc_scratch(ctx, &K2.rhsE, 2 * (p + 2)));  // zeroed: only E rows are ever written
+  RET(alloc_scratch(ctx, &K2.zB, 2 * (p + 2)));
+  RET(alloc_scratch(ctx, &K2.rhsC, 2 * (q + 2)));
+  RET(alloc_scratch(ctx, &K2.zC, 2 * (q + 2)));
+  RET(alloc_scratch(ctx, &ctx->fL2, 2 * (p + 2)));
+  RET(alloc_scratch(ctx, &ctx->g2, 2 * q));
+  RET(alloc_scratch(ctx, &ctx->xb2, 2 * p));
+  RET(alloc_scratch(ctx, &ctx->xF2, 2 * p));
+  RET(alloc_scratch(ctx, &ctx->y0_2, 2 * q));
+  RET(alloc_scratch(ctx, &ctx->y1_2, 2 * q));
+  RET(alloc_scratch(ctx, &ctx->c2, 2 * q));
+  RET(alloc_scratch(ctx, &ctx->yA2, 2 * q));
+  RET(alloc_scratch(ctx, &ctx->yB2, 2 * q));
+  RET(alloc_scratch(ctx, &ctx->yF2, 2 * q));
+  CK(cudaDeviceSynchronize());
+  ctx->K2 = K2;
+  ctx->nv2_ready = true;
+  return PSLR_OK;
+}
+
+// Alg. 3.2 for two vectors at once (b, z: two n-vectors, vector-major): op_apply with every
+// vector interleaved; each vector's arithmetic is the single-vector one bit for bit.
+int op_apply2(pslr_ctx* ctx, int64_t m, const double* b, double* z, cudaStream_t st) {
+  RET(ensure_nv2(ctx));
+  const int64_t q = ctx->q;
+  CKL(launch_permute2(ctx, b, st));
+  RET(mark(ctx, LK_PERMUTE, st));
+  {  // (1) y0 = g - F B^{-1} f
+    StepArgs a;
+    a.b1 = BT_F;
+    a.fL = ctx->fL2;
+    a.xb = ctx->xb2;
+    a.i1 = IT_G;
+    a.g = ctx->g2;
+    a.i2 = IT_FX;
+    a.i2_sub = 1;
+    a.yout = ctx->y0_2;
+    a.tag = LK_FIRST;
+    RET(run_step(ctx, a, st, 2));
+  }
+  // (2) y1 = y0 + V G V^T y0 per vector ; c = C0^{-1} y1
+  const double* y1 = ctx->y0_2;
+  if (ctx->r > 0) {
+    for (int v = 0; v < 2; ++v) {
+      CKL(launch_vt_dot_strided(ctx, ctx->y0_2 + v, 2, st));
+      CKL(launch_vu_add_strided(ctx, ctx->y0_2 + v, 2, ctx->y1_2 + v, 2, st));
+    }
+    RET(mark(ctx, LK_CORE, st));
+    y1 = ctx->y1_2;
+  }
+  double* c = (m == 0) ? ctx->yF2 : ctx->c2;
+  {
+    StepArgs a;
+    a.i1 = IT_G;
+    a.g = y1;
+    a.do_c0 = 1;
+    a.yout = c;
+    a.tag = LK_CORR;
+    RET(run_step(ctx, a, st, 2));
+  }
+  // (3) m Horner steps y = C0^{-1}(Es y) + c
+  const double* src = c;
+  for (int64_t t = 1; t <= m; ++t) {
+    double* dst = (t == m) ? ctx->yF2 : ((t & 1) ? ctx->yA2 : ctx->yB2);
+    StepArgs a;
+    a.b1 = BT_EY;
+    a.yE = src;
+    a.xb = ctx->xb2;
+    a.i1 = IT_FX;
+    a.i2 = IT_CGY;
+    a.i2_sub = 1;
+    a.yC = src;
+    a.do_c0 = 1;
+    a.cadd = c;
+    a.yout = dst;
+    a.tag = LK_HORNER;
+    RET(run_step(ctx, a, st, 2));
+    src = dst;
+  }
+  {  // (4) x = B^{-1}(f - E y)
+    StepArgs a;
+    a.b1 = BT_F;
+    a.fL = ctx->fL2;
+    a.b2 = BT_EY;
+    a.yE = ctx->yF2;
+    a.xb = ctx->xF2;
+    a.tag = LK_LAST;
+    RET(run_step(ctx, a, st, 2));
+  }
+  (void)q;
+  CKL(launch_deinterleave2(ctx, z, st));
+  return PSLR_OK;
+}
+
 int op_apply_err(pslr_ctx* ctx, int64_t m, const double* v, double* out, cudaStream_t st) {
   if (ctx->q == 0) return PSLR_OK;
   double* buf[2] = {ctx->y1, ctx->y2};
@@ -370,7 +482,8 @@ int pslr_ctx_create(pslr_ctx** out, int device, const pslr_system* sys) {
   ctx->K.stage_bytes = (int)SB;
   ctx->K.rhs_stride = (int)(RB / 8);
   ctx->K.smem_bytes = (int)(CTL + W * 8 + 128 + nst * (SB + RB));  // ring + zero slot (padded)
-  if (configure_step_kernel(ctx->K.smem_bytes) != 0)
+  ctx->smem_optin = smem_optin;
+  if (configure_step_kernel(1, ctx->K.smem_bytes) != 0)
     return bail(fail(PSLR_ECUDA, "cannot configure the step kernel's shared memory"));
   ctx->pdl = env_int("PSLR_PDL", 1) != 0;
   if (env_int("PSLR_TRACE", 0)) {  // diagnostics: timeline of CTA 0 (pslr_debug_trace)
@@ -731,6 +844,20 @@ int pslr_debug_trace(pslr_ctx* ctx, int64_t* out, int64_t cap, int64_t* count) {
   return PSLR_OK;
 }
 
+int pslr_apply_multi(pslr_ctx* ctx, int64_t m, int64_t nv, const double* b, double* z, void* stream) {
+  if (m < 0) return fail(PSLR_EDIM, "series degree m must be >= 0");
+  if (nv < 0) return fail(PSLR_EDIM, "number of vectors must be >= 0");
+  RET(unsharded(ctx));
+  RET(set_device(ctx));
+  cudaStream_t st = S(stream);
+  const int64_t n = ctx->n;
+  int64_t v = 0;
+  if (ctx->q > 0 && ctx->p > 0)
+    for (; v + 2 <= nv; v += 2) RET(op_apply2(ctx, m, b + v * n, z + v * n, st));
+  for (; v < nv; ++v) RET(op_apply(ctx, m, b + v * n, z + v * n, st));
+  return PSLR_OK;
+}
+
 // ---------------------------------------------------------------- clones (concurrent applies)
 int pslr_ctx_clone(const pslr_ctx* src, pslr_ctx** out) {
   *out = nullptr;
@@ -747,6 +874,7 @@ int pslr_ctx_clone(const pslr_ctx* src, pslr_ctx** out) {
   ctx->K.trace_cap = 0;
   ctx->kv = ctx->kz = ctx->h_dev = nullptr;
   ctx->kv_len = ctx->kz_len = ctx->h_len = 0;
+  ctx->nv2_ready = false;  // its own two-vector scratch, on first use
   auto bail = [&](int rc) {
     pslr_ctx_destroy(ctx);
     return rc;

@@ -8,6 +8,8 @@
 // sequentially from 0 in CSR order (scipy csr_matvec), so A @ v is bit-exact.
 #include <cuda_runtime.h>
 
+#include <algorithm>
+
 #include "pslr_internal.h"
 
 namespace pslr {
@@ -44,7 +46,7 @@ __global__ void correction_core_kernel(const double* __restrict__ partials, int 
 constexpr int kVtThreads = 256;
 
 __global__ void __launch_bounds__(kVtThreads)
-vt_dot_kernel(const double* __restrict__ V, const double* __restrict__ y, int64_t q, int r,
+vt_dot_kernel(const double* __restrict__ V, const double* __restrict__ y, int64_t ys, int64_t q, int r,
               const double* __restrict__ G, double* __restrict__ partials, double* hu,
               unsigned int* counter) {
   __shared__ double red[kVtThreads / 32][128];
@@ -59,7 +61,7 @@ vt_dot_kernel(const double* __restrict__ V, const double* __restrict__ y, int64_
       double yv[4], vv[4][4];
 #pragma unroll
       for (int u = 0; u < 4; ++u) {
-        yv[u] = __ldg(y + row + u * stride);
+        yv[u] = __ldg(y + (row + u * stride) * ys);
         const double* vr = V + (row + u * stride) * r;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
@@ -74,7 +76,7 @@ vt_dot_kernel(const double* __restrict__ V, const double* __restrict__ y, int64_
           if (c0 + lane + 32 * k < r) acc[k] = acc[k] + vv[u][k] * yv[u];
     }
     for (; row < q; row += stride) {
-      const double yv = __ldg(y + row);
+      const double yv = __ldg(y + row * ys);
       const double* vr = V + row * r;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
@@ -126,8 +128,8 @@ __global__ void gs_kernel(const double* __restrict__ G, const double* __restrict
 
 // out = y + V u (one warp per row, lanes on columns, fixed shuffle-tree reduction)
 __global__ void vu_add_kernel(const double* __restrict__ V, const double* __restrict__ u,
-                              const double* __restrict__ y, double* __restrict__ out, int64_t q,
-                              int r) {
+                              const double* __restrict__ y, int64_t ys, double* __restrict__ out,
+                              int64_t os, int64_t q, int r) {
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
   int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -149,7 +151,7 @@ __global__ void vu_add_kernel(const double* __restrict__ V, const double* __rest
         for (int k = 0; k < 4; ++k) s[k] = s[k] + __shfl_xor_sync(0xffffffffu, s[k], o);
       if (lane == 0)
 #pragma unroll
-        for (int k = 0; k < 4; ++k) out[row + k * nwarps] = __ldg(y + row + k * nwarps) + s[k];
+        for (int k = 0; k < 4; ++k) out[(row + k * nwarps) * os] = __ldg(y + (row + k * nwarps) * ys) + s[k];
     }
   }
   for (; row < q; row += nwarps) {
@@ -158,7 +160,7 @@ __global__ void vu_add_kernel(const double* __restrict__ V, const double* __rest
     for (int c = lane; c < r; c += 32) s = s + __ldg(vr + c) * __ldg(u + c);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s = s + __shfl_xor_sync(0xffffffffu, s, o);
-    if (lane == 0) out[row] = __ldg(y + row) + s;
+    if (lane == 0) out[row * os] = __ldg(y + row * ys) + s;
   }
 }
 
@@ -174,6 +176,57 @@ int launch_permute_f(const pslr_ctx* ctx, const double* f, cudaStream_t st) {
   if (ctx->p == 0) return 0;
   const int blocks = 4 * ctx->sm_count;
   permute_f_kernel<<<blocks, 512, 0, st>>>(ctx->K.LB.lrow, f, ctx->fL, ctx->p);
+  return (int)cudaGetLastError();
+}
+
+// Two right-hand sides ([row][2] interleaved inside the step kernels): b and z are the
+// caller's two vectors of n, vector-major.  fL2[pos][v] = f_v[row at pos], g2[i][v] = g_v[i].
+__global__ void permute2_kernel(const int32_t* __restrict__ lrow, const double* __restrict__ b, int64_t n,
+                                int64_t p, int64_t q, double* __restrict__ fL2, double* __restrict__ g2) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p + q; i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < p) {
+      const int64_t row = __ldg(lrow + i);
+      reinterpret_cast<double2*>(fL2)[i] = make_double2(__ldg(b + row), __ldg(b + n + row));
+    } else {
+      const int64_t k = i - p;
+      reinterpret_cast<double2*>(g2)[k] = make_double2(__ldg(b + p + k), __ldg(b + n + p + k));
+    }
+  }
+}
+
+__global__ void deinterleave2_kernel(const double* __restrict__ x2, const double* __restrict__ y2, int64_t n,
+                                     int64_t p, double* __restrict__ z) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const double2 v = (i < p) ? reinterpret_cast<const double2*>(x2)[i] : reinterpret_cast<const double2*>(y2)[i - p];
+    z[i] = v.x;
+    z[n + i] = v.y;
+  }
+}
+
+int vt_grid(int64_t q, int sm_count);
+
+int launch_permute2(const pslr_ctx* ctx, const double* b, cudaStream_t st) {
+  permute2_kernel<<<4 * ctx->sm_count, 512, 0, st>>>(ctx->K.LB.lrow, b, ctx->n, ctx->p, ctx->q, ctx->fL2, ctx->g2);
+  return (int)cudaGetLastError();
+}
+
+int launch_deinterleave2(const pslr_ctx* ctx, double* z, cudaStream_t st) {
+  deinterleave2_kernel<<<4 * ctx->sm_count, 512, 0, st>>>(ctx->xF2, ctx->yF2, ctx->n, ctx->p, z);
+  return (int)cudaGetLastError();
+}
+
+int launch_vt_dot_strided(pslr_ctx* ctx, const double* y, int64_t ys, cudaStream_t st) {
+  const int g = vt_grid(ctx->q, ctx->sm_count);
+  vt_dot_kernel<<<g, kVtThreads, 0, st>>>(ctx->V, y, ys, ctx->q, (int)ctx->r, ctx->G, ctx->red, ctx->u,
+                                          ctx->counter);
+  return (int)cudaGetLastError();
+}
+
+int launch_vu_add_strided(const pslr_ctx* ctx, const double* y, int64_t ys, double* out, int64_t os,
+                          cudaStream_t st) {
+  const int64_t blocks = std::min<int64_t>((ctx->q + 7) / 8, 8 * (int64_t)ctx->sm_count);
+  vu_add_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, st>>>(ctx->V, ctx->u, y, ys, out, os, ctx->q,
+                                                                        (int)ctx->r);
   return (int)cudaGetLastError();
 }
 
@@ -300,7 +353,7 @@ int vt_grid(int64_t q, int sm_count) {
 // s = V^T y over this context's rows (sharded contexts; h lands in ctx->u[r..2r) first)
 int launch_vt_local(pslr_ctx* ctx, const double* y, double* s, cudaStream_t st) {
   const int g = vt_grid(ctx->q, ctx->sm_count);
-  vt_dot_kernel<<<g, kVtThreads, 0, st>>>(ctx->V, y, ctx->q, (int)ctx->r, nullptr, ctx->red, ctx->u,
+  vt_dot_kernel<<<g, kVtThreads, 0, st>>>(ctx->V, y, 1, ctx->q, (int)ctx->r, nullptr, ctx->red, ctx->u,
                                           ctx->counter);
   if (cudaGetLastError() != cudaSuccess) return 1;
   return (int)cudaMemcpyAsync(s, ctx->u + ctx->r, ctx->r * sizeof(double), cudaMemcpyDeviceToDevice, st);
@@ -314,7 +367,7 @@ int launch_gs(pslr_ctx* ctx, const double* s, cudaStream_t st) {
 // u = G V^T y  (writes ctx->u[0..r), h in ctx->u[r..2r))
 int launch_vt_dot(pslr_ctx* ctx, const double* y, cudaStream_t st) {
   const int g = vt_grid(ctx->q, ctx->sm_count);
-  vt_dot_kernel<<<g, kVtThreads, 0, st>>>(ctx->V, y, ctx->q, (int)ctx->r, ctx->G, ctx->red,
+  vt_dot_kernel<<<g, kVtThreads, 0, st>>>(ctx->V, y, 1, ctx->q, (int)ctx->r, ctx->G, ctx->red,
                                           ctx->u, ctx->counter);
   return (int)cudaGetLastError();
 }
@@ -325,7 +378,7 @@ int launch_vu_add(const pslr_ctx* ctx, const double* y, double* out, cudaStream_
   const int64_t cap = 8 * (int64_t)ctx->sm_count;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  vu_add_kernel<<<(unsigned)blocks, 256, 0, st>>>(ctx->V, ctx->u, y, out, ctx->q, (int)ctx->r);
+  vu_add_kernel<<<(unsigned)blocks, 256, 0, st>>>(ctx->V, ctx->u, y, 1, out, 1, ctx->q, (int)ctx->r);
   return (int)cudaGetLastError();
 }
 

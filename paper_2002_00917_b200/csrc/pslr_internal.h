@@ -142,6 +142,13 @@ struct pslr_ctx {
   int64_t nghost = 0;  // sharded contexts: ghost interface columns of C, Cg and A
   bool pdl = true;     // programmatic dependent launch of the step kernel (PSLR_PDL=0: off)
   const pslr_ctx* parent = nullptr;  // clones: the context whose read-only data they share
+  int smem_optin = 0;
+  // two right-hand sides per launch (pslr_apply_multi): step constants with the doubled
+  // ring / rhs slices and interleaved ([row][2]) scratch, set up on first use
+  bool nv2_ready = false;
+  pslr::StepConst K2;
+  double *fL2 = nullptr, *g2 = nullptr, *xb2 = nullptr, *y0_2 = nullptr, *y1_2 = nullptr;
+  double *c2 = nullptr, *yA2 = nullptr, *yB2 = nullptr, *yF2 = nullptr, *xF2 = nullptr;
   int sm_count = 0;
   std::vector<int64_t> interior_off, interface_off;
   // device-resident state

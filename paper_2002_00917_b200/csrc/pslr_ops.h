@@ -36,8 +36,8 @@ enum LaunchKind : int32_t {
 };
 
 // kernels.cu
-int configure_step_kernel(int smem_bytes);
-int launch_step(const pslr_ctx* ctx, const StepArgs& a, cudaStream_t st);
+int configure_step_kernel(int nv, int smem_bytes);
+int launch_step(const pslr_ctx* ctx, const StepArgs& a, cudaStream_t st, int nv = 1);
 int launch_correction_core(const pslr_ctx* ctx, cudaStream_t st);
 int launch_spmv(const DevCsr& M, const double* x, double* y, cudaStream_t st);
 int launch_multidot(pslr_ctx* ctx, const double* X, int64_t ld, int k, const double* y, int64_t n,
@@ -57,6 +57,12 @@ int launch_vt_local(pslr_ctx* ctx, const double* y, double* s, cudaStream_t st);
 int launch_gs(pslr_ctx* ctx, const double* s, cudaStream_t st);
 int launch_permute_f(const pslr_ctx* ctx, const double* f, cudaStream_t st);
 int launch_vu_add(const pslr_ctx* ctx, const double* y, double* out, cudaStream_t st);
+// two interleaved right-hand sides ([row][2]): strided correction, (de)interleaving
+int launch_vt_dot_strided(pslr_ctx* ctx, const double* y, int64_t ys, cudaStream_t st);
+int launch_vu_add_strided(const pslr_ctx* ctx, const double* y, int64_t ys, double* out, int64_t os,
+                          cudaStream_t st);
+int launch_permute2(const pslr_ctx* ctx, const double* b, cudaStream_t st);
+int launch_deinterleave2(const pslr_ctx* ctx, double* z, cudaStream_t st);
 
 // capi.cu
 int alloc_scratch(pslr_ctx* ctx, double** p, int64_t count);

@@ -195,7 +195,7 @@ __device__ __forceinline__ ChunkDesc load_desc(const ChunkDesc* p) {
 //   rhs cursor:  chunk r_u < d_u gets its rhs slice once its phase's rhs is final;
 //   L2 cursor:   bulk prefetch kL2Ahead bytes beyond the issued data.
 __device__ void producer(const Streams& S, Ctl* ctl, uint8_t* stages, double* rhsbuf, int nst,
-                         int stage_bytes, int rhs_stride, long long* g_dbg_out) {
+                         int stage_bytes, int rhs_stride, int nv, long long* g_dbg_out) {
   if ((threadIdx.x & 31) != 0) return;
   const int np = S.nphase;
   const int total = S.begin[np];
@@ -267,8 +267,9 @@ __device__ void producer(const Streams& S, Ctl* ctl, uint8_t* stages, double* rh
       }
       if (ready & (1u << r_k)) {
         const int2 rr = ctl->rrec[st_r];
-        mbar_expect_tx(&ctl->full[st_r], (uint32_t)rr.y);
-        bulk_load(rhsbuf + (size_t)st_r * rhs_stride, r_rhs + rr.x, (uint32_t)rr.y, &ctl->full[st_r]);
+        mbar_expect_tx(&ctl->full[st_r], (uint32_t)(rr.y * nv));  // nv interleaved right-hand sides
+        bulk_load(rhsbuf + (size_t)st_r * rhs_stride, r_rhs + (size_t)rr.x * nv, (uint32_t)(rr.y * nv),
+                  &ctl->full[st_r]);
         ++r_u;
         if (++st_r == nst) st_r = 0;
         did = true;
@@ -297,19 +298,57 @@ __device__ void producer(const Streams& S, Ctl* ctl, uint8_t* stages, double* rh
 }
 
 // ---------------------------------------------------------------------------------------
+// Right-hand sides per launch: NV = 1, or NV = 2 independent vectors stored interleaved
+// ([row][2]) in every array the step kernel reads or writes.  The two chains of a row share
+// every factor load and interleave (each is the single-vector arithmetic bit for bit).
+template <int NV> struct VecT;
+template <> struct VecT<1> { using T = double; };
+template <> struct VecT<2> { using T = double2; };
+template <int NV> using vt = typename VecT<NV>::T;
+
+template <int NV> __device__ __forceinline__ vt<NV> vzero();
+template <> __device__ __forceinline__ double vzero<1>() { return 0.0; }
+template <> __device__ __forceinline__ double2 vzero<2>() { return make_double2(0.0, 0.0); }
+template <int NV> __device__ __forceinline__ vt<NV> vld(const double* p, int64_t i);
+template <> __device__ __forceinline__ double vld<1>(const double* p, int64_t i) { return p[i]; }
+template <> __device__ __forceinline__ double2 vld<2>(const double* p, int64_t i) {
+  return reinterpret_cast<const double2*>(p)[i];
+}
+template <int NV> __device__ __forceinline__ vt<NV> vldg(const double* p, int64_t i);
+template <> __device__ __forceinline__ double vldg<1>(const double* p, int64_t i) { return __ldg(p + i); }
+template <> __device__ __forceinline__ double2 vldg<2>(const double* p, int64_t i) {
+  return __ldg(reinterpret_cast<const double2*>(p) + i);
+}
+__device__ __forceinline__ void vst(double* p, int64_t i, double v) { p[i] = v; }
+__device__ __forceinline__ void vst(double* p, int64_t i, double2 v) { reinterpret_cast<double2*>(p)[i] = v; }
+// a - v * z, a + v * x, a - b, a + b, a * s  (separately rounded, per component)
+__device__ __forceinline__ double vmsub(double a, double v, double z) { return a - v * z; }
+__device__ __forceinline__ double2 vmsub(double2 a, double v, double2 z) {
+  return make_double2(a.x - v * z.x, a.y - v * z.y);
+}
+__device__ __forceinline__ double vmadd(double a, double v, double x) { return a + v * x; }
+__device__ __forceinline__ double2 vmadd(double2 a, double v, double2 x) {
+  return make_double2(a.x + v * x.x, a.y + v * x.y);
+}
+__device__ __forceinline__ double vsub(double a, double b) { return a - b; }
+__device__ __forceinline__ double2 vsub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__device__ __forceinline__ double vadd(double a, double b) { return a + b; }
+__device__ __forceinline__ double2 vadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double vmul(double a, double s) { return a * s; }
+__device__ __forceinline__ double2 vmul(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
+
 // Consumer side: the level loop.
 //
 // A level's critical path is latency: gather the dependencies from the ring, the
 // sequential DADD chain, store, barrier.  Everything that does not depend on the
 // previous level is loaded one segment ahead: the next segment's header, the row's
-// slots (two groups), its first four values, rhs, U's sd / rcp / invd / cadd.  The step
-// is written as straight-line code (no per-row branches: inactive lanes compute on row
-// 0 of the segment and skip the stores) so the compiler can interleave the next
-// segment's loads and address arithmetic with the current row's gathers and chain.
+// slots (two groups), its first four values, rhs, U's invd / cadd.  The step is written
+// as straight-line code (no per-row branches: inactive lanes compute on row 0 of the
+// segment and skip the stores).
 //
-// Segment layout (pack.cpp): hdr {nrows, w, flags, pos0, S, bytes, nseg, rbase},
-// info[S], [U: sd[S], rcp[S], invd[S]], slot int4[G][S], val double2[G][2][S]; consumer
-// thread tb + t owns row t (tb = flags >> 8), so the segments of one level run side by side.
+// Segment layout (pack.cpp, pslr_internal.h); consumer thread tb + t owns row t
+// (tb = flags >> 8), so the segments of one level run side by side.
+template <int NV>
 struct Row {
   const uint8_t* slots;  // &slot[0][t]  (4 x u16 per row and group)
   const uint8_t* vals;   // &val[0][0][t]
@@ -318,10 +357,11 @@ struct Row {
   bool wact;             // the warp owns rows of this segment (warp-uniform)
   bool active;           // this lane owns a row
   int ridx;              // ring slot of the row
-  int zidx;              // z index: L: U-position ; U: position
+  int zidx;              // z index: L: U-position ; U: position (-1: not a far target)
   int xidx;              // U: xout index (row id)
-  double acc;            // right-hand side (U: already divided by sd)
-  double invd, cadd;     // U epilogue
+  vt<NV> acc;            // right-hand side(s) (U: already divided by sd)
+  double invd;           // U epilogue
+  vt<NV> cadd;
   uint2 s0, s1;          // slot groups 0 and 1 (zero slot when absent)
   double2 va, vb;        // group-0 values
 };
@@ -333,11 +373,14 @@ __device__ __forceinline__ double div_sd(double x, double sd, double rcp) {
   const double q = fma(fma(-q0, sd, x), rcp, q0);
   return (sd == 1.0) ? x : q;
 }
+__device__ __forceinline__ double2 div_sd(double2 x, double sd, double rcp) {
+  return make_double2(div_sd(x.x, sd, rcp), div_sd(x.y, sd, rcp));
+}
 
-template <bool UPPER>
+template <bool UPPER, int NV>
 __device__ __forceinline__ void load_row(const uint8_t* seg, const int4 h0, const int4 h1, const double* rbuf,
                                          int rbase, int base, int mask, int zslot,
-                                         const double* __restrict__ cadd, Row& r) {
+                                         const double* __restrict__ cadd, Row<NV>& r) {
   const int S = h1.x;
   const int G = max(1, (h0.y + 3) >> 2);
   r.flags = h0.z;
@@ -357,7 +400,7 @@ __device__ __forceinline__ void load_row(const uint8_t* seg, const int4 h0, cons
   const uint8_t* p = seg + 48 + 4 * S;
   const int gp = h0.w + t;
   r.ridx = (gp - base) & mask;
-  double x = rbuf[gp - rbase];
+  vt<NV> x = vld<NV>(rbuf, gp - rbase);
   const int inf = info[t];
   if (UPPER) {
     const double* d = reinterpret_cast<const double*>(p);
@@ -372,7 +415,7 @@ __device__ __forceinline__ void load_row(const uint8_t* seg, const int4 h0, cons
     const int row = inf & 0x3fffffff;
     r.zidx = (inf & 0x40000000) ? gp : -1;  // only far-dependency targets go to global z
     r.xidx = row;
-    r.cadd = (cadd && r.active) ? __ldg(cadd + row) : 0.0;
+    r.cadd = (cadd && r.active) ? vldg<NV>(cadd, row) : vzero<NV>();
   } else {
     r.zidx = inf;
   }
@@ -389,38 +432,37 @@ __device__ __forceinline__ void load_row(const uint8_t* seg, const int4 h0, cons
 
 // dependency value: near -> ring slot, far (bit 15) -> the segment's far list -> global
 // position-ordered array
-template <bool FAR>
-__device__ __forceinline__ double gather(const double* ring, const double* z, const int32_t* far,
-                                         unsigned sl) {
-  return (FAR && (sl & 0x8000u)) ? z[far[sl & 0x7fffu]] : ring[sl];
+template <bool FAR, int NV>
+__device__ __forceinline__ vt<NV> gather(const double* ring, const double* z, const int32_t* far, unsigned sl) {
+  return (FAR && (sl & 0x8000u)) ? vld<NV>(z, far[sl & 0x7fffu]) : vld<NV>(ring, sl);
 }
 
-template <bool FAR>
-__device__ __forceinline__ double fold4(double acc, uint2 s, double2 va, double2 vb, const double* ring,
+template <bool FAR, int NV>
+__device__ __forceinline__ vt<NV> fold4(vt<NV> acc, uint2 s, double2 va, double2 vb, const double* ring,
                                         const double* z, const int32_t* far) {
-  const double z0 = gather<FAR>(ring, z, far, s.x & 0xffffu), z1 = gather<FAR>(ring, z, far, s.x >> 16);
-  const double z2 = gather<FAR>(ring, z, far, s.y & 0xffffu), z3 = gather<FAR>(ring, z, far, s.y >> 16);
-  acc = acc - va.x * z0;
-  acc = acc - va.y * z1;
-  acc = acc - vb.x * z2;
-  acc = acc - vb.y * z3;
+  const vt<NV> z0 = gather<FAR, NV>(ring, z, far, s.x & 0xffffu), z1 = gather<FAR, NV>(ring, z, far, s.x >> 16);
+  const vt<NV> z2 = gather<FAR, NV>(ring, z, far, s.y & 0xffffu), z3 = gather<FAR, NV>(ring, z, far, s.y >> 16);
+  acc = vmsub(acc, va.x, z0);
+  acc = vmsub(acc, va.y, z1);
+  acc = vmsub(acc, vb.x, z2);
+  acc = vmsub(acc, vb.y, z3);
   return acc;
 }
 
 // acc -= val_k * z_k over the row's groups in the reference's ascending-column order
 // (padding entries: 0 * 0); group 0's slots and values are in registers.
-template <bool FAR>
-__device__ __forceinline__ double fold_row(double acc, const Row& r, const double* ring, const double* z) {
-  acc = fold4<FAR>(acc, r.s0, r.va, r.vb, ring, z, r.far);
+template <bool FAR, int NV>
+__device__ __forceinline__ vt<NV> fold_row(vt<NV> acc, const Row<NV>& r, const double* ring, const double* z) {
+  acc = fold4<FAR, NV>(acc, r.s0, r.va, r.vb, ring, z, r.far);
   if (r.G > 1) {
     const uint8_t* v = r.vals + 32 * r.S;  // group 1 values
-    acc = fold4<FAR>(acc, r.s1, *reinterpret_cast<const double2*>(v),
-                     *reinterpret_cast<const double2*>(v + 16 * r.S), ring, z, r.far);
+    acc = fold4<FAR, NV>(acc, r.s1, *reinterpret_cast<const double2*>(v),
+                         *reinterpret_cast<const double2*>(v + 16 * r.S), ring, z, r.far);
     for (int g = 2; g < r.G; ++g) {  // long rows: the rest straight from the staged segment
       const uint2 sg = *reinterpret_cast<const uint2*>(r.slots + 8 * g * r.S);
       const uint8_t* w = r.vals + 32 * g * r.S;
-      acc = fold4<FAR>(acc, sg, *reinterpret_cast<const double2*>(w),
-                       *reinterpret_cast<const double2*>(w + 16 * r.S), ring, z, r.far);
+      acc = fold4<FAR, NV>(acc, sg, *reinterpret_cast<const double2*>(w),
+                           *reinterpret_cast<const double2*>(w + 16 * r.S), ring, z, r.far);
     }
   }
   return acc;
@@ -433,9 +475,9 @@ struct Cursor {
   const double* rbuf;
 };
 
-template <bool UPPER>
+template <bool UPPER, int NV>
 __device__ __forceinline__ bool level_step(const StepConst& K, Ctl* ctl, uint8_t* stages, double* rhsbuf,
-                                           Cursor& c, Row& cur, const double* ring_c,
+                                           Cursor& c, Row<NV>& cur, const double* ring_c,
                                            double* ring, int base, double* z, double* xout,
                                            const double* cadd) {
   const int mask = K.ring_mask, zslot = K.ring_mask + 1;
@@ -476,24 +518,24 @@ __device__ __forceinline__ bool level_step(const StepConst& K, Ctl* ctl, uint8_t
                     reinterpret_cast<const int32_t*>(nseg_ptr)[8], 0);  // S, bytes, far_off
   }
   if (cur.wact) {
-    double acc = cur.acc;
     // A + D: gathers and the chain
-    acc = (cur.flags & 2) ? fold_row<true>(acc, cur, ring_c, z) : fold_row<false>(acc, cur, ring_c, z);
+    const vt<NV> acc = (cur.flags & 2) ? fold_row<true, NV>(cur.acc, cur, ring_c, z)
+                                       : fold_row<false, NV>(cur.acc, cur, ring_c, z);
     // F: publish the row
     if (cur.active) {
-      ring[cur.ridx] = acc;
-      if (!UPPER || cur.zidx >= 0) z[cur.zidx] = acc;
+      vst(ring, cur.ridx, acc);
+      if (!UPPER || cur.zidx >= 0) vst(z, cur.zidx, acc);
       if (UPPER) {
-        double x = acc * cur.invd;
-        if (cadd) x = x + cur.cadd;
-        xout[cur.xidx] = x;
+        vt<NV> x = vmul(acc, cur.invd);
+        if (cadd) x = vadd(x, cur.cadd);
+        vst(xout, cur.xidx, x);
       }
     }
   }
   const int cur_flags = cur.flags;
   const int cur_info = (cur.G << 2) | (cur.nrows << 8);
   // E: the next segment's row, loaded in place (everything it needs before its gathers)
-  if (more) load_row<UPPER>(nseg_ptr, nh0, nh1, c.rbuf, c.rbase, base, mask, zslot, cadd, cur);
+  if (more) load_row<UPPER, NV>(nseg_ptr, nh0, nh1, c.rbuf, c.rbase, base, mask, zslot, cadd, cur);
   c.seg = nseg_ptr;
   if (chunk_done) {  // the staged chunk is no longer read by this warp
     __syncwarp();
@@ -511,7 +553,7 @@ __device__ __forceinline__ bool level_step(const StepConst& K, Ctl* ctl, uint8_t
 // Consumer side of one triangular phase.  Callers arrive right after a consumer barrier
 // that follows the last write of the phase's rhs array; the phase ends with the barrier
 // of its last level.
-template <bool UPPER>
+template <bool UPPER, int NV>
 __device__ void tri_phase(const StepConst& K, const Streams& S, Ctl* ctl, uint8_t* stages,
                           double* rhsbuf, int k, double* ring, int base, double* z, double* xout,
                           const double* cadd) {
@@ -536,29 +578,29 @@ __device__ void tri_phase(const StepConst& K, const Streams& S, Ctl* ctl, uint8_
   c.nseg = reinterpret_cast<const int32_t*>(c.seg)[6];
   c.rbase = reinterpret_cast<const int32_t*>(c.seg)[7];
   c.si = 0;
-  Row row;
+  Row<NV> row;
   {
     const int32_t* h = reinterpret_cast<const int32_t*>(c.seg);
-    load_row<UPPER>(c.seg, *reinterpret_cast<const int4*>(c.seg), make_int4(h[4], h[5], h[8], 0), c.rbuf,
-                    c.rbase, base, K.ring_mask, K.ring_mask + 1, cadd, row);
+    load_row<UPPER, NV>(c.seg, *reinterpret_cast<const int4*>(c.seg), make_int4(h[4], h[5], h[8], 0), c.rbuf,
+                        c.rbase, base, K.ring_mask, K.ring_mask + 1, cadd, row);
   }
   const double* ring_c = ring;
-  while (level_step<UPPER>(K, ctl, stages, rhsbuf, c, row, ring_c, ring, base, z, xout, cadd)) {
+  while (level_step<UPPER, NV>(K, ctl, stages, rhsbuf, c, row, ring_c, ring, base, z, xout, cadd)) {
   }
 }
 
 // Four SpMV rows at once (independent gathers in flight): s[j] = sum_e M_ij x_j in CSR
 // order from 0 (scipy csr_matvec).  RO: x is read-only for this launch.
-template <bool RO>
+template <bool RO, int NV>
 __device__ __forceinline__ void spmv4(const DevCsr& M, const int (&row)[4], const bool (&ok)[4],
-                                      const double* x, double (&s)[4]) {
+                                      const double* x, vt<NV> (&s)[4]) {
   int e0[4], e1[4];
   int len = 0;
 #pragma unroll
   for (int j = 0; j < 4; ++j) {
     e0[j] = ok[j] ? __ldg(M.ptr + row[j]) : 0;
     e1[j] = ok[j] ? __ldg(M.ptr + row[j] + 1) : 0;
-    s[j] = 0.0;
+    s[j] = vzero<NV>();
     len = max(len, e1[j] - e0[j]);
   }
   for (int k = 0; k < len; ++k) {
@@ -571,31 +613,33 @@ __device__ __forceinline__ void spmv4(const DevCsr& M, const int (&row)[4], cons
       c[j] = on[j] ? __ldg(M.col + e0[j] + k) : 0;
       v[j] = on[j] ? __ldg(M.val + e0[j] + k) : 0.0;
     }
-    double xv[4];
+    vt<NV> xv[4];
 #pragma unroll
-    for (int j = 0; j < 4; ++j) xv[j] = on[j] ? (RO ? __ldg(x + c[j]) : x[c[j]]) : 0.0;
+    for (int j = 0; j < 4; ++j) xv[j] = on[j] ? (RO ? vldg<NV>(x, c[j]) : vld<NV>(x, c[j])) : vzero<NV>();
 #pragma unroll
     for (int j = 0; j < 4; ++j)
-      if (on[j]) s[j] = s[j] + v[j] * xv[j];
+      if (on[j]) s[j] = vmadd(s[j], v[j], xv[j]);
   }
 }
 
+template <int NV>
 __device__ __forceinline__ void iface_terms4(int kind, const int (&row)[4], const bool (&ok)[4],
-                                             const StepArgs& a, const StepConst& K, double (&t)[4]) {
+                                             const StepArgs& a, const StepConst& K, vt<NV> (&t)[4]) {
   switch (kind) {
     case IT_G:
 #pragma unroll
-      for (int j = 0; j < 4; ++j) t[j] = ok[j] ? __ldg(a.g + row[j]) : 0.0;
+      for (int j = 0; j < 4; ++j) t[j] = ok[j] ? vldg<NV>(a.g, row[j]) : vzero<NV>();
       break;
-    case IT_FX: spmv4<false>(K.F, row, ok, a.xb, t); break;
-    case IT_CY: spmv4<true>(K.C, row, ok, a.yC, t); break;
-    case IT_CGY: spmv4<true>(K.Cg, row, ok, a.yC, t); break;
+    case IT_FX: spmv4<false, NV>(K.F, row, ok, a.xb, t); break;
+    case IT_CY: spmv4<true, NV>(K.C, row, ok, a.yC, t); break;
+    case IT_CGY: spmv4<true, NV>(K.Cg, row, ok, a.yC, t); break;
     default:
 #pragma unroll
-      for (int j = 0; j < 4; ++j) t[j] = 0.0;
+      for (int j = 0; j < 4; ++j) t[j] = vzero<NV>();
   }
 }
 
+template <int NV>
 __global__ void __launch_bounds__(kBlockThreads, 1)
 subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant__ StepConst K) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -605,10 +649,10 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
   const bool do_c = do_i && a.do_c0;
 
   Ctl* ctl = reinterpret_cast<Ctl*>(smem);
-  // [Ctl 256 B][ring: W slots + zero slot, padded to 128 B][nst stages][nst rhs slices]
+  // [Ctl 256 B][ring: (W + zero slot) x NV, padded to 128 B][nst stages][nst rhs slices]
   // The ring sits at a constant offset, so a gather is one address op on its slot.
   double* ring = reinterpret_cast<double*>(smem + 256);
-  uint8_t* stages = smem + 256 + (size_t)(K.ring_mask + 1) * 8 + 128;
+  uint8_t* stages = smem + 256 + (size_t)(K.ring_mask + 1) * 8 * NV + 128;
   double* rhsbuf = reinterpret_cast<double*>(stages + (size_t)K.nst * K.stage_bytes);
 
   // The stream table lives in shared memory: dynamically indexed per-thread arrays would
@@ -645,7 +689,7 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
   }
   __syncthreads();
   if (threadIdx.x >= kStepThreads) {  // producer warp (all 32 lanes)
-    producer(S, ctl, stages, rhsbuf, K.nst, K.stage_bytes, K.rhs_stride,
+    producer(S, ctl, stages, rhsbuf, K.nst, K.stage_bytes, K.rhs_stride, NV,
              (K.trace && K.trace_cap >= (1 << 20)) ? K.trace + 2 + 2 * K.trace_cap - 8 * 4096 + b * 8
                                                    : nullptr);
     return;
@@ -658,7 +702,7 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
   trace_begin(K);
   trace_ev(K, 1, S.begin[S.nphase]);
   trace_cta(K, 0);
-  if (threadIdx.x == 0) ring[K.ring_mask + 1] = 0.0;  // the zero slot (visible after the next barrier)
+  if (threadIdx.x == 0) vst(ring, K.ring_mask + 1, vzero<NV>());  // the zero slot (visible after the next barrier)
   const int ph_LB = 0, ph_UB = 1;
   const int ph_LC = do_b ? 2 : 0, ph_UC = do_b ? 3 : 1;
   const int tid = threadIdx.x;
@@ -675,21 +719,21 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
     } else if (a.b1 == BT_F) {
       constexpr int kIn = 8;  // independent loads in flight per thread
       for (int row0 = r0 + tid; row0 < r1; row0 += kIn * kStepThreads) {
-        double v[kIn];
+        vt<NV> v[kIn];
         int pos[kIn];
 #pragma unroll
         for (int j = 0; j < kIn; ++j) {
           const int row = row0 + j * kStepThreads;
           const bool ok = row < r1;
-          v[j] = ok ? __ldg(a.f + row) : 0.0;
+          v[j] = ok ? vldg<NV>(a.f, row) : vzero<NV>();
           pos[j] = ok ? __ldg(K.LB.lpos + row) : 0;
         }
 #pragma unroll
         for (int j = 0; j < kIn; ++j)
-          if (row0 + j * kStepThreads < r1) K.rhsB[pos[j]] = v[j];
+          if (row0 + j * kStepThreads < r1) vst(K.rhsB, pos[j], v[j]);
       }
     } else {
-      for (int p = r0 + tid; p < r1; p += kStepThreads) K.rhsB[p] = 0.0;
+      for (int p = r0 + tid; p < r1; p += kStepThreads) vst(K.rhsB, p, vzero<NV>());
     }
     // pass 2: rows with E entries get the E y term: f - E y, or E y alone (scipy
     // csr_matvec order), kIn rows per thread in flight; one int4 record per row
@@ -700,21 +744,23 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
       const int4* rec = reinterpret_cast<const int4*>(K.erows);
       for (int i0 = e0 + tid; i0 < e1; i0 += kIn * kStepThreads) {
         int4 r[kIn];
-        double fv[kIn], sum[kIn];
+        vt<NV> fv[kIn], sum[kIn];
         int len = 0;
 #pragma unroll
         for (int j = 0; j < kIn; ++j) {
           const int i = i0 + j * kStepThreads;
           r[j] = i < e1 ? __ldg(rec + i) : make_int4(0, 0, 0, 0);
           len = max(len, r[j].w - r[j].z);
-          sum[j] = 0.0;
+          sum[j] = vzero<NV>();
         }
 #pragma unroll
         for (int j = 0; j < kIn; ++j)
-          fv[j] = (a.b1 == BT_F && r[j].w > r[j].z) ? (a.fL ? a.fL[r[j].x] : __ldg(a.f + r[j].y)) : 0.0;
+          fv[j] = (a.b1 == BT_F && r[j].w > r[j].z) ? (a.fL ? vld<NV>(a.fL, r[j].x) : vldg<NV>(a.f, r[j].y))
+                                                    : vzero<NV>();
         for (int k = 0; k < len; ++k) {
           int c[kIn];
-          double v[kIn], yv[kIn];
+          double v[kIn];
+          vt<NV> yv[kIn];
 #pragma unroll
           for (int j = 0; j < kIn; ++j) {
             const bool on = r[j].z + k < r[j].w;
@@ -722,21 +768,21 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
             v[j] = on ? __ldg(K.E.val + r[j].z + k) : 0.0;
           }
 #pragma unroll
-          for (int j = 0; j < kIn; ++j) yv[j] = (r[j].z + k < r[j].w) ? __ldg(a.yE + c[j]) : 0.0;
+          for (int j = 0; j < kIn; ++j) yv[j] = (r[j].z + k < r[j].w) ? vldg<NV>(a.yE, c[j]) : vzero<NV>();
 #pragma unroll
           for (int j = 0; j < kIn; ++j)
-            if (r[j].z + k < r[j].w) sum[j] = sum[j] + v[j] * yv[j];
+            if (r[j].z + k < r[j].w) sum[j] = vmadd(sum[j], v[j], yv[j]);
         }
 #pragma unroll
         for (int j = 0; j < kIn; ++j)
-          if (i0 + j * kStepThreads < e1) rhs[r[j].x] = (a.b1 == BT_F) ? (fv[j] - sum[j]) : sum[j];
+          if (i0 + j * kStepThreads < e1) vst(rhs, r[j].x, (a.b1 == BT_F) ? vsub(fv[j], sum[j]) : sum[j]);
       }
     }
     consumer_sync();
     trace_ev(K, 3, 0);
     trace_cta(K, 1);
-    tri_phase<false>(K, S, ctl, stages, rhsbuf, ph_LB, ring, r0, K.zB, nullptr, nullptr);
-    tri_phase<true>(K, S, ctl, stages, rhsbuf, ph_UB, ring, r0, K.zB, a.xb, nullptr);
+    tri_phase<false, NV>(K, S, ctl, stages, rhsbuf, ph_LB, ring, r0, K.zB, nullptr, nullptr);
+    tri_phase<true, NV>(K, S, ctl, stages, rhsbuf, ph_UB, ring, r0, K.zB, a.xb, nullptr);
   }
   if (do_i) {
     const int r0 = K.ifc_off[b], r1 = K.ifc_off[b + 1];
@@ -748,56 +794,60 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
         row[j] = row0 + j * kStepThreads;
         ok[j] = row[j] < r1;
       }
-      double w[4], t2[4];
-      iface_terms4(a.i1, row, ok, a, K, w);
+      vt<NV> w[4], t2[4];
+      iface_terms4<NV>(a.i1, row, ok, a, K, w);
       if (a.i2 != IT_NONE) {
-        iface_terms4(a.i2, row, ok, a, K, t2);
+        iface_terms4<NV>(a.i2, row, ok, a, K, t2);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) w[j] = a.i2_sub ? (w[j] - t2[j]) : (w[j] + t2[j]);
+        for (int j = 0; j < 4; ++j) w[j] = a.i2_sub ? vsub(w[j], t2[j]) : vadd(w[j], t2[j]);
       }
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         if (!ok[j]) continue;
         if (do_c) {
-          K.rhsC[__ldg(K.LC.lpos + row[j])] = w[j];
+          vst(K.rhsC, __ldg(K.LC.lpos + row[j]), w[j]);
         } else {
-          double y = w[j];
-          if (a.cadd) y = y + __ldg(a.cadd + row[j]);
-          a.yout[row[j]] = y;
+          vt<NV> y = w[j];
+          if (a.cadd) y = vadd(y, vldg<NV>(a.cadd, row[j]));
+          vst(a.yout, row[j], y);
         }
       }
     }
     consumer_sync();
     trace_ev(K, 30, 0);
     if (do_c) {
-      tri_phase<false>(K, S, ctl, stages, rhsbuf, ph_LC, ring, r0, K.zC, nullptr, nullptr);
-      tri_phase<true>(K, S, ctl, stages, rhsbuf, ph_UC, ring, r0, K.zC, a.yout, a.cadd);
+      tri_phase<false, NV>(K, S, ctl, stages, rhsbuf, ph_LC, ring, r0, K.zC, nullptr, nullptr);
+      tri_phase<true, NV>(K, S, ctl, stages, rhsbuf, ph_UC, ring, r0, K.zC, a.yout, a.cadd);
     }
   }
   trace_cta(K, 6);
 }
 
-int configure_step_kernel(int smem_bytes) {
-  return (int)cudaFuncSetAttribute(subdomain_step_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   smem_bytes);
+int configure_step_kernel(int nv, int smem_bytes) {
+  return nv == 2 ? (int)cudaFuncSetAttribute(subdomain_step_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             smem_bytes)
+                 : (int)cudaFuncSetAttribute(subdomain_step_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             smem_bytes);
 }
 
-int launch_step(const pslr_ctx* ctx, const StepArgs& a, cudaStream_t st) {
+int launch_step(const pslr_ctx* ctx, const StepArgs& a, cudaStream_t st, int nv) {
   if (ctx->s == 0) return 0;
+  const StepConst& K = (nv == 2) ? ctx->K2 : ctx->K;
   // programmatic stream serialization: the step kernel's CTAs (one per subdomain, far
   // fewer than the 148 SMs) launch and stage their first factor chunks while the
   // previous kernel drains; griddepcontrol.wait orders the data accesses
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)ctx->s);
   cfg.blockDim = dim3(kBlockThreads);
-  cfg.dynamicSmemBytes = (size_t)ctx->K.smem_bytes;
+  cfg.dynamicSmemBytes = (size_t)K.smem_bytes;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = ctx->pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return (int)cudaLaunchKernelEx(&cfg, subdomain_step_kernel, a, ctx->K);
+  if (nv == 2) return (int)cudaLaunchKernelEx(&cfg, subdomain_step_kernel<2>, a, K);
+  return (int)cudaLaunchKernelEx(&cfg, subdomain_step_kernel<1>, a, K);
 }
 
 }  // namespace pslr
