@@ -59,6 +59,9 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--streams", type=int, default=0,
                     help="independent applies in flight per GPU (0 = auto: 2 * SMs // subdomains, <= 8)")
+    ap.add_argument("--nv", type=int, default=2,
+                    help="right-hand sides per apply call in the N=1 sweep (pslr_apply_multi: the "
+                         "vectors share one launch sequence); 1 = pslr_apply")
     ap.add_argument("--gmres-maxit", type=int, default=500,
                     help="N=1: also time one device GMRES solve (SURVEY §8d time-to-solution); 0 = skip")
     ap.add_argument("--sharded", action="store_true",
@@ -405,22 +408,35 @@ def main():
     sptr = stream.cuda_stream
     rng = np.random.default_rng(0)
     vecs = [torch.from_numpy(rng.standard_normal(n)).cuda() for _ in range(8)]
+    vmat = torch.stack(vecs).contiguous()
     outs = [torch.empty(n, dtype=torch.float64, device="cuda") for _ in range(2)]
     fn = _lib.fns["pslr_apply"]
+    fm = _lib.fns["pslr_apply_multi"]
     h = dev.handle
     # The sweep's applies are independent and one step launch occupies only s of the
-    # SMs: K applies run concurrently, each on its own stream with its own clone context
-    # (shared factors / correction, private scratch; pslr_ctx_clone).  Every apply is the
-    # single-stream apply bit for bit (tests/test_gpu_parity.py::test_clones_...).
+    # SMs: K apply calls run concurrently, each on its own stream with its own clone
+    # context (shared factors / correction, private scratch; pslr_ctx_clone), and each
+    # call carries NV right-hand sides through one launch sequence (pslr_apply_multi: the
+    # factors stream once for both vectors).  Every vector's result is the single-vector
+    # apply bit for bit (tests/test_gpu_parity.py::test_clones_...,
+    # ::test_apply_multi_bitexact).
     K = args.streams if args.streams > 0 else auto_streams(info["sm_count"], P.system.num_parts)
+    NV = max(1, min(args.nv, 8))
+    calls = -(-args.steps // NV)
+    args.steps = calls * NV  # one step = one vector's apply
     devs = [dev] + [dev.clone() for _ in range(K - 1)]
     streams = [stream] + [torch.cuda.Stream() for _ in range(K - 1)]
-    souts = [[torch.empty(n, dtype=torch.float64, device="cuda") for _ in range(2)] for _ in range(K)]
+    souts = [[torch.empty((NV, n), dtype=torch.float64, device="cuda") for _ in range(2)] for _ in range(K)]
 
     def step(k, kk=None):
         j = k % K if kk is None else kk
-        _lib.check(fn(devs[j].handle, m, vecs[k % 8].data_ptr(), souts[j][(k // K) % 2].data_ptr(),
-                      streams[j].cuda_stream))
+        if NV == 1 or kk is not None:
+            _lib.check(fn(devs[j].handle, m, vecs[k % 8].data_ptr(), souts[j][(k // K) % 2].data_ptr(),
+                          streams[j].cuda_stream))
+        else:
+            v0 = (k * NV) % (8 - NV + 1)
+            _lib.check(fm(devs[j].handle, m, NV, vmat[v0].data_ptr(), souts[j][(k // K) % 2].data_ptr(),
+                          streams[j].cuda_stream))
 
     def sweep(steps, kk=None):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -448,7 +464,7 @@ def main():
     if dist:
         dist.barrier()
     torch.cuda.synchronize()
-    ms = sweep(args.steps)
+    ms = sweep(calls)
     if dist:
         dist.barrier()
     clk = clocks.stop()
@@ -489,13 +505,15 @@ def main():
 
     # e2e through the C-ABI host-buffer call (pinned host memory: b H2D, apply, z D2H
     # inside the timed region every step), the same K applies in flight
-    bhs = [torch.from_numpy(rng.standard_normal(n)).pin_memory() for _ in range(K)]
-    zhs = [torch.empty(n, dtype=torch.float64).pin_memory() for _ in range(K)]
-    fh = _lib.fns["pslr_apply_host_async"]
+    bhs = [torch.from_numpy(rng.standard_normal((NV, n))).pin_memory() for _ in range(K)]
+    zhs = [torch.empty((NV, n), dtype=torch.float64).pin_memory() for _ in range(K)]
+    fh = _lib.fns["pslr_apply_multi_host_async"]
+    e2e_calls = -(-args.e2e_steps // NV)
+    args.e2e_steps = e2e_calls * NV
 
     def e2e_step(k):
         j = k % K
-        _lib.check(fh(devs[j].handle, m, bhs[j].data_ptr(), zhs[j].data_ptr(), streams[j].cuda_stream))
+        _lib.check(fh(devs[j].handle, m, NV, bhs[j].data_ptr(), zhs[j].data_ptr(), streams[j].cuda_stream))
 
     for k in range(3 * K):
         e2e_step(k)
@@ -506,7 +524,7 @@ def main():
     e2.record(stream)
     for st in streams[1:]:
         st.wait_stream(stream)
-    for k in range(args.e2e_steps):
+    for k in range(e2e_calls):
         e2e_step(k)
     for st in streams[1:]:
         stream.wait_stream(st)
@@ -558,8 +576,9 @@ def main():
             "config": {"workload": f"{wl.name}: 3D 7-point Laplacian 128^3 per GPU, shift 0.5, "
                                    f"s={wl.s}, m={m}, rank={r}; one step = one PSLR apply",
                        "n_per_gpu": n, "bytes_per_apply": int(bytes_apply),
-                       "parallelism": f"{K} independent applies in flight (one stream + clone context each)",
-                       "concurrency": K,
+                       "parallelism": f"{K} independent apply calls in flight (one stream + clone "
+                                      f"context each), {NV} right-hand sides per call",
+                       "concurrency": K, "vectors_per_call": NV,
                        "single_stream": {"ms_per_apply": ms_single,
                                          "value": bytes_apply / (ms_single / 1e3) / 1e9},
                        "l2": "no flush: each apply streams %.2f GB (> 126 MB L2)" % (bytes_apply / 1e9),
@@ -575,7 +594,7 @@ def main():
             "cpu_baseline": cpu,
             "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": 8 * n,
                     "d2h_bytes_per_step": 8 * n, "ms_per_step": ms_e2e / args.e2e_steps},
-            "gpu_launches": launches_per_apply * args.steps,
+            "gpu_launches": (launches_per_apply + (0 if NV == 1 else (3 if r > 0 else 1))) * calls,
             "solve": solve,
             "clocks": clk,
             "levels": {k: info[k] for k in ("maxdepth_LB", "maxdepth_UB", "maxdepth_LC", "maxdepth_UC")},

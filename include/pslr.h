@@ -144,6 +144,10 @@ int pslr_apply_host_async(pslr_ctx* ctx, int64_t m, const double* b_host, double
  * interleaves their two dependency chains); every vector's result is the single-vector
  * pslr_apply bit for bit. */
 int pslr_apply_multi(pslr_ctx* ctx, int64_t m, int64_t nv, const double* b, double* z, void* stream);
+/* pslr_apply_multi with HOST buffers (pinned for asynchrony), enqueued on `stream` without
+ * synchronising: nv vector-major n-vectors copied in, applied, copied back. */
+int pslr_apply_multi_host_async(pslr_ctx* ctx, int64_t m, int64_t nv, const double* b_host,
+                                double* z_host, void* stream);
 
 /* ---------------------------------------------------------------- concurrent applies
  * A step launch occupies one SM per subdomain (s of the 148); independent applies (the

@@ -90,6 +90,7 @@ EXPORTS = {
     "pslr_apply_host": (c_int, P, c_i64, P, P, P),
     "pslr_apply_host_async": (c_int, P, c_i64, P, P, P),
     "pslr_apply_multi": (c_int, P, c_i64, c_i64, P, P, P),
+    "pslr_apply_multi_host_async": (c_int, P, c_i64, c_i64, P, P, P),
     "pslr_ctx_clone": (c_int, P, ctypes.POINTER(P)),
     "pslr_apply_first": (c_int, P, P, P, P, P),
     "pslr_apply_mid": (c_int, P, P, P, P, P),

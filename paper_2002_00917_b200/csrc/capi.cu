@@ -305,6 +305,8 @@ static int ensure_nv2(pslr_ctx* ctx) {
   RET(alloc_scratch(ctx, &ctx->yA2, 2 * q));
   RET(alloc_scratch(ctx, &ctx->yB2, 2 * q));
   RET(alloc_scratch(ctx, &ctx->yF2, 2 * q));
+  RET(alloc_scratch(ctx, &ctx->io_b2, 2 * ctx->n));
+  RET(alloc_scratch(ctx, &ctx->io_z2, 2 * ctx->n));
   CK(cudaDeviceSynchronize());
   ctx->K2 = K2;
   ctx->nv2_ready = true;
@@ -926,6 +928,31 @@ int pslr_apply_host_async(pslr_ctx* ctx, int64_t m, const double* b_host, double
   CK(cudaMemcpyAsync(ctx->io_b, b_host, ctx->n * sizeof(double), cudaMemcpyHostToDevice, st));
   RET(op_apply(ctx, m, ctx->io_b, ctx->io_z, st));
   CK(cudaMemcpyAsync(z_host, ctx->io_z, ctx->n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  return PSLR_OK;
+}
+
+int pslr_apply_multi_host_async(pslr_ctx* ctx, int64_t m, int64_t nv, const double* b_host,
+                                double* z_host, void* stream) {
+  if (m < 0) return fail(PSLR_EDIM, "series degree m must be >= 0");
+  if (nv < 0) return fail(PSLR_EDIM, "number of vectors must be >= 0");
+  RET(unsharded(ctx));
+  RET(set_device(ctx));
+  cudaStream_t st = S(stream);
+  const int64_t n = ctx->n;
+  int64_t v = 0;
+  if (ctx->q > 0 && ctx->p > 0 && nv >= 2) {
+    RET(ensure_nv2(ctx));
+    for (; v + 2 <= nv; v += 2) {
+      CK(cudaMemcpyAsync(ctx->io_b2, b_host + v * n, 2 * n * sizeof(double), cudaMemcpyHostToDevice, st));
+      RET(op_apply2(ctx, m, ctx->io_b2, ctx->io_z2, st));
+      CK(cudaMemcpyAsync(z_host + v * n, ctx->io_z2, 2 * n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    }
+  }
+  for (; v < nv; ++v) {
+    CK(cudaMemcpyAsync(ctx->io_b, b_host + v * n, n * sizeof(double), cudaMemcpyHostToDevice, st));
+    RET(op_apply(ctx, m, ctx->io_b, ctx->io_z, st));
+    CK(cudaMemcpyAsync(z_host + v * n, ctx->io_z, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  }
   return PSLR_OK;
 }
 

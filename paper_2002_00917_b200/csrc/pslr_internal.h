@@ -149,6 +149,7 @@ struct pslr_ctx {
   pslr::StepConst K2;
   double *fL2 = nullptr, *g2 = nullptr, *xb2 = nullptr, *y0_2 = nullptr, *y1_2 = nullptr;
   double *c2 = nullptr, *yA2 = nullptr, *yB2 = nullptr, *yF2 = nullptr, *xF2 = nullptr;
+  double *io_b2 = nullptr, *io_z2 = nullptr;  // host-buffer two-vector apply staging
   int sm_count = 0;
   std::vector<int64_t> interior_off, interface_off;
   // device-resident state

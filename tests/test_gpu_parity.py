@@ -365,3 +365,24 @@ def test_apply_multi_bitexact(name, nv):
                                             P.device.stream()))
     for v in range(nv):
         np.testing.assert_array_equal(Z[v].cpu().numpy(), P.apply(B[v]).cpu().numpy())
+
+
+def test_apply_multi_host_async_bitexact():
+    """pslr_apply_multi_host_async (pinned host buffers, pairs through one launch sequence,
+    the odd vector through the single-vector path) == pslr_apply per vector, on a clone
+    context and its own stream."""
+    import torch
+    from paper_2002_00917_b200 import _lib
+    P, meta, d, A = _build("cfg1")
+    P.device.ensure_correction(P.correction)
+    n, nv = P.system.n, 3
+    c = P.device.clone()
+    st = torch.cuda.Stream()
+    B = torch.from_numpy(np.random.default_rng(13).standard_normal((nv, n))).pin_memory()
+    Z = torch.empty((nv, n), dtype=torch.float64).pin_memory()
+    _lib.check(_lib.fns["pslr_apply_multi_host_async"](c.handle, P.series_degree, nv, B.data_ptr(),
+                                                       Z.data_ptr(), st.cuda_stream))
+    st.synchronize()
+    for v in range(nv):
+        np.testing.assert_array_equal(Z[v].numpy(), P.apply(B[v].cuda()).cpu().numpy())
+    del c
