@@ -30,6 +30,17 @@ for _v in ("OMP_NUM_THREADS", "OPENBLAS_NUM_THREADS", "MKL_NUM_THREADS"):
 # the JSON line must be the only stdout output: NCCL's own log lines go to stderr
 os.environ.setdefault("NCCL_DEBUG", "WARN")
 os.environ.setdefault("NCCL_DEBUG_FILE", "/dev/stderr")
+# ... and so does anything else a library prints to fd 1 (NCCL's version banner ignores
+# NCCL_DEBUG_FILE on some builds): fd 1 is pointed at stderr, the JSON line goes to a
+# duplicate of the original stdout
+_JSON_FD = os.dup(1)
+os.dup2(2, 1)
+_JSON_OUT = os.fdopen(_JSON_FD, "w")
+
+
+def emit(line):
+    _JSON_OUT.write(__import__("json").dumps(line) + "\n")
+    _JSON_OUT.flush()
 
 import argparse  # noqa: E402
 import json  # noqa: E402
@@ -218,7 +229,7 @@ def run_reference(args):
                                    "orthonormal V"},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def run_sharded(args, rank, world, local):
@@ -272,11 +283,20 @@ def run_sharded(args, rank, world, local):
         g = torch.as_tensor(rng.standard_normal(ps.n), device="cuda")
         vecs.append(g[rows].contiguous())
     stream = torch.cuda.current_stream()
+    # NV right-hand sides per pipeline call (ShardedPreconditioner.apply2: one launch
+    # sequence, one halo per Horner step and one allreduce for both vectors)
+    NV = 2 if args.nv >= 2 else 1
+    pairs = [torch.stack([vecs[2 * i], vecs[2 * i + 1]]).contiguous() for i in range(4)]
+    calls = -(-args.steps // NV)
+    args.steps = calls * NV
 
     def sweep_step(k, fn=None):
         j = k % K
         with torch.cuda.stream(streams[j]):
-            out = pipes[j].apply(vecs[k % 8] if fn is None else fn(j))
+            if NV == 2:
+                out = pipes[j].apply2(pairs[k % 4] if fn is None else fn(j))
+            else:
+                out = pipes[j].apply(vecs[k % 8] if fn is None else fn(j))
         return out
 
     def sweep(steps):
@@ -300,7 +320,7 @@ def run_sharded(args, rank, world, local):
     time.sleep(0.3)
     dist.barrier()
     torch.cuda.synchronize()
-    ms = sweep(args.steps)
+    ms = sweep(calls)
     dist.barrier()
     clk = clocks.stop()
     tt = torch.tensor([ms], device="cuda", dtype=torch.float64)
@@ -308,13 +328,16 @@ def run_sharded(args, rank, world, local):
     ms = float(tt.item())
     value = bytes_apply * args.steps / (ms / 1e3) / 1e9
     # e2e: host (pinned) b -> device, sharded apply, z -> host, every step
-    bhs = [vecs[j % 8].cpu().pin_memory() for j in range(K)]
+    bhs = [(pairs[j % 4] if NV == 2 else vecs[j % 8]).cpu().pin_memory() for j in range(K)]
     zhs = [torch.empty_like(bhs[0]).pin_memory() for _ in range(K)]
+    e2e_calls = -(-args.e2e_steps // NV)
+    args.e2e_steps = e2e_calls * NV
 
     def e2e_step(k):
         j = k % K
         with torch.cuda.stream(streams[j]):
-            zhs[j].copy_(pipes[j].apply(bhs[j].to("cuda", non_blocking=True)), non_blocking=True)
+            bd = bhs[j].to("cuda", non_blocking=True)
+            zhs[j].copy_(pipes[j].apply2(bd) if NV == 2 else pipes[j].apply(bd), non_blocking=True)
 
     for k in range(3 * K):
         e2e_step(k)
@@ -324,7 +347,7 @@ def run_sharded(args, rank, world, local):
     e2.record(stream)
     for st in streams[1:]:
         st.wait_stream(stream)
-    for k in range(args.e2e_steps):
+    for k in range(e2e_calls):
         e2e_step(k)
     for st in streams[1:]:
         stream.wait_stream(st)
@@ -351,8 +374,9 @@ def run_sharded(args, rank, world, local):
                        "bytes_per_apply": int(bytes_apply),
                        "parallelism": f"subdomain sharding x{world} (NCCL: {m} halo exchanges + 1 "
                                       f"allreduce({r}) per apply; max ghosts/rank {int(nghost.item())}); "
-                                      f"{K} independent applies in flight per GPU (stream + clone + NCCL group each)",
-                       "concurrency": K,
+                                      f"{K} independent apply calls in flight per GPU (stream + clone + NCCL group "
+                                      f"each), {NV} right-hand sides per call",
+                       "concurrency": K, "vectors_per_call": NV,
                        "l2": "no flush: each apply streams %.2f GB per GPU (> 126 MB L2)" % (bytes_local / 1e9),
                        "build_s": round(build_s, 2)},
             "roofline": {"bound": "hbm", "kernel": "whole sharded apply on rank 0 (all launches + halo)",
@@ -362,10 +386,10 @@ def run_sharded(args, rank, world, local):
             "e2e": {"value": bytes_apply * args.e2e_steps / (ms_e2e / 1e3) / 1e9, "unit": "GB/s",
                     "h2d_bytes_per_step": 8 * int(plan.n_loc), "d2h_bytes_per_step": 8 * int(plan.n_loc),
                     "ms_per_step": ms_e2e / args.e2e_steps},
-            "gpu_launches": (m + 7) * args.steps,
+            "gpu_launches": ((m + 7) * args.steps if NV == 1 else (m + 11) * calls),
             "clocks": clk,
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     dist.destroy_process_group()
 
 
@@ -599,7 +623,7 @@ def main():
             "clocks": clk,
             "levels": {k: info[k] for k in ("maxdepth_LB", "maxdepth_UB", "maxdepth_LC", "maxdepth_UC")},
         }
-        print(json.dumps(line), flush=True)
+        emit(line)
     if dist:
         dist.destroy_process_group()
 

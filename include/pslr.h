@@ -173,6 +173,15 @@ int pslr_apply_first(pslr_ctx* ctx, const double* b, double* y0, double* s, void
 int pslr_apply_mid(pslr_ctx* ctx, const double* y0, const double* s, double* c, void* stream);
 int pslr_apply_horner(pslr_ctx* ctx, const double* y, const double* c, double* out, void* stream);
 int pslr_apply_last(pslr_ctx* ctx, const double* b, const double* y, double* z, void* stream);
+/* The same split for TWO right-hand sides sharing every launch (pslr_apply_multi's path;
+ * needs p > 0 and q > 0): b, z two vector-major local n-vectors; y0, c, y, out
+ * interleaved interface vectors (value of vector v at interface row i at [2 i + v],
+ * ghosts after the q local rows); s two vector-major r-vectors.  Each vector's result is
+ * the single-vector split apply's bit for bit. */
+int pslr_apply2_first(pslr_ctx* ctx, const double* b, double* y0, double* s, void* stream);
+int pslr_apply2_mid(pslr_ctx* ctx, const double* y0, const double* s, double* c, void* stream);
+int pslr_apply2_horner(pslr_ctx* ctx, const double* y, const double* c, double* out, void* stream);
+int pslr_apply2_last(pslr_ctx* ctx, const double* b, const double* y, double* z, void* stream);
 /* out = C0^{-1}? (F B^{-1} E v - Cg v) with v extended: one E_rr / Arnoldi operator step
  * (schur.py:83-86, 104-112); do_c0 selects the C0 solve. */
 int pslr_apply_es_step(pslr_ctx* ctx, const double* v, double* out, int do_c0, void* stream);

@@ -96,6 +96,10 @@ EXPORTS = {
     "pslr_apply_mid": (c_int, P, P, P, P, P),
     "pslr_apply_horner": (c_int, P, P, P, P, P),
     "pslr_apply_last": (c_int, P, P, P, P, P),
+    "pslr_apply2_first": (c_int, P, P, P, P, P),
+    "pslr_apply2_mid": (c_int, P, P, P, P, P),
+    "pslr_apply2_horner": (c_int, P, P, P, P, P),
+    "pslr_apply2_last": (c_int, P, P, P, P, P),
     "pslr_apply_es_step": (c_int, P, P, P, c_int, P),
     "pslr_apply_profiled": (c_int, P, c_i64, P, P, P, P, P, c_i64, ctypes.POINTER(c_i64)),
     "pslr_debug_trace": (c_int, P, P, c_i64, ctypes.POINTER(c_i64)),

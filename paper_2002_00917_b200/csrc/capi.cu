@@ -383,7 +383,7 @@ int op_apply2(pslr_ctx* ctx, int64_t m, const double* b, double* z, cudaStream_t
     RET(run_step(ctx, a, st, 2));
   }
   (void)q;
-  CKL(launch_deinterleave2(ctx, z, st));
+  CKL(launch_deinterleave2(ctx, ctx->yF2, z, st));
   return PSLR_OK;
 }
 
@@ -779,6 +779,91 @@ int pslr_apply_last(pslr_ctx* ctx, const double* b, const double* y, double* z, 
   a.xb = z;
   a.tag = LK_LAST;
   return run_step(ctx, a, st);
+}
+
+// ---- the split apply for two right-hand sides (op_apply2 cut where ranks exchange data):
+// b, z two vector-major local n-vectors; y0, c, y, out interleaved interface vectors
+// ([i][v], ghosts after the q local rows); s two r-vectors (vector-major).
+static int split2_ok(pslr_ctx* ctx) {
+  if (ctx->p == 0 || ctx->q == 0) return fail(PSLR_EINVAL, "two-vector split apply needs p > 0 and q > 0");
+  return ensure_nv2(ctx);
+}
+
+int pslr_apply2_first(pslr_ctx* ctx, const double* b, double* y0, double* s, void* stream) {
+  RET(set_device(ctx));
+  RET(split2_ok(ctx));
+  cudaStream_t st = S(stream);
+  CKL(launch_permute2(ctx, b, st));  // fL2 kept for pslr_apply2_last
+  StepArgs a;
+  a.b1 = BT_F;
+  a.fL = ctx->fL2;
+  a.xb = ctx->xb2;
+  a.i1 = IT_G;
+  a.g = ctx->g2;
+  a.i2 = IT_FX;
+  a.i2_sub = 1;
+  a.yout = y0;
+  a.tag = LK_FIRST;
+  RET(run_step(ctx, a, st, 2));
+  if (ctx->r > 0)
+    for (int v = 0; v < 2; ++v) CKL(launch_vt_local_strided(ctx, y0 + v, 2, s + v * ctx->r, st));
+  return PSLR_OK;
+}
+
+int pslr_apply2_mid(pslr_ctx* ctx, const double* y0, const double* s, double* c, void* stream) {
+  RET(set_device(ctx));
+  RET(split2_ok(ctx));
+  cudaStream_t st = S(stream);
+  const double* y1 = y0;
+  if (ctx->r > 0) {
+    for (int v = 0; v < 2; ++v) {
+      CKL(launch_gs(ctx, s + v * ctx->r, st));
+      CKL(launch_vu_add_strided(ctx, y0 + v, 2, ctx->y1_2 + v, 2, st));
+    }
+    y1 = ctx->y1_2;
+  }
+  StepArgs a;
+  a.i1 = IT_G;
+  a.g = y1;
+  a.do_c0 = 1;
+  a.yout = c;
+  a.tag = LK_CORR;
+  return run_step(ctx, a, st, 2);
+}
+
+int pslr_apply2_horner(pslr_ctx* ctx, const double* y, const double* c, double* out, void* stream) {
+  RET(set_device(ctx));
+  RET(split2_ok(ctx));
+  StepArgs a;
+  a.b1 = BT_EY;
+  a.yE = y;
+  a.xb = ctx->xb2;
+  a.i1 = IT_FX;
+  a.i2 = IT_CGY;
+  a.i2_sub = 1;
+  a.yC = y;
+  a.do_c0 = 1;
+  a.cadd = c;
+  a.yout = out;
+  a.tag = LK_HORNER;
+  return run_step(ctx, a, S(stream), 2);
+}
+
+int pslr_apply2_last(pslr_ctx* ctx, const double* b, const double* y, double* z, void* stream) {
+  RET(set_device(ctx));
+  RET(split2_ok(ctx));
+  (void)b;  // its permuted copy fL2 is from pslr_apply2_first of the same b
+  cudaStream_t st = S(stream);
+  StepArgs a;
+  a.b1 = BT_F;
+  a.fL = ctx->fL2;
+  a.b2 = BT_EY;
+  a.yE = y;
+  a.xb = ctx->xF2;
+  a.tag = LK_LAST;
+  RET(run_step(ctx, a, st, 2));
+  CKL(launch_deinterleave2(ctx, y, z, st));
+  return PSLR_OK;
 }
 
 int pslr_spmv(pslr_ctx* ctx, int which, const double* x, double* y, void* stream) {

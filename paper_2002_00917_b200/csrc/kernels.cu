@@ -210,8 +210,8 @@ int launch_permute2(const pslr_ctx* ctx, const double* b, cudaStream_t st) {
   return (int)cudaGetLastError();
 }
 
-int launch_deinterleave2(const pslr_ctx* ctx, double* z, cudaStream_t st) {
-  deinterleave2_kernel<<<4 * ctx->sm_count, 512, 0, st>>>(ctx->xF2, ctx->yF2, ctx->n, ctx->p, z);
+int launch_deinterleave2(const pslr_ctx* ctx, const double* y2, double* z, cudaStream_t st) {
+  deinterleave2_kernel<<<4 * ctx->sm_count, 512, 0, st>>>(ctx->xF2, y2, ctx->n, ctx->p, z);
   return (int)cudaGetLastError();
 }
 
@@ -354,6 +354,15 @@ int vt_grid(int64_t q, int sm_count) {
 int launch_vt_local(pslr_ctx* ctx, const double* y, double* s, cudaStream_t st) {
   const int g = vt_grid(ctx->q, ctx->sm_count);
   vt_dot_kernel<<<g, kVtThreads, 0, st>>>(ctx->V, y, 1, ctx->q, (int)ctx->r, nullptr, ctx->red, ctx->u,
+                                          ctx->counter);
+  if (cudaGetLastError() != cudaSuccess) return 1;
+  return (int)cudaMemcpyAsync(s, ctx->u + ctx->r, ctx->r * sizeof(double), cudaMemcpyDeviceToDevice, st);
+}
+
+// s = V^T y for a strided y (rank-local partial sums; no G)
+int launch_vt_local_strided(pslr_ctx* ctx, const double* y, int64_t ys, double* s, cudaStream_t st) {
+  const int g = vt_grid(ctx->q, ctx->sm_count);
+  vt_dot_kernel<<<g, kVtThreads, 0, st>>>(ctx->V, y, ys, ctx->q, (int)ctx->r, nullptr, ctx->red, ctx->u,
                                           ctx->counter);
   if (cudaGetLastError() != cudaSuccess) return 1;
   return (int)cudaMemcpyAsync(s, ctx->u + ctx->r, ctx->r * sizeof(double), cudaMemcpyDeviceToDevice, st);

@@ -62,7 +62,8 @@ int launch_vt_dot_strided(pslr_ctx* ctx, const double* y, int64_t ys, cudaStream
 int launch_vu_add_strided(const pslr_ctx* ctx, const double* y, int64_t ys, double* out, int64_t os,
                           cudaStream_t st);
 int launch_permute2(const pslr_ctx* ctx, const double* b, cudaStream_t st);
-int launch_deinterleave2(const pslr_ctx* ctx, double* z, cudaStream_t st);
+int launch_deinterleave2(const pslr_ctx* ctx, const double* y2, double* z, cudaStream_t st);
+int launch_vt_local_strided(pslr_ctx* ctx, const double* y, int64_t ys, double* s, cudaStream_t st);
 
 // capi.cu
 int alloc_scratch(pslr_ctx* ctx, double** p, int64_t count);

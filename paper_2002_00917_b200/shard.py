@@ -297,6 +297,30 @@ class DeviceShardOps:
         self._call("pslr_apply_last", b.data_ptr(), y.data_ptr(), z.data_ptr())
         return z
 
+    # two right-hand sides per launch (pslr_apply2_*): b (2, n) vector-major, interface
+    # vectors (q [+ ghosts], 2) interleaved, s (2, r)
+    def first2(self, b2):
+        y0 = self.t.empty((self.q, 2), dtype=self.t.float64, device=self.device)
+        s = self.t.zeros((2, max(self.r, 1)), dtype=self.t.float64, device=self.device)
+        self._call("pslr_apply2_first", b2.data_ptr(), y0.data_ptr(), s.data_ptr())
+        return y0, s[:, :self.r].contiguous()
+
+    def mid2(self, y0, s):
+        c = self.t.zeros((self.q + self.ng, 2), dtype=self.t.float64, device=self.device)
+        sp_ = s if self.r else self.zeros(2)
+        self._call("pslr_apply2_mid", y0.data_ptr(), sp_.data_ptr(), c.data_ptr())
+        return c
+
+    def horner2(self, y_ext, c):
+        out = self.t.zeros((self.q + self.ng, 2), dtype=self.t.float64, device=self.device)
+        self._call("pslr_apply2_horner", y_ext.data_ptr(), c.data_ptr(), out.data_ptr())
+        return out
+
+    def last2(self, b2, y):
+        z = self.t.empty((2, self.n), dtype=self.t.float64, device=self.device)
+        self._call("pslr_apply2_last", b2.data_ptr(), y.data_ptr(), z.data_ptr())
+        return z
+
     def solve_C0(self, g):
         out = self.zeros(self.q + self.ng)
         self._call("pslr_solve_C0", g.data_ptr(), out.data_ptr())
@@ -386,6 +410,45 @@ class ShardedPreconditioner:
                     halo.exchange(out)
                 y = out
         return ops.last(b, y[:ops.q].contiguous())
+
+    def apply2(self, b2):
+        """Two right-hand sides (rows of b2, shape (2, n_loc)) through one launch sequence
+        and one set of collectives (halo rows carry both vectors; one allreduce of 2r);
+        each result row is apply() of that row bit for bit.  Ranks without the two-vector
+        kernels (p or q empty, or a backend without them) run the vectors one by one
+        between the SAME collectives, so every rank issues the same sequence."""
+        ops, halo, m = self.ops, self.halo, self.series_degree
+        t = ops.t
+        if tuple(b2.shape) != (2, ops.n):
+            raise ValueError(f"expected shape (2, {ops.n}), got {tuple(b2.shape)}")
+        b2 = b2.contiguous()
+        if ops.q == 0 and self.plan.world == 1:
+            return t.stack([ops.last(b2[v], ops.zeros(0)) for v in range(2)])
+        native = ops.q > 0 and ops.p > 0 and hasattr(ops, "first2")
+        cols = lambda x: [x[:, v].contiguous() for v in range(2)]  # noqa: E731
+        if native:
+            y0, s = ops.first2(b2)
+        else:
+            f = [ops.first(b2[v]) for v in range(2)]
+            y0, s = t.stack([f[0][0], f[1][0]], 1), t.stack([f[0][1], f[1][1]])
+        if ops.r:
+            halo.allreduce(s)
+        c = ops.mid2(y0, s) if native else t.stack([ops.mid(yv, s[v].clone()) for v, yv in enumerate(cols(y0))], 1)
+        y = c
+        if m > 0:
+            halo.exchange(c)
+            cc = None if native else cols(c)
+            for k in range(m):
+                if native:
+                    out = ops.horner2(y, c)
+                else:
+                    out = t.stack([ops.horner(yv, cc[v]) for v, yv in enumerate(cols(y))], 1)
+                if k < m - 1:
+                    halo.exchange(out)
+                y = out
+        if native:
+            return ops.last2(b2, y[:ops.q].contiguous())
+        return t.stack([ops.last(b2[v], yv) for v, yv in enumerate(cols(y[:ops.q]))])
 
 
 def build_sharded(ps: PartitionedSystem, cfg, group=None, device=None):

@@ -142,3 +142,52 @@ def test_sharded_gmres_one_rank_matches_device_gmres(flexible):
     k = min(len(hist), len(rep.history))
     assert np.allclose(np.asarray(hist[:k]), np.asarray(rep.history[:k]), rtol=1e-6, atol=1e-14)
     assert conv == rep.converged
+
+
+@pytest.mark.parametrize("world", [1, 2, 4])
+def test_split_apply2_matches_split_apply(world):
+    """The two-vector split apply (pslr_apply2_*: one launch sequence and one halo per step
+    for both vectors, interleaved interface vectors with ghosts) == the single-vector split
+    apply of each vector, bit for bit, through ShardedPreconditioner.apply2 on a lockstep
+    sharding (the halo object only sees 2-column tensors)."""
+    import torch
+    import paper_2002_00917_b200 as pg
+    from paper_2002_00917_b200 import shard, workloads
+    A = workloads.laplacian3d(14, 14, 14, 0.5)
+    m = 3
+    cfg = pg.PslrConfig(num_subdomains=8, series_degree=m, rank=8, droptol=1e-2, seed=0)
+    P = pg.build(A, cfg)
+    ps = P.system
+    plans = [shard.plan_shard(ps, world, r) for r in range(world)]
+    ops = [shard.DeviceShardOps(pl) for pl in plans]
+    V, G = np.asarray(P.correction.V), P.correction.G
+    for pl, o in zip(plans, ops):
+        o.set_correction(torch.as_tensor(np.ascontiguousarray(V[pl.ifc_lo:pl.ifc_hi]), device="cuda"), G)
+    halo = LocalHalo(plans, "cuda")
+    rng = np.random.default_rng(9)
+    B = [torch.as_tensor(rng.standard_normal(ps.n), device="cuda") for _ in range(2)]
+    z1 = [_lockstep_apply(plans, ops, halo, b, ps.p, m) for b in B]
+    # lockstep apply2: the same orchestration on (q, 2) / (2, r) tensors
+    rows = [torch.as_tensor(shard.local_rows(pl, ps.p), device="cuda") for pl in plans]
+    b2 = [torch.stack([B[0][r_], B[1][r_]]).contiguous() for r_ in rows]
+    first = [o.first2(x) for o, x in zip(ops, b2)]
+    s = sum(f[1] for f in first)
+    c = [o.mid2(f[0], s.clone()) for o, f in zip(ops, first)]
+    y = c
+    halo.exchange(c)
+    for k in range(m):
+        out = [o.horner2(yy, cc) for o, yy, cc in zip(ops, y, c)]
+        if k < m - 1:
+            halo.exchange(out)
+        y = out
+    z2 = torch.empty((2, ps.n), dtype=torch.float64, device="cuda")
+    for r_, o, x, yy in zip(rows, ops, b2, y):
+        z2[:, r_] = o.last2(x, yy[:o.q].contiguous())
+    for v in range(2):
+        assert torch.equal(z2[v], z1[v]), v
+    # and the ShardedPreconditioner entry point on a one-rank sharding
+    if world == 1:
+        SP = shard.ShardedPreconditioner(plans[0], ops[0], shard.Halo(plans[0], "cuda"), m)
+        zz = SP.apply2(b2[0])
+        assert torch.equal(zz[0], SP.apply(b2[0][0].contiguous()))
+        assert torch.equal(zz[1], SP.apply(b2[0][1].contiguous()))

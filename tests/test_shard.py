@@ -134,7 +134,9 @@ def _worker(rank, world, port, n, s, m, r, out):
         rows = shard.local_rows(plan, ps.p)
         import torch
         z = P.apply(torch.as_tensor(b[rows]))
-        np.savez(os.path.join(out, f"r{rank}.npz"), z=z.numpy(), rows=rows, H=H, V=Vl.numpy(),
+        b2 = np.random.default_rng(2).standard_normal(ps.n)
+        z2 = P.apply2(torch.as_tensor(np.stack([b[rows], b2[rows]])))
+        np.savez(os.path.join(out, f"r{rank}.npz"), z=z.numpy(), z2=z2.numpy(), rows=rows, H=H, V=Vl.numpy(),
                  ifc=np.arange(plan.ifc_lo, plan.ifc_hi))
     finally:
         dist.destroy_process_group()
@@ -159,15 +161,21 @@ def test_sharded_apply_matches_single_process(tmp_path, world, n, s):
     b = np.random.default_rng(1).standard_normal(ps.n)
     z_ref = P.apply(b)
     z = np.zeros(ps.n)
+    zb = np.zeros(ps.n)
     Vs = np.zeros_like(V)
     for k in range(world):
         d = np.load(tmp_path / f"r{k}.npz")
         z[d["rows"]] = d["z"]
+        # apply2 (two right-hand sides, one set of collectives): row 0 is apply() exactly
+        np.testing.assert_array_equal(d["z2"][0], d["z"])
+        zb[d["rows"]] = d["z2"][1]
         # Arnoldi: the same H on every rank, the rank's rows of V
         assert np.allclose(d["H"], H, rtol=1e-10, atol=1e-12)
         Vs[d["ifc"]] = d["V"]
     assert np.allclose(Vs, V, rtol=1e-9, atol=1e-11)
     assert np.max(np.abs(z - z_ref)) <= 1e-10 * np.max(np.abs(z_ref))
+    zb_ref = P.apply(np.random.default_rng(2).standard_normal(ps.n))
+    assert np.max(np.abs(zb - zb_ref)) <= 1e-10 * np.max(np.abs(zb_ref))
 
 
 def _gmres_worker(rank, world, port, n, s, m, r, out):
