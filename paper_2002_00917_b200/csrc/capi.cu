@@ -497,6 +497,7 @@ int pslr_ctx_create(pslr_ctx** out, int device, const pslr_system* sys) {
     ctx->allocations.push_back(d);
     ctx->K.trace = static_cast<long long*>(d);
     ctx->K.trace_cap = cap;
+    ctx->K.trace_block = env_int("PSLR_TRACE_CTA", 0);
   }
   int64_t farB = 0, farC = 0;
   if ((rc = build_pair(ctx, sys->LB, sys->UB, ctx->interior_off, aLB, aUB, W, SB, &ctx->K.LB,

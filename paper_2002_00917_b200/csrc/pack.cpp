@@ -207,20 +207,33 @@ int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAna
         // grow a segment while it fits a stage
         int64_t s1 = s0, nnz = 0, w = 0, nfar = 0;
         bool expl = false;
-        while (s1 < lend && s1 - s0 < seg_rows - tb) {
-          const int64_t len = A.len[A.row_at_pos[s1]];
-          const int64_t w2 = std::max(w, len);
-          const int64_t f2 = nfar + row_far(s1, lend);
-          const bool e2 = expl || (upper && !sd_plain(A.row_at_pos[s1]));
-          if (seg_bytes(s1 - s0 + 1, w2, f2, e2) > stage_bytes || f2 >= 0x8000) break;
-          w = w2;
-          nnz += len;
-          nfar = f2;
-          expl = e2;
-          ++s1;
-        }
+        auto grow = [&](int64_t cap) {
+          s1 = s0, nnz = 0, w = 0, nfar = 0;
+          expl = false;
+          while (s1 < lend && s1 - s0 < cap) {
+            const int64_t len = A.len[A.row_at_pos[s1]];
+            const int64_t w2 = std::max(w, len);
+            const int64_t f2 = nfar + row_far(s1, lend);
+            const bool e2 = expl || (upper && !sd_plain(A.row_at_pos[s1]));
+            if (seg_bytes(s1 - s0 + 1, w2, f2, e2) > stage_bytes || f2 >= 0x8000) break;
+            w = w2;
+            nnz += len;
+            nfar = f2;
+            expl = e2;
+            ++s1;
+          }
+        };
+        grow(seg_rows - tb);
         if (s1 == s0)
           return fail(PSLR_EINVAL, std::string(name) + ": a row is too long for the streaming format");
+        // A segment cut by the stage size ends on a warp boundary (tb + nrows a multiple
+        // of 32), so the level's next segment starts on a fresh warp: no warp owns rows
+        // of both, and every warp still takes one step per 480 rows of the level (a
+        // straddling warp would take two, and the level ends with its slowest warp).
+        if (s1 < lend && s1 - s0 < seg_rows - tb) {
+          const int64_t end_t = ((tb + (s1 - s0)) / 32) * 32;
+          if (end_t > tb && end_t - tb < s1 - s0) grow(end_t - tb);
+        }
         const int64_t nrows = s1 - s0;
         const int64_t bytes = seg_bytes(nrows, w, nfar, expl);
         if ((int64_t)out.data.size() - chunk_start + bytes > stage_bytes ||

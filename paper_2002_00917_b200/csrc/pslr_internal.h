@@ -131,6 +131,7 @@ struct StepConst {
   int smem_bytes = 0;
   long long* trace = nullptr;  // PSLR_TRACE: [count, pad, (code, ns)...] of CTA 0
   long long trace_cap = 0;
+  int trace_block = 0;       // the CTA whose timeline trace builds record (PSLR_TRACE_CTA)
 };
 
 }  // namespace pslr

@@ -112,11 +112,12 @@ __device__ __forceinline__ double spmv_row_rw(const DevCsr& M, int row, const do
 #endif
 __shared__ long long* g_trace_ptr;
 __shared__ int g_trace_n;
+__shared__ int g_trace_tag;
 
 constexpr int kTraceWindow = 1 << 15;
 
 __device__ __forceinline__ void trace_begin(const StepConst& K) {
-  if (PSLR_TRACE_BUILD && K.trace && blockIdx.x == 0 && threadIdx.x == 0) {
+  if (PSLR_TRACE_BUILD && K.trace && blockIdx.x == K.trace_block && threadIdx.x == 0) {
     const unsigned long long i =
         atomicAdd(reinterpret_cast<unsigned long long*>(K.trace), (unsigned long long)kTraceWindow);
     g_trace_ptr = (i + kTraceWindow <= (unsigned long long)K.trace_cap) ? K.trace + 2 + 2 * i : nullptr;
@@ -124,7 +125,7 @@ __device__ __forceinline__ void trace_begin(const StepConst& K) {
   }
 }
 __device__ __forceinline__ void trace_ev(const StepConst& K, int code, int arg) {
-  if (PSLR_TRACE_BUILD && K.trace && blockIdx.x == 0 && threadIdx.x == 0 && g_trace_ptr &&
+  if (PSLR_TRACE_BUILD && K.trace && blockIdx.x == K.trace_block && threadIdx.x == 0 && g_trace_ptr &&
       g_trace_n < kTraceWindow) {
     unsigned long long ns;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
@@ -137,7 +138,7 @@ __device__ __forceinline__ void trace_ev(const StepConst& K, int code, int arg) 
 // =3 builds: one (code|arg, clock64) record per level-loop step, cheap enough (no
 // %globaltimer) to time individual levels in cycles
 __device__ __forceinline__ void trace_clk(const StepConst& K, int code, int arg) {
-  if (PSLR_TRACE_BUILD == 3 && K.trace && blockIdx.x == 0 && threadIdx.x == 0 && g_trace_ptr &&
+  if (PSLR_TRACE_BUILD == 3 && K.trace && blockIdx.x == K.trace_block && threadIdx.x == 0 && g_trace_ptr &&
       g_trace_n < kTraceWindow) {
     g_trace_ptr[2 * g_trace_n] = ((long long)code << 32) | (unsigned)arg;
     g_trace_ptr[2 * g_trace_n + 1] = clock64();
@@ -146,12 +147,14 @@ __device__ __forceinline__ void trace_clk(const StepConst& K, int code, int arg)
 }
 
 // trace builds: every CTA stamps its phase boundaries (slot 0 start, 1 prepass done,
-// 2..5 phase k start, 6 end) into rows 1024 + b of the counter area (last launch wins)
+// 2..5 phase k start, 6 end) into row 1024 + 64 * (launch kind) + b of the counter area
+// (the last launch of each kind wins; b < 64)
 __device__ __forceinline__ void trace_cta(const StepConst& K, int slot) {
-  if (PSLR_TRACE_BUILD && K.trace && threadIdx.x == 0 && K.trace_cap >= (1 << 20) && blockIdx.x < 1024) {
+  if (PSLR_TRACE_BUILD && K.trace && threadIdx.x == 0 && K.trace_cap >= (1 << 20) && blockIdx.x < 64) {
     unsigned long long ns;
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(ns));
-    K.trace[2 + 2 * K.trace_cap - 8 * 4096 + (1024 + blockIdx.x) * 8 + slot] = (long long)ns;
+    K.trace[2 + 2 * K.trace_cap - 8 * 4096 + (1024 + 64 * (g_trace_tag & 15) + blockIdx.x) * 8 + slot] =
+        (long long)ns;
   }
 }
 
@@ -699,6 +702,7 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
   // consumers wait here for its completion before reading any vector it produced or
   // writing any buffer it may still read.  A no-op for ordinary launches.
   asm volatile("griddepcontrol.wait;" ::: "memory");
+  if (PSLR_TRACE_BUILD && threadIdx.x == 0) g_trace_tag = a.tag;
   trace_begin(K);
   trace_ev(K, 1, S.begin[S.nphase]);
   trace_cta(K, 0);

@@ -1,5 +1,5 @@
 """Timeline of CTA 0 of the fused step kernel over one PSLR apply (PSLR_TRACE=1).
-usage: PSLR_TRACE=1 python tools/trace_apply.py [cfg5]"""
+usage: PSLR_TRACE=1 python tools/trace_apply.py [cfg5] [nv]   (nv=2: one pslr_apply_multi call)"""
 import ctypes
 import os
 import sys
@@ -17,13 +17,26 @@ name = sys.argv[1] if len(sys.argv) > 1 else "cfg5"
 wl = workloads.CONFIGS[name]
 P = pg.build(wl.matrix(), wl.config())
 print(P.device.info(), flush=True)
+nv = int(sys.argv[2]) if len(sys.argv) > 2 else 1
 b = torch.from_numpy(np.random.default_rng(0).standard_normal(P.system.n)).cuda()
-P.apply(b)
+if nv > 1:
+    P.device.ensure_correction(P.correction)
+    B2 = torch.from_numpy(np.random.default_rng(0).standard_normal((nv, P.system.n))).cuda()
+    Z2 = torch.empty_like(B2)
+
+    class _Multi:
+        def apply(self, _b):
+            _lib.check(_lib.fns["pslr_apply_multi"](P.device.handle, wl.m, nv, B2.data_ptr(), Z2.data_ptr(),
+                                                    P.device.stream()))
+    P_run = _Multi()
+else:
+    P_run = P
+P_run.apply(b)
 torch.cuda.synchronize()
 buf = np.zeros(2 * (1 << 20), dtype=np.int64)  # == 2*trace_cap: whole buffer
 cnt = ctypes.c_int64()
 _lib.fns["pslr_debug_trace"](P.device.handle, buf.ctypes.data, buf.size, ctypes.byref(cnt))  # reset
-P.apply(b)
+P_run.apply(b)
 torch.cuda.synchronize()
 _lib.check(_lib.fns["pslr_debug_trace"](P.device.handle, buf.ctypes.data, buf.size, ctypes.byref(cnt)))
 n = cnt.value
@@ -119,19 +132,28 @@ if i51.size:
     for k in sorted(set(phase_of[i51].tolist())):
         sel = phase_of[i51] == k
         print(f"   phase {k}: n={sel.sum()}, mean {w[sel].mean():.0f}, sum {w[sel].sum() / 1.965e3:.1f} us")
-# per-CTA phase stamps of the LAST launch traced (trace builds): which block is critical
-cs = buf[2 * (1 << 20) - 8 * 4096:].reshape(4096, 8)[1024:1024 + P.system.num_parts].astype(np.float64)
-if cs[:, 0].sum() > 0:
+# per-CTA phase stamps, the last launch of each kind (trace builds): which block is critical
+kinds = {2: "first_step", 3: "correction_c0", 4: "horner_step", 5: "last_step"}
+names_s = ["start", "prepass", "L_B", "U_B", "L_C0", "U_C0", "end"]
+area = buf[2 * (1 << 20) - 8 * 4096:].reshape(4096, 8)
+dump = {}
+for tag, kname in kinds.items():
+    cs = area[1024 + 64 * tag:1024 + 64 * tag + P.system.num_parts].astype(np.float64)
+    if cs[:, 0].sum() <= 0:
+        continue
+    dump[kname] = cs
     t0 = cs[:, 0].min()
     end = (cs[:, 6] - t0) / 1e3
-    names_s = ["start", "prepass", "L_B", "U_B", "L_C0", "U_C0", "end"]
-    print("last launch, per CTA (us from the first CTA start): end min %.1f median %.1f max %.1f (CTA %d)"
-          % (end.min(), np.median(end), end.max(), int(end.argmax())))
-    order = np.argsort(-end)[:6]
+    print("%s, per CTA (us from the first CTA start): end min %.1f median %.1f max %.1f (CTA %d)"
+          % (kname, end.min(), np.median(end), end.max(), int(end.argmax())))
+    order = np.argsort(-end)[:4]
     for b in order:
         row = cs[b]
         seg = []
-        marks = [(i, row[i]) for i in range(7) if row[i] > 0]
+        marks = [(i, row[i]) for i in range(7) if row[i] >= row[0] > 0]
         for (i, tv), (j, tn) in zip(marks, marks[1:]):
             seg.append(f"{names_s[i]} {(tn - tv) / 1e3:.1f}")
         print(f"   CTA {b:3d}: start {(row[0] - t0) / 1e3:6.1f} end {(row[6] - t0) / 1e3:6.1f}  |  " + ", ".join(seg))
+out = os.environ.get("TRACE_DUMP")
+if out:
+    np.savez(out, **dump)
