@@ -386,3 +386,68 @@ def test_apply_multi_host_async_bitexact():
     for v in range(nv):
         np.testing.assert_array_equal(Z[v].numpy(), P.apply(B[v].cuda()).cpu().numpy())
     del c
+
+
+def _multi(P, m, B):
+    import torch
+    from paper_2002_00917_b200 import _lib
+    Bt = torch.as_tensor(np.ascontiguousarray(B), device="cuda")
+    Z = torch.empty_like(Bt)
+    _lib.check(_lib.fns["pslr_apply_multi"](P.device.handle, m, Bt.shape[0], Bt.data_ptr(), Z.data_ptr(),
+                                            P.device.stream()))
+    return Z.cpu().numpy()
+
+
+@pytest.mark.parametrize("m", [0, 1, 5])
+def test_apply_multi_series_degrees(m):
+    """Two vectors per launch at series degrees 0 (no Horner launch), 1 and 5: each vector
+    equals the single-vector apply bit for bit."""
+    P, meta, d, A = _build("lap3d6_s4_dt1e-2")
+    P.device.ensure_correction(P.correction)
+    n = P.system.n
+    B = np.random.default_rng(20 + m).standard_normal((2, n))
+    Z = _multi(P, m, B)
+    for v in range(2):
+        np.testing.assert_array_equal(Z[v], P.device.vec_op("pslr_apply", B[v], n, n, m))
+
+
+def test_apply_multi_rank_zero_and_explicit_sd(monkeypatch):
+    """Two vectors per launch with no low-rank correction (bit-exact with the oracle's
+    apply) and with the explicit sd / rcp U layout (bit-exact with the flag layout)."""
+    import paper_2002_00917_b200 as pg
+    from oracle import pslr_oracle as O
+    meta = G["apply"]["lap3d6_s4_dt1e-2"]
+    d = load_npz("apply_lap3d6_s4_dt1e-2.npz")
+    A = csr_from(d, "A")
+    P = pg.build(A, pg.PslrConfig(num_subdomains=meta["s"], series_degree=meta["m"], rank=0,
+                                  droptol=meta["droptol"], seed=meta["seed"]))
+    octx = _oracle_ctx(P)
+    OP = O.Preconditioner(octx.system, octx, meta["m"], O.Correction(np.zeros((P.system.q, 0)),
+                                                                      np.zeros((0, 0)), np.zeros((0, 0)), 0))
+    B = np.random.default_rng(21).standard_normal((2, P.system.n))
+    Z = _multi(P, meta["m"], B)
+    for v in range(2):
+        np.testing.assert_array_equal(Z[v], OP.apply(B[v]))
+    monkeypatch.setenv("PSLR_EXPLICIT_SD", "1")
+    Pe = pg.build(A, pg.PslrConfig(num_subdomains=meta["s"], series_degree=meta["m"], rank=0,
+                                   droptol=meta["droptol"], seed=meta["seed"]))
+    np.testing.assert_array_equal(_multi(Pe, meta["m"], B), Z)
+
+
+def test_apply_multi_small_counts_and_errors():
+    """nv = 0 is a no-op, nv = 1 is pslr_apply; negative nv / m are rejected (ValueError)."""
+    import torch
+    from paper_2002_00917_b200 import _lib
+    P, meta, d, A = _build("lap3d6_s4_dt1e-2")
+    P.device.ensure_correction(P.correction)
+    n, m = P.system.n, meta["m"]
+    B = np.random.default_rng(22).standard_normal((1, n))
+    np.testing.assert_array_equal(_multi(P, m, B)[0], P.apply(B[0]))
+    Z = torch.full((1, n), 7.0, dtype=torch.float64, device="cuda")
+    Bt = torch.as_tensor(B, device="cuda")
+    _lib.check(_lib.fns["pslr_apply_multi"](P.device.handle, m, 0, Bt.data_ptr(), Z.data_ptr(), P.device.stream()))
+    assert bool((Z == 7.0).all())
+    for bad_m, bad_nv in ((-1, 2), (m, -1)):
+        with pytest.raises(ValueError):
+            _lib.check(_lib.fns["pslr_apply_multi"](P.device.handle, bad_m, bad_nv, Bt.data_ptr(), Z.data_ptr(),
+                                                    P.device.stream()))
