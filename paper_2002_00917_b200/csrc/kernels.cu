@@ -52,9 +52,40 @@ vt_dot_kernel(const double* __restrict__ V, const double* __restrict__ y, int64_
   __shared__ double red[kVtThreads / 32][128];
   __shared__ bool last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = kVtThreads / 32;
-  for (int c0 = 0; c0 < r; c0 += 128) {
+  const int64_t stride = (int64_t)gridDim.x * nw;
+  if (r <= 64) {
+    // two columns per lane, eight rows in flight per warp (V rows are 512 B at r = 64)
+    double a0 = 0.0, a1 = 0.0;
+    const bool v0 = lane < r, v1 = lane + 32 < r;
+    int64_t row = (int64_t)blockIdx.x * nw + warp;
+    for (; row < q; row += 8 * stride) {  // predicated batches: the tail is one batch too
+      double yv[8], x0[8], x1[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const int64_t ru = row + u * stride;
+        const bool ok = ru < q;
+        const double* vr = V + ru * r;
+        yv[u] = ok ? __ldg(y + ru * ys) : 0.0;
+        x0[u] = (ok && v0) ? __ldg(vr + lane) : 0.0;
+        x1[u] = (ok && v1) ? __ldg(vr + lane + 32) : 0.0;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        a0 = a0 + x0[u] * yv[u];
+        a1 = a1 + x1[u] * yv[u];
+      }
+    }
+    red[warp][lane] = a0;
+    red[warp][lane + 32] = a1;
+    __syncthreads();
+    for (int c = threadIdx.x; c < r; c += kVtThreads) {
+      double sum = 0.0;
+      for (int w = 0; w < nw; ++w) sum = sum + red[w][c];
+      partials[(int64_t)blockIdx.x * r + c] = sum;
+    }
+  }
+  for (int c0 = 0; c0 < r && r > 64; c0 += 128) {
     double acc[4] = {0.0, 0.0, 0.0, 0.0};
-    const int64_t stride = (int64_t)gridDim.x * nw;
     int64_t row = (int64_t)blockIdx.x * nw + warp;
     // four rows per iteration: their loads are independent and in flight together
     for (; row + 3 * stride < q; row += 4 * stride) {
@@ -88,9 +119,9 @@ vt_dot_kernel(const double* __restrict__ V, const double* __restrict__ y, int64_
     for (int k = 0; k < 4; ++k) red[warp][lane + 32 * k] = acc[k];
     __syncthreads();
     for (int c = threadIdx.x; c < 128 && c0 + c < r; c += kVtThreads) {
-      double s = 0.0;
-      for (int w = 0; w < nw; ++w) s = s + red[w][c];
-      partials[(int64_t)blockIdx.x * r + c0 + c] = s;
+      double sum = 0.0;
+      for (int w = 0; w < nw; ++w) sum = sum + red[w][c];
+      partials[(int64_t)blockIdx.x * r + c0 + c] = sum;
     }
     __syncthreads();
   }
@@ -135,13 +166,17 @@ __global__ void vu_add_kernel(const double* __restrict__ V, const double* __rest
   int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (r <= 64) {  // two columns per lane, four rows in flight per warp
     const double u0 = lane < r ? __ldg(u + lane) : 0.0, u1 = lane + 32 < r ? __ldg(u + lane + 32) : 0.0;
-    for (; row + 3 * nwarps < q; row += 4 * nwarps) {
-      double s[4];
+    for (; row < q; row += 4 * nwarps) {  // predicated batches: the tail is one batch too
+      double s[4], yv[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        yv[k] = (lane == 0 && row + k * nwarps < q) ? __ldg(y + (row + k * nwarps) * ys) : 0.0;
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
+        const bool ok = row + k * nwarps < q;
         const double* vr = V + (row + k * nwarps) * r;
-        const double a = lane < r ? __ldg(vr + lane) : 0.0;
-        const double b = lane + 32 < r ? __ldg(vr + lane + 32) : 0.0;
+        const double a = (ok && lane < r) ? __ldg(vr + lane) : 0.0;
+        const double b = (ok && lane + 32 < r) ? __ldg(vr + lane + 32) : 0.0;
         s[k] = (lane < r ? a * u0 : 0.0);
         s[k] = s[k] + (lane + 32 < r ? b * u1 : 0.0);
       }
@@ -151,8 +186,10 @@ __global__ void vu_add_kernel(const double* __restrict__ V, const double* __rest
         for (int k = 0; k < 4; ++k) s[k] = s[k] + __shfl_xor_sync(0xffffffffu, s[k], o);
       if (lane == 0)
 #pragma unroll
-        for (int k = 0; k < 4; ++k) out[(row + k * nwarps) * os] = __ldg(y + (row + k * nwarps) * ys) + s[k];
+        for (int k = 0; k < 4; ++k)
+          if (row + k * nwarps < q) out[(row + k * nwarps) * os] = yv[k] + s[k];
     }
+    return;
   }
   for (; row < q; row += nwarps) {
     const double* vr = V + row * r;
@@ -237,56 +274,124 @@ __global__ void spmv_kernel(DevCsr M, const double* __restrict__ x, double* __re
 }
 
 // ---------------------------------------------------------------- Krylov building blocks
-// out[c] = sum_i X[c*ld + i] * y[i], c < k.  Grid-stride partials + last-block
-// reduction in a fixed order (deterministic, no atomics on values).
-constexpr int kDotThreads = 256;
-constexpr int kDotCols = 4;
+// Column-major Krylov basis passes (X: k columns, ld = n), the blocks of CGS2
+// (krylov.py:75-80, lowrank.py:62-67).  One kernel, three modes, each ONE pass over X:
+//   kDot:     h = X^T w
+//   kSubDot:  w = w - X h0 ; h = X^T w        (first projection fused with the second dot)
+//   kSubNorm: w = w - X h0 ; h[0] = w . w     (second projection fused with the norm)
+// so CGS2 + norm reads the basis three times instead of four plus one.  A CTA walks
+// 256-row tiles (grid-stride): phase A (thread = row) forms w_i - sum_c X[c,i] h0[c]
+// in column order (numpy's w - V@h); phase B (warp = column set c = warp + 8j, lanes on
+// rows) accumulates X[c, tile] . w_tile lane-locally, re-reading the tile phase A just
+// brought into L1.  Per-CTA partials are summed by the last CTA in a fixed order
+// (deterministic, no atomics on values).
+constexpr int kCgsThreads = 256;
+constexpr int kCgsWarps = kCgsThreads / 32;
+constexpr int kCgsMaxCols = 128;
+enum CgsMode : int { kDot = 0, kSubDot = 1, kSubNorm = 2 };
 
-__global__ void __launch_bounds__(kDotThreads)
-multidot_kernel(const double* __restrict__ X, int64_t ld, int k, const double* __restrict__ y,
-                int64_t n, double* __restrict__ partials, double* __restrict__ out,
+template <int MODE, int CPW>  // CPW: columns per warp (k <= 8 * CPW)
+__global__ void __launch_bounds__(kCgsThreads, 2)
+cgs_pass_kernel(const double* __restrict__ X, int64_t ld, int k, double* __restrict__ w, int64_t n,
+                const double* __restrict__ h0, double* __restrict__ partials, double* __restrict__ out,
                 unsigned int* counter) {
-  __shared__ double sh[kDotCols][kDotThreads / 32];
+  __shared__ double hs[kCgsMaxCols];
+  __shared__ double ws[kCgsThreads];
+  __shared__ double nred[kCgsWarps];
   __shared__ bool last;
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int c0 = 0; c0 < k; c0 += kDotCols) {
-    double acc[kDotCols] = {0.0, 0.0, 0.0, 0.0};
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
-      const double yi = y[i];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (MODE != kDot)
+    for (int c = tid; c < k; c += kCgsThreads) hs[c] = h0[c];
+  __syncthreads();
+  double acc[CPW];
 #pragma unroll
-      for (int t = 0; t < kDotCols; ++t)
-        if (c0 + t < k) acc[t] = acc[t] + X[(int64_t)(c0 + t) * ld + i] * yi;
+  for (int j = 0; j < CPW; ++j) acc[j] = 0.0;
+  double nacc = 0.0;
+  const int64_t ntiles = (n + kCgsThreads - 1) / kCgsThreads;
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t base = t * kCgsThreads;
+    const int64_t i = base + tid;
+    double wi = (i < n) ? w[i] : 0.0;
+    if (MODE != kDot) {
+      double s = 0.0;
+      if (i < n) {
+        const double* xi = X + i;
+        int c = 0;
+        for (; c + 8 <= k; c += 8) {
+          double v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v[u] = xi[(int64_t)(c + u) * ld];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) s = s + v[u] * hs[c + u];
+        }
+        for (; c < k; ++c) s = s + xi[(int64_t)c * ld] * hs[c];
+        wi = wi - s;
+        w[i] = wi;
+      }
     }
+    if (MODE == kSubNorm) {
+      nacc = nacc + wi * wi;
+      continue;
+    }
+    ws[tid] = wi;
+    __syncthreads();
+    // Branch-free so every load of the tile can be in flight at once: rows past n read
+    // row rows-1 against ws = 0 (adds +0), columns past k re-read column k-1 into
+    // accumulators that are never stored.
+    const int rlast = ((n - base < kCgsThreads) ? (int)(n - base) : kCgsThreads) - 1;
+    const double* xt = X + base;
 #pragma unroll
-    for (int t = 0; t < kDotCols; ++t) {
-      double v = acc[t];
-      for (int o = 16; o > 0; o >>= 1) v = v + __shfl_down_sync(0xffffffffu, v, o);
-      if (lane == 0) sh[t][warp] = v;
+    for (int rr = 0; rr < kCgsThreads / 32; ++rr) {  // rows outer: the column chains interleave
+      const int r = lane + 32 * rr;
+      const int rc = r < rlast ? r : rlast;
+      const double wr = ws[r];
+#pragma unroll
+      for (int j = 0; j < CPW; ++j) {
+        const int c = min(warp + kCgsWarps * j, k - 1);
+        acc[j] = acc[j] + xt[(int64_t)c * ld + rc] * wr;
+      }
     }
     __syncthreads();
-    if (threadIdx.x < kDotCols && c0 + (int)threadIdx.x < k) {
-      double v = 0.0;
-      for (int w = 0; w < kDotThreads / 32; ++w) v = v + sh[threadIdx.x][w];
-      partials[(int64_t)blockIdx.x * k + c0 + threadIdx.x] = v;
-    }
+  }
+  const int kk = (MODE == kSubNorm) ? 1 : k;
+  if (MODE == kSubNorm) {
+    double v = nacc;
+    for (int o = 16; o > 0; o >>= 1) v = v + __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) nred[warp] = v;
     __syncthreads();
+    if (tid == 0) {
+      double s = 0.0;
+      for (int q = 0; q < kCgsWarps; ++q) s = s + nred[q];
+      partials[blockIdx.x] = s;
+    }
+  } else {
+#pragma unroll
+    for (int j = 0; j < CPW; ++j) {
+      const int c = warp + kCgsWarps * j;
+      if (c < k) {  // warp-uniform
+        double v = acc[j];
+        for (int o = 16; o > 0; o >>= 1) v = v + __shfl_xor_sync(0xffffffffu, v, o);
+        if (lane == 0) partials[(int64_t)blockIdx.x * k + c] = v;
+      }
+    }
   }
   __threadfence();
-  if (threadIdx.x == 0) last = (atomicAdd(counter, 1u) == gridDim.x - 1);
   __syncthreads();
-  if (last) {
-    __threadfence();
-    for (int c = threadIdx.x; c < k; c += blockDim.x) {
-      double v = 0.0;
-      for (int g = 0; g < (int)gridDim.x; ++g) v = v + ((volatile double*)partials)[(int64_t)g * k + c];
-      out[c] = v;
-    }
-    if (threadIdx.x == 0) *counter = 0u;
+  if (tid == 0) last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const int g = (int)gridDim.x;
+  for (int c = warp; c < kk; c += kCgsWarps) {  // warp per column, lanes over CTAs
+    double v = 0.0;
+    for (int b = lane; b < g; b += 32) v = v + __ldcg(partials + (int64_t)b * kk + c);
+    for (int o = 16; o > 0; o >>= 1) v = v + __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) out[c] = v;
   }
+  if (tid == 0) *counter = 0u;
 }
 
-// w[i] = w[i] - sum_c X[c*ld + i] * h[c]   (w - V h, numpy order: V@h first)
+// w[i] = w[i] - sum_c X[c*ld + i] * h[c]   (w - V h, numpy order: V@h first; k > 128 passes)
 __global__ void gemv_sub_kernel(const double* __restrict__ X, int64_t ld, int k,
                                 const double* __restrict__ h, double* __restrict__ w, int64_t n) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -327,13 +432,13 @@ __global__ void div_scalar_kernel(const double* __restrict__ x, const double* __
 }
 
 // row-major (q x r) <- column-major (ld = q) transpose for the Arnoldi basis
-__global__ void colmajor_to_rowmajor_kernel(const double* __restrict__ X, int64_t q, int r,
+__global__ void colmajor_to_rowmajor_kernel(const double* __restrict__ X, int64_t ld, int64_t q, int r,
                                             double* __restrict__ Y) {
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= q * r) return;
   const int64_t i = idx / r;
   const int c = (int)(idx % r);
-  Y[idx] = X[(int64_t)c * q + i];
+  Y[idx] = X[(int64_t)c * ld + i];
 }
 
 // ---------------------------------------------------------------- host-side launchers
@@ -344,7 +449,7 @@ int launch_correction_core(const pslr_ctx* ctx, cudaStream_t st) {
 
 int vt_grid(int64_t q, int sm_count) {
   int64_t g = (q + 8 * 16 - 1) / (8 * 16);
-  const int64_t cap = 2 * (int64_t)sm_count;
+  const int64_t cap = 4 * (int64_t)sm_count;
   if (g > cap) g = cap;
   if (g < 1) g = 1;
   return (int)g;
@@ -398,26 +503,70 @@ int launch_spmv(const DevCsr& M, const double* x, double* y, cudaStream_t st) {
 }
 
 int dot_grid(int64_t n, int sm_count) {
-  int64_t g = (n + kDotThreads * 4 - 1) / (kDotThreads * 4);
-  const int64_t cap = 2 * (int64_t)sm_count;
+  // small k passes have few loads in flight per thread: more CTAs per SM
+  int64_t g = (n + kCgsThreads - 1) / kCgsThreads;
+  const int64_t cap = 4 * (int64_t)sm_count;
   if (g > cap) g = cap;
   if (g < 1) g = 1;
   return (int)g;
 }
 
-int launch_multidot(pslr_ctx* ctx, const double* X, int64_t ld, int k, const double* y, int64_t n,
-                    double* out, cudaStream_t st) {
-  if (k <= 0) return 0;
-  const int g = dot_grid(n, ctx->sm_count);
-  multidot_kernel<<<g, kDotThreads, 0, st>>>(X, ld, k, y, n, ctx->red, out, ctx->counter);
+template <int MODE, int CPW>
+static int launch_cgs_w(pslr_ctx* ctx, const double* X, int64_t ld, int k, double* w, int64_t n,
+                        const double* h0, double* out, cudaStream_t st) {
+  static int resident = 0;  // CTAs per SM at this instance's register count (one full wave)
+  if (!resident) {
+    int b = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, cgs_pass_kernel<MODE, CPW>, kCgsThreads, 0) !=
+            cudaSuccess || b < 1)
+      b = 2;
+    resident = std::min(b, 4);
+  }
+  const int g = (int)std::min<int64_t>(dot_grid(n, ctx->sm_count), (int64_t)resident * ctx->sm_count);
+  cgs_pass_kernel<MODE, CPW><<<g, kCgsThreads, 0, st>>>(X, ld, k, w, n, h0, ctx->red, out, ctx->counter);
   return (int)cudaGetLastError();
 }
 
-int launch_gemv_sub(const double* X, int64_t ld, int k, const double* h, double* w, int64_t n,
-                    cudaStream_t st) {
+template <int MODE>
+static int launch_cgs(pslr_ctx* ctx, const double* X, int64_t ld, int k, double* w, int64_t n,
+                      const double* h0, double* out, cudaStream_t st) {
+  if (MODE == kSubNorm || k <= kCgsWarps) return launch_cgs_w<MODE, 1>(ctx, X, ld, k, w, n, h0, out, st);
+  if (k <= 2 * kCgsWarps) return launch_cgs_w<MODE, 2>(ctx, X, ld, k, w, n, h0, out, st);
+  if (k <= 4 * kCgsWarps) return launch_cgs_w<MODE, 4>(ctx, X, ld, k, w, n, h0, out, st);
+  if (k <= 8 * kCgsWarps) return launch_cgs_w<MODE, 8>(ctx, X, ld, k, w, n, h0, out, st);
+  return launch_cgs_w<MODE, 16>(ctx, X, ld, k, w, n, h0, out, st);
+}
+
+// (bases wider than kCgsMaxCols: the projection as its own pass, dots 128 columns at a time)
+static int launch_gemv_sub(const double* X, int64_t ld, int k, const double* h, double* w, int64_t n,
+                           cudaStream_t st) {
   if (n == 0) return 0;
   gemv_sub_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(X, ld, k, h, w, n);
   return (int)cudaGetLastError();
+}
+
+int launch_multidot(pslr_ctx* ctx, const double* X, int64_t ld, int k, const double* y, int64_t n,
+                    double* out, cudaStream_t st) {
+  for (int c0 = 0; c0 < k; c0 += kCgsMaxCols) {
+    const int e = launch_cgs<kDot>(ctx, X + (int64_t)c0 * ld, ld, std::min(kCgsMaxCols, k - c0),
+                                   const_cast<double*>(y), n, nullptr, out + c0, st);
+    if (e) return e;
+  }
+  return 0;
+}
+
+int launch_sub_dot(pslr_ctx* ctx, const double* X, int64_t ld, int k, const double* h0, double* w,
+                   int64_t n, double* out, cudaStream_t st) {
+  if (k <= kCgsMaxCols) return launch_cgs<kSubDot>(ctx, X, ld, k, w, n, h0, out, st);
+  const int e = launch_gemv_sub(X, ld, k, h0, w, n, st);
+  return e ? e : launch_multidot(ctx, X, ld, k, w, n, out, st);
+}
+
+int launch_sub_norm(pslr_ctx* ctx, const double* X, int64_t ld, int k, const double* h0, double* w,
+                    int64_t n, double* out, cudaStream_t st) {
+  if (k <= kCgsMaxCols) return launch_cgs<kSubNorm>(ctx, X, ld, k, w, n, h0, out, st);
+  const int e = launch_gemv_sub(X, ld, k, h0, w, n, st);
+  return e ? e : launch_multidot(ctx, w, n, 1, w, n, out, st);
 }
 
 int launch_gemv(const double* X, int64_t ld, int k, const double* h, double* y, int64_t n,
@@ -445,9 +594,9 @@ int launch_div_scalar(const double* x, const double* s, double* y, int64_t n, cu
   return (int)cudaGetLastError();
 }
 
-int launch_transpose_basis(const double* X, int64_t q, int r, double* Y, cudaStream_t st) {
+int launch_transpose_basis(const double* X, int64_t ld, int64_t q, int r, double* Y, cudaStream_t st) {
   if (q * r == 0) return 0;
-  colmajor_to_rowmajor_kernel<<<(unsigned)((q * r + 255) / 256), 256, 0, st>>>(X, q, r, Y);
+  colmajor_to_rowmajor_kernel<<<(unsigned)((q * r + 255) / 256), 256, 0, st>>>(X, ld, q, r, Y);
   return (int)cudaGetLastError();
 }
 

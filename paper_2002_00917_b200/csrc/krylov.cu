@@ -15,6 +15,15 @@ namespace pslr {
 
 static cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
 
+// Leading dimension of a column-major Krylov basis: n rounded up to 32 doubles and made an
+// odd multiple of 256 B, so the columns of one row tile do not share L1/L2 sets (a
+// power-of-two n, e.g. 128^3, would put every column of a tile in the same set).
+static int64_t basis_ld(int64_t n) {
+  int64_t ld = (n + 31) / 32 * 32;
+  if (((ld / 32) & 1) == 0) ld += 32;
+  return ld;
+}
+
 static int dnorm(pslr_ctx* ctx, const double* x, int64_t n, double* out_host, cudaStream_t st) {
   RET(ensure(ctx, &ctx->red, &ctx->red_len, (int64_t)dot_grid(n, ctx->sm_count) * 1 + 8));
   RET(ensure(ctx, &ctx->h_dev, &ctx->h_len, 8));
@@ -28,19 +37,18 @@ static int dnorm(pslr_ctx* ctx, const double* x, int64_t n, double* out_host, cu
 
 // Classical Gram-Schmidt with one reorthogonalisation against the first k columns
 // of X (column-major, ld = n): krylov.py:75-80 / lowrank.py:62-67.  h_host = h1 + h2,
-// hnorm = ||w|| after both passes.
-static int cgs2(pslr_ctx* ctx, const double* X, int64_t n, int k, double* w, double* h_host,
+// hnorm = ||w|| after both passes.  Three passes over X (each projection fused with the
+// following dot / norm) and one host synchronisation.
+static int cgs2(pslr_ctx* ctx, const double* X, int64_t ld, int64_t n, int k, double* w, double* h_host,
                 double* hnorm, cudaStream_t st) {
   RET(ensure(ctx, &ctx->red, &ctx->red_len, (int64_t)dot_grid(n, ctx->sm_count) * (k + 1) + 8));
   RET(ensure(ctx, &ctx->h_dev, &ctx->h_len, 2 * (int64_t)k + 8));
   double* h1 = ctx->h_dev;
   double* h2 = ctx->h_dev + k;
   double* nn = ctx->h_dev + 2 * k;
-  CKL(launch_multidot(ctx, X, n, k, w, n, h1, st));
-  CKL(launch_gemv_sub(X, n, k, h1, w, n, st));
-  CKL(launch_multidot(ctx, X, n, k, w, n, h2, st));
-  CKL(launch_gemv_sub(X, n, k, h2, w, n, st));
-  CKL(launch_multidot(ctx, w, n, 1, w, n, nn, st));
+  CKL(launch_multidot(ctx, X, ld, k, w, n, h1, st));      // h1 = X^T w
+  CKL(launch_sub_dot(ctx, X, ld, k, h1, w, n, h2, st));   // w -= X h1 ; h2 = X^T w
+  CKL(launch_sub_norm(ctx, X, ld, k, h2, w, n, nn, st));  // w -= X h2 ; nn = w.w
   std::vector<double> tmp(2 * k + 1);
   CK(cudaMemcpyAsync(tmp.data(), ctx->h_dev, (2 * k + 1) * sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -65,18 +73,19 @@ int pslr_arnoldi(pslr_ctx* ctx, int64_t m, int64_t rank, const double* v0, doubl
   rank = std::min(rank, q);
   *r_out = 0;
   if (q == 0 || rank == 0) return PSLR_OK;
-  RET(ensure(ctx, &ctx->kv, &ctx->kv_len, q * (rank + 1)));
-  double* Vc = ctx->kv;  // column-major q x (rank+1)
-  CK(cudaMemsetAsync(Vc, 0, q * (rank + 1) * sizeof(double), st));
+  const int64_t ldq = basis_ld(q);
+  RET(ensure(ctx, &ctx->kv, &ctx->kv_len, ldq * (rank + 1)));
+  double* Vc = ctx->kv;  // column-major q x (rank+1), leading dimension ldq
+  CK(cudaMemsetAsync(Vc, 0, ldq * (rank + 1) * sizeof(double), st));
   CK(cudaMemcpyAsync(Vc, v0, q * sizeof(double), cudaMemcpyHostToDevice, st));
   std::vector<double> Hb((rank + 1) * rank, 0.0);  // row-major (rank+1) x rank
   std::vector<double> h(rank + 1);
   int64_t r = rank;
   double* w = ctx->kw;
   for (int64_t j = 0; j < rank; ++j) {
-    RET(op_apply_err(ctx, m, Vc + j * q, w, st));
+    RET(op_apply_err(ctx, m, Vc + j * ldq, w, st));
     double hn = 0.0;
-    RET(cgs2(ctx, Vc, q, (int)(j + 1), w, h.data(), &hn, st));
+    RET(cgs2(ctx, Vc, ldq, q, (int)(j + 1), w, h.data(), &hn, st));
     for (int64_t i = 0; i <= j; ++i) Hb[i * rank + j] = h[i];
     Hb[(j + 1) * rank + j] = hn;
     if (hn <= 1e-14) {  // lowrank.py:69-71 (BREAKDOWN_RTOL, start vector has norm 1)
@@ -84,9 +93,9 @@ int pslr_arnoldi(pslr_ctx* ctx, int64_t m, int64_t rank, const double* v0, doubl
       break;
     }
     CK(cudaMemcpyAsync(ctx->h_dev, &hn, sizeof(double), cudaMemcpyHostToDevice, st));
-    CKL(launch_div_scalar(w, ctx->h_dev, Vc + (j + 1) * q, q, st));
+    CKL(launch_div_scalar(w, ctx->h_dev, Vc + (j + 1) * ldq, q, st));
   }
-  CKL(launch_transpose_basis(Vc, q, (int)r, V_dev, st));
+  CKL(launch_transpose_basis(Vc, ldq, q, (int)r, V_dev, st));
   for (int64_t i = 0; i < r; ++i)
     for (int64_t j = 0; j < r; ++j) H[i * r + j] = Hb[i * rank + j];
   CK(cudaStreamSynchronize(st));
@@ -141,7 +150,8 @@ int pslr_gmres(pslr_ctx* ctx, int64_t m, const double* b, double* x, double tol,
       break;
     }
     const int64_t cycle = restart <= 0 ? maxit - total : std::min(restart, maxit - total);
-    RET(ensure(ctx, &ctx->kv, &ctx->kv_len, n * (cycle + 1)));
+    const int64_t ld = basis_ld(n);
+    RET(ensure(ctx, &ctx->kv, &ctx->kv_len, ld * (cycle + 1)));
     if (flexible) RET(ensure(ctx, &ctx->kz, &ctx->kz_len, n * cycle));
     double* Vb = ctx->kv;
     std::vector<double> Hc((cycle + 1) * cycle, 0.0);  // row-major (cycle+1) x cycle
@@ -156,10 +166,10 @@ int pslr_gmres(pslr_ctx* ctx, int64_t m, const double* b, double* x, double tol,
     while (j < cycle) {
       // w = A M v_j                                          krylov.py:74
       double* mv = flexible ? ctx->kz + j * n : t;
-      RET(apply_M(Vb + j * n, mv));
+      RET(apply_M(Vb + j * ld, mv));
       CKL(launch_spmv(ctx->A, mv, w, st));
       double hnext = 0.0;
-      RET(cgs2(ctx, Vb, n, (int)(j + 1), w, h.data(), &hnext, st));
+      RET(cgs2(ctx, Vb, ld, n, (int)(j + 1), w, h.data(), &hnext, st));
       bool finite = std::isfinite(hnext);
       for (int64_t i = 0; i <= j; ++i) finite = finite && std::isfinite(h[i]);
       if (!finite) return fail(PSLR_ENONFINITE, "GMRES diverged: non-finite values in the recurrence");
@@ -192,7 +202,7 @@ int pslr_gmres(pslr_ctx* ctx, int64_t m, const double* b, double* x, double tol,
       if (est <= tol) break;
       if (j < cycle) {
         CK(cudaMemcpyAsync(ctx->h_dev, &hnext, sizeof(double), cudaMemcpyHostToDevice, st));
-        CKL(launch_div_scalar(w, ctx->h_dev, Vb + j * n, n, st));
+        CKL(launch_div_scalar(w, ctx->h_dev, Vb + j * ld, n, st));
       }
     }
     if (j > 0) {  // krylov.py:110-114
@@ -207,7 +217,7 @@ int pslr_gmres(pslr_ctx* ctx, int64_t m, const double* b, double* x, double tol,
         CKL(launch_gemv(ctx->kz, n, (int)j, ctx->h_dev, t, n, st));
         CKL(launch_add_inplace(x, t, n, st));
       } else {
-        CKL(launch_gemv(Vb, n, (int)j, ctx->h_dev, r, n, st));
+        CKL(launch_gemv(Vb, ld, (int)j, ctx->h_dev, r, n, st));
         RET(apply_M(r, t));
         CKL(launch_add_inplace(x, t, n, st));
       }

@@ -42,14 +42,17 @@ int launch_correction_core(const pslr_ctx* ctx, cudaStream_t st);
 int launch_spmv(const DevCsr& M, const double* x, double* y, cudaStream_t st);
 int launch_multidot(pslr_ctx* ctx, const double* X, int64_t ld, int k, const double* y, int64_t n,
                     double* out, cudaStream_t st);
-int launch_gemv_sub(const double* X, int64_t ld, int k, const double* h, double* w, int64_t n,
-                    cudaStream_t st);
+// CGS2 passes (k <= 128 columns): w -= X h0 then h = X^T w  /  w -= X h0 then out[0] = w.w
+int launch_sub_dot(pslr_ctx* ctx, const double* X, int64_t ld, int k, const double* h0, double* w,
+                   int64_t n, double* out, cudaStream_t st);
+int launch_sub_norm(pslr_ctx* ctx, const double* X, int64_t ld, int k, const double* h0, double* w,
+                    int64_t n, double* out, cudaStream_t st);
 int launch_gemv(const double* X, int64_t ld, int k, const double* h, double* y, int64_t n,
                 cudaStream_t st);
 int launch_sub(const double* a, const double* b, double* y, int64_t n, cudaStream_t st);
 int launch_add_inplace(double* y, const double* a, int64_t n, cudaStream_t st);
 int launch_div_scalar(const double* x, const double* s, double* y, int64_t n, cudaStream_t st);
-int launch_transpose_basis(const double* X, int64_t q, int r, double* Y, cudaStream_t st);
+int launch_transpose_basis(const double* X, int64_t ld, int64_t q, int r, double* Y, cudaStream_t st);
 int dot_grid(int64_t n, int sm_count);
 int vt_grid(int64_t q, int sm_count);
 int launch_vt_dot(pslr_ctx* ctx, const double* y, cudaStream_t st);
