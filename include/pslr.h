@@ -15,6 +15,7 @@
  *   PSLR_ENONFINITE         -> ArithmeticError       (krylov.py:81-82, 122-123)
  *   PSLR_ESINGULAR          -> CorrectionSingularError (lowrank.py:88-93)
  *   PSLR_ECUDA / PSLR_ENOMEM-> RuntimeError
+ *   PSLR_ENOTSPD            -> NotSpdError           (krylov.py:18-19, 153-154)
  * pslr_last_error() returns a thread-local message for the last failure.
  *
  * Threading: one context per GPU per process; calls on one context are
@@ -37,6 +38,7 @@ extern "C" {
 #define PSLR_EINVAL 5
 #define PSLR_ENOMEM 6
 #define PSLR_ENCCL 7
+#define PSLR_ENOTSPD 8
 
 typedef struct pslr_ctx pslr_ctx;
 typedef struct pslr_factors pslr_factors;
@@ -198,6 +200,12 @@ int pslr_arnoldi(pslr_ctx* ctx, int64_t m, int64_t rank, const double* v0, doubl
 int pslr_gmres(pslr_ctx* ctx, int64_t m, const double* b, double* x, double tol, int64_t maxit,
                int64_t restart, int precond, int flexible, int64_t* iterations, int* converged,
                double* final_relres, double* history, int64_t* history_len, void* stream);
+/* krylov.py:132-174: preconditioned CG (zero initial guess) on the same operators,
+ * the CLI's `--krylov cg` path (cli.py:138-139).  PSLR_ENOTSPD when p.Ap <= 0
+ * (krylov.py:153-154).  b, x: device n-vectors; history: host, maxit+1 doubles. */
+int pslr_cg(pslr_ctx* ctx, int64_t m, const double* b, double* x, double tol, int64_t maxit, int precond,
+            int64_t* iterations, int* converged, double* final_relres, double* history,
+            int64_t* history_len, void* stream);
 
 #ifdef __cplusplus
 }

@@ -15,7 +15,7 @@ every hot-path operator requires a CUDA device.
 
 from ._lib import CorrectionSingularError
 from .ilu import BlockILU, IluFactor, factor_blocks, ilut
-from .krylov import NotSpdError, SolveReport, fgmres, gmres, gmres_device
+from .krylov import NotSpdError, SolveReport, cg, cg_device, fgmres, gmres, gmres_device
 from .lowrank import LowRankCorrection, apply_correction, arnoldi, arnoldi_device, build_correction
 from .partition import PartitionedSystem, PartitionSpec, classify_and_reorder, partition_graph
 from .preconditioner import FillStats, PslrConfig, PslrPreconditioner, build, with_correction
@@ -27,7 +27,7 @@ __version__ = "0.1.0"
 
 __all__ = [
     "CorrectionSingularError", "BlockILU", "IluFactor", "factor_blocks", "ilut", "NotSpdError",
-    "SolveReport", "fgmres", "gmres", "gmres_device", "LowRankCorrection", "apply_correction",
+    "SolveReport", "cg", "cg_device", "fgmres", "gmres", "gmres_device", "LowRankCorrection", "apply_correction",
     "arnoldi", "arnoldi_device", "build_correction", "PartitionedSystem", "PartitionSpec",
     "classify_and_reorder", "partition_graph", "FillStats", "PslrConfig", "PslrPreconditioner",
     "build", "with_correction", "ErrOperator", "SchurContext", "apply_Err", "apply_Es",

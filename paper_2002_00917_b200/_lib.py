@@ -19,7 +19,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PSLR_LIB") or os.path.join(_HERE, "lib", "libpslr.so")
 
 PSLR_OK, PSLR_EDIM, PSLR_ENONFINITE, PSLR_ESINGULAR, PSLR_ECUDA, PSLR_EINVAL, PSLR_ENOMEM, \
-    PSLR_ENCCL = range(8)
+    PSLR_ENCCL, PSLR_ENOTSPD = range(9)
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
@@ -107,6 +107,8 @@ EXPORTS = {
     "pslr_gmres": (c_int, P, c_i64, P, P, c_dbl, c_i64, c_i64, c_int, c_int,
                    ctypes.POINTER(c_i64), ctypes.POINTER(c_int), ctypes.POINTER(c_dbl), P,
                    ctypes.POINTER(c_i64), P),
+    "pslr_cg": (c_int, P, c_i64, P, P, c_dbl, c_i64, c_int, ctypes.POINTER(c_i64), ctypes.POINTER(c_int),
+                ctypes.POINTER(c_dbl), P, ctypes.POINTER(c_i64), P),
 }
 
 fns = {name: _sig(name, sig[0], *sig[1:]) for name, sig in EXPORTS.items()}
@@ -114,6 +116,10 @@ fns = {name: _sig(name, sig[0], *sig[1:]) for name, sig in EXPORTS.items()}
 
 class CorrectionSingularError(RuntimeError):
     """I - H is numerically singular (lowrank.py:22-23)."""
+
+
+class NotSpdError(RuntimeError):
+    """CG hit a non-positive curvature direction: matrix not SPD (krylov.py:18-19)."""
 
 
 def check(rc: int):
@@ -127,6 +133,8 @@ def check(rc: int):
         raise ArithmeticError(msg)
     if rc == PSLR_ESINGULAR:
         raise CorrectionSingularError(msg)
+    if rc == PSLR_ENOTSPD:
+        raise NotSpdError(msg)
     raise RuntimeError(f"libpslr error {rc}: {msg}")
 
 

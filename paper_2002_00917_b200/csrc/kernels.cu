@@ -391,6 +391,71 @@ cgs_pass_kernel(const double* __restrict__ X, int64_t ld, int k, double* __restr
   if (tid == 0) *counter = 0u;
 }
 
+// ---------------------------------------------------------------- CG vector updates
+// krylov.py:156-158 fused with the residual norm: x += alpha p ; r -= alpha Ap ; out = r.r
+// (numpy order: alpha * p first, then the add), deterministic two-level reduction.
+__global__ void __launch_bounds__(256)
+cg_update_kernel(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
+                 const double* __restrict__ Ap, double alpha, int64_t n, double* __restrict__ partials,
+                 double* __restrict__ out, unsigned int* counter) {
+  __shared__ double red[8];
+  __shared__ bool last;
+  double acc = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += 4 * stride) {
+    double pv[4], av[4], xv[4], rv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t j = i + u * stride;
+      const bool ok = j < n;
+      pv[u] = ok ? p[j] : 0.0;
+      av[u] = ok ? Ap[j] : 0.0;
+      xv[u] = ok ? x[j] : 0.0;
+      rv[u] = ok ? r[j] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t j = i + u * stride;
+      const double xn = xv[u] + alpha * pv[u];
+      const double rn = rv[u] - alpha * av[u];
+      if (j < n) {
+        x[j] = xn;
+        r[j] = rn;
+        acc = acc + rn * rn;
+      }
+    }
+  }
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int o = 16; o > 0; o >>= 1) acc = acc + __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) red[warp] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s = s + red[w];
+    partials[blockIdx.x] = s;
+    __threadfence();
+    last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  if (warp == 0) {
+    double v = 0.0;
+    for (int b = lane; b < (int)gridDim.x; b += 32) v = v + __ldcg(partials + b);
+    for (int o = 16; o > 0; o >>= 1) v = v + __shfl_xor_sync(0xffffffffu, v, o);
+    if (lane == 0) {
+      out[0] = v;
+      *counter = 0u;
+    }
+  }
+}
+
+// p = z + beta p (krylov.py:163)
+__global__ void xpby_kernel(const double* __restrict__ z, double beta, double* __restrict__ p, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    p[i] = z[i] + beta * p[i];
+}
+
 // w[i] = w[i] - sum_c X[c*ld + i] * h[c]   (w - V h, numpy order: V@h first; k > 128 passes)
 __global__ void gemv_sub_kernel(const double* __restrict__ X, int64_t ld, int k,
                                 const double* __restrict__ h, double* __restrict__ w, int64_t n) {
@@ -567,6 +632,19 @@ int launch_sub_norm(pslr_ctx* ctx, const double* X, int64_t ld, int k, const dou
   if (k <= kCgsMaxCols) return launch_cgs<kSubNorm>(ctx, X, ld, k, w, n, h0, out, st);
   const int e = launch_gemv_sub(X, ld, k, h0, w, n, st);
   return e ? e : launch_multidot(ctx, w, n, 1, w, n, out, st);
+}
+
+int launch_cg_update(pslr_ctx* ctx, double* x, double* r, const double* p, const double* Ap, double alpha,
+                     int64_t n, double* out, cudaStream_t st) {
+  const int g = dot_grid(n, ctx->sm_count);
+  cg_update_kernel<<<g, 256, 0, st>>>(x, r, p, Ap, alpha, n, ctx->red, out, ctx->counter);
+  return (int)cudaGetLastError();
+}
+
+int launch_xpby(const double* z, double beta, double* p, int64_t n, cudaStream_t st) {
+  if (n == 0) return 0;
+  xpby_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, st>>>(z, beta, p, n);
+  return (int)cudaGetLastError();
 }
 
 int launch_gemv(const double* X, int64_t ld, int k, const double* h, double* y, int64_t n,

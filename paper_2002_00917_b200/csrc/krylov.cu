@@ -243,4 +243,92 @@ int pslr_gmres(pslr_ctx* ctx, int64_t m, const double* b, double* x, double tol,
   return PSLR_OK;
 }
 
+// krylov.py:132-174.  Device vectors; the scalar recurrence (alpha, beta, the SPD check,
+// the residual test) is host code with the reference's exact control flow.
+int pslr_cg(pslr_ctx* ctx, int64_t m, const double* b, double* x, double tol, int64_t maxit, int precond,
+            int64_t* iterations, int* converged, double* final_relres, double* history,
+            int64_t* history_len, void* stream) {
+  RET(set_device(ctx));
+  if (ctx->nghost) return fail(PSLR_EINVAL, "sharded context: run the Krylov loop in shard.py");
+  if (maxit < 0) return fail(PSLR_EDIM, "maxit must be >= 0");
+  cudaStream_t st = S(stream);
+  const int64_t n = ctx->n;
+  std::vector<double> hist;
+  auto finish = [&](bool conv, int64_t its, double rel) {
+    *iterations = its;
+    *converged = conv ? 1 : 0;
+    *final_relres = rel;
+    const size_t cnt = std::min<size_t>(hist.size(), (size_t)maxit + 1);
+    for (size_t i = 0; i < cnt; ++i) history[i] = hist[i];
+    *history_len = (int64_t)cnt;
+  };
+  double bnorm = 0.0;
+  RET(dnorm(ctx, b, n, &bnorm, st));
+  CK(cudaMemsetAsync(x, 0, n * sizeof(double), st));
+  if (bnorm == 0.0) {  // krylov.py:138-139
+    hist.push_back(1.0);
+    finish(true, 0, 0.0);
+    CK(cudaStreamSynchronize(st));
+    return PSLR_OK;
+  }
+  RET(ensure(ctx, &ctx->kv, &ctx->kv_len, n));
+  RET(ensure(ctx, &ctx->red, &ctx->red_len, (int64_t)dot_grid(n, ctx->sm_count) + 8));
+  RET(ensure(ctx, &ctx->h_dev, &ctx->h_len, 8));
+  double* r = ctx->kr;
+  double* z = ctx->kt;
+  double* Ap = ctx->kw;
+  double* p = ctx->kv;
+  auto apply_M = [&](const double* in, double* out) -> int {
+    if (precond) return op_apply(ctx, m, in, out, st);
+    CK(cudaMemcpyAsync(out, in, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    return PSLR_OK;
+  };
+  auto dot = [&](const double* u, const double* v, double* out) -> int {
+    CKL(launch_multidot(ctx, u, n, 1, v, n, ctx->h_dev, st));
+    CK(cudaMemcpyAsync(out, ctx->h_dev, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    return PSLR_OK;
+  };
+  CK(cudaMemcpyAsync(r, b, n * sizeof(double), cudaMemcpyDeviceToDevice, st));  // r = b
+  RET(apply_M(r, z));                                                          // z = M r
+  CK(cudaMemcpyAsync(p, z, n * sizeof(double), cudaMemcpyDeviceToDevice, st));  // p = z
+  double rz = 0.0;
+  RET(dot(r, z, &rz));
+  hist.push_back(1.0);
+  bool conv = false;
+  double relres = 1.0;
+  int64_t it = 0;
+  for (it = 1; it <= maxit; ++it) {
+    CKL(launch_spmv(ctx->A, p, Ap, st));  // krylov.py:152
+    double pAp = 0.0;
+    RET(dot(p, Ap, &pAp));
+    if (pAp <= 0.0) {  // krylov.py:153-154
+      CK(cudaStreamSynchronize(st));
+      return fail(PSLR_ENOTSPD, "matrix not SPD: non-positive curvature encountered");
+    }
+    const double alpha = rz / pAp;
+    CKL(launch_cg_update(ctx, x, r, p, Ap, alpha, n, ctx->h_dev, st));  // x, r, r.r
+    double rr = 0.0;
+    CK(cudaMemcpyAsync(&rr, ctx->h_dev, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    relres = std::sqrt(rr) / bnorm;
+    hist.push_back(relres);
+    if (relres <= tol) {
+      conv = true;
+      break;
+    }
+    RET(apply_M(r, z));
+    double rz_new = 0.0;
+    RET(dot(r, z, &rz_new));
+    CKL(launch_xpby(z, rz_new / rz, p, n, st));  // krylov.py:163
+    rz = rz_new;
+  }
+  const int64_t its = conv ? it : maxit;
+  if (!conv)
+    while ((int64_t)hist.size() < maxit + 1) hist.push_back(relres);
+  finish(conv, its, relres);
+  CK(cudaStreamSynchronize(st));
+  return PSLR_OK;
+}
+
 }  // extern "C"

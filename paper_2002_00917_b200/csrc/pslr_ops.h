@@ -49,6 +49,10 @@ int launch_sub_norm(pslr_ctx* ctx, const double* X, int64_t ld, int k, const dou
                     int64_t n, double* out, cudaStream_t st);
 int launch_gemv(const double* X, int64_t ld, int k, const double* h, double* y, int64_t n,
                 cudaStream_t st);
+// CG (krylov.py:156-163): x += alpha p ; r -= alpha Ap ; out[0] = r.r   /   p = z + beta p
+int launch_cg_update(pslr_ctx* ctx, double* x, double* r, const double* p, const double* Ap, double alpha,
+                     int64_t n, double* out, cudaStream_t st);
+int launch_xpby(const double* z, double beta, double* p, int64_t n, cudaStream_t st);
 int launch_sub(const double* a, const double* b, double* y, int64_t n, cudaStream_t st);
 int launch_add_inplace(double* y, const double* a, int64_t n, cudaStream_t st);
 int launch_div_scalar(const double* x, const double* s, double* y, int64_t n, cudaStream_t st);

@@ -1,11 +1,11 @@
-"""Right-preconditioned restarted GMRES and FGMRES (mirrors pslr/krylov.py).
+"""Right-preconditioned restarted GMRES / FGMRES and preconditioned CG (mirrors pslr/krylov.py).
 
 When the operator pair is a PSLR preconditioner's own (A = P.matvec,
 M = P.apply — the pairing cli._solve_with uses, cli.py:131-143 — or their
 original-space versions), the whole solve runs on the device: pslr_gmres
 drives the apply, the A-SpMV and the CGS2 kernels with the reference's exact
 control flow (krylov.py:55-127), only the (cycle+1)-sized Givens/least-squares
-bookkeeping is scalar host code.  Arbitrary Python callables keep the
+bookkeeping is scalar host code; pslr_cg does the same for CG (krylov.py:132-174).  Arbitrary Python callables keep the
 reference's generic contract.
 """
 
@@ -20,8 +20,7 @@ import numpy as np
 from . import _lib
 
 
-class NotSpdError(RuntimeError):
-    """CG hit a non-positive curvature direction: matrix not SPD (krylov.py:18-19)."""
+NotSpdError = _lib.NotSpdError  # krylov.py:18-19 (raised by the device CG through its status code)
 
 
 @dataclass
@@ -97,6 +96,92 @@ def gmres_device(P, b, tol: float = 1e-8, maxit: int = 500, restart: int = 0,
     rep = SolveReport(bool(conv.value), int(its.value), float(rel.value),
                       hist[:hlen.value].tolist(), elapsed)
     return (xd if is_tensor else xd.cpu().numpy()), rep
+
+
+def cg(apply_A, apply_M, b, tol: float = 1e-8, maxit: int = 500):
+    """Preconditioned conjugate gradient for SPD systems, zero initial guess (krylov.py:132-174).
+    On a PSLR preconditioner's own operator pair (the CLI's `--krylov cg`, cli.py:138-139)
+    the whole loop runs on the device (pslr_cg)."""
+    P = _bound(apply_M, "apply")
+    if P is not None and _bound(apply_A, "matvec") is P:
+        return cg_device(P, b, tol, maxit)
+    P = _bound(apply_M, "apply_original")
+    if P is not None and _bound(apply_A, "matvec_original") is P:
+        perm = P.system.perm
+        x, rep = cg_device(P, np.asarray(b, dtype=np.float64)[perm.inverse], tol, maxit)
+        return x[perm.forward], rep
+    return _cg_generic(apply_A, apply_M, b, tol, maxit)
+
+
+def cg_device(P, b, tol: float = 1e-8, maxit: int = 500, precond: bool = True):
+    """The device CG (pslr_cg) in P's reordered space; b numpy or CUDA tensor."""
+    from .device import torch_mod
+    t = torch_mod()
+    dev = P.device
+    dev.ensure_correction(P.correction)
+    n = P.system.n
+    is_tensor = hasattr(b, "data_ptr")
+    if is_tensor:
+        bd = b.contiguous()
+    else:
+        b = np.asarray(b, dtype=np.float64)
+        if b.shape[0] != n:
+            raise ValueError(f"vector has length {b.shape[0]}, system is {n}-dimensional")
+        bd = t.from_numpy(np.ascontiguousarray(b)).to(dev.dev)
+    xd = t.empty(n, dtype=t.float64, device=dev.dev)
+    hist = np.zeros(max(int(maxit), 0) + 1)
+    its, conv, rel, hlen = ctypes.c_int64(), ctypes.c_int(), ctypes.c_double(), ctypes.c_int64()
+    t0 = time.perf_counter()
+    _lib.check(_lib.fns["pslr_cg"](
+        dev.handle, int(P.series_degree), bd.data_ptr(), xd.data_ptr(), float(tol), int(maxit),
+        1 if precond else 0, ctypes.byref(its), ctypes.byref(conv), ctypes.byref(rel),
+        hist.ctypes.data, ctypes.byref(hlen), dev.stream()))
+    elapsed = time.perf_counter() - t0
+    rep = SolveReport(bool(conv.value), int(its.value), float(rel.value),
+                      hist[:hlen.value].tolist(), elapsed)
+    return (xd if is_tensor else xd.cpu().numpy()), rep
+
+
+def _cg_generic(apply_A, apply_M, b, tol, maxit):
+    """The reference recurrence for arbitrary callables (krylov.py:132-174)."""
+    if apply_M is None:
+        apply_M = _identity
+    b = np.asarray(b, dtype=np.float64)
+    n = b.shape[0]
+    t0 = time.perf_counter()
+    bnorm = np.linalg.norm(b)
+    if bnorm == 0.0:
+        return np.zeros(n), SolveReport(True, 0, 0.0, [1.0], time.perf_counter() - t0)
+    x = np.zeros(n)
+    r = b.copy()
+    z = np.asarray(apply_M(r), dtype=np.float64)
+    p = z.copy()
+    rz = r @ z
+    history = [1.0]
+    converged = False
+    relres = 1.0
+    it = 0
+    for it in range(1, maxit + 1):
+        Ap = np.asarray(apply_A(p), dtype=np.float64)
+        pAp = p @ Ap
+        if pAp <= 0.0:
+            raise NotSpdError("matrix not SPD: non-positive curvature encountered")
+        alpha = rz / pAp
+        x = x + alpha * p
+        r = r - alpha * Ap
+        relres = np.linalg.norm(r) / bnorm
+        history.append(relres)
+        if relres <= tol:
+            converged = True
+            break
+        z = np.asarray(apply_M(r), dtype=np.float64)
+        rz_new = r @ z
+        p = z + (rz_new / rz) * p
+        rz = rz_new
+    iterations = it if converged else maxit
+    if not converged:
+        history.extend([relres] * (maxit + 1 - len(history)))
+    return x, SolveReport(converged, iterations, relres, history, time.perf_counter() - t0)
 
 
 def _gmres_generic(apply_A, apply_M, b, tol, maxit, restart, flexible):

@@ -183,6 +183,25 @@ def test_gmres_cfg1_fails_at_maxit_like_reference():
     assert np.max(np.abs(h - hr) / hr) <= 2e-2
 
 
+@pytest.mark.parametrize("cfg,relres", [("cfg2", 1.56e-5), ("cfg3", 1.55e-3)])
+def test_gmres_full_size_fails_at_maxit_like_reference(cfg, relres):
+    """SURVEY §8d rule at BASELINE size: the reference fails at maxit 500 on cfg2
+    (GMRES(50), relres 1.56e-5) and cfg3 (restart 50, stagnating at 1.55e-3, SURVEY §6);
+    the device solve must fail at maxit too, at the same residual level."""
+    import paper_2002_00917_b200 as pg
+    from paper_2002_00917_b200 import workloads
+    wl = workloads.CONFIGS[cfg]
+    A = wl.matrix()
+    P = pg.build(A, wl.config())
+    b = workloads.seeded_rhs(A, 0)
+    x, rep = pg.gmres(P.matvec_original, P.apply_original, b, tol=wl.tol, maxit=wl.maxit,
+                      restart=wl.restart, flexible=wl.flexible)
+    assert not rep.converged and rep.iterations == wl.maxit and len(rep.history) == wl.maxit + 1
+    true_rel = np.linalg.norm(b - A @ x) / np.linalg.norm(b)
+    assert abs(true_rel - relres) <= 0.02 * relres  # the survey quotes 3 significant digits
+    assert abs(rep.final_relres - true_rel) <= 1e-6 * true_rel
+
+
 @pytest.mark.parametrize("m", [3, 5])
 def test_gmres_crit07(m):
     import paper_2002_00917_b200 as pg
@@ -218,10 +237,11 @@ def test_gmres_original_space_driver():
 
 
 # ---------------------------------------------------------------- BASELINE-size parity
-@pytest.mark.parametrize("cfg", ["cfg2"])
+@pytest.mark.parametrize("cfg", ["cfg2", "cfg3", "cfg5"])
 def test_full_size_apply_matches_oracle(cfg):
-    """cfg2 (64^3, s=16, m=3, r=32): device apply vs the oracle's on identical
-    factors and correction state; solves bit-exact, apply <= 1e-10."""
+    """BASELINE sizes — cfg2 (64^3, s=16, m=3, r=32), cfg3 (128^3 upwind, s=64, m=5, r=64),
+    cfg5 (the bench workload: 128^3, s=32, m=3, r=64): device apply vs the oracle's on
+    identical factors and correction state; solves bit-exact, apply <= 1e-10."""
     import paper_2002_00917_b200 as pg
     from paper_2002_00917_b200 import workloads
     from oracle import pslr_oracle as O
