@@ -22,6 +22,7 @@ from .preconditioner import FillStats, PslrConfig, PslrPreconditioner, build, wi
 from .schur import (ErrOperator, SchurContext, apply_Err, apply_Es, apply_neumann, apply_S,
                     build_schur_context, solve_B, solve_C0)
 from .sparse import Permutation, canonical, extract_submatrix, matvec, permute_symmetric
+from .sweep import SWEEP_COLUMNS, sweep
 
 __version__ = "0.1.0"
 
@@ -32,5 +33,5 @@ __all__ = [
     "classify_and_reorder", "partition_graph", "FillStats", "PslrConfig", "PslrPreconditioner",
     "build", "with_correction", "ErrOperator", "SchurContext", "apply_Err", "apply_Es",
     "apply_neumann", "apply_S", "build_schur_context", "solve_B", "solve_C0", "Permutation",
-    "canonical", "extract_submatrix", "matvec", "permute_symmetric",
+    "canonical", "extract_submatrix", "matvec", "permute_symmetric", "SWEEP_COLUMNS", "sweep",
 ]
