@@ -251,10 +251,23 @@ def run_sharded(args, rank, world, local):
     t0 = time.perf_counter()
     A = workloads.laplacian3d(nx, ny, nz * world, base.shift)
     s_glob = base.s * world
-    spec = partition_graph(A, s_glob, seed=0)
-    ps = classify_and_reorder(A, spec)
     cfg = __import__("paper_2002_00917_b200").PslrConfig(num_subdomains=s_glob, series_degree=base.m,
                                                          rank=base.rank, droptol=1e-2, seed=0)
+    # the global reordering is the same on every rank: rank 0 computes it (or finds it in
+    # the setup cache) and the others load it (setup_cache.py; content-keyed, so a stale
+    # file can never be picked up)
+    from paper_2002_00917_b200 import setup_cache as SC
+    order_path = os.path.join(SC.cache_dir() or "/tmp/pslr_setup_cache",
+                              f"order_{SC.setup_key(SC.matrix_digest(A), cfg)}.npz")
+    hit = SC.load_setup(order_path, A, need_factors=False) if rank == 0 else None
+    if rank == 0 and hit is None:
+        ps = classify_and_reorder(A, partition_graph(A, s_glob, seed=0))
+        SC.save_setup(order_path, ps)
+    elif rank == 0:
+        ps = hit[0]
+    dist.barrier()
+    if rank != 0:
+        ps = SC.load_setup(order_path, A, need_factors=False)[0]
     P = shard.build_sharded(ps, cfg, device=local)
     # K independent sharded applies in flight (as at N=1): pipeline j has its own clone
     # context, stream and process group (its NCCL communicator), so every group sees its

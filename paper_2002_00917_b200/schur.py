@@ -47,12 +47,16 @@ def _block_diag_part(C, sizes) -> sp.csr_matrix:
 
 
 def build_schur_context(ps: PartitionedSystem, droptol: float = 1e-2, fill_cap: int | None = None,
-                        device=None) -> SchurContext:
+                        device=None, factors=None) -> SchurContext:
     """Factor the B_i and C_i diagonal blocks (host, native C++) and upload everything
-    to the device (schur.py:52-59)."""
-    b_ilu = factor_blocks(ps.B, ps.interior_sizes, droptol=droptol, fill_cap=fill_cap)
+    to the device (schur.py:52-59).  `factors` = (b_ilu, c0_ilu) from the setup cache
+    skips the factorisation."""
     C0 = _block_diag_part(ps.C, ps.interface_sizes)
-    c0_ilu = factor_blocks(C0, ps.interface_sizes, droptol=droptol, fill_cap=fill_cap)
+    if factors is not None:
+        b_ilu, c0_ilu = factors
+    else:
+        b_ilu = factor_blocks(ps.B, ps.interior_sizes, droptol=droptol, fill_cap=fill_cap)
+        c0_ilu = factor_blocks(C0, ps.interface_sizes, droptol=droptol, fill_cap=fill_cap)
     Cg = canonical(ps.C - C0)
     dev = DeviceContext(ps, b_ilu, c0_ilu, C0, Cg, device=device)
     return SchurContext(system=ps, b_ilu=b_ilu, c0_ilu=c0_ilu, C0=C0, Cg=Cg, device=dev)
