@@ -370,6 +370,26 @@ def run_sharded(args, rank, world, local):
     tt = torch.tensor([ms_e2e], device="cuda", dtype=torch.float64)
     dist.all_reduce(tt, op=dist.ReduceOp.MAX)
     ms_e2e = float(tt.item())
+    # GMRES time-to-solution of the coupled N-GPU system: b = A x*, x*
+    # seeded; shard.sharded_gmres (one sharded apply + halo'd A-SpMV + three allreduced CGS2
+    # passes per iteration), wall time max over ranks
+    solve = None
+    if args.gmres_maxit > 0:
+        xs = np.random.default_rng(0).standard_normal(ps.n)
+        b_loc = torch.as_tensor((ps.matrix @ xs), device="cuda")[rows].contiguous()
+        rs = base.restart if base.restart > 0 else 50
+        torch.cuda.synchronize()
+        dist.barrier()
+        t0s = time.perf_counter()
+        _, conv, its, rel, _ = shard.sharded_gmres(P, b_loc, tol=base.tol, maxit=args.gmres_maxit,
+                                                   restart=rs)
+        torch.cuda.synchronize()
+        tsol = torch.tensor([time.perf_counter() - t0s], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tsol, op=dist.ReduceOp.MAX)
+        ts = float(tsol.item())
+        solve = {"solver": "GMRES", "restart": rs, "tol": base.tol, "maxit": args.gmres_maxit,
+                 "iterations": its, "converged": conv, "final_relres": rel, "time_s": ts,
+                 "ms_per_iteration": ts * 1e3 / max(its, 1), "timing": "wall clock, max over ranks"}
     peak, peak_src = hbm_peak()
     per_gpu = bytes_local / (ms / args.steps / 1e3) / 1e9
     nghost = torch.tensor([float(plan.nghost)], device="cuda", dtype=torch.float64)
@@ -400,6 +420,7 @@ def run_sharded(args, rank, world, local):
                     "h2d_bytes_per_step": 8 * int(plan.n_loc), "d2h_bytes_per_step": 8 * int(plan.n_loc),
                     "ms_per_step": ms_e2e / args.e2e_steps},
             "gpu_launches": ((m + 7) * args.steps if NV == 1 else (m + 11) * calls),
+            "solve": solve,
             "clocks": clk,
         }
         emit(line)

@@ -200,6 +200,14 @@ int pslr_arnoldi(pslr_ctx* ctx, int64_t m, int64_t rank, const double* v0, doubl
 int pslr_gmres(pslr_ctx* ctx, int64_t m, const double* b, double* x, double tol, int64_t maxit,
                int64_t restart, int precond, int flexible, int64_t* iterations, int* converged,
                double* final_relres, double* history, int64_t* history_len, void* stream);
+/* One CGS2 pass over a column-major basis X (k columns of n rows, leading dimension ld)
+ * and a vector w, all device pointers (krylov.py:75-80, lowrank.py:62-67):
+ *   mode 0: out[0..k) = X^T w ;  mode 1: w -= X h0, then out[0..k) = X^T w ;
+ *   mode 2: w -= X h0, then out[0] = w.w .
+ * The sharded Krylov loops (shard.py) run the three passes with an allreduce of `out`
+ * between them; the single-GPU drivers use the same kernels inside pslr_gmres/pslr_arnoldi. */
+int pslr_cgs_pass(pslr_ctx* ctx, int mode, const double* X, int64_t ld, int64_t n, int64_t k, double* w,
+                  const double* h0, double* out, void* stream);
 /* krylov.py:132-174: preconditioned CG (zero initial guess) on the same operators,
  * the CLI's `--krylov cg` path (cli.py:138-139).  PSLR_ENOTSPD when p.Ap <= 0
  * (krylov.py:153-154).  b, x: device n-vectors; history: host, maxit+1 doubles. */

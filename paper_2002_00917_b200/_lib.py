@@ -107,6 +107,7 @@ EXPORTS = {
     "pslr_gmres": (c_int, P, c_i64, P, P, c_dbl, c_i64, c_i64, c_int, c_int,
                    ctypes.POINTER(c_i64), ctypes.POINTER(c_int), ctypes.POINTER(c_dbl), P,
                    ctypes.POINTER(c_i64), P),
+    "pslr_cgs_pass": (c_int, P, c_int, P, c_i64, c_i64, c_i64, P, P, P, P),
     "pslr_cg": (c_int, P, c_i64, P, P, c_dbl, c_i64, c_int, ctypes.POINTER(c_i64), ctypes.POINTER(c_int),
                 ctypes.POINTER(c_dbl), P, ctypes.POINTER(c_i64), P),
 }

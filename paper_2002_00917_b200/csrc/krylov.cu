@@ -243,6 +243,20 @@ int pslr_gmres(pslr_ctx* ctx, int64_t m, const double* b, double* x, double tol,
   return PSLR_OK;
 }
 
+int pslr_cgs_pass(pslr_ctx* ctx, int mode, const double* X, int64_t ld, int64_t n, int64_t k, double* w,
+                  const double* h0, double* out, void* stream) {
+  RET(set_device(ctx));
+  if (mode < 0 || mode > 2) return fail(PSLR_EINVAL, "cgs pass mode must be 0, 1 or 2");
+  if (n < 0 || k < 1 || ld < n) return fail(PSLR_EDIM, "cgs pass: need k >= 1, n >= 0, ld >= n");
+  if (mode != 0 && !h0) return fail(PSLR_EINVAL, "cgs pass: projection coefficients missing");
+  cudaStream_t st = S(stream);
+  RET(ensure(ctx, &ctx->red, &ctx->red_len, (int64_t)dot_grid(n, ctx->sm_count) * (k + 1) + 8));
+  if (mode == 0) CKL(launch_multidot(ctx, X, ld, (int)k, w, n, out, st));
+  if (mode == 1) CKL(launch_sub_dot(ctx, X, ld, (int)k, h0, w, n, out, st));
+  if (mode == 2) CKL(launch_sub_norm(ctx, X, ld, (int)k, h0, w, n, out, st));
+  return PSLR_OK;
+}
+
 // krylov.py:132-174.  Device vectors; the scalar recurrence (alpha, beta, the SPD check,
 // the residual test) is host code with the reference's exact control flow.
 int pslr_cg(pslr_ctx* ctx, int64_t m, const double* b, double* x, double tol, int64_t maxit, int precond,

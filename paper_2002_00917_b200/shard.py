@@ -340,6 +340,38 @@ class DeviceShardOps:
                                          self.dev.stream()))
         return y
 
+    def basis(self, rows, n):
+        """Krylov basis storage: `rows` vectors of length n (row-major, padded stride)."""
+        return _basis(self.t, rows, n, self.device)
+
+    def cgs_pass(self, mode, V, k, w, h0=None):
+        """One CGS2 pass over V[:k] (pslr_cgs_pass): 0 -> V w ; 1 -> w -= h0 V, then V w ;
+        2 -> w -= h0 V, then [w.w].  w is updated in place; returns the rank-local partial."""
+        out = self.t.empty(max(k, 1) if mode != 2 else 1, dtype=self.t.float64, device=self.device)
+        self._call("pslr_cgs_pass", int(mode), V.data_ptr(), int(V.stride(0)), int(w.shape[0]), int(k),
+                   w.data_ptr(), h0.data_ptr() if h0 is not None else None, out.data_ptr())
+        return out
+
+
+def _basis(t, rows, n, device):
+    """rows x n view of a rows x ld buffer, ld = n rounded up to 32 doubles and made an odd
+    multiple of 256 B (krylov.cu basis_ld: the columns of one row tile must not share
+    cache sets)."""
+    ld = (n + 31) // 32 * 32
+    if (ld // 32) % 2 == 0:
+        ld += 32
+    return t.zeros((rows, ld), dtype=t.float64, device=device)[:, :n]
+
+
+def cgs2(ops, halo, V, k, w):
+    """krylov.py:75-80 / lowrank.py:62-67 over the rank's rows: three passes over the basis
+    with the projections allreduced in between (h1 = V^T w; w -= V h1 with h2 = V^T w;
+    w -= V h2 with ||w||^2).  w is updated in place; returns (h1 + h2 as numpy, ||w||)."""
+    h1 = halo.allreduce(ops.cgs_pass(0, V, k, w))
+    h2 = halo.allreduce(ops.cgs_pass(1, V, k, w, h1))
+    nn = halo.allreduce(ops.cgs_pass(2, V, k, w, h2))
+    return (h1 + h2).cpu().numpy(), float(nn.sqrt().item())
+
 
 # ---------------------------------------------------------------------------- sharded algorithms
 def sharded_arnoldi(ops, halo: Halo, q_global: int, ifc_lo: int, m: int, rank: int, seed: int = 0):
@@ -352,7 +384,7 @@ def sharded_arnoldi(ops, halo: Halo, q_global: int, ifc_lo: int, m: int, rank: i
     if rank == 0:
         return ops.zeros(q * 0).reshape(q, 0), np.zeros((0, 0)), 0
     v0 = _start_vector(q_global, seed)[ifc_lo:ifc_lo + q]  # the rank's rows of the global draw
-    V = t.zeros((rank + 1, q), dtype=t.float64, device=ops.device)  # rows = basis vectors
+    V = ops.basis(rank + 1, q)  # rows = basis vectors
     V[0] = t.as_tensor(np.ascontiguousarray(v0), device=ops.device)
     Hbar = np.zeros((rank + 1, rank))
     r = rank
@@ -365,15 +397,9 @@ def sharded_arnoldi(ops, halo: Halo, q_global: int, ifc_lo: int, m: int, rank: i
         return src[:q]
 
     for j in range(rank):
-        w = op(V[j].clone())
-        Vj = V[:j + 1]
-        h = halo.allreduce(Vj @ w)
-        w = w - h @ Vj
-        h2 = halo.allreduce(Vj @ w)
-        w = w - h2 @ Vj
-        hh = (h + h2).cpu().numpy()
+        w = op(V[j].clone()).contiguous()
+        hh, nrm = cgs2(ops, halo, V, j + 1, w)
         Hbar[:j + 1, j] = hh
-        nrm = float(halo.dot(w, w).sqrt().item())
         Hbar[j + 1, j] = nrm
         if nrm <= BREAKDOWN_RTOL:
             r = j + 1
@@ -513,7 +539,7 @@ def sharded_gmres(P: ShardedPreconditioner, b, tol=1e-8, maxit=500, restart=0, p
             conv = True
             break
         cyc = maxit - total if restart <= 0 else min(restart, maxit - total)
-        V = t.zeros((cyc + 1, n), dtype=t.float64, device=ops.device)
+        V = ops.basis(cyc + 1, n)
         Z = t.zeros((cyc, n), dtype=t.float64, device=ops.device) if flexible else None
         Hc = np.zeros((cyc + 1, cyc))
         cs, sn, g = np.zeros(cyc), np.zeros(cyc), np.zeros(cyc + 1)
@@ -524,14 +550,8 @@ def sharded_gmres(P: ShardedPreconditioner, b, tol=1e-8, maxit=500, restart=0, p
             zj = M(V[j].contiguous())
             if flexible:
                 Z[j] = zj
-            w = matvec(zj)
-            Vj = V[:j + 1]
-            h = halo.allreduce(Vj @ w)
-            w = w - h @ Vj
-            h2 = halo.allreduce(Vj @ w)
-            w = w - h2 @ Vj
-            h = (h + h2).cpu().numpy()
-            hn = norm(w)
+            w = matvec(zj).contiguous()
+            h, hn = cgs2(ops, halo, V, j + 1, w)
             if not (np.all(np.isfinite(h)) and np.isfinite(hn)):
                 raise ArithmeticError("GMRES diverged: non-finite values in the recurrence")
             Hc[:j + 1, j] = h

@@ -112,6 +112,16 @@ class OracleShardOps:
         e = self._es(v_ext)
         return self._ext(O.block_solve(self.c0, e) if do_c0 else e)
 
+    def basis(self, rows, n):
+        return self.zeros(rows * n).reshape(rows, n)
+
+    def cgs_pass(self, mode, V, k, w, h0=None):
+        """The CGS2 passes in plain torch (the device backend runs pslr_cgs_pass)."""
+        Vk = V[:k]
+        if mode != 0:
+            w -= h0 @ Vk
+        return (w @ w).reshape(1) if mode == 2 else Vk @ w
+
     def spmv_A(self, x_ext):
         return self._t(self.plan.local.matrix @ x_ext.numpy())
 
