@@ -453,6 +453,7 @@ int pslr_ctx_create(pslr_ctx** out, int device, const pslr_system* sys) {
   int smem_optin = 0;
   cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
   if (smem_optin <= 0) smem_optin = 232448;
+  smem_optin = (int)std::min<int64_t>(smem_optin, env_int("PSLR_SMEM_CAP", smem_optin));
   pslr_ctx_info_t& I = ctx->info;
 
   // ---- level analysis of the four factors, then the ring size W and the stage plan

@@ -75,8 +75,12 @@ struct TriHost {
 
 int analyze_factor(const pslr_csr& M, const std::vector<int64_t>& off, bool upper, TriAnalysis& A,
                    const char* name);
-// threads per CTA of the fused step kernel = max rows per packed segment
-constexpr int kStepThreads = 480;
+// consumer threads per CTA of the fused step kernel = max rows per packed segment
+// (PSLR_STEP_THREADS: timing-experiment builds under lib_variants/ only)
+#ifndef PSLR_STEP_THREADS
+#define PSLR_STEP_THREADS 480
+#endif
+constexpr int kStepThreads = PSLR_STEP_THREADS;
 
 int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAnalysis& A, int64_t W,
                 int64_t stage_bytes, int64_t seg_rows, const std::vector<int32_t>& far_index,

@@ -642,8 +642,11 @@ __device__ __forceinline__ void iface_terms4(int kind, const int (&row)[4], cons
   }
 }
 
+#ifndef PSLR_STEP_MINB
+#define PSLR_STEP_MINB 1
+#endif
 template <int NV>
-__global__ void __launch_bounds__(kBlockThreads, 1)
+__global__ void __launch_bounds__(kBlockThreads, PSLR_STEP_MINB)
 subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant__ StepConst K) {
   extern __shared__ __align__(128) uint8_t smem[];
   const int b = blockIdx.x;
