@@ -237,9 +237,10 @@ def test_gmres_original_space_driver():
 
 
 # ---------------------------------------------------------------- BASELINE-size parity
-@pytest.mark.parametrize("cfg", ["cfg2", "cfg3", "cfg5"])
+@pytest.mark.parametrize("cfg", ["cfg2", "cfg3", "cfg4", "cfg5"])
 def test_full_size_apply_matches_oracle(cfg):
     """BASELINE sizes — cfg2 (64^3, s=16, m=3, r=32), cfg3 (128^3 upwind, s=64, m=5, r=64),
+    cfg4 (2048^2 2D, s=128, m=5, r=128: up to 1421 + 2130 dependent levels per B solve),
     cfg5 (the bench workload: 128^3, s=32, m=3, r=64): device apply vs the oracle's on
     identical factors and correction state; solves bit-exact, apply <= 1e-10."""
     import paper_2002_00917_b200 as pg
