@@ -601,6 +601,9 @@ void pslr_ctx_destroy(pslr_ctx* ctx) {
   cudaSetDevice(ctx->device);
   for (void* p : ctx->allocations) cudaFree(p);
   for (cudaEvent_t ev : ctx->prof_events) cudaEventDestroy(ev);
+  if (ctx->hpin) cudaFreeHost(ctx->hpin);
+  for (cudaEvent_t ev : ctx->kev)
+    if (ev) cudaEventDestroy(ev);
   delete ctx;
 }
 
@@ -963,6 +966,9 @@ int pslr_ctx_clone(const pslr_ctx* src, pslr_ctx** out) {
   ctx->K.trace_cap = 0;
   ctx->kv = ctx->kz = ctx->h_dev = nullptr;
   ctx->kv_len = ctx->kz_len = ctx->h_len = 0;
+  ctx->hpin = nullptr;  // host staging and events are per context
+  ctx->hpin_len = 0;
+  ctx->kev[0] = ctx->kev[1] = nullptr;
   ctx->nv2_ready = false;  // its own two-vector scratch, on first use
   auto bail = [&](int rc) {
     pslr_ctx_destroy(ctx);

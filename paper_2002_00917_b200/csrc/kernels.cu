@@ -450,6 +450,9 @@ cg_update_kernel(double* __restrict__ x, double* __restrict__ r, const double* _
   }
 }
 
+// out = sqrt(in) (the GMRES hnext = ||w||, krylov.py:80, kept on the device for w / hnext)
+__global__ void sqrt_kernel(const double* __restrict__ in, double* __restrict__ out) { *out = sqrt(*in); }
+
 // p = z + beta p (krylov.py:163)
 __global__ void xpby_kernel(const double* __restrict__ z, double beta, double* __restrict__ p, int64_t n) {
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
@@ -638,6 +641,11 @@ int launch_cg_update(pslr_ctx* ctx, double* x, double* r, const double* p, const
                      int64_t n, double* out, cudaStream_t st) {
   const int g = dot_grid(n, ctx->sm_count);
   cg_update_kernel<<<g, 256, 0, st>>>(x, r, p, Ap, alpha, n, ctx->red, out, ctx->counter);
+  return (int)cudaGetLastError();
+}
+
+int launch_sqrt(const double* in, double* out, cudaStream_t st) {
+  sqrt_kernel<<<1, 1, 0, st>>>(in, out);
   return (int)cudaGetLastError();
 }
 

@@ -158,21 +158,60 @@ int pslr_gmres(pslr_ctx* ctx, int64_t m, const double* b, double* x, double tol,
     auto Hat = [&](int64_t i, int64_t j) -> double& { return Hc[i * cycle + j]; };
     std::vector<double> cs(cycle, 0.0), sn(cycle, 0.0), g(cycle + 1, 0.0), h(cycle + 1);
     g[0] = beta;
-    RET(ensure(ctx, &ctx->h_dev, &ctx->h_len, 2 * (cycle + 1) + 8));
+    // Iteration j's device work (apply, A-SpMV, the three CGS2 passes, hnext = ||w||,
+    // v_{j+1} = w / hnext) and the copy of its coefficients to pinned host memory are
+    // enqueued one iteration AHEAD of the host's scalar recurrence: while the host waits
+    // for iteration j's coefficients the device already runs iteration j+1, so the
+    // host round trip leaves the critical path.  A speculative iteration past a stop is
+    // discarded (it only writes scratch and basis columns the cycle end does not read).
+    const int64_t SL = 2 * (cycle + 1) + 8;  // one coefficient slot: h1 | h2 | nn | hnext
+    RET(ensure(ctx, &ctx->h_dev, &ctx->h_len, 2 * SL));
+    // reduction partials for the widest pass of the cycle (sized once: no reallocation
+    // while iterations are in flight)
+    RET(ensure(ctx, &ctx->red, &ctx->red_len, (int64_t)dot_grid(n, ctx->sm_count) * (cycle + 2) + 8));
+    if (ctx->hpin_len < 2 * SL) {
+      if (ctx->hpin) cudaFreeHost(ctx->hpin);
+      ctx->hpin = nullptr;
+      ctx->hpin_len = 0;
+      CK(cudaMallocHost(&ctx->hpin, 2 * SL * sizeof(double)));
+      ctx->hpin_len = 2 * SL;
+    }
+    for (auto& ev : ctx->kev)
+      if (!ev) CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
     CK(cudaMemcpyAsync(ctx->h_dev, &beta, sizeof(double), cudaMemcpyHostToDevice, st));
     CKL(launch_div_scalar(r, ctx->h_dev, Vb, n, st));
+    auto enqueue = [&](int64_t jj) -> int {
+      const int k = (int)(jj + 1);
+      double* mv = flexible ? ctx->kz + jj * n : t;  // w = A M v_j   krylov.py:74
+      RET(apply_M(Vb + jj * ld, mv));
+      CKL(launch_spmv(ctx->A, mv, w, st));
+      double* hs = ctx->h_dev + (jj & 1) * SL;
+      CKL(launch_multidot(ctx, Vb, ld, k, w, n, hs, st));           // h1 = V^T w
+      CKL(launch_sub_dot(ctx, Vb, ld, k, hs, w, n, hs + k, st));      // w -= V h1 ; h2 = V^T w
+      CKL(launch_sub_norm(ctx, Vb, ld, k, hs + k, w, n, hs + 2 * k, st));  // w -= V h2 ; ||w||^2
+      CKL(launch_sqrt(hs + 2 * k, hs + 2 * k + 1, st));
+      CK(cudaMemcpyAsync(ctx->hpin + (jj & 1) * SL, hs, (2 * k + 2) * sizeof(double),
+                         cudaMemcpyDeviceToHost, st));
+      CK(cudaEventRecord(ctx->kev[jj & 1], st));
+      if (jj + 1 < cycle) CKL(launch_div_scalar(w, hs + 2 * k + 1, Vb + (jj + 1) * ld, n, st));
+      return PSLR_OK;
+    };
     int64_t j = 0;
     bool breakdown = false;
+    RET(enqueue(0));
     while (j < cycle) {
-      // w = A M v_j                                          krylov.py:74
-      double* mv = flexible ? ctx->kz + j * n : t;
-      RET(apply_M(Vb + j * ld, mv));
-      CKL(launch_spmv(ctx->A, mv, w, st));
-      double hnext = 0.0;
-      RET(cgs2(ctx, Vb, ld, n, (int)(j + 1), w, h.data(), &hnext, st));
+      if (j + 1 < cycle) RET(enqueue(j + 1));
+      CK(cudaEventSynchronize(ctx->kev[j & 1]));
+      const double* hp = ctx->hpin + (j & 1) * SL;
+      const int64_t k = j + 1;
+      for (int64_t i = 0; i < k; ++i) h[i] = hp[i] + hp[k + i];  // h = h1 + h2
+      const double hnext = hp[2 * k + 1];
       bool finite = std::isfinite(hnext);
       for (int64_t i = 0; i <= j; ++i) finite = finite && std::isfinite(h[i]);
-      if (!finite) return fail(PSLR_ENONFINITE, "GMRES diverged: non-finite values in the recurrence");
+      if (!finite) {
+        CK(cudaStreamSynchronize(st));
+        return fail(PSLR_ENONFINITE, "GMRES diverged: non-finite values in the recurrence");
+      }
       for (int64_t i = 0; i <= j; ++i) Hat(i, j) = h[i];
       Hat(j + 1, j) = hnext;
       for (int64_t i = 0; i < j; ++i) {  // krylov.py:86-97
@@ -200,10 +239,6 @@ int pslr_gmres(pslr_ctx* ctx, int64_t m, const double* b, double* x, double tol,
         break;
       }
       if (est <= tol) break;
-      if (j < cycle) {
-        CK(cudaMemcpyAsync(ctx->h_dev, &hnext, sizeof(double), cudaMemcpyHostToDevice, st));
-        CKL(launch_div_scalar(w, ctx->h_dev, Vb + j * ld, n, st));
-      }
     }
     if (j > 0) {  // krylov.py:110-114
       std::vector<double> y(j, 0.0);

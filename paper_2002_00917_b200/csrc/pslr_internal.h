@@ -186,6 +186,9 @@ struct pslr_ctx {
   double* kr = nullptr;          // n
   double* io_b = nullptr;        // n device staging for host apply
   double* io_z = nullptr;        // n
+  double* hpin = nullptr;        // pinned host: the GMRES coefficients of two iterations
+  int64_t hpin_len = 0;
+  cudaEvent_t kev[2] = {nullptr, nullptr};  // their device-to-host copies landed
   std::vector<void*> allocations;
   bool prof_on = false;
   std::vector<cudaEvent_t> prof_events;

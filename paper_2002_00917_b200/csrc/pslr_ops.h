@@ -53,6 +53,7 @@ int launch_gemv(const double* X, int64_t ld, int k, const double* h, double* y, 
 int launch_cg_update(pslr_ctx* ctx, double* x, double* r, const double* p, const double* Ap, double alpha,
                      int64_t n, double* out, cudaStream_t st);
 int launch_xpby(const double* z, double beta, double* p, int64_t n, cudaStream_t st);
+int launch_sqrt(const double* in, double* out, cudaStream_t st);
 int launch_sub(const double* a, const double* b, double* y, int64_t n, cudaStream_t st);
 int launch_add_inplace(double* y, const double* a, int64_t n, cudaStream_t st);
 int launch_div_scalar(const double* x, const double* s, double* y, int64_t n, cudaStream_t st);
