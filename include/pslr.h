@@ -188,6 +188,22 @@ int pslr_apply2_last(pslr_ctx* ctx, const double* b, const double* y, double* z,
  * (schur.py:83-86, 104-112); do_c0 selects the C0 solve. */
 int pslr_apply_es_step(pslr_ctx* ctx, const double* v, double* out, int do_c0, void* stream);
 
+/* ---------------------------------------------------------------- multi-GPU (NCCL) */
+/* One process per GPU; each rank holds a rank-local context (pslr_ctx_create on its
+ * subdomains' rows; C, Cg and A carry nghost ghost interface columns).  With a
+ * communicator and a halo plan, pslr_apply / pslr_apply_Err / pslr_arnoldi / pslr_gmres /
+ * pslr_cg on that context run the coupled problem: m halo exchanges + 1 allreduce(r) per
+ * apply, a halo per A-SpMV, an allreduce per CGS2 pass.  NCCL is loaded
+ * at run time (libnccl.so.2).
+ * pslr_comm_unique_id: rank 0 creates the 128-byte ncclUniqueId; the caller broadcasts it.
+ * pslr_ctx_set_halo: per peer rank (world entries), the number of local interface values
+ * sent (send_idx: their local interface indices, peers in ascending rank) and of ghosts
+ * received (stored after the q local interface rows, peers in ascending rank). */
+int pslr_comm_unique_id(void* out_128_bytes);
+int pslr_comm_init(pslr_ctx* ctx, const void* nccl_unique_id, int nranks, int rank);
+int pslr_ctx_set_halo(pslr_ctx* ctx, int world, const int64_t* send_counts, const int32_t* send_idx,
+                      const int64_t* recv_counts);
+
 /* ---------------------------------------------------------------- Krylov (device) */
 /* lowrank.py:39-73 on op = E_rr(m) (schur.py:104-112), preconditioner.py:133-136.
  * v0: host start vector (q doubles, NOT normalised — the seeded draw); V_dev: q x rank

@@ -107,6 +107,9 @@ EXPORTS = {
     "pslr_gmres": (c_int, P, c_i64, P, P, c_dbl, c_i64, c_i64, c_int, c_int,
                    ctypes.POINTER(c_i64), ctypes.POINTER(c_int), ctypes.POINTER(c_dbl), P,
                    ctypes.POINTER(c_i64), P),
+    "pslr_comm_unique_id": (c_int, P),
+    "pslr_comm_init": (c_int, P, P, c_int, c_int),
+    "pslr_ctx_set_halo": (c_int, P, c_int, P, P, P),
     "pslr_cgs_pass": (c_int, P, c_int, P, c_i64, c_i64, c_i64, P, P, P, P),
     "pslr_cg": (c_int, P, c_i64, P, P, c_dbl, c_i64, c_int, ctypes.POINTER(c_i64), ctypes.POINTER(c_int),
                 ctypes.POINTER(c_dbl), P, ctypes.POINTER(c_i64), P),

@@ -215,6 +215,7 @@ int op_horner(pslr_ctx* ctx, int64_t m, const double* c, double* out, cudaStream
 }
 
 int op_apply(pslr_ctx* ctx, int64_t m, const double* b, double* z, cudaStream_t st) {
+  if (ctx->comm) return op_apply_sharded(ctx, m, b, z, st);
   const int64_t p = ctx->p, q = ctx->q;
   if (q == 0) return op_solve_B(ctx, b, z, st);
   // (0) f in L-position order, shared by the first and the last step
@@ -388,6 +389,7 @@ int op_apply2(pslr_ctx* ctx, int64_t m, const double* b, double* z, cudaStream_t
 }
 
 int op_apply_err(pslr_ctx* ctx, int64_t m, const double* v, double* out, cudaStream_t st) {
+  if (ctx->comm) return op_apply_err_sharded(ctx, m, v, out, st);
   if (ctx->q == 0) return PSLR_OK;
   double* buf[2] = {ctx->y1, ctx->y2};
   RET(op_solve_C0(ctx, v, buf[0], st));
@@ -599,6 +601,7 @@ int pslr_ctx_create(pslr_ctx** out, int device, const pslr_system* sys) {
 void pslr_ctx_destroy(pslr_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
+  comm_destroy(ctx);
   for (void* p : ctx->allocations) cudaFree(p);
   for (cudaEvent_t ev : ctx->prof_events) cudaEventDestroy(ev);
   if (ctx->hpin) cudaFreeHost(ctx->hpin);
@@ -691,7 +694,7 @@ int pslr_apply_neumann(pslr_ctx* ctx, int64_t m, const double* v, double* out, v
 }
 
 int pslr_apply_Err(pslr_ctx* ctx, int64_t m, const double* v, double* out, void* stream) {
-  RET(unsharded(ctx));
+  if (!ctx->comm) RET(unsharded(ctx));
   if (m < 0) return fail(PSLR_EDIM, "series degree m must be >= 0");
   RET(set_device(ctx));
   return op_apply_err(ctx, m, v, out, S(stream));
@@ -710,7 +713,7 @@ int pslr_apply_correction(pslr_ctx* ctx, const double* y, double* out, void* str
 }
 
 int pslr_apply(pslr_ctx* ctx, int64_t m, const double* b, double* z, void* stream) {
-  RET(unsharded(ctx));
+  if (!ctx->comm) RET(unsharded(ctx));  // with a communicator: the sharded apply (comm.cu)
   if (m < 0) return fail(PSLR_EDIM, "series degree m must be >= 0");
   RET(set_device(ctx));
   return op_apply(ctx, m, b, z, S(stream));
@@ -966,6 +969,14 @@ int pslr_ctx_clone(const pslr_ctx* src, pslr_ctx** out) {
   ctx->K.trace_cap = 0;
   ctx->kv = ctx->kz = ctx->h_dev = nullptr;
   ctx->kv_len = ctx->kz_len = ctx->h_len = 0;
+  ctx->comm = nullptr;  // a clone has no communicator of its own
+  ctx->world = 1;
+  ctx->rank = 0;
+  ctx->halo_idx = nullptr;
+  ctx->halo_buf = nullptr;
+  ctx->halo_nsend = 0;
+  ctx->sh_a = ctx->sh_b = ctx->sh_c = ctx->sh_s = ctx->sh_x = nullptr;
+  ctx->sh_a_len = ctx->sh_b_len = ctx->sh_c_len = ctx->sh_s_len = ctx->sh_x_len = 0;
   ctx->hpin = nullptr;  // host staging and events are per context
   ctx->hpin_len = 0;
   ctx->kev[0] = ctx->kev[1] = nullptr;

@@ -28,6 +28,7 @@ static int dnorm(pslr_ctx* ctx, const double* x, int64_t n, double* out_host, cu
   RET(ensure(ctx, &ctx->red, &ctx->red_len, (int64_t)dot_grid(n, ctx->sm_count) * 1 + 8));
   RET(ensure(ctx, &ctx->h_dev, &ctx->h_len, 8));
   CKL(launch_multidot(ctx, x, n, 1, x, n, ctx->h_dev, st));
+  RET(comm_allreduce(ctx, ctx->h_dev, 1, st));
   double d = 0.0;
   CK(cudaMemcpyAsync(&d, ctx->h_dev, sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -47,8 +48,11 @@ static int cgs2(pslr_ctx* ctx, const double* X, int64_t ld, int64_t n, int k, do
   double* h2 = ctx->h_dev + k;
   double* nn = ctx->h_dev + 2 * k;
   CKL(launch_multidot(ctx, X, ld, k, w, n, h1, st));      // h1 = X^T w
+  RET(comm_allreduce(ctx, h1, k, st));                    // (sharded: over the ranks' rows)
   CKL(launch_sub_dot(ctx, X, ld, k, h1, w, n, h2, st));   // w -= X h1 ; h2 = X^T w
+  RET(comm_allreduce(ctx, h2, k, st));
   CKL(launch_sub_norm(ctx, X, ld, k, h2, w, n, nn, st));  // w -= X h2 ; nn = w.w
+  RET(comm_allreduce(ctx, nn, 1, st));
   std::vector<double> tmp(2 * k + 1);
   CK(cudaMemcpyAsync(tmp.data(), ctx->h_dev, (2 * k + 1) * sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
@@ -66,7 +70,8 @@ extern "C" {
 int pslr_arnoldi(pslr_ctx* ctx, int64_t m, int64_t rank, const double* v0, double* V_dev, double* H,
                  int64_t* r_out, void* stream) {
   RET(set_device(ctx));
-  if (ctx->nghost) return fail(PSLR_EINVAL, "sharded context: run the Krylov loop in shard.py");
+  if (ctx->nghost && !ctx->comm)
+    return fail(PSLR_EINVAL, "sharded context: pslr_comm_init + pslr_ctx_set_halo first (or shard.py)");
   cudaStream_t st = S(stream);
   const int64_t q = ctx->q;
   if (rank < 0) return fail(PSLR_EDIM, "rank must be >= 0");
@@ -107,7 +112,8 @@ int pslr_gmres(pslr_ctx* ctx, int64_t m, const double* b, double* x, double tol,
                int64_t restart, int precond, int flexible, int64_t* iterations, int* converged,
                double* final_relres, double* history, int64_t* history_len, void* stream) {
   RET(set_device(ctx));
-  if (ctx->nghost) return fail(PSLR_EINVAL, "sharded context: run the Krylov loop in shard.py");
+  if (ctx->nghost && !ctx->comm)
+    return fail(PSLR_EINVAL, "sharded context: pslr_comm_init + pslr_ctx_set_halo first (or shard.py)");
   cudaStream_t st = S(stream);
   const int64_t n = ctx->n;
   std::vector<double> hist;
@@ -140,7 +146,7 @@ int pslr_gmres(pslr_ctx* ctx, int64_t m, const double* b, double* x, double tol,
   };
   while (total < maxit && !conv) {
     // r = b - A x                                            krylov.py:56
-    CKL(launch_spmv(ctx->A, x, t, st));
+    RET(op_spmv_A_sharded(ctx, x, t, st));
     CKL(launch_sub(b, t, r, n, st));
     double beta = 0.0;
     RET(dnorm(ctx, r, n, &beta, st));
@@ -184,11 +190,14 @@ int pslr_gmres(pslr_ctx* ctx, int64_t m, const double* b, double* x, double tol,
       const int k = (int)(jj + 1);
       double* mv = flexible ? ctx->kz + jj * n : t;  // w = A M v_j   krylov.py:74
       RET(apply_M(Vb + jj * ld, mv));
-      CKL(launch_spmv(ctx->A, mv, w, st));
+      RET(op_spmv_A_sharded(ctx, mv, w, st));
       double* hs = ctx->h_dev + (jj & 1) * SL;
       CKL(launch_multidot(ctx, Vb, ld, k, w, n, hs, st));           // h1 = V^T w
+      RET(comm_allreduce(ctx, hs, k, st));                           // (sharded: all ranks' rows)
       CKL(launch_sub_dot(ctx, Vb, ld, k, hs, w, n, hs + k, st));      // w -= V h1 ; h2 = V^T w
+      RET(comm_allreduce(ctx, hs + k, k, st));
       CKL(launch_sub_norm(ctx, Vb, ld, k, hs + k, w, n, hs + 2 * k, st));  // w -= V h2 ; ||w||^2
+      RET(comm_allreduce(ctx, hs + 2 * k, 1, st));
       CKL(launch_sqrt(hs + 2 * k, hs + 2 * k + 1, st));
       CK(cudaMemcpyAsync(ctx->hpin + (jj & 1) * SL, hs, (2 * k + 2) * sizeof(double),
                          cudaMemcpyDeviceToHost, st));
@@ -257,7 +266,7 @@ int pslr_gmres(pslr_ctx* ctx, int64_t m, const double* b, double* x, double tol,
         CKL(launch_add_inplace(x, t, n, st));
       }
     }
-    CKL(launch_spmv(ctx->A, x, t, st));
+    RET(op_spmv_A_sharded(ctx, x, t, st));
     CKL(launch_sub(b, t, r, n, st));
     double rn = 0.0;
     RET(dnorm(ctx, r, n, &rn, st));
@@ -298,7 +307,8 @@ int pslr_cg(pslr_ctx* ctx, int64_t m, const double* b, double* x, double tol, in
             int64_t* iterations, int* converged, double* final_relres, double* history,
             int64_t* history_len, void* stream) {
   RET(set_device(ctx));
-  if (ctx->nghost) return fail(PSLR_EINVAL, "sharded context: run the Krylov loop in shard.py");
+  if (ctx->nghost && !ctx->comm)
+    return fail(PSLR_EINVAL, "sharded context: pslr_comm_init + pslr_ctx_set_halo first (or shard.py)");
   if (maxit < 0) return fail(PSLR_EDIM, "maxit must be >= 0");
   cudaStream_t st = S(stream);
   const int64_t n = ctx->n;
@@ -334,6 +344,7 @@ int pslr_cg(pslr_ctx* ctx, int64_t m, const double* b, double* x, double tol, in
   };
   auto dot = [&](const double* u, const double* v, double* out) -> int {
     CKL(launch_multidot(ctx, u, n, 1, v, n, ctx->h_dev, st));
+    RET(comm_allreduce(ctx, ctx->h_dev, 1, st));
     CK(cudaMemcpyAsync(out, ctx->h_dev, sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
     return PSLR_OK;
@@ -348,7 +359,7 @@ int pslr_cg(pslr_ctx* ctx, int64_t m, const double* b, double* x, double tol, in
   double relres = 1.0;
   int64_t it = 0;
   for (it = 1; it <= maxit; ++it) {
-    CKL(launch_spmv(ctx->A, p, Ap, st));  // krylov.py:152
+    RET(op_spmv_A_sharded(ctx, p, Ap, st));  // krylov.py:152
     double pAp = 0.0;
     RET(dot(p, Ap, &pAp));
     if (pAp <= 0.0) {  // krylov.py:153-154
@@ -357,6 +368,7 @@ int pslr_cg(pslr_ctx* ctx, int64_t m, const double* b, double* x, double tol, in
     }
     const double alpha = rz / pAp;
     CKL(launch_cg_update(ctx, x, r, p, Ap, alpha, n, ctx->h_dev, st));  // x, r, r.r
+    RET(comm_allreduce(ctx, ctx->h_dev, 1, st));
     double rr = 0.0;
     CK(cudaMemcpyAsync(&rr, ctx->h_dev, sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));

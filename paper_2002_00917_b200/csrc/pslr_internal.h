@@ -186,6 +186,15 @@ struct pslr_ctx {
   double* kr = nullptr;          // n
   double* io_b = nullptr;        // n device staging for host apply
   double* io_z = nullptr;        // n
+  // multi-GPU (comm.cu): NCCL communicator and halo plan of a rank-local context
+  void* comm = nullptr;          // ncclComm_t
+  int world = 1, rank = 0;
+  std::vector<int64_t> halo_send_cnt, halo_send_off, halo_recv_cnt, halo_recv_off;  // per peer rank
+  int32_t* halo_idx = nullptr;   // local interface indices to send, peers in rank order
+  double* halo_buf = nullptr;    // their gathered values
+  int64_t halo_nsend = 0;
+  double *sh_a = nullptr, *sh_b = nullptr, *sh_c = nullptr, *sh_s = nullptr, *sh_x = nullptr;
+  int64_t sh_a_len = 0, sh_b_len = 0, sh_c_len = 0, sh_s_len = 0, sh_x_len = 0;
   double* hpin = nullptr;        // pinned host: the GMRES coefficients of two iterations
   int64_t hpin_len = 0;
   cudaEvent_t kev[2] = {nullptr, nullptr};  // their device-to-host copies landed

@@ -73,6 +73,14 @@ int launch_permute2(const pslr_ctx* ctx, const double* b, cudaStream_t st);
 int launch_deinterleave2(const pslr_ctx* ctx, const double* y2, double* z, cudaStream_t st);
 int launch_vt_local_strided(pslr_ctx* ctx, const double* y, int64_t ys, double* s, cudaStream_t st);
 
+// comm.cu (multi-GPU contexts; no-ops without a communicator)
+int comm_allreduce(pslr_ctx* ctx, double* x, int64_t n, cudaStream_t st);
+int comm_halo(pslr_ctx* ctx, double* v_ext, cudaStream_t st);
+int comm_destroy(pslr_ctx* ctx);
+int op_apply_sharded(pslr_ctx* ctx, int64_t m, const double* b, double* z, cudaStream_t st);
+int op_apply_err_sharded(pslr_ctx* ctx, int64_t m, const double* v, double* out, cudaStream_t st);
+int op_spmv_A_sharded(pslr_ctx* ctx, const double* x, double* w, cudaStream_t st);
+
 // capi.cu
 int alloc_scratch(pslr_ctx* ctx, double** p, int64_t count);
 void free_ptr(pslr_ctx* ctx, void* p);

@@ -353,6 +353,31 @@ class DeviceShardOps:
         return out
 
 
+def nccl_unique_id() -> bytes:
+    """A fresh ncclUniqueId (128 bytes) for pslr_comm_init; rank 0 makes it, the caller
+    broadcasts it (torch.distributed.broadcast_object_list, MPI, a file ...)."""
+    from . import _lib
+    buf = ctypes.create_string_buffer(128)
+    _lib.check(_lib.fns["pslr_comm_unique_id"](buf))
+    return buf.raw
+
+
+def attach_nccl(ops: "DeviceShardOps", plan: "ShardPlan", unique_id: bytes) -> None:
+    """Give the rank-local context its own NCCL communicator and this rank's halo plan:
+    pslr_apply / pslr_apply_Err / pslr_arnoldi / pslr_gmres / pslr_cg on ops.dev.handle then
+    run the coupled problem inside libpslr (include/pslr.h pslr_comm_init /
+    pslr_ctx_set_halo) — the C-ABI route a non-Python caller uses."""
+    from . import _lib
+    uid = ctypes.create_string_buffer(bytes(unique_id), 128)
+    _lib.check(_lib.fns["pslr_comm_init"](ops.dev.handle, uid, int(plan.world), int(plan.rank)))
+    send_counts = np.asarray([ix.size for ix in plan.send_idx], dtype=np.int64)
+    send_idx = (np.concatenate(plan.send_idx).astype(np.int32) if send_counts.sum()
+                else np.zeros(1, dtype=np.int32))
+    recv_counts = np.ascontiguousarray(plan.recv_counts, dtype=np.int64)
+    _lib.check(_lib.fns["pslr_ctx_set_halo"](ops.dev.handle, int(plan.world), send_counts.ctypes.data,
+                                             send_idx.ctypes.data, recv_counts.ctypes.data))
+
+
 def _basis(t, rows, n, device):
     """rows x n view of a rows x ld buffer, ld = n rounded up to 32 doubles and made an odd
     multiple of 256 B (krylov.cu basis_ld: the columns of one row tile must not share

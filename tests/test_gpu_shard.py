@@ -191,3 +191,67 @@ def test_split_apply2_matches_split_apply(world):
         zz = SP.apply2(b2[0])
         assert torch.equal(zz[0], SP.apply(b2[0][0].contiguous()))
         assert torch.equal(zz[1], SP.apply(b2[0][1].contiguous()))
+
+
+def test_native_comm_world1_apply_err_arnoldi_gmres_cg():
+    """The C-ABI multi-GPU route (pslr_comm_init + pslr_ctx_set_halo, include/pslr.h) on a
+    one-rank NCCL communicator: pslr_apply / pslr_apply_Err / pslr_arnoldi / pslr_gmres /
+    pslr_cg on the rank-local context run the sharded sequence inside libpslr (allreduces
+    and halos are the world-1 no-ops) and must equal the fused context's results: apply and
+    E_rr bit-exact, Arnoldi V/H to 1e-12, GMRES / CG iterations and histories identical."""
+    import ctypes
+    import torch
+    import paper_2002_00917_b200 as pg
+    from paper_2002_00917_b200 import _lib, shard, workloads
+    from paper_2002_00917_b200.krylov import cg_device, gmres_device
+    A = workloads.laplacian3d(14, 12, 10, 0.3)
+    m, r = 3, 8
+    P = pg.build(A, pg.PslrConfig(num_subdomains=6, series_degree=m, rank=r))
+    ps = P.system
+    plan = shard.plan_shard(ps, 1, 0)
+    ops = shard.DeviceShardOps(plan)
+    shard.attach_nccl(ops, plan, shard.nccl_unique_id())
+    V = torch.as_tensor(np.ascontiguousarray(P.correction.V), device="cuda")
+    ops.set_correction(V, P.correction.G)
+    h, st = ops.dev.handle, ops.dev.stream()
+    b = torch.as_tensor(np.random.default_rng(0).standard_normal(ps.n), device="cuda")
+    z = torch.empty_like(b)
+    _lib.check(_lib.fns["pslr_apply"](h, m, b.data_ptr(), z.data_ptr(), st))
+    assert torch.equal(z, P.apply(b))
+    v = torch.as_tensor(np.random.default_rng(1).standard_normal(ps.q), device="cuda")
+    e = torch.empty_like(v)
+    _lib.check(_lib.fns["pslr_apply_Err"](h, m, v.data_ptr(), e.data_ptr(), st))
+    assert torch.equal(e, pg.apply_Err(P.ctx, m, v))
+    # Arnoldi through the communicator context == the build's device Arnoldi
+    from paper_2002_00917_b200.lowrank import _start_vector
+    v0 = np.ascontiguousarray(_start_vector(ps.q, 0))
+    Vd = torch.empty((ps.q, r), dtype=torch.float64, device="cuda")
+    H = np.zeros((r, r))
+    ro = ctypes.c_int64()
+    _lib.check(_lib.fns["pslr_arnoldi"](h, m, r, v0.ctypes.data, Vd.data_ptr(), H.ctypes.data, ctypes.byref(ro), st))
+    assert ro.value == P.correction.rank
+    assert np.abs(Vd.cpu().numpy() - P.correction.V).max() <= 1e-12
+    assert np.abs(H - P.correction.H).max() <= 1e-12 * np.abs(P.correction.H).max()
+    # GMRES and CG: the Python wrappers on a preconditioner-like view of the rank context
+    bb = torch.as_tensor(ps.matrix @ np.random.default_rng(2).standard_normal(ps.n), device="cuda")
+
+    class View:  # what gmres_device / cg_device read from a preconditioner
+        device, series_degree, correction, system = ops.dev, m, P.correction, ps
+    ops.dev._bound = P.correction  # the correction is already on the rank context
+    for flexible in (False, True):
+        x1, r1 = gmres_device(P, bb, tol=1e-8, maxit=60, restart=20, flexible=flexible)
+        x2, r2 = gmres_device(View, bb, tol=1e-8, maxit=60, restart=20, flexible=flexible)
+        assert r1.iterations == r2.iterations and r1.history == r2.history
+        assert torch.equal(x1, x2)
+    Q = pg.build(workloads.laplacian3d(10, 10, 9, 0.0), pg.PslrConfig(num_subdomains=4, series_degree=3, rank=0))
+    qplan = shard.plan_shard(Q.system, 1, 0)
+    qops = shard.DeviceShardOps(qplan)
+    shard.attach_nccl(qops, qplan, shard.nccl_unique_id())
+
+    class QView:
+        device, series_degree, correction, system = qops.dev, 3, Q.correction, Q.system
+    qops.dev._bound = Q.correction
+    bq = torch.as_tensor(Q.system.matrix @ np.random.default_rng(3).standard_normal(Q.system.n), device="cuda")
+    x1, r1 = cg_device(Q, bq, tol=1e-8)
+    x2, r2 = cg_device(QView, bq, tol=1e-8)
+    assert r1.converged and r1.iterations == r2.iterations and r1.history == r2.history
