@@ -91,7 +91,7 @@ __global__ void halo_gather_kernel(const double* __restrict__ v, const int32_t* 
 bool sharded_comm(const pslr_ctx* ctx) { return ctx->comm != nullptr; }
 
 int comm_allreduce(pslr_ctx* ctx, double* x, int64_t n, cudaStream_t st) {
-  if (!ctx->comm || ctx->world == 1 || n == 0) return PSLR_OK;
+  if (!ctx->comm || n == 0) return PSLR_OK;  // (a one-rank communicator still runs NCCL)
   NCK(nccl().allReduce(x, x, (size_t)n, ncclDouble, ncclSum, static_cast<ncclComm_t>(ctx->comm), st),
       "ncclAllReduce");
   return PSLR_OK;
@@ -99,7 +99,7 @@ int comm_allreduce(pslr_ctx* ctx, double* x, int64_t n, cudaStream_t st) {
 
 // v_ext = [q local interface values | nghost ghosts]: fill the ghosts from their owners
 int comm_halo(pslr_ctx* ctx, double* v_ext, cudaStream_t st) {
-  if (!ctx->comm || ctx->world == 1) return PSLR_OK;
+  if (!ctx->comm) return PSLR_OK;
   const int64_t ns = ctx->halo_nsend;
   if (ns > 0) {
     const int64_t blocks = std::min<int64_t>((ns + 255) / 256, 4 * (int64_t)ctx->sm_count);
@@ -185,7 +185,7 @@ int op_apply_err_sharded(pslr_ctx* ctx, int64_t m, const double* v, double* out,
 // w = A x on the rank's rows: x's interface part refreshed with the owners' ghosts first
 int op_spmv_A_sharded(pslr_ctx* ctx, const double* x, double* w, cudaStream_t st) {
   const int64_t n = ctx->n, p = ctx->p;
-  if (!ctx->comm || ctx->world == 1) {
+  if (!ctx->comm) {
     CKL(launch_spmv(ctx->A, x, w, st));
     return PSLR_OK;
   }
