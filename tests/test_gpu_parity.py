@@ -202,6 +202,50 @@ def test_gmres_full_size_fails_at_maxit_like_reference(cfg, relres):
     assert abs(rep.final_relres - true_rel) <= 1e-6 * true_rel
 
 
+@pytest.mark.parametrize("m,its", [(3, 4), (5, 3)])
+def test_gmres_crit06_n2000_exact_factors(m, its):
+    """Acceptance criterion 06 (test_acceptance.py:136-150; golden pkg/test_output.txt):
+    1 x 8 x 250 Laplacian, s=5, EXACT factors (droptol 0), rank 15, full GMRES tol 1e-8,
+    original space -> 4 iterations at m=3, 3 at m=5."""
+    import paper_2002_00917_b200 as pg
+    from oracle import pslr_oracle as O
+    A = O.laplacian3d(1, 8, 250, 0.0)
+    P = pg.build(A, pg.PslrConfig(num_subdomains=5, series_degree=m, rank=15, droptol=0.0))
+    b = A @ np.random.default_rng(0).standard_normal(A.shape[0])
+    x, rep = pg.gmres(P.matvec_original, P.apply_original, b, tol=1e-8)
+    assert rep.converged and abs(rep.iterations - its) <= 2
+    assert np.linalg.norm(b - A @ x) <= 1e-8 * np.linalg.norm(b)
+
+
+@pytest.mark.parametrize("rank,its", [(0, 136), (30, 145)])
+def test_gmres_crit08_rank_dichotomy_counts(rank, its):
+    """Acceptance criterion 08 (test_acceptance.py:169-183), the reference's known-red test:
+    32^3 shift 0.16, s=35, m=3, seed 0, full GMRES tol 1e-8 — the reference converges in 136
+    iterations at rank 0 (so its own criterion fails) and 145 at rank 30; the device path
+    reproduces both counts (+-2)."""
+    import paper_2002_00917_b200 as pg
+    from oracle import pslr_oracle as O
+    A = O.laplacian3d(32, 32, 32, shift=0.16)
+    P = pg.build(A, pg.PslrConfig(num_subdomains=35, series_degree=3, rank=rank, seed=0))
+    b = A @ np.random.default_rng(0).standard_normal(A.shape[0])
+    x, rep = pg.gmres(P.matvec_original, P.apply_original, b, tol=1e-8, maxit=500)
+    assert rep.converged and abs(rep.iterations - its) <= 2
+
+
+def test_gmres_twin_cfg3_hv1_21_iterations():
+    """SURVEY §4 twin table: upwind 32^3, shift 0.2, hv = 1.0 (the other cell-Peclet
+    reading), s=16, m=5, r=64, GMRES(50) tol 1e-6 -> 21 iterations (reference)."""
+    import paper_2002_00917_b200 as pg
+    from paper_2002_00917_b200 import workloads
+    A = workloads.upwind3d(32, 32, 32, 0.2, 1.0)
+    P = pg.build(A, pg.PslrConfig(num_subdomains=16, series_degree=5, rank=64))
+    b = workloads.seeded_rhs(A, 0)
+    for flexible in (False, True):
+        x, rep = pg.gmres(P.matvec_original, P.apply_original, b, tol=1e-6, maxit=500, restart=50,
+                          flexible=flexible)
+        assert rep.converged and abs(rep.iterations - 21) <= 2
+
+
 @pytest.mark.parametrize("m", [3, 5])
 def test_gmres_crit07(m):
     import paper_2002_00917_b200 as pg
