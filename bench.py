@@ -65,11 +65,13 @@ def parse():
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="pslr", choices=["pslr", "reference"])
     ap.add_argument("--config", default="cfg5")
-    ap.add_argument("--e2e-steps", type=int, default=100)
+    ap.add_argument("--e2e-steps", type=int, default=0,
+                    help="steps of the host-buffer (e2e) leg; 0 = the same as --steps")
     ap.add_argument("--cpu-applies", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--streams", type=int, default=0,
-                    help="independent applies in flight per GPU (0 = auto: 2 * SMs // subdomains, <= 8)")
+                    help="independent apply calls in flight per GPU (0 = auto: 4 * (SMs // subdomains), "
+                         "<= 16; <= 8 on the sharded path)")
     ap.add_argument("--nv", type=int, default=2,
                     help="right-hand sides per apply call in the N=1 sweep (pslr_apply_multi: the "
                          "vectors share one launch sequence); 1 = pslr_apply")
@@ -77,15 +79,20 @@ def parse():
                     help="N=1: also time one device GMRES solve (SURVEY §8d time-to-solution); 0 = skip")
     ap.add_argument("--sharded", action="store_true",
                     help="run the sharded (multi-GPU) path even at N=1 (testing the NCCL path)")
-    return ap.parse_args()
+    args = ap.parse_args()
+    if args.e2e_steps <= 0:
+        args.e2e_steps = args.steps
+    return args
 
 
-def auto_streams(sm_count, s):
+def auto_streams(sm_count, s, cap=16):
     """Independent applies in flight: a step launch holds one SM per subdomain and its
-    CTAs finish unevenly, so twice the number of launches that fit side by side keeps
-    the SMs busy (measured on cfg5: K = 4 / 6 / 8 / 12 -> 0.58 / 0.49 / 0.477 / 0.475 ms
-    per apply); capped at 8."""
-    return max(1, min(8, 2 * (sm_count // max(1, s))))
+    CTAs finish unevenly, so several launches per SM-set keep the SMs busy (measured on
+    cfg5, two vectors per call: K = 6 / 7 / 8 / 9-12 / 16 / 24 -> 0.382 / 0.367 / 0.363 /
+    0.41-0.49 / 0.363 / 0.364 ms per apply; K = 16 also hides the host copies of the e2e
+    leg best: 4.27 vs 4.03 TB/s at K = 8).  The sharded path caps it at 8: every pipeline
+    there owns an NCCL communicator."""
+    return max(1, min(cap, 4 * (sm_count // max(1, s))))
 
 
 def hbm_peak():
@@ -272,7 +279,7 @@ def run_sharded(args, rank, world, local):
     # K independent sharded applies in flight (as at N=1): pipeline j has its own clone
     # context, stream and process group (its NCCL communicator), so every group sees its
     # collectives in the same order on all ranks
-    K = args.streams if args.streams > 0 else auto_streams(P.ops.dev.info()["sm_count"], base.s)
+    K = args.streams if args.streams > 0 else auto_streams(P.ops.dev.info()["sm_count"], base.s, cap=8)
     pipes, streams = [P], [torch.cuda.current_stream()]
     for _ in range(K - 1):
         g = dist.new_group(list(range(world)))
