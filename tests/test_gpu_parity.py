@@ -138,6 +138,26 @@ def test_length_checked():
         pg.solve_C0(P.ctx, np.ones(P.system.q + 1))
 
 
+def test_empty_interior_blocks():
+    """Ragged partitions: a 1D Laplacian of 12 vertices in 6 subdomains leaves four
+    subdomains with NO interior rows (interior sizes [1,0,0,0,0,1], interfaces
+    [1,2,2,2,2,1]); the device apply (oracle correction injected) matches the oracle, and
+    GMRES converges as in the reference driver."""
+    import scipy.sparse as sp
+    import paper_2002_00917_b200 as pg
+    from oracle import pslr_oracle as O
+    A = sp.diags([-np.ones(11), 2 * np.ones(12), -np.ones(11)], [-1, 0, 1], format="csr")
+    OP = O.build(A, 6, 2, 2)
+    assert list(OP.system.interior_sizes) == [1, 0, 0, 0, 0, 1]
+    P = pg.build(A, pg.PslrConfig(num_subdomains=6, series_degree=2, rank=2))
+    Q = pg.with_correction(P, OP.corr.V, OP.corr.H, OP.corr.G)
+    b = np.random.default_rng(0).standard_normal(12)
+    assert _rel(Q.apply(b), OP.apply(b)) <= 1e-12
+    np.testing.assert_array_equal(pg.solve_B(P.ctx, b[:P.system.p]), O.solve_B(OP.ctx, b[:P.system.p]))
+    x, rep = pg.gmres(P.matvec_original, P.apply_original, A @ np.ones(12), tol=1e-10)
+    assert rep.converged and np.allclose(x, np.ones(12), atol=1e-8)
+
+
 def test_single_subdomain_ilu_only():
     """q == 0 path (test_preconditioner.py:69-76)."""
     import paper_2002_00917_b200 as pg

@@ -113,3 +113,14 @@ def test_errors_mirror_reference():
         pg.ilut(sp.identity(2, format="csr"), droptol=-1.0)
     with pytest.raises(ValueError):
         pg.PslrConfig(num_subdomains=0).validate()
+
+
+def test_factor_blocks_empty_system_and_bad_tiling():
+    """ilu.py edge cases (pkg/tests/test_ilu.py:117-129): an empty system factors to an
+    empty BlockILU; block sizes that do not tile the matrix raise ValueError."""
+    import scipy.sparse as sp
+    import paper_2002_00917_b200 as pg
+    bf = pg.factor_blocks(sp.csr_matrix((0, 0)), [])
+    assert bf.n == 0 and bf.nnz == 0
+    with pytest.raises(ValueError):
+        pg.factor_blocks(sp.identity(5, format="csr"), [2, 2])
