@@ -109,12 +109,14 @@ struct StepArgs {
   double* yout = nullptr;      // q output
   double* partials = nullptr;  // [s][r] V^T yout partial sums (nullable)
   int tag = 0;                 // launch kind, for pslr_apply_profiled
+  int xpos = 0;                // set by launch_step: xb in U-position order (F read via Fpos)
 };
 
 // Everything the fused kernel reads besides StepArgs (constant per context).
 struct StepConst {
   DevTri LB, UB, LC, UC;
   DevCsr E, F, C, Cg;
+  DevCsr Fpos;  // F with its columns mapped to the interior rows' U-positions
   const int32_t* int_off = nullptr;
   const int32_t* ifc_off = nullptr;
   const int32_t* erows = nullptr;     // int4 per interior row with E entries, grouped by block:

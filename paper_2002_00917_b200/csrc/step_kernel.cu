@@ -383,7 +383,7 @@ __device__ __forceinline__ double2 div_sd(double2 x, double sd, double rcp) {
 template <bool UPPER, int NV>
 __device__ __forceinline__ void load_row(const uint8_t* seg, const int4 h0, const int4 h1, const double* rbuf,
                                          int rbase, int base, int mask, int zslot,
-                                         const double* __restrict__ cadd, Row<NV>& r) {
+                                         const double* __restrict__ cadd, bool xpos, Row<NV>& r) {
   const int S = h1.x;
   const int G = max(1, (h0.y + 3) >> 2);
   r.flags = h0.z;
@@ -417,7 +417,7 @@ __device__ __forceinline__ void load_row(const uint8_t* seg, const int4 h0, cons
     }
     const int row = inf & 0x3fffffff;
     r.zidx = (inf & 0x40000000) ? gp : -1;  // only far-dependency targets go to global z
-    r.xidx = row;
+    r.xidx = xpos ? gp : row;  // x in U-position order when only this kernel's F reads it
     r.cadd = (cadd && r.active) ? vldg<NV>(cadd, row) : vzero<NV>();
   } else {
     r.zidx = inf;
@@ -474,6 +474,7 @@ __device__ __forceinline__ vt<NV> fold_row(vt<NV> acc, const Row<NV>& r, const d
 struct Cursor {
   int u, u1, st, nst, si, nseg, rbase;
   uint32_t par;
+  bool xpos;  // U rows store x at their position (coalesced) instead of their row
   const uint8_t* seg;
   const double* rbuf;
 };
@@ -538,7 +539,7 @@ __device__ __forceinline__ bool level_step(const StepConst& K, Ctl* ctl, uint8_t
   const int cur_flags = cur.flags;
   const int cur_info = (cur.G << 2) | (cur.nrows << 8);
   // E: the next segment's row, loaded in place (everything it needs before its gathers)
-  if (more) load_row<UPPER, NV>(nseg_ptr, nh0, nh1, c.rbuf, c.rbase, base, mask, zslot, cadd, cur);
+  if (more) load_row<UPPER, NV>(nseg_ptr, nh0, nh1, c.rbuf, c.rbase, base, mask, zslot, cadd, c.xpos, cur);
   c.seg = nseg_ptr;
   if (chunk_done) {  // the staged chunk is no longer read by this warp
     __syncwarp();
@@ -559,7 +560,7 @@ __device__ __forceinline__ bool level_step(const StepConst& K, Ctl* ctl, uint8_t
 template <bool UPPER, int NV>
 __device__ void tri_phase(const StepConst& K, const Streams& S, Ctl* ctl, uint8_t* stages,
                           double* rhsbuf, int k, double* ring, int base, double* z, double* xout,
-                          const double* cadd) {
+                          const double* cadd, bool xpos = false) {
   trace_ev(K, 10 + k, 0);
   trace_cta(K, 2 + k);
   if (threadIdx.x == 0) {
@@ -581,11 +582,12 @@ __device__ void tri_phase(const StepConst& K, const Streams& S, Ctl* ctl, uint8_
   c.nseg = reinterpret_cast<const int32_t*>(c.seg)[6];
   c.rbase = reinterpret_cast<const int32_t*>(c.seg)[7];
   c.si = 0;
+  c.xpos = xpos;
   Row<NV> row;
   {
     const int32_t* h = reinterpret_cast<const int32_t*>(c.seg);
     load_row<UPPER, NV>(c.seg, *reinterpret_cast<const int4*>(c.seg), make_int4(h[4], h[5], h[8], 0), c.rbuf,
-                        c.rbase, base, K.ring_mask, K.ring_mask + 1, cadd, row);
+                        c.rbase, base, K.ring_mask, K.ring_mask + 1, cadd, xpos, row);
   }
   const double* ring_c = ring;
   while (level_step<UPPER, NV>(K, ctl, stages, rhsbuf, c, row, ring_c, ring, base, z, xout, cadd)) {
@@ -633,7 +635,7 @@ __device__ __forceinline__ void iface_terms4(int kind, const int (&row)[4], cons
 #pragma unroll
       for (int j = 0; j < 4; ++j) t[j] = ok[j] ? vldg<NV>(a.g, row[j]) : vzero<NV>();
       break;
-    case IT_FX: spmv4<false, NV>(K.F, row, ok, a.xb, t); break;
+    case IT_FX: spmv4<false, NV>(a.xpos ? K.Fpos : K.F, row, ok, a.xb, t); break;
     case IT_CY: spmv4<true, NV>(K.C, row, ok, a.yC, t); break;
     case IT_CGY: spmv4<true, NV>(K.Cg, row, ok, a.yC, t); break;
     default:
@@ -789,7 +791,7 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
     trace_ev(K, 3, 0);
     trace_cta(K, 1);
     tri_phase<false, NV>(K, S, ctl, stages, rhsbuf, ph_LB, ring, r0, K.zB, nullptr, nullptr);
-    tri_phase<true, NV>(K, S, ctl, stages, rhsbuf, ph_UB, ring, r0, K.zB, a.xb, nullptr);
+    tri_phase<true, NV>(K, S, ctl, stages, rhsbuf, ph_UB, ring, r0, K.zB, a.xb, nullptr, a.xpos != 0);
   }
   if (do_i) {
     const int r0 = K.ifc_off[b], r1 = K.ifc_off[b + 1];
@@ -837,8 +839,13 @@ int configure_step_kernel(int nv, int smem_bytes) {
                                              smem_bytes);
 }
 
-int launch_step(const pslr_ctx* ctx, const StepArgs& a, cudaStream_t st, int nv) {
+int launch_step(const pslr_ctx* ctx, const StepArgs& a_in, cudaStream_t st, int nv) {
   if (ctx->s == 0) return 0;
+  // x_B is read only by this launch's F SpMV: store it in U-position order (coalesced
+  // stores from the level loop) and read it through the position-mapped F.  Launches
+  // whose x_B leaves the kernel (the last step, solve_B) keep row order.
+  StepArgs a = a_in;
+  a.xpos = (a.b1 != BT_NONE && (a.i1 == IT_FX || a.i2 == IT_FX)) ? 1 : 0;
   const StepConst& K = (nv == 2) ? ctx->K2 : ctx->K;
   // programmatic stream serialization: the step kernel's CTAs (one per subdomain, far
   // fewer than the 148 SMs) launch and stage their first factor chunks while the
