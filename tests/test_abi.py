@@ -21,7 +21,9 @@ def test_header_declares_the_hot_path():
     syms = declared_symbols()
     for needed in ("pslr_apply", "pslr_solve_B", "pslr_solve_C0", "pslr_apply_Es",
                    "pslr_apply_neumann", "pslr_apply_Err", "pslr_arnoldi", "pslr_gmres",
-                   "pslr_spmv", "pslr_ilut_blocks", "pslr_partition_bisect"):
+                   "pslr_spmv", "pslr_ilut_blocks", "pslr_partition_bisect", "pslr_cg",
+                   "pslr_cgs_pass", "pslr_comm_init", "pslr_ctx_set_halo", "pslr_ctx_create",
+                   "pslr_ctx_set_correction", "pslr_ctx_destroy", "pslr_last_error"):
         assert needed in syms
 
 
