@@ -524,13 +524,6 @@ int pslr_ctx_create(pslr_ctx** out, int device, const pslr_system* sys) {
 
   if ((rc = upload_csr(ctx, sys->E, &ctx->K.E))) return bail(rc);
   if ((rc = upload_csr(ctx, sys->F, &ctx->K.F))) return bail(rc);
-  {  // F over U-positions: same rows, entry order and values, columns renumbered
-    pslr_csr Fp = sys->F;
-    std::vector<int32_t> pcol(sys->F.indices, sys->F.indices + sys->F.nnz);
-    for (auto& j : pcol) j = aUB.pos_of_row[j];
-    Fp.indices = pcol.data();
-    if ((rc = upload_csr(ctx, Fp, &ctx->K.Fpos))) return bail(rc);
-  }
   if ((rc = upload_csr(ctx, sys->C, &ctx->K.C))) return bail(rc);
   if ((rc = upload_csr(ctx, sys->C0, &ctx->C0))) return bail(rc);
   if ((rc = upload_csr(ctx, sys->Cg, &ctx->K.Cg))) return bail(rc);
@@ -600,6 +593,14 @@ int pslr_ctx_create(pslr_ctx** out, int device, const pslr_system* sys) {
   I.nnz_A = sys->A.nnz;
   I.sm_count = ctx->sm_count;
   I.nghost = nghost;
+  {  // F over U-positions: same rows, entry order and values, columns renumbered (allocated
+     // last: the other arrays keep the placement they were tuned with)
+    pslr_csr Fp = sys->F;
+    std::vector<int32_t> pcol(sys->F.indices, sys->F.indices + sys->F.nnz);
+    for (auto& j : pcol) j = aUB.pos_of_row[j];
+    Fp.indices = pcol.data();
+    if ((rc = upload_csr(ctx, Fp, &ctx->K.Fpos))) return bail(rc);
+  }
   if (cudaDeviceSynchronize() != cudaSuccess) return bail(fail(PSLR_ECUDA, "upload failed"));
   *out = ctx;
   return PSLR_OK;

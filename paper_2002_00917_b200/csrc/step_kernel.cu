@@ -380,10 +380,10 @@ __device__ __forceinline__ double2 div_sd(double2 x, double sd, double rcp) {
   return make_double2(div_sd(x.x, sd, rcp), div_sd(x.y, sd, rcp));
 }
 
-template <bool UPPER, int NV>
+template <bool UPPER, int NV, bool XPOS = false>
 __device__ __forceinline__ void load_row(const uint8_t* seg, const int4 h0, const int4 h1, const double* rbuf,
                                          int rbase, int base, int mask, int zslot,
-                                         const double* __restrict__ cadd, bool xpos, Row<NV>& r) {
+                                         const double* __restrict__ cadd, Row<NV>& r) {
   const int S = h1.x;
   const int G = max(1, (h0.y + 3) >> 2);
   r.flags = h0.z;
@@ -417,7 +417,7 @@ __device__ __forceinline__ void load_row(const uint8_t* seg, const int4 h0, cons
     }
     const int row = inf & 0x3fffffff;
     r.zidx = (inf & 0x40000000) ? gp : -1;  // only far-dependency targets go to global z
-    r.xidx = xpos ? gp : row;  // x in U-position order when only this kernel's F reads it
+    r.xidx = XPOS ? gp : row;  // x in U-position order when only this kernel's F reads it
     r.cadd = (cadd && r.active) ? vldg<NV>(cadd, row) : vzero<NV>();
   } else {
     r.zidx = inf;
@@ -474,12 +474,11 @@ __device__ __forceinline__ vt<NV> fold_row(vt<NV> acc, const Row<NV>& r, const d
 struct Cursor {
   int u, u1, st, nst, si, nseg, rbase;
   uint32_t par;
-  bool xpos;  // U rows store x at their position (coalesced) instead of their row
   const uint8_t* seg;
   const double* rbuf;
 };
 
-template <bool UPPER, int NV>
+template <bool UPPER, int NV, bool XPOS = false>
 __device__ __forceinline__ bool level_step(const StepConst& K, Ctl* ctl, uint8_t* stages, double* rhsbuf,
                                            Cursor& c, Row<NV>& cur, const double* ring_c,
                                            double* ring, int base, double* z, double* xout,
@@ -539,7 +538,7 @@ __device__ __forceinline__ bool level_step(const StepConst& K, Ctl* ctl, uint8_t
   const int cur_flags = cur.flags;
   const int cur_info = (cur.G << 2) | (cur.nrows << 8);
   // E: the next segment's row, loaded in place (everything it needs before its gathers)
-  if (more) load_row<UPPER, NV>(nseg_ptr, nh0, nh1, c.rbuf, c.rbase, base, mask, zslot, cadd, c.xpos, cur);
+  if (more) load_row<UPPER, NV, XPOS>(nseg_ptr, nh0, nh1, c.rbuf, c.rbase, base, mask, zslot, cadd, cur);
   c.seg = nseg_ptr;
   if (chunk_done) {  // the staged chunk is no longer read by this warp
     __syncwarp();
@@ -557,10 +556,10 @@ __device__ __forceinline__ bool level_step(const StepConst& K, Ctl* ctl, uint8_t
 // Consumer side of one triangular phase.  Callers arrive right after a consumer barrier
 // that follows the last write of the phase's rhs array; the phase ends with the barrier
 // of its last level.
-template <bool UPPER, int NV>
+template <bool UPPER, int NV, bool XPOS = false>
 __device__ void tri_phase(const StepConst& K, const Streams& S, Ctl* ctl, uint8_t* stages,
                           double* rhsbuf, int k, double* ring, int base, double* z, double* xout,
-                          const double* cadd, bool xpos = false) {
+                          const double* cadd) {
   trace_ev(K, 10 + k, 0);
   trace_cta(K, 2 + k);
   if (threadIdx.x == 0) {
@@ -582,15 +581,14 @@ __device__ void tri_phase(const StepConst& K, const Streams& S, Ctl* ctl, uint8_
   c.nseg = reinterpret_cast<const int32_t*>(c.seg)[6];
   c.rbase = reinterpret_cast<const int32_t*>(c.seg)[7];
   c.si = 0;
-  c.xpos = xpos;
   Row<NV> row;
   {
     const int32_t* h = reinterpret_cast<const int32_t*>(c.seg);
-    load_row<UPPER, NV>(c.seg, *reinterpret_cast<const int4*>(c.seg), make_int4(h[4], h[5], h[8], 0), c.rbuf,
-                        c.rbase, base, K.ring_mask, K.ring_mask + 1, cadd, xpos, row);
+    load_row<UPPER, NV, XPOS>(c.seg, *reinterpret_cast<const int4*>(c.seg), make_int4(h[4], h[5], h[8], 0), c.rbuf,
+                        c.rbase, base, K.ring_mask, K.ring_mask + 1, cadd, row);
   }
   const double* ring_c = ring;
-  while (level_step<UPPER, NV>(K, ctl, stages, rhsbuf, c, row, ring_c, ring, base, z, xout, cadd)) {
+  while (level_step<UPPER, NV, XPOS>(K, ctl, stages, rhsbuf, c, row, ring_c, ring, base, z, xout, cadd)) {
   }
 }
 
@@ -627,7 +625,7 @@ __device__ __forceinline__ void spmv4(const DevCsr& M, const int (&row)[4], cons
   }
 }
 
-template <int NV>
+template <int NV, bool XPOS>
 __device__ __forceinline__ void iface_terms4(int kind, const int (&row)[4], const bool (&ok)[4],
                                              const StepArgs& a, const StepConst& K, vt<NV> (&t)[4]) {
   switch (kind) {
@@ -635,7 +633,7 @@ __device__ __forceinline__ void iface_terms4(int kind, const int (&row)[4], cons
 #pragma unroll
       for (int j = 0; j < 4; ++j) t[j] = ok[j] ? vldg<NV>(a.g, row[j]) : vzero<NV>();
       break;
-    case IT_FX: spmv4<false, NV>(a.xpos ? K.Fpos : K.F, row, ok, a.xb, t); break;
+    case IT_FX: spmv4<false, NV>(XPOS ? K.Fpos : K.F, row, ok, a.xb, t); break;
     case IT_CY: spmv4<true, NV>(K.C, row, ok, a.yC, t); break;
     case IT_CGY: spmv4<true, NV>(K.Cg, row, ok, a.yC, t); break;
     default:
@@ -647,7 +645,7 @@ __device__ __forceinline__ void iface_terms4(int kind, const int (&row)[4], cons
 #ifndef PSLR_STEP_MINB
 #define PSLR_STEP_MINB 1
 #endif
-template <int NV>
+template <int NV, bool XPOS>
 __global__ void __launch_bounds__(kBlockThreads, PSLR_STEP_MINB)
 subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant__ StepConst K) {
   extern __shared__ __align__(128) uint8_t smem[];
@@ -791,7 +789,7 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
     trace_ev(K, 3, 0);
     trace_cta(K, 1);
     tri_phase<false, NV>(K, S, ctl, stages, rhsbuf, ph_LB, ring, r0, K.zB, nullptr, nullptr);
-    tri_phase<true, NV>(K, S, ctl, stages, rhsbuf, ph_UB, ring, r0, K.zB, a.xb, nullptr, a.xpos != 0);
+    tri_phase<true, NV, XPOS>(K, S, ctl, stages, rhsbuf, ph_UB, ring, r0, K.zB, a.xb, nullptr);
   }
   if (do_i) {
     const int r0 = K.ifc_off[b], r1 = K.ifc_off[b + 1];
@@ -804,9 +802,9 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
         ok[j] = row[j] < r1;
       }
       vt<NV> w[4], t2[4];
-      iface_terms4<NV>(a.i1, row, ok, a, K, w);
+      iface_terms4<NV, XPOS>(a.i1, row, ok, a, K, w);
       if (a.i2 != IT_NONE) {
-        iface_terms4<NV>(a.i2, row, ok, a, K, t2);
+        iface_terms4<NV, XPOS>(a.i2, row, ok, a, K, t2);
 #pragma unroll
         for (int j = 0; j < 4; ++j) w[j] = a.i2_sub ? vsub(w[j], t2[j]) : vadd(w[j], t2[j]);
       }
@@ -833,10 +831,15 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
 }
 
 int configure_step_kernel(int nv, int smem_bytes) {
-  return nv == 2 ? (int)cudaFuncSetAttribute(subdomain_step_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             smem_bytes)
-                 : (int)cudaFuncSetAttribute(subdomain_step_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             smem_bytes);
+  auto set = [&](auto kern) {
+    return (int)cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
+  };
+  if (nv == 2) {
+    const int e = set(subdomain_step_kernel<2, false>);
+    return e ? e : set(subdomain_step_kernel<2, true>);
+  }
+  const int e = set(subdomain_step_kernel<1, false>);
+  return e ? e : set(subdomain_step_kernel<1, true>);
 }
 
 int launch_step(const pslr_ctx* ctx, const StepArgs& a_in, cudaStream_t st, int nv) {
@@ -860,8 +863,11 @@ int launch_step(const pslr_ctx* ctx, const StepArgs& a_in, cudaStream_t st, int 
   attr[0].val.programmaticStreamSerializationAllowed = ctx->pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (nv == 2) return (int)cudaLaunchKernelEx(&cfg, subdomain_step_kernel<2>, a, K);
-  return (int)cudaLaunchKernelEx(&cfg, subdomain_step_kernel<1>, a, K);
+  if (nv == 2)
+    return (int)(a.xpos ? cudaLaunchKernelEx(&cfg, subdomain_step_kernel<2, true>, a, K)
+                        : cudaLaunchKernelEx(&cfg, subdomain_step_kernel<2, false>, a, K));
+  return (int)(a.xpos ? cudaLaunchKernelEx(&cfg, subdomain_step_kernel<1, true>, a, K)
+                      : cudaLaunchKernelEx(&cfg, subdomain_step_kernel<1, false>, a, K));
 }
 
 }  // namespace pslr
