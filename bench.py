@@ -603,8 +603,9 @@ def main():
     e2e_value = world * bytes_apply * args.e2e_steps / (ms_e2e / 1e3) / 1e9
 
     # GMRES time-to-solution: b = A x*, x* seeded; the device solve with the
-    # reference's control flow (krylov.py:35-129); bytes per iteration j of a cycle =
-    # apply + A-SpMV + CGS2 (4 passes over j+1 basis vectors) + 16 n
+    # reference's control flow (krylov.py:35-129); algorithmic bytes per iteration j of a
+    # cycle = apply + A-SpMV + CGS2 (3 passes over j+1 basis vectors: the projections fuse
+    # with the following dot / norm) + 16 n
     solve = None
     if args.gmres_maxit > 0:
         from paper_2002_00917_b200.krylov import gmres_device
@@ -616,7 +617,7 @@ def main():
                                flexible=wl.flexible)
         torch.cuda.synchronize()
         spmv_b = 12 * info["nnz_A"] + 16 * n
-        gb = sum(bytes_apply + spmv_b + 8 * n * ((k % rs) + 1) * 4 + 16 * n for k in range(rep.iterations))
+        gb = sum(bytes_apply + spmv_b + 8 * n * ((k % rs) + 1) * 3 + 16 * n for k in range(rep.iterations))
         solve = {"solver": "FGMRES" if wl.flexible else "GMRES", "restart": rs, "tol": wl.tol,
                  "maxit": args.gmres_maxit, "iterations": rep.iterations, "converged": rep.converged,
                  "final_relres": rep.final_relres, "time_s": rep.time_s,
