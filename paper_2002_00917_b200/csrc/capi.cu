@@ -281,7 +281,7 @@ static int ensure_nv2(pslr_ctx* ctx) {
   if (ctx->nv2_ready) return PSLR_OK;
   const int64_t p = ctx->p, q = ctx->q;
   StepConst K2 = ctx->K;
-  const int64_t W = (int64_t)ctx->K.ring_mask + 1, SB = ctx->K.stage_bytes, CTL = 256;
+  const int64_t W = (int64_t)ctx->K.ring_mask + 1, SB = ctx->K.stage_bytes, CTL = kCtlBytes;
   const int64_t RB2 = ((16 * (kChunkRows + 2)) + 127) / 128 * 128;
   int64_t nst = (ctx->smem_optin - 1024 - CTL - W * 16 - 128) / (SB + RB2);
   nst = std::min<int64_t>(nst, 8);
@@ -474,7 +474,7 @@ int pslr_ctx_create(pslr_ctx** out, int device, const pslr_system* sys) {
   int64_t wmax = env_int("PSLR_RING", 4096);
   int64_t W = 2048;  // >= 2048: the ring doubles as the V^T y reduction scratch
   while (W < reach && W < wmax) W *= 2;
-  const int64_t CTL = 256;  // mbarriers
+  const int64_t CTL = kCtlBytes;  // mbarriers + descriptor queue
   int64_t nst = (smem_optin - 1024 - CTL - W * 8 - 128) / (SB + RB);
   while (nst < 2 && W > 2048) {
     W /= 2;
@@ -491,6 +491,8 @@ int pslr_ctx_create(pslr_ctx** out, int device, const pslr_system* sys) {
   if (configure_step_kernel(1, ctx->K.smem_bytes) != 0)
     return bail(fail(PSLR_ECUDA, "cannot configure the step kernel's shared memory"));
   ctx->pdl = env_int("PSLR_PDL", 1) != 0;
+  ctx->K.dbg = (int)env_int("PSLR_DBG", 0);
+  ctx->K.l2ahead = env_int("PSLR_L2AHEAD", 0);
   if (env_int("PSLR_TRACE", 0)) {  // diagnostics: timeline of CTA 0 (pslr_debug_trace)
     const int64_t cap = 1 << 20;
     void* d = nullptr;

@@ -122,7 +122,7 @@ int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAna
   out.segments = 0;
   std::vector<uint8_t> seg;
   // ELL segment, S = a4(nrows) row slots, G = ceil(w/4) groups of 4 entries per row:
-  //   hdr int32[12] {nrows, w, flags, pos0, S, bytes, nseg, rbase, far_off, 0, 0, 0}
+  //   hdr int32[12] {nrows | w << 16, flags | tb << 8, pos0, bytes, S, far_off, rbase, 0, 0, 0, 0, 0}
   //   info int32[S]     L: U-position ; U: row id, bit 31 set when sd = 1 - 2^-53
   //   U: invd f64[S], and only for flags bit 2 ("explicit sd"): sd f64[S], rcp f64[S]
   //   slot u16[G][S][4] near: ring slot (< W), W = zero slot; far: 0x8000 | far-list index
@@ -172,9 +172,11 @@ int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAna
     }
   }
   // current chunk being filled
-  int64_t chunk_start = 0, chunk_nseg = 0, chunk_pos0 = 0, chunk_rows = 0;
+  int64_t chunk_start = 0, chunk_nseg = 0, chunk_pos0 = 0, chunk_rows = 0, last_seg = 0;
   auto close_chunk = [&]() {
     if (chunk_nseg == 0) return;
+    // the chunk's last segment carries flag bit 3 (the consumers move to the next stage)
+    reinterpret_cast<int32_t*>(out.data.data() + last_seg)[1] |= 8;
     ChunkDesc d;
     d.off16 = (uint32_t)(chunk_start / 16);
     d.bytes = (uint32_t)((int64_t)out.data.size() - chunk_start);
@@ -182,10 +184,8 @@ int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAna
     d.rpos = (int32_t)p0;
     d.rbytes = (uint32_t)(((chunk_pos0 + chunk_rows - p0 + 1) & ~int64_t(1)) * 8);
     chunk_rows = 0;
-    // the kernel reads the segment count from the first segment's header (word 6)
-    reinterpret_cast<int32_t*>(out.data.data() + chunk_start)[6] = (int32_t)chunk_nseg;
-    // ... and the base position of the chunk's rhs slice (word 7, even for 16-B TMA alignment)
-    reinterpret_cast<int32_t*>(out.data.data() + chunk_start)[7] = (int32_t)(chunk_pos0 & ~int64_t(1));
+    // the base position of the chunk's rhs slice: first segment, word 6 (even: 16-B TMA alignment)
+    reinterpret_cast<int32_t*>(out.data.data() + chunk_start)[6] = (int32_t)(chunk_pos0 & ~int64_t(1));
     out.chunks.push_back(d);
     chunk_nseg = 0;
     chunk_start = (int64_t)out.data.size();
@@ -243,14 +243,15 @@ int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAna
         chunk_rows += nrows;
         seg.assign(bytes, 0);
         int32_t* h = reinterpret_cast<int32_t*>(seg.data());
-        h[0] = (int32_t)nrows;
-        h[1] = (int32_t)w;
-        h[2] = ((s1 == lend) ? 1 : 0) | (expl ? 4 : 0) | (int32_t)(tb << 8);  // bit0 level end, bit2 explicit sd
+        if (w > 0xffff) return fail(PSLR_EINVAL, std::string(name) + ": a row is too long for the streaming format");
+        h[0] = (int32_t)(nrows | (w << 16));
+        h[1] = ((s1 == lend) ? 1 : 0) | (expl ? 4 : 0) | (int32_t)(tb << 8);  // bit0 level end, bit2 explicit sd
         const int64_t S = a4(nrows);
         const int64_t G = std::max<int64_t>(1, (w + 3) / 4);
-        h[3] = (int32_t)s0;
+        h[2] = (int32_t)s0;
+        h[3] = (int32_t)bytes;
         h[4] = (int32_t)S;
-        h[5] = (int32_t)bytes;
+        last_seg = (int64_t)out.data.size();
         int32_t* info = h + 12;
         uint8_t* p = reinterpret_cast<uint8_t*>(info + S);
         double* invd = nullptr;
@@ -268,7 +269,7 @@ int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAna
         uint16_t* slot = reinterpret_cast<uint16_t*>(p);
         double* val = reinterpret_cast<double*>(p + 8 * G * S);
         int32_t* far = reinterpret_cast<int32_t*>(p + 40 * G * S);
-        h[8] = (int32_t)(reinterpret_cast<uint8_t*>(far) - seg.data());
+        h[5] = (int32_t)(reinterpret_cast<uint8_t*>(far) - seg.data());
         auto slot_at = [&](int64_t t, int64_t kk) -> uint16_t& { return slot[((kk >> 2) * S + t) * 4 + (kk & 3)]; };
         auto val_at = [&](int64_t t, int64_t kk) -> double& {
           return val[(((kk >> 2) * 2 + ((kk >> 1) & 1)) * S + t) * 2 + (kk & 1)];
@@ -312,7 +313,7 @@ int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAna
               slot_at(t, kk) = (uint16_t)(0x8000 | nf);
               ++nf;
               out.far++;
-              h[2] |= 2;  // the segment has far dependencies (kernel gather variant)
+              h[1] |= 2;  // the segment has far dependencies (kernel gather variant)
             }
             ++kk;
           }

@@ -37,11 +37,15 @@ struct alignas(16) ChunkDesc {
 
 // max rows per chunk: bounds the per-stage right-hand-side buffer
 constexpr int kChunkRows = 1024;
+// bytes of the step kernel's shared-memory control block (mbarriers, descriptor queue)
+constexpr int kCtlBytes = 512;
 
 // Segment layout inside a chunk (all parts 16-byte aligned; pack.cpp emit_factor):
-//   int32 hdr[12] = {nrows, w, flags, pos0, S, bytes, nseg (first seg), rbase (first seg),
-//                    far_off, 0, 0, 0}; flags: bit0 ends a level, bit1 has far deps,
-//                    bit2 explicit sd/rcp, bits 8.. first consumer thread
+//   int32 hdr[12] = {nrows | w << 16, flags | tb << 8, pos0, bytes, S, far_off,
+//                    rbase (first segment of a chunk), 0, 0, 0, 0, 0}
+//                    flags: bit0 ends a level, bit1 has far deps, bit2 explicit sd/rcp,
+//                    bit3 last segment of its chunk; tb = first consumer thread
+//                    (the first 16 bytes are all a consumer warp needs to follow the stream)
 //   S = nrows rounded up to 4; G = max(1, ceil(w/4)) groups of 4 entries (no-op padding)
 //   int32 info[S]   L: U-position of the row ; U: row id | bit 31: sd = 1 - 2^-53
 //                   | bit 30: the row is a far dependency (its value also goes to global z)
@@ -138,6 +142,9 @@ struct StepConst {
   long long* trace = nullptr;  // PSLR_TRACE: [count, pad, (code, ns)...] of CTA 0
   long long trace_cap = 0;
   int trace_block = 0;       // the CTA whose timeline trace builds record (PSLR_TRACE_CTA)
+  int dbg = 0;               // PSLR_DBG timing experiments (wrong results): bit0 skip rows,
+                             // bit1 skip next-row loads, bit3 no producer back-off
+  long long l2ahead = 0;     // bytes of the factor stream prefetched into L2 ahead (0: default)
 };
 
 }  // namespace pslr

@@ -25,7 +25,6 @@ namespace pslr {
 
 constexpr int kConsumerWarps = kStepThreads / 32;
 constexpr int kBlockThreads = kStepThreads + 32;  // + one producer warp
-constexpr int kL2Ahead = 8 * 32 * 1024;           // bytes prefetched into L2 beyond the smem stages
 constexpr int kBatch = 8;                          // entries gathered per batch in the row loop
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -77,6 +76,10 @@ __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async;" ::: "memory"); }
+// every consumer thread after writing a phase's right-hand-side array (global, generic
+// proxy) and before the barrier after which the producer's TMA reads it (async proxy);
+// a CTA-local ordering, unlike a GPU-scope membar
+__device__ __forceinline__ void fence_rhs_written() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 __device__ __forceinline__ void fence_mbar_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
@@ -164,8 +167,17 @@ __device__ __forceinline__ void trace_fine(const StepConst& K, int code, int arg
   if (PSLR_TRACE_BUILD >= 2) trace_ev(K, code, arg);
 }
 
+// The kernel's dynamic shared memory (file scope: the level loop addresses staged
+// segments by 32-bit offsets into it, which keeps its pointers in one register each)
+extern __shared__ __align__(128) uint8_t smem[];
+template <class T>
+__device__ __forceinline__ const T* sp(uint32_t off) {
+  return reinterpret_cast<const T*>(smem + off);
+}
+
 // Shared-memory control block
 struct Ctl {
+  uint4 dq[16];           // producer: descriptors of the next chunks (cp.async ring)
   uint64_t full[8];       // data + rhs landed (2 arrivals + tx bytes)
   uint64_t empty[8];      // all consumer warps done with the stage (kConsumerWarps arrivals)
   uint64_t rhs_ready[4];  // phase k's rhs array is final (1 arrival)
@@ -191,112 +203,113 @@ __device__ __forceinline__ ChunkDesc load_desc(const ChunkDesc* p) {
   return d;
 }
 
-// Producer: one thread (lane 0 of the producer warp).  The loop is latency-bound on a
-// single thread, so everything per chunk is precomputed (ChunkDesc) and the next
-// descriptor load is in flight while the producer waits for a free stage.
-//   data cursor: chunk d_u goes to stage d_u % nst once the consumers released it;
-//   rhs cursor:  chunk r_u < d_u gets its rhs slice once its phase's rhs is final;
-//   L2 cursor:   bulk prefetch kL2Ahead bytes beyond the issued data.
+static_assert(sizeof(Ctl) <= kCtlBytes, "the control block must fit the header of the shared memory plan");
+
+// Producer: one thread (lane 0 of the producer warp) streams the chunks of the launch's
+// phases, in order, into the nst stages with TMA bulk copies: chunk u's packed segments
+// into stage u % nst, and its right-hand-side slice (a contiguous piece of the phase's
+// position-ordered rhs array) into the stage's rhs buffer, both completing on full[st].
+// A slice can only be copied once its phase's rhs is final (rhs_ready, signalled by the
+// consumers at the phase start), so slices of chunks staged ahead of their phase are
+// deferred.  The thread polls (test_wait + a short sleep) in one place only: before
+// reusing a stage it issues every deferred slice whose phase became ready (the stage's
+// previous occupant needs its slice before the consumers can free it, and the consumers'
+// look-ahead needs the next chunk's), then checks the stage.  Descriptors come from a
+// cp.async queue twelve chunks ahead, so no issue waits on a global load.  (Measured on
+// cfg5: this loop streams ~25% faster than a loop that also runs L2 prefetches and
+// re-tests every condition each iteration; L2 prefetching did not pay.)
 __device__ void producer(const Streams& S, Ctl* ctl, uint8_t* stages, double* rhsbuf, int nst,
-                         int stage_bytes, int rhs_stride, int nv, long long* g_dbg_out) {
+                         int stage_bytes, int rhs_stride, int nv, long long* g_dbg_out, int dbg,
+                         long long* g_tma) {
   if ((threadIdx.x & 31) != 0) return;
   const int np = S.nphase;
   const int total = S.begin[np];
   if (total == 0) return;
-  const int64_t l2ahead = kL2Ahead;
   // data cursor
-  int d_u = 0, d_k = 0;
+  int d_k = 0;
   while (S.begin[d_k + 1] == 0) ++d_k;
-  int d_end = S.begin[d_k + 1], d_base = 0;
+  int d_end = S.begin[d_k + 1];
   const uint8_t* d_data = S.data[d_k];
-  const ChunkDesc* d_ops = S.chunks[d_k];
-  ChunkDesc dop = load_desc(d_ops);
-  int st_d = 0, use_d = 0;
-  // rhs cursor
-  int r_u = 0, r_k = d_k, r_end = d_end, st_r = 0;
-  const double* r_rhs = S.rhs[r_k];
-  uint32_t ready = 0;
-  // L2 cursor over the byte ranges of the phases (chunks of a phase are contiguous)
-  int pf_k = d_k;
-  int64_t pf_off = 0, pf_hi = 0, issued = 0, prefetched = 0;
-  auto pf_range = [&](int k) {
-    const int n = S.begin[k + 1] - S.begin[k];
-    if (n == 0) {
-      pf_off = pf_hi = 0;
-      return;
+  // descriptor queue: chunk u's 16-B descriptor is copied into ctl->dq[u & 15]
+  int q_u = 0, q_k = d_k, q_base = 0, q_end = d_end;
+  auto q_issue = [&]() {
+    if (q_u < total) {
+      while (q_u >= q_end) {
+        ++q_k;
+        q_base = S.begin[q_k];
+        q_end = S.begin[q_k + 1];
+      }
+      asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_addr(&ctl->dq[q_u & 15])),
+                   "l"(S.chunks[q_k] + (q_u - q_base))
+                   : "memory");
     }
-    const ChunkDesc a = load_desc(S.chunks[k]), z = load_desc(S.chunks[k] + n - 1);
-    pf_off = (int64_t)a.off16 * 16;
-    pf_hi = (int64_t)z.off16 * 16 + z.bytes;
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    ++q_u;
   };
-  pf_range(pf_k);
-  long long c_idle = 0, n_it = 0;
+  for (int i = 0; i < 12; ++i) q_issue();
+  // rhs cursor: chunks < r_u have their slice issued
+  int r_u = 0, r_k = d_k, r_end = d_end;
+  uint32_t ready = 0;  // phases whose rhs is final
+  auto r_ready = [&]() -> bool {  // is the phase of chunk r_u ready?
+    while (r_u >= r_end) {
+      ++r_k;
+      r_end = S.begin[r_k + 1];
+    }
+    if (ready & (1u << r_k)) return true;
+    if (!mbar_test(&ctl->rhs_ready[r_k], 0)) return false;
+    ready |= 1u << r_k;
+    fence_proxy_async();  // the consumers' generic-proxy rhs writes, before TMA reads them
+    return true;
+  };
+  auto r_issue = [&]() {
+    const int st = r_u % nst;
+    const int2 rr = ctl->rrec[st];
+    if (dbg & 64) {
+      mbar_arrive(&ctl->full[st]);
+    } else {
+      mbar_expect_tx(&ctl->full[st], (uint32_t)(rr.y * nv));  // nv interleaved right-hand sides
+      const double* src = (dbg & 1024) ? reinterpret_cast<const double*>(S.data[r_k]) : S.rhs[r_k];
+      bulk_load(rhsbuf + (size_t)st * rhs_stride, src + (size_t)rr.x * nv, (uint32_t)(rr.y * nv), &ctl->full[st]);
+    }
+    ++r_u;
+  };
+  long long c_poll = 0;
   const long long c_all = clock64();
-  while (r_u < total) {
-    bool did = false;
-    ++n_it;
-    const long long c_it = clock64();
-    if (d_u < total && (use_d == 0 || mbar_test(&ctl->empty[st_d], (uint32_t)((use_d - 1) & 1)))) {
-      mbar_expect_tx(&ctl->full[st_d], dop.bytes);
-      bulk_load(stages + (size_t)st_d * stage_bytes, d_data + (size_t)dop.off16 * 16, dop.bytes,
-                &ctl->full[st_d]);
-      ctl->rrec[st_d] = make_int2(dop.rpos, (int)dop.rbytes);
-      issued += dop.bytes;
-      if (++st_d == nst) {
-        st_d = 0;
-        ++use_d;
+  for (int u = 0; u < total; ++u) {
+    const int st = u % nst;
+    if (u >= nst) {
+      const long long c0 = clock64();
+      const uint32_t par = (uint32_t)(((u / nst) - 1) & 1);
+      for (;;) {
+        while (r_u < u && r_ready()) r_issue();
+        if (mbar_test(&ctl->empty[st], par)) break;
+        __nanosleep(20);
       }
-      if (++d_u < total) {
-        while (d_u >= d_end) {
-          ++d_k;
-          d_base = S.begin[d_k];
-          d_end = S.begin[d_k + 1];
-          d_data = S.data[d_k];
-          d_ops = S.chunks[d_k];
-        }
-        dop = load_desc(d_ops + (d_u - d_base));
-      }
-      did = true;
+      c_poll += clock64() - c0;
     }
-    if (r_u < d_u) {
-      while (r_u >= r_end) {
-        ++r_k;
-        r_end = S.begin[r_k + 1];
-        r_rhs = S.rhs[r_k];
-      }
-      if (!(ready & (1u << r_k)) && mbar_test(&ctl->rhs_ready[r_k], 0)) {
-        ready |= 1u << r_k;
-        fence_proxy_async();
-      }
-      if (ready & (1u << r_k)) {
-        const int2 rr = ctl->rrec[st_r];
-        mbar_expect_tx(&ctl->full[st_r], (uint32_t)(rr.y * nv));  // nv interleaved right-hand sides
-        bulk_load(rhsbuf + (size_t)st_r * rhs_stride, r_rhs + (size_t)rr.x * nv, (uint32_t)(rr.y * nv),
-                  &ctl->full[st_r]);
-        ++r_u;
-        if (++st_r == nst) st_r = 0;
-        did = true;
-      }
+    while (u >= d_end) {
+      ++d_k;
+      d_end = S.begin[d_k + 1];
+      d_data = S.data[d_k];
     }
-    while (prefetched < issued + l2ahead && pf_k < np) {
-      if (pf_off >= pf_hi) {
-        if (++pf_k < np) pf_range(pf_k);
-        continue;
-      }
-      const int64_t len = (pf_hi - pf_off) < 32768 ? (pf_hi - pf_off) : 32768;
-      bulk_prefetch_l2(S.data[pf_k] + pf_off, (uint32_t)len);
-      pf_off += len;
-      prefetched += len;
-    }
-    if (!did) {
-      __nanosleep(20);
-      c_idle += clock64() - c_it;
-    }
+    asm volatile("cp.async.wait_group 11;" ::: "memory");
+    const uint4 dv = ctl->dq[u & 15];  // off16, bytes, rpos, rbytes (ChunkDesc)
+    q_issue();
+    mbar_expect_tx(&ctl->full[st], dv.y);
+    bulk_load(stages + (size_t)st * stage_bytes, d_data + (size_t)dv.x * 16, dv.y, &ctl->full[st]);
+    if (PSLR_TRACE_BUILD && g_tma && u < 8192) g_tma[2 * u] = clock64();
+    ctl->rrec[st] = make_int2((int32_t)dv.z, (int)dv.w);
+    if (r_u == u && r_ready()) r_issue();
+  }
+  for (;;) {  // the slices still deferred at the end (the last phase's first chunks)
+    while (r_u < total && r_ready()) r_issue();
+    if (r_u == total) break;
+    __nanosleep(20);
   }
   if (g_dbg_out) {
-    atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg_out + 5), (unsigned long long)c_idle);
+    atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg_out + 5), (unsigned long long)c_poll);
     atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg_out + 7), (unsigned long long)(clock64() - c_all));
-    atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg_out + 4), (unsigned long long)n_it);
+    atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg_out + 4), (unsigned long long)total);
   }
 }
 
@@ -342,32 +355,69 @@ __device__ __forceinline__ double2 vmul(double2 a, double s) { return make_doubl
 
 // Consumer side: the level loop.
 //
-// A level's critical path is latency: gather the dependencies from the ring, the
-// sequential DADD chain, store, barrier.  Everything that does not depend on the
-// previous level is loaded one segment ahead: the next segment's header, the row's
-// slots (two groups), its first four values, rhs, U's invd / cadd.  The step is written
-// as straight-line code (no per-row branches: inactive lanes compute on row 0 of the
-// segment and skip the stores).
+// A level's critical path is: barrier -> ring gathers -> the row's DMUL/DADD chain ->
+// ring store -> barrier.  Two things decide how close a level gets to it:
+//  * ISSUE: all consumer warps walk the segment stream, but most levels have far fewer
+//    rows than threads, so a warp owning no row of a segment must cost almost nothing.
+//    The first 16 bytes of a segment header say everything needed to follow the stream
+//    (rows, first thread, flags, size); a warp without rows reads that one word and
+//    moves on (and arrives on the stage's empty barrier once per chunk).
+//  * LATENCY: the header of the segment after next is read two ahead (a chunk
+//    transition and its mbarrier wait happen a level early); the next row's raw
+//    operands (slots, info, right-hand side) are loaded before the barrier and consumed
+//    after it (the Markstein division overlaps the gathers); values and U's invd are
+//    loaded after the barrier beside the gathers; the chain has w entries rounded up to
+//    an even count (w = the segment's longest row; rows of a level are sorted by length,
+//    shorter rows fold exact no-ops 0 * 0), not 4-entry groups.
+// Inactive lanes of an active warp compute on row 0 of the segment and skip the stores.
 //
-// Segment layout (pack.cpp, pslr_internal.h); consumer thread tb + t owns row t
-// (tb = flags >> 8), so the segments of one level run side by side.
+// Segment layout (pack.cpp, pslr_internal.h); consumer thread tb + t owns row t.
+constexpr int kLevelEnd = 1, kFar = 2, kExplicitSd = 4, kChunkEnd = 8;
+
+// one row's operands, loaded before the barrier of the level that precedes it
 template <int NV>
-struct Row {
-  const uint8_t* slots;  // &slot[0][t]  (4 x u16 per row and group)
-  const uint8_t* vals;   // &val[0][0][t]
-  const int32_t* far;    // the segment's far list (U-positions)
-  int bytes, flags, G, S, nrows;
-  bool wact;             // the warp owns rows of this segment (warp-uniform)
-  bool active;           // this lane owns a row
-  int ridx;              // ring slot of the row
-  int zidx;              // z index: L: U-position ; U: position (-1: not a far target)
-  int xidx;              // U: xout index (row id)
-  vt<NV> acc;            // right-hand side(s) (U: already divided by sd)
-  double invd;           // U epilogue
-  vt<NV> cadd;
-  uint2 s0, s1;          // slot groups 0 and 1 (zero slot when absent)
-  double2 va, vb;        // group-0 values
+struct RowOps {
+  int t;          // row in the segment (0 for inactive lanes)
+  bool active;    // this lane owns a row
+  int info;       // L: U-position ; U: row id | bit 31 sd = 1 - 2^-53 | bit 30 far target
+  uint32_t vals;  // smem offsets (computed before the barrier: no address arithmetic between
+  uint32_t far;   //   the barrier and the gathers): val[0][0][t], the far list, U's invd[t]
+  uint32_t invd;
+  vt<NV> rhs;     // raw right-hand side(s)
+  uint2 s0, s1;   // slot groups 0 and 1 (zero slot when absent)
+  vt<NV> cadd;    // U epilogue addend
 };
+
+__device__ __forceinline__ int hdr_rows(int4 h) { return h.x & 0xffff; }
+__device__ __forceinline__ int hdr_w(int4 h) { return h.x >> 16; }
+__device__ __forceinline__ int hdr_S(int4 h) { return ((h.x & 0xffff) + 3) & ~3; }
+__device__ __forceinline__ uint32_t pre_bytes(bool upper, int S, int flags) {
+  return 48 + 4 * S + (upper ? ((flags & kExplicitSd) ? 24 : 8) * S : 0);
+}
+// does this warp own rows of the segment?
+__device__ __forceinline__ bool warp_owns(int4 h) {
+  const int tb = h.y >> 8, w0 = (int)threadIdx.x & ~31;
+  return w0 < tb + hdr_rows(h) && w0 + 32 > tb;
+}
+
+template <bool UPPER, int NV>
+__device__ __forceinline__ void load_ops(uint32_t seg, int4 h, uint32_t rbuf, int rbase, int zslot,
+                                         RowOps<NV>& r) {
+  int t = (int)threadIdx.x - (h.y >> 8);
+  r.active = (unsigned)t < (unsigned)hdr_rows(h);
+  t = r.active ? t : 0;  // inactive lanes read row 0 (in bounds); their results are not stored
+  r.t = t;
+  const int S = hdr_S(h), G = max(1, (hdr_w(h) + 3) >> 2);
+  r.far = seg + (uint32_t)sp<int32_t>(seg)[5];
+  r.info = sp<int32_t>(seg + 48)[t];
+  r.rhs = vld<NV>(sp<double>(rbuf), h.z + t - rbase);
+  const uint32_t slots = seg + pre_bytes(UPPER, S, h.y) + 8 * t;
+  r.s0 = *sp<uint2>(slots);
+  const unsigned z2 = (unsigned)zslot | ((unsigned)zslot << 16);
+  r.s1 = (hdr_w(h) > 4) ? *sp<uint2>(slots + 8 * S) : make_uint2(z2, z2);
+  r.vals = slots + 8 * G * S + 8 * t;  // val[0][0][t] = pre + 8GS + 16t
+  r.invd = seg + 48 + 4 * S + 8 * t;
+}
 
 // U rows start from rhs / sd.  rcp = RN(1/sd): q0 = RN(x rcp) is within an ulp of x/sd
 // and one fma-corrected step gives RN(x/sd) (Markstein); sd == 1 keeps x as is.
@@ -380,217 +430,207 @@ __device__ __forceinline__ double2 div_sd(double2 x, double sd, double rcp) {
   return make_double2(div_sd(x.x, sd, rcp), div_sd(x.y, sd, rcp));
 }
 
-template <bool UPPER, int NV, bool XPOS = false>
-__device__ __forceinline__ void load_row(const uint8_t* seg, const int4 h0, const int4 h1, const double* rbuf,
-                                         int rbase, int base, int mask, int zslot,
-                                         const double* __restrict__ cadd, Row<NV>& r) {
-  const int S = h1.x;
-  const int G = max(1, (h0.y + 3) >> 2);
-  r.flags = h0.z;
-  r.S = S;
-  r.G = G;
-  r.nrows = h0.x;
-  r.bytes = h1.y;
-  // warps owning no row of the segment skip it entirely (the four schedulers are shared
-  // by all consumer warps, so idle warps must not spend issue slots)
-  const int tb = h0.z >> 8, w0 = (int)threadIdx.x & ~31;
-  r.wact = w0 < tb + h0.x && w0 + 32 > tb;
-  if (!r.wact) return;
-  int t = (int)threadIdx.x - tb;
-  r.active = (unsigned)t < (unsigned)h0.x;
-  t = r.active ? t : 0;  // inactive lanes read row 0 (in bounds); their results are not stored
-  const int32_t* info = reinterpret_cast<const int32_t*>(seg + 48);
-  const uint8_t* p = seg + 48 + 4 * S;
-  const int gp = h0.w + t;
-  r.ridx = (gp - base) & mask;
-  vt<NV> x = vld<NV>(rbuf, gp - rbase);
-  const int inf = info[t];
-  if (UPPER) {
-    const double* d = reinterpret_cast<const double*>(p);
-    r.invd = d[t];
-    if (h0.z & 4) {  // explicit sd / rcp arrays
-      x = div_sd(x, d[S + t], d[2 * S + t]);
-      p += 24 * S;
-    } else {         // info bit 31: sd = 1 - 2^-53 (rcp = 1 + 2^-52), else sd = 1
-      if (inf < 0) x = div_sd(x, 0x1.fffffffffffffp-1, 0x1.0000000000001p+0);
-      p += 8 * S;
-    }
-    const int row = inf & 0x3fffffff;
-    r.zidx = (inf & 0x40000000) ? gp : -1;  // only far-dependency targets go to global z
-    r.xidx = XPOS ? gp : row;  // x in U-position order when only this kernel's F reads it
-    r.cadd = (cadd && r.active) ? vldg<NV>(cadd, row) : vzero<NV>();
-  } else {
-    r.zidx = inf;
-  }
-  r.acc = x;
-  r.slots = p + 8 * t;
-  r.s0 = *reinterpret_cast<const uint2*>(r.slots);
-  const unsigned z2 = (unsigned)zslot | ((unsigned)zslot << 16);
-  r.s1 = (G > 1) ? *reinterpret_cast<const uint2*>(r.slots + 8 * S) : make_uint2(z2, z2);
-  r.vals = p + 8 * G * S + 16 * t;
-  r.va = *reinterpret_cast<const double2*>(r.vals);
-  r.vb = *reinterpret_cast<const double2*>(r.vals + 16 * S);
-  r.far = reinterpret_cast<const int32_t*>(seg + h1.z);
-}
-
 // dependency value: near -> ring slot, far (bit 15) -> the segment's far list -> global
 // position-ordered array
 template <bool FAR, int NV>
-__device__ __forceinline__ vt<NV> gather(const double* ring, const double* z, const int32_t* far, unsigned sl) {
-  return (FAR && (sl & 0x8000u)) ? vld<NV>(z, far[sl & 0x7fffu]) : vld<NV>(ring, sl);
+__device__ __forceinline__ vt<NV> gather(const double* ring, const double* z, uint32_t far, unsigned sl) {
+  return (FAR && (sl & 0x8000u)) ? vld<NV>(z, sp<int32_t>(far)[sl & 0x7fffu]) : vld<NV>(ring, sl);
 }
 
-template <bool FAR, int NV>
-__device__ __forceinline__ vt<NV> fold4(vt<NV> acc, uint2 s, double2 va, double2 vb, const double* ring,
-                                        const double* z, const int32_t* far) {
-  const vt<NV> z0 = gather<FAR, NV>(ring, z, far, s.x & 0xffffu), z1 = gather<FAR, NV>(ring, z, far, s.x >> 16);
-  const vt<NV> z2 = gather<FAR, NV>(ring, z, far, s.y & 0xffffu), z3 = gather<FAR, NV>(ring, z, far, s.y >> 16);
-  acc = vmsub(acc, va.x, z0);
-  acc = vmsub(acc, va.y, z1);
-  acc = vmsub(acc, vb.x, z2);
-  acc = vmsub(acc, vb.y, z3);
+__device__ __forceinline__ unsigned slot_of(const uint2 s0, const uint2 s1, int k) {
+  const uint32_t w = (k < 4) ? ((k < 2) ? s0.x : s0.y) : ((k < 6) ? s1.x : s1.y);
+  return (k & 1) ? (w >> 16) : (w & 0xffffu);
+}
+
+// acc -= val_k * z_k for the first NE (even, <= 8) entries in the reference's
+// ascending-column order; prep() yields the starting value after the loads are issued.
+template <int NE, bool FAR, int NV, class Prep>
+__device__ __forceinline__ vt<NV> fold_n(const RowOps<NV>& r, int S, uint32_t vals, uint32_t far,
+                                         const double* ring, const double* z, Prep&& prep) {
+  vt<NV> zz[NE];
+#pragma unroll
+  for (int k = 0; k < NE; ++k) zz[k] = gather<FAR, NV>(ring, z, far, slot_of(r.s0, r.s1, k));
+  double2 d[NE / 2];
+#pragma unroll
+  for (int p = 0; p < NE / 2; ++p) d[p] = *sp<double2>(vals + 16 * S * p);
+  vt<NV> acc = prep();
+#pragma unroll
+  for (int k = 0; k < NE; ++k) acc = vmsub(acc, (k & 1) ? d[k >> 1].y : d[k >> 1].x, zz[k]);
   return acc;
 }
 
-// acc -= val_k * z_k over the row's groups in the reference's ascending-column order
-// (padding entries: 0 * 0); group 0's slots and values are in registers.
+// rows longer than 8 entries: groups of four beyond the first two (padding: exact
+// no-ops), slots straight from the staged segment (out of line: rare)
 template <bool FAR, int NV>
-__device__ __forceinline__ vt<NV> fold_row(vt<NV> acc, const Row<NV>& r, const double* ring, const double* z) {
-  acc = fold4<FAR, NV>(acc, r.s0, r.va, r.vb, ring, z, r.far);
-  if (r.G > 1) {
-    const uint8_t* v = r.vals + 32 * r.S;  // group 1 values
-    acc = fold4<FAR, NV>(acc, r.s1, *reinterpret_cast<const double2*>(v),
-                         *reinterpret_cast<const double2*>(v + 16 * r.S), ring, z, r.far);
-    for (int g = 2; g < r.G; ++g) {  // long rows: the rest straight from the staged segment
-      const uint2 sg = *reinterpret_cast<const uint2*>(r.slots + 8 * g * r.S);
-      const uint8_t* w = r.vals + 32 * g * r.S;
-      acc = fold4<FAR, NV>(acc, sg, *reinterpret_cast<const double2*>(w),
-                           *reinterpret_cast<const double2*>(w + 16 * r.S), ring, z, r.far);
-    }
+__device__ __noinline__ vt<NV> fold_tail(vt<NV> acc, uint32_t slots, uint32_t vals, uint32_t far, int S, int G,
+                                         const double* ring, const double* z) {
+  for (int g = 2; g < G; ++g) {
+    const uint2 sg = *sp<uint2>(slots + 8 * g * S);
+    const vt<NV> z0 = gather<FAR, NV>(ring, z, far, sg.x & 0xffffu), z1 = gather<FAR, NV>(ring, z, far, sg.x >> 16);
+    const vt<NV> z2 = gather<FAR, NV>(ring, z, far, sg.y & 0xffffu), z3 = gather<FAR, NV>(ring, z, far, sg.y >> 16);
+    const double2 a = *sp<double2>(vals + 16 * S * (2 * g));
+    const double2 b = *sp<double2>(vals + 16 * S * (2 * g + 1));
+    acc = vmsub(acc, a.x, z0);
+    acc = vmsub(acc, a.y, z1);
+    acc = vmsub(acc, b.x, z2);
+    acc = vmsub(acc, b.y, z3);
   }
   return acc;
 }
 
-struct Cursor {
-  int u, u1, st, nst, si, nseg, rbase;
-  uint32_t par;
-  const uint8_t* seg;
-  const double* rbuf;
-};
+template <bool FAR, int NV, class Prep>
+__device__ __forceinline__ vt<NV> fold_w(const RowOps<NV>& r, int w, int S, uint32_t vals,
+                                         uint32_t far, const double* ring, const double* z, Prep&& prep) {
+  // two chain lengths (one uniform branch): a padded entry costs one dependent DADD,
+  // a finer dispatch costs more in branch resolution
+  if (w <= 4) return fold_n<4, FAR, NV>(r, S, vals, far, ring, z, prep);
+  if (w <= 8) return fold_n<8, FAR, NV>(r, S, vals, far, ring, z, prep);
+  const int G = (w + 3) >> 2;
+  return fold_tail<FAR, NV>(fold_n<8, FAR, NV>(r, S, vals, far, ring, z, prep), vals - 8 * G * S - 8 * r.t, vals,
+                            far, S, G, ring, z);
+}
 
-template <bool UPPER, int NV, bool XPOS = false>
-__device__ __forceinline__ bool level_step(const StepConst& K, Ctl* ctl, uint8_t* stages, double* rhsbuf,
-                                           Cursor& c, Row<NV>& cur, const double* ring_c,
-                                           double* ring, int base, double* z, double* xout,
-                                           const double* cadd) {
-  const int mask = K.ring_mask, zslot = K.ring_mask + 1;
-  // C: locate the next segment (next chunk: wait for it; it is normally staged already)
-  //    and issue its header loads, so they are in flight while this row is computed
-  const uint8_t* nseg_ptr = c.seg + cur.bytes;
-  const int cur_st = c.st;
-  bool chunk_done = false, more = true;
-  if (++c.si == c.nseg) {
-    chunk_done = true;
-    if (++c.u == c.u1) {
-      more = false;
+// compute one row of the segment (seg, h): gathers, chain, publish
+template <bool UPPER, int NV, bool XPOS>
+__device__ __forceinline__ void compute_row(const StepConst& K, uint32_t seg, int4 h, const RowOps<NV>& r,
+                                            double* ring, int base, double* z, double* xout, const double* cadd) {
+  const int S = hdr_S(h), w = hdr_w(h), flags = h.y;
+  const uint32_t vals = r.vals, far = r.far;
+  const double invd = UPPER ? *sp<double>(r.invd) : 0.0;  // beside the gathers
+  auto prep = [&]() -> vt<NV> {
+    if (!UPPER) return r.rhs;
+    if (flags & kExplicitSd) {  // explicit sd / rcp arrays
+      const double* d = sp<double>(r.invd);
+      return div_sd(r.rhs, d[S], d[2 * S]);
+    }
+    // info bit 31: sd = 1 - 2^-53 (rcp = 1 + 2^-52), else sd = 1
+    return (r.info < 0) ? div_sd(r.rhs, 0x1.fffffffffffffp-1, 0x1.0000000000001p+0) : r.rhs;
+  };
+  const vt<NV> acc = (flags & kFar) ? fold_w<true, NV>(r, w, S, vals, far, ring, z, prep)
+                                    : fold_w<false, NV>(r, w, S, vals, far, ring, z, prep);
+  if (r.active) {
+    const int gp = h.z + r.t;
+    vst(ring, (gp - base) & K.ring_mask, acc);
+    if (UPPER) {
+      if (r.info & 0x40000000) vst(z, gp, acc);  // only far-dependency targets go to global z
+      vt<NV> x = vmul(acc, invd);
+      if (cadd) x = vadd(x, r.cadd);
+      vst(xout, XPOS ? gp : (r.info & 0x3fffffff), x);  // U-position order when only F reads x
     } else {
-      if (++c.st == c.nst) {
-        c.st = 0;
-        c.par ^= 1u;
-      }
-      trace_fine(K, 19, c.u);
-#if PSLR_TRACE_BUILD == 3
-      const long long tw0 = clock64();
-      mbar_wait(&ctl->full[c.st], c.par);
-      trace_clk(K, 51, (int)(clock64() - tw0));
-#else
-      mbar_wait(&ctl->full[c.st], c.par);
-#endif
-      trace_fine(K, 20, c.u);
-      nseg_ptr = stages + (size_t)c.st * K.stage_bytes;
-      c.rbuf = rhsbuf + (size_t)c.st * K.rhs_stride;
-      c.nseg = reinterpret_cast<const int32_t*>(nseg_ptr)[6];
-      c.rbase = reinterpret_cast<const int32_t*>(nseg_ptr)[7];
-      c.si = 0;
+      vst(z, r.info, acc);  // the U phase's right-hand side, at the row's U-position
     }
   }
-  int4 nh0 = make_int4(0, 0, 0, 0), nh1 = make_int4(0, 0, 0, 0);
-  if (more) {
-    nh0 = *reinterpret_cast<const int4*>(nseg_ptr);
-    nh1 = make_int4(reinterpret_cast<const int32_t*>(nseg_ptr)[4], reinterpret_cast<const int32_t*>(nseg_ptr)[5],
-                    reinterpret_cast<const int32_t*>(nseg_ptr)[8], 0);  // S, bytes, far_off
-  }
-  if (cur.wact) {
-    // A + D: gathers and the chain
-    const vt<NV> acc = (cur.flags & 2) ? fold_row<true, NV>(cur.acc, cur, ring_c, z)
-                                       : fold_row<false, NV>(cur.acc, cur, ring_c, z);
-    // F: publish the row
-    if (cur.active) {
-      vst(ring, cur.ridx, acc);
-      if (!UPPER || cur.zidx >= 0) vst(z, cur.zidx, acc);
-      if (UPPER) {
-        vt<NV> x = vmul(acc, cur.invd);
-        if (cadd) x = vadd(x, cur.cadd);
-        vst(xout, cur.xidx, x);
-      }
-    }
-  }
-  const int cur_flags = cur.flags;
-  const int cur_info = (cur.G << 2) | (cur.nrows << 8);
-  // E: the next segment's row, loaded in place (everything it needs before its gathers)
-  if (more) load_row<UPPER, NV, XPOS>(nseg_ptr, nh0, nh1, c.rbuf, c.rbase, base, mask, zslot, cadd, cur);
-  c.seg = nseg_ptr;
-  if (chunk_done) {  // the staged chunk is no longer read by this warp
-    __syncwarp();
-    if ((threadIdx.x & 31) == 0) mbar_arrive(&ctl->empty[cur_st]);
-  }
-  if (cur_flags & 1) {
-    trace_fine(K, 40, 0);
-    consumer_sync();
-    trace_fine(K, 41, 0);
-  }
-  trace_clk(K, 50, (cur_flags & 1) | (chunk_done ? 2 : 0) | cur_info);
-  return more;
 }
 
 // Consumer side of one triangular phase.  Callers arrive right after a consumer barrier
 // that follows the last write of the phase's rhs array; the phase ends with the barrier
-// of its last level.
+// of its last level.  rel: the release cursor over the stages (carried across phases).
 template <bool UPPER, int NV, bool XPOS = false>
-__device__ void tri_phase(const StepConst& K, const Streams& S, Ctl* ctl, uint8_t* stages,
-                          double* rhsbuf, int k, double* ring, int base, double* z, double* xout,
+__device__ void tri_phase(const StepConst& K, const Streams& Sm, Ctl* ctl, uint8_t* stages_p,
+                          double* rhsbuf_p, int k, double* ring, int base, double* z, double* xout,
                           const double* cadd) {
   trace_ev(K, 10 + k, 0);
   trace_cta(K, 2 + k);
-  if (threadIdx.x == 0) {
-    __threadfence();
-    fence_proxy_async();
-    mbar_arrive(&ctl->rhs_ready[k]);
+  if (threadIdx.x == 0) mbar_arrive(&ctl->rhs_ready[k]);  // writers fenced before the last barrier
+  int u = Sm.begin[k];
+  const int u1 = Sm.begin[k + 1];
+  if (u == u1) return;
+  const uint32_t stages = (uint32_t)(stages_p - smem), rhsbuf = (uint32_t)((uint8_t*)rhsbuf_p - smem);
+  const int nst = K.nst, zslot = K.ring_mask + 1;
+  int st = u % nst;
+  uint32_t par = (uint32_t)((u / nst) & 1);
+  if (K.dbg & 16) {  // timing experiment: the stream alone (every chunk waited for and released)
+    for (; u < u1; ++u) {
+      if (!(K.dbg & 256)) mbar_wait(&ctl->full[st], par);
+      if (PSLR_TRACE_BUILD && K.trace && blockIdx.x == K.trace_block && threadIdx.x == 0 && u < 8192)
+        K.trace[2 + 2 * 65536 + 2 * u + 1] = clock64();
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive(&ctl->empty[st]);
+      if (++st == nst) {
+        st = 0;
+        par ^= 1u;
+      }
+    }
+    consumer_sync();
+    return;
   }
-  Cursor c;
-  c.u = S.begin[k];
-  c.u1 = S.begin[k + 1];
-  if (c.u == c.u1) return;
-  c.nst = K.nst;
-  c.st = c.u % c.nst;
-  c.par = (uint32_t)((c.u / c.nst) & 1);
-  mbar_wait(&ctl->full[c.st], c.par);
-  trace_fine(K, 20, c.u);
-  c.seg = stages + (size_t)c.st * K.stage_bytes;
-  c.rbuf = rhsbuf + (size_t)c.st * K.rhs_stride;
-  c.nseg = reinterpret_cast<const int32_t*>(c.seg)[6];
-  c.rbase = reinterpret_cast<const int32_t*>(c.seg)[7];
-  c.si = 0;
-  Row<NV> row;
-  {
-    const int32_t* h = reinterpret_cast<const int32_t*>(c.seg);
-    load_row<UPPER, NV, XPOS>(c.seg, *reinterpret_cast<const int4*>(c.seg), make_int4(h[4], h[5], h[8], 0), c.rbuf,
-                        c.rbase, base, K.ring_mask, K.ring_mask + 1, cadd, row);
+  // segment A (computed this step), B (its operands loaded this step), C (header read)
+  mbar_wait(&ctl->full[st], par);
+  uint32_t segA = stages + (uint32_t)(st * K.stage_bytes);
+  int stA = st, stB = st;  // stages holding A and B (released after their chunk's last segment)
+  uint32_t rbuf = rhsbuf + (uint32_t)(st * K.rhs_stride * 8);
+  int rbase = sp<int32_t>(segA)[6];
+  int4 hA = *sp<int4>(segA);
+  bool actA = warp_owns(hA);
+  RowOps<NV> ra;
+  if (actA) load_ops<UPPER, NV>(segA, hA, rbuf, rbase, zslot, ra);
+  // the cursor moves to the segment after `seg` (header h); false at the end of the phase
+  auto next = [&](uint32_t seg, int4 h, uint32_t& nseg) -> bool {
+    if (h.y & kChunkEnd) {
+      if (++u == u1) return false;
+      if (++st == nst) {
+        st = 0;
+        par ^= 1u;
+      }
+      mbar_wait(&ctl->full[st], par);
+      nseg = stages + (uint32_t)(st * K.stage_bytes);
+      rbuf = rhsbuf + (uint32_t)(st * K.rhs_stride * 8);
+      rbase = sp<int32_t>(nseg)[6];
+    } else {
+      nseg = seg + (uint32_t)h.w;
+    }
+    return true;
+  };
+  uint32_t segB = 0;
+  uint32_t rbufB = rbuf;
+  int rbaseB = rbase;
+  bool validB = next(segA, hA, segB);
+  stB = st;
+  int4 hB = validB ? *sp<int4>(segB) : make_int4(0, 0, 0, 0);
+  if (validB) {
+    rbufB = rbuf;
+    rbaseB = rbase;
   }
-  const double* ring_c = ring;
-  while (level_step<UPPER, NV, XPOS>(K, ctl, stages, rhsbuf, c, row, ring_c, ring, base, z, xout, cadd)) {
+  if (UPPER && actA) ra.cadd = (cadd && ra.active) ? vldg<NV>(cadd, ra.info & 0x3fffffff) : vzero<NV>();
+  for (;;) {
+    trace_clk(K, 50, hA.y & 0xff);
+    if (actA && !(K.dbg & 1)) compute_row<UPPER, NV, XPOS>(K, segA, hA, ra, ring, base, z, xout, cadd);
+    trace_clk(K, 52, 0);
+    if (hA.y & kChunkEnd) {  // this warp no longer reads A's stage
+      __syncwarp();
+      if ((threadIdx.x & 31) == 0) mbar_arrive(&ctl->empty[stA]);
+    }
+    const int flagsA = hA.y;
+    if (!validB) {
+      fence_rhs_written();  // z (an L phase's output) is the next phase's right-hand side
+      if (flagsA & kLevelEnd) consumer_sync();
+      break;
+    }
+    // B: this warp's row operands (before the barrier; consumed after it)
+    const bool actB = warp_owns(hB);
+    if (actB && !(K.dbg & 2)) load_ops<UPPER, NV>(segB, hB, rbufB, rbaseB, zslot, ra);
+    trace_clk(K, 53, 0);
+    // C: the header after B
+    uint32_t segC = 0;
+    const bool validC = next(segB, hB, segC);
+    const int4 hC = validC ? *sp<int4>(segC) : make_int4(0, 0, 0, 0);
+    trace_clk(K, 54, 0);
+    if (flagsA & kLevelEnd) consumer_sync();
+    if (UPPER && actB)  // the epilogue addend: a global load a level ahead of its use
+      ra.cadd = (cadd && ra.active) ? vldg<NV>(cadd, ra.info & 0x3fffffff) : vzero<NV>();
+    segA = segB;
+    hA = hB;
+    actA = actB;
+    stA = stB;
+    stB = st;
+    segB = segC;
+    hB = hC;
+    validB = validC;
+    rbufB = rbuf;
+    rbaseB = rbase;
   }
 }
+
 
 // Four SpMV rows at once (independent gathers in flight): s[j] = sum_e M_ij x_j in CSR
 // order from 0 (scipy csr_matvec).  RO: x is read-only for this launch.
@@ -648,7 +688,6 @@ __device__ __forceinline__ void iface_terms4(int kind, const int (&row)[4], cons
 template <int NV, bool XPOS>
 __global__ void __launch_bounds__(kBlockThreads, PSLR_STEP_MINB)
 subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant__ StepConst K) {
-  extern __shared__ __align__(128) uint8_t smem[];
   const int b = blockIdx.x;
   const bool do_b = a.b1 != BT_NONE;
   const bool do_i = a.i1 != IT_NONE;
@@ -657,8 +696,8 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
   Ctl* ctl = reinterpret_cast<Ctl*>(smem);
   // [Ctl 256 B][ring: (W + zero slot) x NV, padded to 128 B][nst stages][nst rhs slices]
   // The ring sits at a constant offset, so a gather is one address op on its slot.
-  double* ring = reinterpret_cast<double*>(smem + 256);
-  uint8_t* stages = smem + 256 + (size_t)(K.ring_mask + 1) * 8 * NV + 128;
+  double* ring = reinterpret_cast<double*>(smem + kCtlBytes);
+  uint8_t* stages = smem + kCtlBytes + (size_t)(K.ring_mask + 1) * 8 * NV + 128;
   double* rhsbuf = reinterpret_cast<double*>(stages + (size_t)K.nst * K.stage_bytes);
 
   // The stream table lives in shared memory: dynamically indexed per-thread arrays would
@@ -697,7 +736,9 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
   if (threadIdx.x >= kStepThreads) {  // producer warp (all 32 lanes)
     producer(S, ctl, stages, rhsbuf, K.nst, K.stage_bytes, K.rhs_stride, NV,
              (K.trace && K.trace_cap >= (1 << 20)) ? K.trace + 2 + 2 * K.trace_cap - 8 * 4096 + b * 8
-                                                   : nullptr);
+                                                   : nullptr,
+             K.dbg,
+             (PSLR_TRACE_BUILD && K.trace && b == K.trace_block) ? K.trace + 2 + 2 * 65536 : nullptr);
     return;
   }
   // Programmatic dependent launch: this grid may start while the previous kernel of the
@@ -785,6 +826,7 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
           if (i0 + j * kStepThreads < e1) vst(rhs, r[j].x, (a.b1 == BT_F) ? vsub(fv[j], sum[j]) : sum[j]);
       }
     }
+    fence_rhs_written();  // the L_B right-hand side (f / E y rows) is read by TMA next
     consumer_sync();
     trace_ev(K, 3, 0);
     trace_cta(K, 1);
@@ -820,6 +862,7 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
         }
       }
     }
+    fence_rhs_written();  // rhsC is the L_C0 right-hand side
     consumer_sync();
     trace_ev(K, 30, 0);
     if (do_c) {
