@@ -206,8 +206,13 @@ int pslr_ctx_set_halo(pslr_ctx* ctx, int world, const int64_t* send_counts, cons
 
 /* ---------------------------------------------------------------- Krylov (device) */
 /* lowrank.py:39-73 on op = E_rr(m) (schur.py:104-112), preconditioner.py:133-136.
- * v0: host start vector (q doubles, NOT normalised — the seeded draw); V_dev: q x rank
- * row-major output; H: host rank x rank row-major; r_out: achieved rank. */
+ * v0: host start vector (this rank's q rows of the global seeded draw).  It is used as is
+ * when its (global) 2-norm is 1 to within 1e-14 — the Python wrapper normalises it with
+ * numpy, as the reference — and divided by its norm otherwise.
+ * V_dev: q x r_out row-major output, PACKED (leading dimension r_out, the achieved rank;
+ * room for q x rank doubles); H: host r_out x r_out row-major (room for rank x rank);
+ * r_out: achieved rank (< rank on happy breakdown).  On a sharded context the rank is
+ * capped by the global interface dimension and every rank runs the same collectives. */
 int pslr_arnoldi(pslr_ctx* ctx, int64_t m, int64_t rank, const double* v0, double* V_dev,
                  double* H, int64_t* r_out, void* stream);
 /* krylov.py:35-129 on (A = reordered matrix, M = PSLR apply (precond!=0) or identity).

@@ -631,6 +631,8 @@ static int set_correction_common(pslr_ctx* ctx, int64_t r, const double* V, bool
                                  const double* G) {
   if (r < 0) return fail(PSLR_EDIM, "rank must be >= 0");
   if (ctx->parent) return fail(PSLR_EINVAL, "a cloned context shares its parent's correction");
+  if (ctx->family.use_count() > 1)
+    return fail(PSLR_EINVAL, "the context has live clones sharing its correction: destroy them first");
   RET(set_device(ctx));
   free_ptr(ctx, ctx->V);
   free_ptr(ctx, ctx->G);
@@ -952,11 +954,16 @@ int pslr_debug_trace(pslr_ctx* ctx, int64_t* out, int64_t cap, int64_t* count) {
 int pslr_apply_multi(pslr_ctx* ctx, int64_t m, int64_t nv, const double* b, double* z, void* stream) {
   if (m < 0) return fail(PSLR_EDIM, "series degree m must be >= 0");
   if (nv < 0) return fail(PSLR_EDIM, "number of vectors must be >= 0");
-  RET(unsharded(ctx));
+  if (!ctx->comm) RET(unsharded(ctx));
   RET(set_device(ctx));
   cudaStream_t st = S(stream);
   const int64_t n = ctx->n;
   int64_t v = 0;
+  if (ctx->comm) {  // sharded: pairs through one launch sequence + one set of collectives
+    for (; v + 2 <= nv; v += 2) RET(op_apply2_sharded(ctx, m, b + v * n, z + v * n, st));
+    for (; v < nv; ++v) RET(op_apply_sharded(ctx, m, b + v * n, z + v * n, st));
+    return PSLR_OK;
+  }
   if (ctx->q > 0 && ctx->p > 0)
     for (; v + 2 <= nv; v += 2) RET(op_apply2(ctx, m, b + v * n, z + v * n, st));
   for (; v < nv; ++v) RET(op_apply(ctx, m, b + v * n, z + v * n, st));
@@ -970,6 +977,7 @@ int pslr_ctx_clone(const pslr_ctx* src, pslr_ctx** out) {
   RET(set_device(src));
   auto* ctx = new pslr_ctx(*src);  // shares every read-only device array of src
   ctx->parent = src->parent ? src->parent : src;
+  // ctx->family (copied) now counts this clone until pslr_ctx_destroy deletes it
   ctx->allocations.clear();
   ctx->prof_events.clear();
   ctx->prof_kinds.clear();
@@ -979,6 +987,8 @@ int pslr_ctx_clone(const pslr_ctx* src, pslr_ctx** out) {
   ctx->K.trace_cap = 0;
   ctx->kv = ctx->kz = ctx->h_dev = nullptr;
   ctx->kv_len = ctx->kz_len = ctx->h_len = 0;
+  ctx->red = nullptr;  // reduction partials are per context (Krylov / dnorm on a clone)
+  ctx->red_len = 0;
   ctx->comm = nullptr;  // a clone has no communicator of its own
   ctx->world = 1;
   ctx->rank = 0;
@@ -987,6 +997,10 @@ int pslr_ctx_clone(const pslr_ctx* src, pslr_ctx** out) {
   ctx->halo_nsend = 0;
   ctx->sh_a = ctx->sh_b = ctx->sh_c = ctx->sh_s = ctx->sh_x = nullptr;
   ctx->sh_a_len = ctx->sh_b_len = ctx->sh_c_len = ctx->sh_s_len = ctx->sh_x_len = 0;
+  ctx->sh2_y0 = ctx->sh2_a = ctx->sh2_b = ctx->sh2_c = ctx->halo_buf2 = nullptr;
+  ctx->sh2_y0_len = ctx->sh2_a_len = ctx->sh2_b_len = ctx->sh2_c_len = ctx->halo_buf2_len = 0;
+  ctx->halo_send_cnt.assign(ctx->halo_send_cnt.size(), 0);
+  ctx->halo_recv_cnt.assign(ctx->halo_recv_cnt.size(), 0);
   ctx->hpin = nullptr;  // host staging and events are per context
   ctx->hpin_len = 0;
   ctx->kev[0] = ctx->kev[1] = nullptr;
@@ -1022,8 +1036,7 @@ int pslr_ctx_clone(const pslr_ctx* src, pslr_ctx** out) {
     ctx->counter = static_cast<unsigned int*>(d);
   }
   if (ctx->r > 0) {  // V and G are shared; the reduction scratch is private
-    ctx->partials = ctx->u = ctx->red = nullptr;
-    ctx->red_len = 0;
+    ctx->partials = ctx->u = nullptr;
     if ((rc = alloc_scratch(ctx, &ctx->partials, ctx->s * ctx->r))) return bail(rc);
     if ((rc = alloc_scratch(ctx, &ctx->u, 2 * ctx->r))) return bail(rc);
     if ((rc = ensure(ctx, &ctx->red, &ctx->red_len, (int64_t)vt_grid(ctx->q, ctx->sm_count) * ctx->r + 8)))

@@ -87,6 +87,12 @@ __global__ void halo_gather_kernel(const double* __restrict__ v, const int32_t* 
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     out[i] = v[idx[i]];
 }
+// two interleaved right-hand sides ([i][2]): one 16-byte pair per sent index
+__global__ void halo_gather2_kernel(const double2* __restrict__ v, const int32_t* __restrict__ idx,
+                                    double2* __restrict__ out, int64_t n) {
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    out[i] = v[idx[i]];
+}
 
 bool sharded_comm(const pslr_ctx* ctx) { return ctx->comm != nullptr; }
 
@@ -115,6 +121,34 @@ int comm_halo(pslr_ctx* ctx, double* v_ext, cudaStream_t st) {
     if (ctx->halo_recv_cnt[r])
       NCK(nccl().recv(v_ext + ctx->q + ctx->halo_recv_off[r], (size_t)ctx->halo_recv_cnt[r], ncclDouble, r, comm,
                       st),
+          "ncclRecv");
+  }
+  NCK(nccl().groupEnd(), "ncclGroupEnd");
+  return PSLR_OK;
+}
+
+// the same exchange for an interleaved two-vector interface array v2 ([i][2]): ghosts after
+// the 2q local values, every count doubled
+int comm_halo2(pslr_ctx* ctx, double* v2_ext, cudaStream_t st) {
+  if (!ctx->comm) return PSLR_OK;
+  const int64_t ns = ctx->halo_nsend;
+  if (ns > 0) {
+    RET(ensure(ctx, &ctx->halo_buf2, &ctx->halo_buf2_len, 2 * ns));
+    const int64_t blocks = std::min<int64_t>((ns + 255) / 256, 4 * (int64_t)ctx->sm_count);
+    halo_gather2_kernel<<<(unsigned)blocks, 256, 0, st>>>(reinterpret_cast<const double2*>(v2_ext), ctx->halo_idx,
+                                                         reinterpret_cast<double2*>(ctx->halo_buf2), ns);
+    CK(cudaGetLastError());
+  }
+  auto comm = static_cast<ncclComm_t>(ctx->comm);
+  NCK(nccl().groupStart(), "ncclGroupStart");
+  for (int r = 0; r < ctx->world; ++r) {
+    if (ctx->halo_send_cnt[r])
+      NCK(nccl().send(ctx->halo_buf2 + 2 * ctx->halo_send_off[r], (size_t)(2 * ctx->halo_send_cnt[r]), ncclDouble,
+                      r, comm, st),
+          "ncclSend");
+    if (ctx->halo_recv_cnt[r])
+      NCK(nccl().recv(v2_ext + 2 * (ctx->q + ctx->halo_recv_off[r]), (size_t)(2 * ctx->halo_recv_cnt[r]),
+                      ncclDouble, r, comm, st),
           "ncclRecv");
   }
   NCK(nccl().groupEnd(), "ncclGroupEnd");
@@ -160,6 +194,42 @@ int op_apply_sharded(pslr_ctx* ctx, int64_t m, const double* b, double* z, cudaS
     }
   }
   return pslr_apply_last(ctx, b, y, z, sv);
+}
+
+// Two right-hand sides (b2, z2: two vector-major local n-vectors) through one launch
+// sequence and one set of collectives: the split two-vector entry points (each vector's
+// arithmetic is the single-vector one bit for bit), halos of interleaved pairs, one
+// allreduce of 2r.  Ranks without interior or interface rows run the vectors one by one
+// between the SAME collectives (shard.py ShardedPreconditioner.apply2's contract).
+int op_apply2_sharded(pslr_ctx* ctx, int64_t m, const double* b2, double* z2, cudaStream_t st) {
+  void* sv = static_cast<void*>(st);
+  const int64_t n = ctx->n, q = ctx->q, ng = ctx->nghost, r = ctx->r;
+  if (ctx->p == 0 || q == 0) {  // no two-vector kernels here: per vector, same collectives
+    for (int v = 0; v < 2; ++v) RET(op_apply_sharded(ctx, m, b2 + v * n, z2 + v * n, st));
+    return PSLR_OK;
+  }
+  RET(ensure(ctx, &ctx->sh2_y0, &ctx->sh2_y0_len, 2 * q + 2));
+  RET(ensure(ctx, &ctx->sh2_c, &ctx->sh2_c_len, 2 * (q + ng) + 2));
+  RET(ensure(ctx, &ctx->sh2_a, &ctx->sh2_a_len, 2 * (q + ng) + 2));
+  RET(ensure(ctx, &ctx->sh2_b, &ctx->sh2_b_len, 2 * (q + ng) + 2));
+  RET(ensure(ctx, &ctx->sh_s, &ctx->sh_s_len, 2 * std::max<int64_t>(r, 1) + 2));
+  CK(cudaMemsetAsync(ctx->sh_s, 0, (2 * std::max<int64_t>(r, 1) + 2) * sizeof(double), st));
+  RET(pslr_apply2_first(ctx, b2, ctx->sh2_y0, ctx->sh_s, sv));
+  if (r > 0) RET(comm_allreduce(ctx, ctx->sh_s, 2 * r, st));
+  CK(cudaMemsetAsync(ctx->sh2_c, 0, 2 * (q + ng) * sizeof(double), st));
+  RET(pslr_apply2_mid(ctx, ctx->sh2_y0, ctx->sh_s, ctx->sh2_c, sv));
+  const double* y = ctx->sh2_c;
+  if (m > 0) {
+    RET(comm_halo2(ctx, ctx->sh2_c, st));
+    double* outs[2] = {ctx->sh2_a, ctx->sh2_b};
+    for (int64_t k = 0; k < m; ++k) {
+      double* out = outs[k & 1];
+      RET(pslr_apply2_horner(ctx, y, ctx->sh2_c, out, sv));
+      if (k < m - 1) RET(comm_halo2(ctx, out, st));
+      y = out;
+    }
+  }
+  return pslr_apply2_last(ctx, b2, y, z2, sv);
 }
 
 // E_rr(m) v on the rank's rows (schur.py:104-112; shard.py sharded_arnoldi's operator)
@@ -211,7 +281,8 @@ int pslr_comm_unique_id(void* out) {
 int pslr_comm_init(pslr_ctx* ctx, const void* nccl_unique_id, int nranks, int rank) {
   if (!ctx) return fail(PSLR_EINVAL, "null context");
   if (nranks < 1 || rank < 0 || rank >= nranks) return fail(PSLR_EINVAL, "bad rank / nranks");
-  if (ctx->parent) return fail(PSLR_EINVAL, "a cloned context cannot own a communicator");
+  // a clone may own a communicator of its own: an independent pipeline of the same
+  // sharded problem (its collectives are ordered on its communicator alone)
   RET(nccl_ready());
   RET(set_device(ctx));
   RET(comm_destroy(ctx));

@@ -75,14 +75,37 @@ int pslr_arnoldi(pslr_ctx* ctx, int64_t m, int64_t rank, const double* v0, doubl
   cudaStream_t st = S(stream);
   const int64_t q = ctx->q;
   if (rank < 0) return fail(PSLR_EDIM, "rank must be >= 0");
-  rank = std::min(rank, q);
   *r_out = 0;
-  if (q == 0 || rank == 0) return PSLR_OK;
+  // the rank is capped by the GLOBAL interface dimension (lowrank.py:49): on a sharded
+  // context every rank must take the same decision and run the same collectives, even a
+  // rank that owns no interface row
+  int64_t qg = q;
+  if (ctx->comm) {
+    RET(ensure(ctx, &ctx->h_dev, &ctx->h_len, 8));
+    double qd = (double)q;
+    CK(cudaMemcpyAsync(ctx->h_dev, &qd, sizeof(double), cudaMemcpyHostToDevice, st));
+    RET(comm_allreduce(ctx, ctx->h_dev, 1, st));
+    CK(cudaMemcpyAsync(&qd, ctx->h_dev, sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    qg = (int64_t)qd;
+  }
+  rank = std::min(rank, qg);
+  if (qg == 0 || rank == 0) return PSLR_OK;
   const int64_t ldq = basis_ld(q);
   RET(ensure(ctx, &ctx->kv, &ctx->kv_len, ldq * (rank + 1)));
   double* Vc = ctx->kv;  // column-major q x (rank+1), leading dimension ldq
   CK(cudaMemsetAsync(Vc, 0, ldq * (rank + 1) * sizeof(double), st));
-  CK(cudaMemcpyAsync(Vc, v0, q * sizeof(double), cudaMemcpyHostToDevice, st));
+  if (q) CK(cudaMemcpyAsync(Vc, v0, q * sizeof(double), cudaMemcpyHostToDevice, st));
+  // lowrank.py:52-57 normalises the seeded draw.  A start vector that already has unit
+  // norm (the Python wrapper normalises it with numpy, bit for bit as the reference) is
+  // used as is; anything else is divided by its (allreduced) norm here.
+  double v0n = 0.0;
+  RET(dnorm(ctx, Vc, q, &v0n, st));
+  if (!(v0n > 0.0) || !std::isfinite(v0n)) return fail(PSLR_EDIM, "Arnoldi start vector has no direction");
+  if (std::fabs(v0n - 1.0) > 1e-14) {
+    CK(cudaMemcpyAsync(ctx->h_dev, &v0n, sizeof(double), cudaMemcpyHostToDevice, st));
+    CKL(launch_div_scalar(Vc, ctx->h_dev, Vc, q, st));
+  }
   std::vector<double> Hb((rank + 1) * rank, 0.0);  // row-major (rank+1) x rank
   std::vector<double> h(rank + 1);
   int64_t r = rank;
@@ -100,6 +123,7 @@ int pslr_arnoldi(pslr_ctx* ctx, int64_t m, int64_t rank, const double* v0, doubl
     CK(cudaMemcpyAsync(ctx->h_dev, &hn, sizeof(double), cudaMemcpyHostToDevice, st));
     CKL(launch_div_scalar(w, ctx->h_dev, Vc + (j + 1) * ldq, q, st));
   }
+  // V_dev: the rank's q rows x r columns, row-major with leading dimension r (packed)
   CKL(launch_transpose_basis(Vc, ldq, q, (int)r, V_dev, st));
   for (int64_t i = 0; i < r; ++i)
     for (int64_t j = 0; j < r; ++j) H[i * r + j] = Hb[i * rank + j];

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdint>
+#include <memory>
 #include <string>
 #include <vector>
 
@@ -156,6 +157,8 @@ struct pslr_ctx {
   int64_t nghost = 0;  // sharded contexts: ghost interface columns of C, Cg and A
   bool pdl = true;     // programmatic dependent launch of the step kernel (PSLR_PDL=0: off)
   const pslr_ctx* parent = nullptr;  // clones: the context whose read-only data they share
+  // shared by a context and its clones: use_count() - 1 = live clones of the parent
+  std::shared_ptr<int> family = std::make_shared<int>(0);
   int smem_optin = 0;
   // two right-hand sides per launch (pslr_apply_multi): step constants with the doubled
   // ring / rhs slices and interleaved ([row][2]) scratch, set up on first use
@@ -204,6 +207,8 @@ struct pslr_ctx {
   int64_t halo_nsend = 0;
   double *sh_a = nullptr, *sh_b = nullptr, *sh_c = nullptr, *sh_s = nullptr, *sh_x = nullptr;
   int64_t sh_a_len = 0, sh_b_len = 0, sh_c_len = 0, sh_s_len = 0, sh_x_len = 0;
+  double *sh2_y0 = nullptr, *sh2_a = nullptr, *sh2_b = nullptr, *sh2_c = nullptr, *halo_buf2 = nullptr;
+  int64_t sh2_y0_len = 0, sh2_a_len = 0, sh2_b_len = 0, sh2_c_len = 0, halo_buf2_len = 0;
   double* hpin = nullptr;        // pinned host: the GMRES coefficients of two iterations
   int64_t hpin_len = 0;
   cudaEvent_t kev[2] = {nullptr, nullptr};  // their device-to-host copies landed

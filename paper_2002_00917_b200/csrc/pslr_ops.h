@@ -78,6 +78,8 @@ int comm_allreduce(pslr_ctx* ctx, double* x, int64_t n, cudaStream_t st);
 int comm_halo(pslr_ctx* ctx, double* v_ext, cudaStream_t st);
 int comm_destroy(pslr_ctx* ctx);
 int op_apply_sharded(pslr_ctx* ctx, int64_t m, const double* b, double* z, cudaStream_t st);
+int op_apply2_sharded(pslr_ctx* ctx, int64_t m, const double* b2, double* z2, cudaStream_t st);
+int comm_halo2(pslr_ctx* ctx, double* v2_ext, cudaStream_t st);
 int op_apply_err_sharded(pslr_ctx* ctx, int64_t m, const double* v, double* out, cudaStream_t st);
 int op_spmv_A_sharded(pslr_ctx* ctx, const double* x, double* w, cudaStream_t st);
 

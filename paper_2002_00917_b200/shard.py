@@ -364,17 +364,23 @@ def nccl_unique_id() -> bytes:
 
 def attach_nccl(ops: "DeviceShardOps", plan: "ShardPlan", unique_id: bytes) -> None:
     """Give the rank-local context its own NCCL communicator and this rank's halo plan:
-    pslr_apply / pslr_apply_Err / pslr_arnoldi / pslr_gmres / pslr_cg on ops.dev.handle then
-    run the coupled problem inside libpslr (include/pslr.h pslr_comm_init /
-    pslr_ctx_set_halo) — the C-ABI route a non-Python caller uses."""
+    pslr_apply / pslr_apply_multi / pslr_apply_Err / pslr_arnoldi / pslr_gmres / pslr_cg on
+    ops.dev.handle then run the coupled problem inside libpslr (include/pslr.h
+    pslr_comm_init / pslr_ctx_set_halo) — the C-ABI route a non-Python caller uses."""
+    attach_nccl_ctx(ops.dev, plan, unique_id)
+
+
+def attach_nccl_ctx(dev, plan: "ShardPlan", unique_id: bytes) -> None:
+    """attach_nccl for a DeviceContext (the built one or a pslr_ctx_clone of it: each
+    independent pipeline owns a communicator)."""
     from . import _lib
     uid = ctypes.create_string_buffer(bytes(unique_id), 128)
-    _lib.check(_lib.fns["pslr_comm_init"](ops.dev.handle, uid, int(plan.world), int(plan.rank)))
+    _lib.check(_lib.fns["pslr_comm_init"](dev.handle, uid, int(plan.world), int(plan.rank)))
     send_counts = np.asarray([ix.size for ix in plan.send_idx], dtype=np.int64)
     send_idx = (np.concatenate(plan.send_idx).astype(np.int32) if send_counts.sum()
                 else np.zeros(1, dtype=np.int32))
     recv_counts = np.ascontiguousarray(plan.recv_counts, dtype=np.int64)
-    _lib.check(_lib.fns["pslr_ctx_set_halo"](ops.dev.handle, int(plan.world), send_counts.ctypes.data,
+    _lib.check(_lib.fns["pslr_ctx_set_halo"](dev.handle, int(plan.world), send_counts.ctypes.data,
                                              send_idx.ctypes.data, recv_counts.ctypes.data))
 
 
