@@ -39,8 +39,13 @@ extern "C" {
 #define PSLR_ENOMEM 6
 #define PSLR_ENCCL 7
 #define PSLR_ENOTSPD 8
+#define PSLR_ECALLBACK 9  /* a caller-supplied operator callback failed (its own error stands) */
 
 typedef struct pslr_ctx pslr_ctx;
+/* A caller-supplied linear operator for the *_op Krylov drivers: y = op(x) on device
+ * vectors of the driver's dimension, enqueued on (or synchronised with) `stream`;
+ * returns 0 on success.  It is called from the thread that called the driver. */
+typedef int (*pslr_vec_fn)(void* user, const double* x_dev, double* y_dev, void* stream);
 typedef struct pslr_factors pslr_factors;
 
 /* A CSR matrix in host memory (sorted column indices, no duplicates). */
@@ -215,9 +220,27 @@ int pslr_ctx_set_halo(pslr_ctx* ctx, int world, const int64_t* send_counts, cons
  * capped by the global interface dimension and every rank runs the same collectives. */
 int pslr_arnoldi(pslr_ctx* ctx, int64_t m, int64_t rank, const double* v0, double* V_dev,
                  double* H, int64_t* r_out, void* stream);
+/* lowrank.py:39-73 for any operator (the reference's `op` callable): the same device CGS2
+ * Arnoldi, V_dev dim x r_out packed; ctx only provides device scratch (a
+ * pslr_workspace_create context will do). */
+int pslr_arnoldi_op(pslr_ctx* ctx, int64_t dim, pslr_vec_fn op, void* user, int64_t rank, const double* v0,
+                    double* V_dev, double* H, int64_t* r_out, void* stream);
+/* A context without a system: device scratch for the *_op drivers on generic operators
+ * (krylov.py's gmres / cg with arbitrary apply_A / apply_M).  Destroy with pslr_ctx_destroy. */
+int pslr_workspace_create(pslr_ctx** out, int device);
+/* y = M x for a device CSR matrix (int32 indptr / indices, fp64 data), scipy csr_matvec
+ * order (bit-identical to A @ x): the generic drivers' operator for a scipy matrix. */
+int pslr_csr_spmv(int64_t nrows, int64_t ncols, const int32_t* indptr, const int32_t* indices, const double* data,
+                  const double* x, double* y, void* stream);
 /* krylov.py:35-129 on (A = reordered matrix, M = PSLR apply (precond!=0) or identity).
  * flexible!=0: FGMRES (Z_j = M v_j stored, x += Z y) — config 3's accelerator.
  * b, x: device n-vectors. history: host buffer of maxit+1 doubles. */
+/* krylov.py:35-129 for any operator pair on device n-vectors: A_fn NULL -> the context's
+ * reordered matrix; M_fn NULL -> the context's PSLR apply (precond != 0) or the identity. */
+int pslr_gmres_op(pslr_ctx* ctx, int64_t m, int64_t n, pslr_vec_fn A_fn, void* A_user, pslr_vec_fn M_fn,
+                  void* M_user, int precond, const double* b, double* x, double tol, int64_t maxit,
+                  int64_t restart, int flexible, int64_t* iterations, int* converged, double* final_relres,
+                  double* history, int64_t* history_len, void* stream);
 int pslr_gmres(pslr_ctx* ctx, int64_t m, const double* b, double* x, double tol, int64_t maxit,
                int64_t restart, int precond, int flexible, int64_t* iterations, int* converged,
                double* final_relres, double* history, int64_t* history_len, void* stream);
@@ -235,6 +258,11 @@ int pslr_cgs_pass(pslr_ctx* ctx, int mode, const double* X, int64_t ld, int64_t 
 int pslr_cg(pslr_ctx* ctx, int64_t m, const double* b, double* x, double tol, int64_t maxit, int precond,
             int64_t* iterations, int* converged, double* final_relres, double* history,
             int64_t* history_len, void* stream);
+/* krylov.py:132-174 for any operator pair (same conventions as pslr_gmres_op). */
+int pslr_cg_op(pslr_ctx* ctx, int64_t m, int64_t n, pslr_vec_fn A_fn, void* A_user, pslr_vec_fn M_fn,
+               void* M_user, int precond, const double* b, double* x, double tol, int64_t maxit,
+               int64_t* iterations, int* converged, double* final_relres, double* history, int64_t* history_len,
+               void* stream);
 
 #ifdef __cplusplus
 }

@@ -19,7 +19,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("PSLR_LIB") or os.path.join(_HERE, "lib", "libpslr.so")
 
 PSLR_OK, PSLR_EDIM, PSLR_ENONFINITE, PSLR_ESINGULAR, PSLR_ECUDA, PSLR_EINVAL, PSLR_ENOMEM, \
-    PSLR_ENCCL, PSLR_ENOTSPD = range(9)
+    PSLR_ENCCL, PSLR_ENOTSPD, PSLR_ECALLBACK = range(10)
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(
@@ -32,6 +32,8 @@ c_i64 = ctypes.c_int64
 c_int = ctypes.c_int
 c_dbl = ctypes.c_double
 P = ctypes.c_void_p
+# pslr_vec_fn: int (*)(void* user, const double* x_dev, double* y_dev, void* stream)
+VEC_FN = ctypes.CFUNCTYPE(c_int, P, P, P, P)
 
 
 class Csr(ctypes.Structure):
@@ -113,6 +115,15 @@ EXPORTS = {
     "pslr_cgs_pass": (c_int, P, c_int, P, c_i64, c_i64, c_i64, P, P, P, P),
     "pslr_cg": (c_int, P, c_i64, P, P, c_dbl, c_i64, c_int, ctypes.POINTER(c_i64), ctypes.POINTER(c_int),
                 ctypes.POINTER(c_dbl), P, ctypes.POINTER(c_i64), P),
+    "pslr_workspace_create": (c_int, ctypes.POINTER(P), c_int),
+    "pslr_csr_spmv": (c_int, c_i64, c_i64, P, P, P, P, P, P),
+    "pslr_arnoldi_op": (c_int, P, c_i64, VEC_FN, P, c_i64, P, P, P, ctypes.POINTER(c_i64), P),
+    "pslr_gmres_op": (c_int, P, c_i64, c_i64, VEC_FN, P, VEC_FN, P, c_int, P, P, c_dbl, c_i64, c_i64, c_int,
+                      ctypes.POINTER(c_i64), ctypes.POINTER(c_int), ctypes.POINTER(c_dbl), P,
+                      ctypes.POINTER(c_i64), P),
+    "pslr_cg_op": (c_int, P, c_i64, c_i64, VEC_FN, P, VEC_FN, P, c_int, P, P, c_dbl, c_i64,
+                   ctypes.POINTER(c_i64), ctypes.POINTER(c_int), ctypes.POINTER(c_dbl), P,
+                   ctypes.POINTER(c_i64), P),
 }
 
 fns = {name: _sig(name, sig[0], *sig[1:]) for name, sig in EXPORTS.items()}

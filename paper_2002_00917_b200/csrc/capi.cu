@@ -608,6 +608,28 @@ int pslr_ctx_create(pslr_ctx** out, int device, const pslr_system* sys) {
   return PSLR_OK;
 }
 
+int pslr_workspace_create(pslr_ctx** out, int device) {
+  *out = nullptr;
+  auto* ctx = new pslr_ctx();
+  ctx->device = device;
+  if (cudaSetDevice(device) != cudaSuccess) {
+    delete ctx;
+    return fail(PSLR_ECUDA, "cudaSetDevice failed");
+  }
+  cudaDeviceGetAttribute(&ctx->sm_count, cudaDevAttrMultiProcessorCount, device);
+  if (ctx->sm_count <= 0) ctx->sm_count = 148;
+  void* d = nullptr;
+  if (cudaMalloc(&d, 64) != cudaSuccess) {
+    delete ctx;
+    return fail(PSLR_ECUDA, "cudaMalloc counter");
+  }
+  cudaMemset(d, 0, 64);
+  ctx->allocations.push_back(d);
+  ctx->counter = static_cast<unsigned int*>(d);
+  *out = ctx;
+  return PSLR_OK;
+}
+
 void pslr_ctx_destroy(pslr_ctx* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
@@ -987,6 +1009,8 @@ int pslr_ctx_clone(const pslr_ctx* src, pslr_ctx** out) {
   ctx->K.trace_cap = 0;
   ctx->kv = ctx->kz = ctx->h_dev = nullptr;
   ctx->kv_len = ctx->kz_len = ctx->h_len = 0;
+  ctx->gr = ctx->gw = ctx->gt = nullptr;
+  ctx->g_len = ctx->gw_len = ctx->gt_len = 0;
   ctx->red = nullptr;  // reduction partials are per context (Krylov / dnorm on a clone)
   ctx->red_len = 0;
   ctx->comm = nullptr;  // a clone has no communicator of its own

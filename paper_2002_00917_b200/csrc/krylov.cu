@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <functional>
 #include <vector>
 
 #include "pslr_ops.h"
@@ -61,6 +62,81 @@ static int cgs2(pslr_ctx* ctx, const double* X, int64_t ld, int64_t n, int k, do
   return PSLR_OK;
 }
 
+// y = op(x) on device n-vectors, stream-ordered; returns a PSLR status
+using VecOp = std::function<int(const double*, double*)>;
+
+// A caller-supplied operator (C-ABI callback): PSLR_ECALLBACK when it reports failure
+static VecOp callback_op(pslr_vec_fn fn, void* user, cudaStream_t st) {
+  return [fn, user, st](const double* x, double* y) -> int {
+    if (fn(user, x, y, static_cast<void*>(st)) != 0)
+      return fail(PSLR_ECALLBACK, "operator callback reported an error");
+    return PSLR_OK;
+  };
+}
+
+// Krylov work vectors of length n (the context's own n, or a generic operator's)
+static int krylov_vectors(pslr_ctx* ctx, int64_t n, double** r, double** w, double** t) {
+  if (n <= ctx->n) {
+    *r = ctx->kr;
+    *w = ctx->kw;
+    *t = ctx->kt;
+    return PSLR_OK;
+  }
+  RET(ensure(ctx, &ctx->gr, &ctx->g_len, n));
+  RET(ensure(ctx, &ctx->gw, &ctx->gw_len, n));
+  RET(ensure(ctx, &ctx->gt, &ctx->gt_len, n));
+  *r = ctx->gr;
+  *w = ctx->gw;
+  *t = ctx->gt;
+  return PSLR_OK;
+}
+
+// lowrank.py:39-73: r-step CGS2 Arnoldi on op over `dim` rows (this rank's rows when
+// sharded), V0 in Vc column 0 (unit norm).  V_dev: dim x r_out packed row-major.
+static int arnoldi_core(pslr_ctx* ctx, int64_t dim, int64_t rank, const VecOp& op, const double* v0,
+                        double* V_dev, double* H, int64_t* r_out, cudaStream_t st) {
+  const int64_t ldq = basis_ld(dim);
+  RET(ensure(ctx, &ctx->kv, &ctx->kv_len, ldq * (rank + 1)));
+  double *wr = nullptr, *w = nullptr, *wt = nullptr;
+  RET(krylov_vectors(ctx, dim, &wr, &w, &wt));
+  double* Vc = ctx->kv;  // column-major dim x (rank+1), leading dimension ldq
+  CK(cudaMemsetAsync(Vc, 0, ldq * (rank + 1) * sizeof(double), st));
+  if (dim) CK(cudaMemcpyAsync(Vc, v0, dim * sizeof(double), cudaMemcpyHostToDevice, st));
+  // lowrank.py:52-57 normalises the seeded draw.  A start vector that already has unit
+  // norm (the Python wrapper normalises it with numpy, bit for bit as the reference) is
+  // used as is; anything else is divided by its (allreduced) norm here.
+  double v0n = 0.0;
+  RET(dnorm(ctx, Vc, dim, &v0n, st));
+  if (!(v0n > 0.0) || !std::isfinite(v0n)) return fail(PSLR_EDIM, "Arnoldi start vector has no direction");
+  if (std::fabs(v0n - 1.0) > 1e-14) {
+    CK(cudaMemcpyAsync(ctx->h_dev, &v0n, sizeof(double), cudaMemcpyHostToDevice, st));
+    CKL(launch_div_scalar(Vc, ctx->h_dev, Vc, dim, st));
+  }
+  std::vector<double> Hb((rank + 1) * rank, 0.0);  // row-major (rank+1) x rank
+  std::vector<double> h(rank + 1);
+  int64_t r = rank;
+  for (int64_t j = 0; j < rank; ++j) {
+    RET(op(Vc + j * ldq, w));
+    double hn = 0.0;
+    RET(cgs2(ctx, Vc, ldq, dim, (int)(j + 1), w, h.data(), &hn, st));
+    for (int64_t i = 0; i <= j; ++i) Hb[i * rank + j] = h[i];
+    Hb[(j + 1) * rank + j] = hn;
+    if (hn <= 1e-14) {  // lowrank.py:69-71 (BREAKDOWN_RTOL, start vector has norm 1)
+      r = j + 1;
+      break;
+    }
+    CK(cudaMemcpyAsync(ctx->h_dev, &hn, sizeof(double), cudaMemcpyHostToDevice, st));
+    CKL(launch_div_scalar(w, ctx->h_dev, Vc + (j + 1) * ldq, dim, st));
+  }
+  // V_dev: dim rows x r columns, row-major with leading dimension r (packed)
+  CKL(launch_transpose_basis(Vc, ldq, dim, (int)r, V_dev, st));
+  for (int64_t i = 0; i < r; ++i)
+    for (int64_t j = 0; j < r; ++j) H[i * r + j] = Hb[i * rank + j];
+  CK(cudaStreamSynchronize(st));
+  *r_out = r;
+  return PSLR_OK;
+}
+
 }  // namespace pslr
 
 using namespace pslr;
@@ -91,55 +167,28 @@ int pslr_arnoldi(pslr_ctx* ctx, int64_t m, int64_t rank, const double* v0, doubl
   }
   rank = std::min(rank, qg);
   if (qg == 0 || rank == 0) return PSLR_OK;
-  const int64_t ldq = basis_ld(q);
-  RET(ensure(ctx, &ctx->kv, &ctx->kv_len, ldq * (rank + 1)));
-  double* Vc = ctx->kv;  // column-major q x (rank+1), leading dimension ldq
-  CK(cudaMemsetAsync(Vc, 0, ldq * (rank + 1) * sizeof(double), st));
-  if (q) CK(cudaMemcpyAsync(Vc, v0, q * sizeof(double), cudaMemcpyHostToDevice, st));
-  // lowrank.py:52-57 normalises the seeded draw.  A start vector that already has unit
-  // norm (the Python wrapper normalises it with numpy, bit for bit as the reference) is
-  // used as is; anything else is divided by its (allreduced) norm here.
-  double v0n = 0.0;
-  RET(dnorm(ctx, Vc, q, &v0n, st));
-  if (!(v0n > 0.0) || !std::isfinite(v0n)) return fail(PSLR_EDIM, "Arnoldi start vector has no direction");
-  if (std::fabs(v0n - 1.0) > 1e-14) {
-    CK(cudaMemcpyAsync(ctx->h_dev, &v0n, sizeof(double), cudaMemcpyHostToDevice, st));
-    CKL(launch_div_scalar(Vc, ctx->h_dev, Vc, q, st));
-  }
-  std::vector<double> Hb((rank + 1) * rank, 0.0);  // row-major (rank+1) x rank
-  std::vector<double> h(rank + 1);
-  int64_t r = rank;
-  double* w = ctx->kw;
-  for (int64_t j = 0; j < rank; ++j) {
-    RET(op_apply_err(ctx, m, Vc + j * ldq, w, st));
-    double hn = 0.0;
-    RET(cgs2(ctx, Vc, ldq, q, (int)(j + 1), w, h.data(), &hn, st));
-    for (int64_t i = 0; i <= j; ++i) Hb[i * rank + j] = h[i];
-    Hb[(j + 1) * rank + j] = hn;
-    if (hn <= 1e-14) {  // lowrank.py:69-71 (BREAKDOWN_RTOL, start vector has norm 1)
-      r = j + 1;
-      break;
-    }
-    CK(cudaMemcpyAsync(ctx->h_dev, &hn, sizeof(double), cudaMemcpyHostToDevice, st));
-    CKL(launch_div_scalar(w, ctx->h_dev, Vc + (j + 1) * ldq, q, st));
-  }
-  // V_dev: the rank's q rows x r columns, row-major with leading dimension r (packed)
-  CKL(launch_transpose_basis(Vc, ldq, q, (int)r, V_dev, st));
-  for (int64_t i = 0; i < r; ++i)
-    for (int64_t j = 0; j < r; ++j) H[i * r + j] = Hb[i * rank + j];
-  CK(cudaStreamSynchronize(st));
-  *r_out = r;
-  return PSLR_OK;
+  RET(ensure(ctx, &ctx->h_dev, &ctx->h_len, 8));
+  const VecOp op = [ctx, m, st](const double* x, double* y) { return op_apply_err(ctx, m, x, y, st); };
+  return arnoldi_core(ctx, q, rank, op, v0, V_dev, H, r_out, st);
 }
 
-int pslr_gmres(pslr_ctx* ctx, int64_t m, const double* b, double* x, double tol, int64_t maxit,
-               int64_t restart, int precond, int flexible, int64_t* iterations, int* converged,
-               double* final_relres, double* history, int64_t* history_len, void* stream) {
+int pslr_arnoldi_op(pslr_ctx* ctx, int64_t dim, pslr_vec_fn op_fn, void* user, int64_t rank, const double* v0,
+                    double* V_dev, double* H, int64_t* r_out, void* stream) {
   RET(set_device(ctx));
-  if (ctx->nghost && !ctx->comm)
-    return fail(PSLR_EINVAL, "sharded context: pslr_comm_init + pslr_ctx_set_halo first (or shard.py)");
+  if (!op_fn) return fail(PSLR_EINVAL, "operator callback missing");
+  if (dim < 0 || rank < 0) return fail(PSLR_EDIM, "dim and rank must be >= 0");
   cudaStream_t st = S(stream);
-  const int64_t n = ctx->n;
+  *r_out = 0;
+  rank = std::min(rank, dim);
+  if (dim == 0 || rank == 0) return PSLR_OK;
+  RET(ensure(ctx, &ctx->h_dev, &ctx->h_len, 8));
+  return arnoldi_core(ctx, dim, rank, callback_op(op_fn, user, st), v0, V_dev, H, r_out, st);
+}
+
+// krylov.py:35-129 for any operator pair on device n-vectors (A, M: stream-ordered)
+static int gmres_core(pslr_ctx* ctx, int64_t n, const VecOp& A, const VecOp& apply_M, const double* b, double* x,
+                      double tol, int64_t maxit, int64_t restart, int flexible, int64_t* iterations, int* converged,
+                      double* final_relres, double* history, int64_t* history_len, cudaStream_t st) {
   std::vector<double> hist;
   auto finish = [&](bool conv, int64_t its, double rel) {
     *iterations = its;
@@ -160,17 +209,11 @@ int pslr_gmres(pslr_ctx* ctx, int64_t m, const double* b, double* x, double tol,
   int64_t total = 0;
   bool conv = false;
   double relres = 1.0;
-  double* r = ctx->kr;
-  double* w = ctx->kw;
-  double* t = ctx->kt;
-  auto apply_M = [&](const double* in, double* out) -> int {
-    if (precond) return op_apply(ctx, m, in, out, st);
-    if (out != in) CK(cudaMemcpyAsync(out, in, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
-    return PSLR_OK;
-  };
+  double *r = nullptr, *w = nullptr, *t = nullptr;
+  RET(krylov_vectors(ctx, n, &r, &w, &t));
   while (total < maxit && !conv) {
     // r = b - A x                                            krylov.py:56
-    RET(op_spmv_A_sharded(ctx, x, t, st));
+    RET(A(x, t));
     CKL(launch_sub(b, t, r, n, st));
     double beta = 0.0;
     RET(dnorm(ctx, r, n, &beta, st));
@@ -214,7 +257,7 @@ int pslr_gmres(pslr_ctx* ctx, int64_t m, const double* b, double* x, double tol,
       const int k = (int)(jj + 1);
       double* mv = flexible ? ctx->kz + jj * n : t;  // w = A M v_j   krylov.py:74
       RET(apply_M(Vb + jj * ld, mv));
-      RET(op_spmv_A_sharded(ctx, mv, w, st));
+      RET(A(mv, w));
       double* hs = ctx->h_dev + (jj & 1) * SL;
       CKL(launch_multidot(ctx, Vb, ld, k, w, n, hs, st));           // h1 = V^T w
       RET(comm_allreduce(ctx, hs, k, st));                           // (sharded: all ranks' rows)
@@ -290,7 +333,7 @@ int pslr_gmres(pslr_ctx* ctx, int64_t m, const double* b, double* x, double tol,
         CKL(launch_add_inplace(x, t, n, st));
       }
     }
-    RET(op_spmv_A_sharded(ctx, x, t, st));
+    RET(A(x, t));
     CKL(launch_sub(b, t, r, n, st));
     double rn = 0.0;
     RET(dnorm(ctx, r, n, &rn, st));
@@ -311,6 +354,58 @@ int pslr_gmres(pslr_ctx* ctx, int64_t m, const double* b, double* x, double tol,
   return PSLR_OK;
 }
 
+int pslr_gmres(pslr_ctx* ctx, int64_t m, const double* b, double* x, double tol, int64_t maxit,
+               int64_t restart, int precond, int flexible, int64_t* iterations, int* converged,
+               double* final_relres, double* history, int64_t* history_len, void* stream) {
+  RET(set_device(ctx));
+  if (ctx->nghost && !ctx->comm)
+    return fail(PSLR_EINVAL, "sharded context: pslr_comm_init + pslr_ctx_set_halo first (or shard.py)");
+  cudaStream_t st = S(stream);
+  const int64_t n = ctx->n;
+  const VecOp A = [ctx, st](const double* in, double* out) { return op_spmv_A_sharded(ctx, in, out, st); };
+  const VecOp M = [ctx, m, precond, n, st](const double* in, double* out) -> int {
+    if (precond) return op_apply(ctx, m, in, out, st);
+    if (out != in) CK(cudaMemcpyAsync(out, in, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    return PSLR_OK;
+  };
+  return gmres_core(ctx, n, A, M, b, x, tol, maxit, restart, flexible, iterations, converged, final_relres,
+                    history, history_len, st);
+}
+
+// A / M: NULL -> the context's reordered matrix / its PSLR apply (precond != 0) or the
+// identity (precond == 0); otherwise the callback (any operator on device n-vectors)
+static int ctx_ops(pslr_ctx* ctx, int64_t m, int64_t n, pslr_vec_fn A_fn, void* A_user, pslr_vec_fn M_fn,
+                   void* M_user, int precond, cudaStream_t st, VecOp* A, VecOp* M) {
+  if (!A_fn && n != ctx->n) return fail(PSLR_EDIM, "the context's matrix has another dimension");
+  if (!M_fn && precond && n != ctx->n) return fail(PSLR_EDIM, "the context's preconditioner has another dimension");
+  if (A_fn)
+    *A = callback_op(A_fn, A_user, st);
+  else
+    *A = [ctx, st](const double* in, double* out) { return op_spmv_A_sharded(ctx, in, out, st); };
+  if (M_fn)
+    *M = callback_op(M_fn, M_user, st);
+  else
+    *M = [ctx, m, precond, n, st](const double* in, double* out) -> int {
+      if (precond) return op_apply(ctx, m, in, out, st);
+      if (out != in) CK(cudaMemcpyAsync(out, in, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      return PSLR_OK;
+    };
+  return PSLR_OK;
+}
+
+int pslr_gmres_op(pslr_ctx* ctx, int64_t m, int64_t n, pslr_vec_fn A_fn, void* A_user, pslr_vec_fn M_fn,
+                  void* M_user, int precond, const double* b, double* x, double tol, int64_t maxit,
+                  int64_t restart, int flexible, int64_t* iterations, int* converged, double* final_relres,
+                  double* history, int64_t* history_len, void* stream) {
+  RET(set_device(ctx));
+  if (n < 0) return fail(PSLR_EDIM, "negative dimension");
+  cudaStream_t st = S(stream);
+  VecOp A, M;
+  RET(ctx_ops(ctx, m, n, A_fn, A_user, M_fn, M_user, precond, st, &A, &M));
+  return gmres_core(ctx, n, A, M, b, x, tol, maxit, restart, flexible, iterations, converged, final_relres,
+                    history, history_len, st);
+}
+
 int pslr_cgs_pass(pslr_ctx* ctx, int mode, const double* X, int64_t ld, int64_t n, int64_t k, double* w,
                   const double* h0, double* out, void* stream) {
   RET(set_device(ctx));
@@ -327,15 +422,10 @@ int pslr_cgs_pass(pslr_ctx* ctx, int mode, const double* X, int64_t ld, int64_t 
 
 // krylov.py:132-174.  Device vectors; the scalar recurrence (alpha, beta, the SPD check,
 // the residual test) is host code with the reference's exact control flow.
-int pslr_cg(pslr_ctx* ctx, int64_t m, const double* b, double* x, double tol, int64_t maxit, int precond,
-            int64_t* iterations, int* converged, double* final_relres, double* history,
-            int64_t* history_len, void* stream) {
-  RET(set_device(ctx));
-  if (ctx->nghost && !ctx->comm)
-    return fail(PSLR_EINVAL, "sharded context: pslr_comm_init + pslr_ctx_set_halo first (or shard.py)");
+static int cg_core(pslr_ctx* ctx, int64_t n, const VecOp& A, const VecOp& apply_M, const double* b, double* x,
+                   double tol, int64_t maxit, int64_t* iterations, int* converged, double* final_relres,
+                   double* history, int64_t* history_len, cudaStream_t st) {
   if (maxit < 0) return fail(PSLR_EDIM, "maxit must be >= 0");
-  cudaStream_t st = S(stream);
-  const int64_t n = ctx->n;
   std::vector<double> hist;
   auto finish = [&](bool conv, int64_t its, double rel) {
     *iterations = its;
@@ -357,15 +447,9 @@ int pslr_cg(pslr_ctx* ctx, int64_t m, const double* b, double* x, double tol, in
   RET(ensure(ctx, &ctx->kv, &ctx->kv_len, n));
   RET(ensure(ctx, &ctx->red, &ctx->red_len, (int64_t)dot_grid(n, ctx->sm_count) + 8));
   RET(ensure(ctx, &ctx->h_dev, &ctx->h_len, 8));
-  double* r = ctx->kr;
-  double* z = ctx->kt;
-  double* Ap = ctx->kw;
+  double *r = nullptr, *z = nullptr, *Ap = nullptr;
+  RET(krylov_vectors(ctx, n, &r, &Ap, &z));
   double* p = ctx->kv;
-  auto apply_M = [&](const double* in, double* out) -> int {
-    if (precond) return op_apply(ctx, m, in, out, st);
-    CK(cudaMemcpyAsync(out, in, n * sizeof(double), cudaMemcpyDeviceToDevice, st));
-    return PSLR_OK;
-  };
   auto dot = [&](const double* u, const double* v, double* out) -> int {
     CKL(launch_multidot(ctx, u, n, 1, v, n, ctx->h_dev, st));
     RET(comm_allreduce(ctx, ctx->h_dev, 1, st));
@@ -383,7 +467,7 @@ int pslr_cg(pslr_ctx* ctx, int64_t m, const double* b, double* x, double tol, in
   double relres = 1.0;
   int64_t it = 0;
   for (it = 1; it <= maxit; ++it) {
-    RET(op_spmv_A_sharded(ctx, p, Ap, st));  // krylov.py:152
+    RET(A(p, Ap));  // krylov.py:152
     double pAp = 0.0;
     RET(dot(p, Ap, &pAp));
     if (pAp <= 0.0) {  // krylov.py:153-154
@@ -413,6 +497,44 @@ int pslr_cg(pslr_ctx* ctx, int64_t m, const double* b, double* x, double tol, in
     while ((int64_t)hist.size() < maxit + 1) hist.push_back(relres);
   finish(conv, its, relres);
   CK(cudaStreamSynchronize(st));
+  return PSLR_OK;
+}
+
+int pslr_cg(pslr_ctx* ctx, int64_t m, const double* b, double* x, double tol, int64_t maxit, int precond,
+            int64_t* iterations, int* converged, double* final_relres, double* history,
+            int64_t* history_len, void* stream) {
+  RET(set_device(ctx));
+  if (ctx->nghost && !ctx->comm)
+    return fail(PSLR_EINVAL, "sharded context: pslr_comm_init + pslr_ctx_set_halo first (or shard.py)");
+  cudaStream_t st = S(stream);
+  VecOp A, M;
+  RET(ctx_ops(ctx, m, ctx->n, nullptr, nullptr, nullptr, nullptr, precond, st, &A, &M));
+  return cg_core(ctx, ctx->n, A, M, b, x, tol, maxit, iterations, converged, final_relres, history, history_len,
+                 st);
+}
+
+int pslr_cg_op(pslr_ctx* ctx, int64_t m, int64_t n, pslr_vec_fn A_fn, void* A_user, pslr_vec_fn M_fn,
+               void* M_user, int precond, const double* b, double* x, double tol, int64_t maxit,
+               int64_t* iterations, int* converged, double* final_relres, double* history, int64_t* history_len,
+               void* stream) {
+  RET(set_device(ctx));
+  if (n < 0) return fail(PSLR_EDIM, "negative dimension");
+  cudaStream_t st = S(stream);
+  VecOp A, M;
+  RET(ctx_ops(ctx, m, n, A_fn, A_user, M_fn, M_user, precond, st, &A, &M));
+  return cg_core(ctx, n, A, M, b, x, tol, maxit, iterations, converged, final_relres, history, history_len, st);
+}
+
+int pslr_csr_spmv(int64_t nrows, int64_t ncols, const int32_t* indptr, const int32_t* indices, const double* data,
+                  const double* x, double* y, void* stream) {
+  if (nrows < 0 || ncols < 0 || nrows > 0x7fffffffLL) return fail(PSLR_EDIM, "bad CSR dimensions");
+  DevCsr M;
+  M.nrows = (int32_t)nrows;
+  M.ncols = (int32_t)ncols;
+  M.ptr = indptr;
+  M.col = indices;
+  M.val = data;
+  CKL(launch_spmv(M, x, y, S(stream)));
   return PSLR_OK;
 }
 

@@ -196,6 +196,8 @@ struct pslr_ctx {
   double* kw = nullptr;          // n
   double* kt = nullptr;          // n
   double* kr = nullptr;          // n
+  double *gr = nullptr, *gw = nullptr, *gt = nullptr;  // Krylov vectors of a generic operator
+  int64_t g_len = 0, gw_len = 0, gt_len = 0;            //   longer than n (pslr_*_op)
   double* io_b = nullptr;        // n device staging for host apply
   double* io_z = nullptr;        // n
   // multi-GPU (comm.cu): NCCL communicator and halo plan of a rank-local context

@@ -107,7 +107,6 @@ class DeviceContext:
 
     def set_correction(self, V, G):
         """Upload a LowRankCorrection (V host numpy or device tensor, G host)."""
-        self._bound = None
         t = torch_mod()
         r = 0 if V is None else int(V.shape[1])
         G = np.ascontiguousarray(G if G is not None else np.zeros((0, 0)), dtype=np.float64)
@@ -115,10 +114,12 @@ class DeviceContext:
             V = V.contiguous()
             _lib.check(_lib.fns["pslr_ctx_set_correction_device"](self.handle, r, V.data_ptr(),
                                                                   G.ctypes.data))
+            self._bound = None
         else:
             Vh = np.ascontiguousarray(V if V is not None else np.zeros((self.q, 0)), dtype=np.float64)
             _lib.check(_lib.fns["pslr_ctx_set_correction"](self.handle, r, Vh.ctypes.data,
                                                            G.ctypes.data))
+        self._bound = None  # the state no longer belongs to a LowRankCorrection object
 
     def vec_op(self, name, x, n_in, n_out, *scalars):
         """Run a vector->vector C-ABI operator on numpy (copied) or CUDA-tensor (zero-copy) input."""

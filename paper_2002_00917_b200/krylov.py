@@ -1,12 +1,17 @@
 """Right-preconditioned restarted GMRES / FGMRES and preconditioned CG (mirrors pslr/krylov.py).
 
-When the operator pair is a PSLR preconditioner's own (A = P.matvec,
-M = P.apply — the pairing cli._solve_with uses, cli.py:131-143 — or their
-original-space versions), the whole solve runs on the device: pslr_gmres
-drives the apply, the A-SpMV and the CGS2 kernels with the reference's exact
-control flow (krylov.py:55-127), only the (cycle+1)-sized Givens/least-squares
-bookkeeping is scalar host code; pslr_cg does the same for CG (krylov.py:132-174).  Arbitrary Python callables keep the
-reference's generic contract.
+Every solve runs on the device with the reference's exact control flow
+(krylov.py:35-174): the Krylov basis, the CGS2 projections and norms are libpslr
+kernels, only the (cycle+1)-sized Givens / least-squares scalars are host code.
+
+  * A PSLR preconditioner's own operator pair (A = P.matvec, M = P.apply — the pairing
+    cli._solve_with uses, cli.py:131-143 — or their original-space versions) runs
+    entirely inside libpslr (pslr_gmres / pslr_cg);
+  * any other apply_A / apply_M (the reference accepts arbitrary callables) reaches the
+    same device loop as an operator callback (pslr_gmres_op / pslr_cg_op,
+    operators.py): P's operators and scipy sparse matrices stay on the device, other
+    callables are called on host vectors.
+There is no host Krylov loop and no CPU fallback: without a CUDA device every solve raises.
 """
 
 from __future__ import annotations
@@ -60,7 +65,7 @@ def gmres(apply_A, apply_M, b, tol: float = 1e-8, maxit: int = 500, restart: int
         x, rep = gmres_device(P, np.asarray(b, dtype=np.float64)[perm.inverse], tol, maxit,
                               restart, flexible)
         return x[perm.forward], rep
-    return _gmres_generic(apply_A, apply_M, b, tol, maxit, restart, flexible)
+    return _solve_ops("gmres", apply_A, apply_M, b, tol, maxit, restart, flexible)
 
 
 def fgmres(apply_A, apply_M, b, tol: float = 1e-8, maxit: int = 500, restart: int = 0):
@@ -110,7 +115,7 @@ def cg(apply_A, apply_M, b, tol: float = 1e-8, maxit: int = 500):
         perm = P.system.perm
         x, rep = cg_device(P, np.asarray(b, dtype=np.float64)[perm.inverse], tol, maxit)
         return x[perm.forward], rep
-    return _cg_generic(apply_A, apply_M, b, tol, maxit)
+    return _solve_ops("cg", apply_A, apply_M, b, tol, maxit)
 
 
 def cg_device(P, b, tol: float = 1e-8, maxit: int = 500, precond: bool = True):
@@ -142,133 +147,60 @@ def cg_device(P, b, tol: float = 1e-8, maxit: int = 500, precond: bool = True):
     return (xd if is_tensor else xd.cpu().numpy()), rep
 
 
-def _cg_generic(apply_A, apply_M, b, tol, maxit):
-    """The reference recurrence for arbitrary callables (krylov.py:132-174)."""
-    if apply_M is None:
-        apply_M = _identity
-    b = np.asarray(b, dtype=np.float64)
-    n = b.shape[0]
+def _solve_ops(kind, apply_A, apply_M, b, tol, maxit, restart=0, flexible=False):
+    """The device loop for any operator pair (pslr_gmres_op / pslr_cg_op).  The context is
+    the preconditioner's when M is P.apply (its apply runs inside libpslr), else a
+    device workspace; A is a device operator callback (operators.py)."""
+    from . import operators as ops_
+    from .device import require_cuda
+    t = require_cuda()
+    is_tensor = hasattr(b, "data_ptr")
+    P = _bound(apply_M, "apply")
+    if P is not None:
+        dev, handle, m, precond = P.device.dev, P.device.handle, int(P.series_degree), 1
+        P.device.ensure_correction(P.correction)
+        M_op = None
+    else:
+        owner = getattr(apply_M, "__self__", None) or getattr(apply_A, "__self__", None)
+        odev = getattr(owner, "device", None)
+        dev = odev.dev if hasattr(odev, "dev") else (b.device if is_tensor else
+                                                     t.device("cuda", t.cuda.current_device()))
+        handle, m, precond = ops_.workspace(dev.index if dev.index is not None else 0).handle, 0, 0
+        M_op = None
+    if is_tensor:
+        bd = b.to(device=dev, dtype=t.float64).contiguous()
+    else:
+        bn = np.asarray(b, dtype=np.float64)
+        if bn.ndim != 1:
+            raise ValueError("right-hand side must be a vector")
+        bd = t.from_numpy(np.ascontiguousarray(bn)).to(dev)
+    n = int(bd.shape[0])
+    if P is not None and n != P.system.n:
+        raise ValueError(f"vector has length {n}, system is {P.system.n}-dimensional")
+    A_op = ops_.make_operator(apply_A, n, dev)
+    if P is None and apply_M is not None:
+        M_op = ops_.make_operator(apply_M, n, dev)
+    xd = t.empty(n, dtype=t.float64, device=dev)
+    hist = np.zeros(max(int(maxit), 0) + 1)
+    its, conv, rel, hlen = ctypes.c_int64(), ctypes.c_int(), ctypes.c_double(), ctypes.c_int64()
+    st = t.cuda.current_stream(dev).cuda_stream
+    Mf = M_op.cfunc if M_op is not None else ops_.null_fn()
     t0 = time.perf_counter()
-    bnorm = np.linalg.norm(b)
-    if bnorm == 0.0:
-        return np.zeros(n), SolveReport(True, 0, 0.0, [1.0], time.perf_counter() - t0)
-    x = np.zeros(n)
-    r = b.copy()
-    z = np.asarray(apply_M(r), dtype=np.float64)
-    p = z.copy()
-    rz = r @ z
-    history = [1.0]
-    converged = False
-    relres = 1.0
-    it = 0
-    for it in range(1, maxit + 1):
-        Ap = np.asarray(apply_A(p), dtype=np.float64)
-        pAp = p @ Ap
-        if pAp <= 0.0:
-            raise NotSpdError("matrix not SPD: non-positive curvature encountered")
-        alpha = rz / pAp
-        x = x + alpha * p
-        r = r - alpha * Ap
-        relres = np.linalg.norm(r) / bnorm
-        history.append(relres)
-        if relres <= tol:
-            converged = True
-            break
-        z = np.asarray(apply_M(r), dtype=np.float64)
-        rz_new = r @ z
-        p = z + (rz_new / rz) * p
-        rz = rz_new
-    iterations = it if converged else maxit
-    if not converged:
-        history.extend([relres] * (maxit + 1 - len(history)))
-    return x, SolveReport(converged, iterations, relres, history, time.perf_counter() - t0)
-
-
-def _gmres_generic(apply_A, apply_M, b, tol, maxit, restart, flexible):
-    """The reference recurrence for arbitrary callables (krylov.py:35-129)."""
-    if apply_M is None:
-        apply_M = _identity
-    b = np.asarray(b, dtype=np.float64)
-    n = b.shape[0]
-    t0 = time.perf_counter()
-    bnorm = np.linalg.norm(b)
-    if bnorm == 0.0:
-        return np.zeros(n), SolveReport(True, 0, 0.0, [1.0], time.perf_counter() - t0)
-    x = np.zeros(n)
-    history = [1.0]
-    total = 0
-    converged = False
-    relres = 1.0
-    while total < maxit and not converged:
-        r = b - np.asarray(apply_A(x))
-        beta = np.linalg.norm(r)
-        relres = beta / bnorm
-        if relres <= tol:
-            converged = True
-            break
-        cycle = maxit - total if restart <= 0 else min(restart, maxit - total)
-        V = np.zeros((n, cycle + 1))
-        Z = np.zeros((n, cycle)) if flexible else None
-        Hcol = np.zeros((cycle + 1, cycle))
-        cs = np.zeros(cycle)
-        sn = np.zeros(cycle)
-        g = np.zeros(cycle + 1)
-        g[0] = beta
-        V[:, 0] = r / beta
-        j = 0
-        breakdown = False
-        while j < cycle:
-            mv = np.asarray(apply_M(V[:, j]))
-            if flexible:
-                Z[:, j] = mv
-            w = np.asarray(apply_A(mv), dtype=np.float64)
-            h = V[:, :j + 1].T @ w
-            w = w - V[:, :j + 1] @ h
-            h2 = V[:, :j + 1].T @ w
-            w = w - V[:, :j + 1] @ h2
-            h = h + h2
-            hnext = np.linalg.norm(w)
-            if not (np.all(np.isfinite(h)) and np.isfinite(hnext)):
-                raise ArithmeticError("GMRES diverged: non-finite values in the recurrence")
-            Hcol[:j + 1, j] = h
-            Hcol[j + 1, j] = hnext
-            for i in range(j):
-                tmp = cs[i] * Hcol[i, j] + sn[i] * Hcol[i + 1, j]
-                Hcol[i + 1, j] = -sn[i] * Hcol[i, j] + cs[i] * Hcol[i + 1, j]
-                Hcol[i, j] = tmp
-            denom = np.hypot(Hcol[j, j], hnext)
-            if denom == 0.0:
-                cs[j], sn[j] = 1.0, 0.0
-            else:
-                cs[j], sn[j] = Hcol[j, j] / denom, hnext / denom
-            Hcol[j, j] = denom
-            g[j + 1] = -sn[j] * g[j]
-            g[j] = cs[j] * g[j]
-            total += 1
-            j += 1
-            est = abs(g[j]) / bnorm
-            history.append(est)
-            if hnext <= 1e-14 * beta:
-                breakdown = True
-                break
-            if est <= tol:
-                break
-            if j < cycle:
-                V[:, j] = w / hnext
-        if j > 0:
-            y = np.zeros(j)
-            for i in range(j - 1, -1, -1):
-                y[i] = (g[i] - Hcol[i, i + 1:j] @ y[i + 1:j]) / Hcol[i, i]
-            x = x + (Z[:, :j] @ y if flexible else np.asarray(apply_M(V[:, :j] @ y)))
-        relres = np.linalg.norm(b - np.asarray(apply_A(x))) / bnorm
-        history[-1] = relres
-        if relres <= tol:
-            converged = True
-        elif breakdown:
-            break
-    if not converged and total < maxit and not np.isfinite(relres):
-        raise ArithmeticError("GMRES diverged: non-finite residual")
-    iterations = total if converged else maxit
-    if not converged:
-        history.extend([relres] * (maxit + 1 - len(history)))
-    return x, SolveReport(converged, iterations, relres, history, time.perf_counter() - t0)
+    with t.cuda.device(dev):
+        if kind == "gmres":
+            rc = _lib.fns["pslr_gmres_op"](handle, m, n, A_op.cfunc, None, Mf, None, precond, bd.data_ptr(),
+                                           xd.data_ptr(), float(tol), int(maxit), int(restart),
+                                           1 if flexible else 0, ctypes.byref(its), ctypes.byref(conv),
+                                           ctypes.byref(rel), hist.ctypes.data, ctypes.byref(hlen), st)
+        else:
+            rc = _lib.fns["pslr_cg_op"](handle, m, n, A_op.cfunc, None, Mf, None, precond, bd.data_ptr(),
+                                        xd.data_ptr(), float(tol), int(maxit), ctypes.byref(its),
+                                        ctypes.byref(conv), ctypes.byref(rel), hist.ctypes.data,
+                                        ctypes.byref(hlen), st)
+    A_op.check(rc)
+    if M_op is not None:
+        M_op.check(rc)
+    _lib.check(rc)
+    elapsed = time.perf_counter() - t0
+    rep = SolveReport(bool(conv.value), int(its.value), float(rel.value), hist[:hlen.value].tolist(), elapsed)
+    return (xd if is_tensor else xd.cpu().numpy()), rep

@@ -1,7 +1,8 @@
 """CG (krylov.py:132-174): the oracle against golden vectors of the
-real reference (tests/golden/make_golden_cg.py), the package's generic host path against
-the reference's own CG tests (pkg/tests/test_krylov.py:105-140), and — on a GPU — the
-device CG (pslr_cg through the C-ABI) against the golden iteration counts.
+real reference (tests/golden/make_golden_cg.py) and — on a GPU — the device CG: on
+generic operators (pslr_cg_op, operator callbacks) against the reference's own CG tests
+(pkg/tests/test_krylov.py:105-140), and on the PSLR operators (pslr_cg through the C-ABI)
+against the golden iteration counts.
 
 Bars: oracle iterations exact and histories to 1e-9 relative (rank-0 PSLR applies are
 scipy-only, so the oracle reproduces the reference's arithmetic); device iterations
@@ -51,23 +52,31 @@ def test_oracle_cg_failure_contract():
     np.testing.assert_allclose(rep.history, ref["history"], rtol=1e-12)
 
 
-# ---------------------------------------------------------------- CPU: the generic host path
+# ---------------------------------------------------------------- GPU: generic operators
 def _dense_spd(n, seed):
     rng = np.random.default_rng(seed)
     Q = rng.standard_normal((n, n))
     return Q @ Q.T + n * np.eye(n)
 
 
-def test_generic_cg_matches_oracle_spd():
-    from paper_2002_00917_b200.krylov import _cg_generic
+@pytest.mark.gpu
+@pytest.mark.skipif(not have_cuda(), reason="needs a CUDA device")
+@pytest.mark.parametrize("as_matrix", [False, True])
+def test_generic_cg_matches_oracle_spd(as_matrix):
+    """The device CG on a generic operator (a host callable, or the scipy matrix itself:
+    libpslr's CSR SpMV) against the oracle's restatement of the reference loop."""
+    import paper_2002_00917_b200 as pg
     A = sp.csr_matrix(_dense_spd(60, 10))
     b = A @ np.random.default_rng(11).standard_normal(60)
-    x, rep = _cg_generic(lambda v: A @ v, None, b, 1e-10, 500)
+    x, rep = pg.cg(A if as_matrix else (lambda v: A @ v), None, b, tol=1e-10)
     xo, repo = O.cg(lambda v: A @ v, None, b, tol=1e-10)
     assert rep.converged and rep.iterations == repo.iterations
-    np.testing.assert_array_equal(x, xo)
+    np.testing.assert_allclose(x, xo, rtol=0, atol=1e-10 * np.abs(xo).max())
+    np.testing.assert_allclose(rep.history, repo.history, rtol=1e-8)
 
 
+@pytest.mark.gpu
+@pytest.mark.skipif(not have_cuda(), reason="needs a CUDA device")
 def test_generic_cg_reference_contracts():
     """pkg/tests/test_krylov.py:115-140: Jacobi helps, indefinite raises, failure
     contract, zero right-hand side."""
