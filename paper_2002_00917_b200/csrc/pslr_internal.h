@@ -37,7 +37,10 @@ struct alignas(16) ChunkDesc {
 };
 
 // max rows per chunk: bounds the per-stage right-hand-side buffer
-constexpr int kChunkRows = 1024;
+#ifndef PSLR_CHUNK_ROWS
+#define PSLR_CHUNK_ROWS 1024
+#endif
+constexpr int kChunkRows = PSLR_CHUNK_ROWS;
 // bytes of the step kernel's shared-memory control block (mbarriers, descriptor queue)
 constexpr int kCtlBytes = 512;
 

@@ -52,6 +52,12 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity);
+// spin on test_wait (no hardware suspend): timing experiment PSLR_DBG bit 2048
+__device__ __forceinline__ void mbar_spin(uint64_t* bar, uint32_t parity) {
+  while (!mbar_test(bar, parity)) {
+  }
+}
 __device__ __forceinline__ bool mbar_test(uint64_t* bar, uint32_t parity) {
   uint32_t ok;
   asm volatile(
@@ -211,13 +217,14 @@ static_assert(sizeof(Ctl) <= kCtlBytes, "the control block must fit the header o
 // position-ordered rhs array) into the stage's rhs buffer, both completing on full[st].
 // A slice can only be copied once its phase's rhs is final (rhs_ready, signalled by the
 // consumers at the phase start), so slices of chunks staged ahead of their phase are
-// deferred.  The thread polls (test_wait + a short sleep) in one place only: before
-// reusing a stage it issues every deferred slice whose phase became ready (the stage's
-// previous occupant needs its slice before the consumers can free it, and the consumers'
-// look-ahead needs the next chunk's), then checks the stage.  Descriptors come from a
-// cp.async queue twelve chunks ahead, so no issue waits on a global load.  (Measured on
-// cfg5: this loop streams ~25% faster than a loop that also runs L2 prefetches and
-// re-tests every condition each iteration; L2 prefetching did not pay.)
+// deferred and issued as soon as the phase is seen ready.
+//
+// The stream's rate is bounded by this ONE thread's dependent-instruction latency per
+// chunk (measured: ~800 cycles per chunk for a loop that re-derived every quantity,
+// i.e. ~55 GB/s per SM at 22 KB chunks): the steady-state path is a handful of
+// instructions — poll the stage, read the next descriptor (prefetched into shared
+// memory by cp.async twelve chunks ahead and into registers one chunk ahead), two
+// expect_tx + bulk-copy pairs.  Phase bookkeeping only runs at phase boundaries.
 __device__ void producer(const Streams& S, Ctl* ctl, uint8_t* stages, double* rhsbuf, int nst,
                          int stage_bytes, int rhs_stride, int nv, long long* g_dbg_out, int dbg,
                          long long* g_tma) {
@@ -225,13 +232,8 @@ __device__ void producer(const Streams& S, Ctl* ctl, uint8_t* stages, double* rh
   const int np = S.nphase;
   const int total = S.begin[np];
   if (total == 0) return;
-  // data cursor
-  int d_k = 0;
-  while (S.begin[d_k + 1] == 0) ++d_k;
-  int d_end = S.begin[d_k + 1];
-  const uint8_t* d_data = S.data[d_k];
   // descriptor queue: chunk u's 16-B descriptor is copied into ctl->dq[u & 15]
-  int q_u = 0, q_k = d_k, q_base = 0, q_end = d_end;
+  int q_u = 0, q_k = 0, q_base = 0, q_end = S.begin[1];
   auto q_issue = [&]() {
     if (q_u < total) {
       while (q_u >= q_end) {
@@ -247,67 +249,94 @@ __device__ void producer(const Streams& S, Ctl* ctl, uint8_t* stages, double* rh
     ++q_u;
   };
   for (int i = 0; i < 12; ++i) q_issue();
-  // rhs cursor: chunks < r_u have their slice issued
-  int r_u = 0, r_k = d_k, r_end = d_end;
-  uint32_t ready = 0;  // phases whose rhs is final
-  auto r_ready = [&]() -> bool {  // is the phase of chunk r_u ready?
-    while (r_u >= r_end) {
-      ++r_k;
-      r_end = S.begin[r_k + 1];
-    }
-    if (ready & (1u << r_k)) return true;
-    if (!mbar_test(&ctl->rhs_ready[r_k], 0)) return false;
-    ready |= 1u << r_k;
-    fence_proxy_async();  // the consumers' generic-proxy rhs writes, before TMA reads them
-    return true;
-  };
-  auto r_issue = [&]() {
-    const int st = r_u % nst;
-    const int2 rr = ctl->rrec[st];
+  asm volatile("cp.async.wait_group 11;" ::: "memory");
+  uint4 dv = ctl->dq[0];  // chunk u's descriptor: off16, bytes, rpos, rbytes
+  // data cursor: phase k of chunk u, its end, data and rhs arrays
+  int k = 0;
+  while (S.begin[k + 1] == 0) ++k;
+  int k_end = S.begin[k + 1];
+  const uint8_t* data = S.data[k];
+  const double* rhs = S.rhs[k];
+  bool k_ready = false;
+  // deferred slices: chunks [r_u, r_hi) of phase r_k (always the current or the next phase)
+  int r_u = 0, r_hi = 0, r_k = k;
+  auto rhs_copy = [&](int st, const double* src, uint32_t rpos, uint32_t rbytes) {
     if (dbg & 64) {
       mbar_arrive(&ctl->full[st]);
     } else {
-      mbar_expect_tx(&ctl->full[st], (uint32_t)(rr.y * nv));  // nv interleaved right-hand sides
-      const double* src = (dbg & 1024) ? reinterpret_cast<const double*>(S.data[r_k]) : S.rhs[r_k];
-      bulk_load(rhsbuf + (size_t)st * rhs_stride, src + (size_t)rr.x * nv, (uint32_t)(rr.y * nv), &ctl->full[st]);
+      mbar_expect_tx(&ctl->full[st], rbytes * nv);  // nv interleaved right-hand sides
+      bulk_load(rhsbuf + (size_t)st * rhs_stride, src + (size_t)rpos * nv, rbytes * nv, &ctl->full[st]);
     }
-    ++r_u;
   };
-  long long c_poll = 0;
+  auto phase_test = [&](int kk, bool block) -> bool {
+    if (block) {
+      mbar_wait(&ctl->rhs_ready[kk], 0);
+    } else if (!mbar_test(&ctl->rhs_ready[kk], 0)) {
+      return false;
+    }
+    fence_proxy_async();  // the consumers' generic-proxy rhs writes, before TMA reads them
+    return true;
+  };
+  // issue the deferred slices once their phase is ready (block: wait for it)
+  auto flush = [&](bool block) {
+    if (r_u == r_hi) return;
+    if (!phase_test(r_k, block)) return;
+    for (; r_u < r_hi; ++r_u) {
+      const int st = r_u % nst;
+      const int2 rr = ctl->rrec[st];
+      rhs_copy(st, S.rhs[r_k], (uint32_t)rr.x, (uint32_t)rr.y);
+    }
+    if (r_k == k) k_ready = true;
+  };
+  int st = 0;
+  uint32_t par = 1;  // parity of the empty-barrier phase a reused stage waits for
   const long long c_all = clock64();
   for (int u = 0; u < total; ++u) {
-    const int st = u % nst;
+    if (u == k_end) {  // next phase (its slices are deferred until it is ready)
+      flush(true);     // the previous phase's deferred slices (consumers need them first)
+      do {
+        ++k;
+      } while (S.begin[k + 1] == S.begin[k]);
+      k_end = S.begin[k + 1];
+      data = S.data[k];
+      rhs = S.rhs[k];
+      k_ready = false;
+      r_k = k;
+      r_u = r_hi = u;
+    }
     if (u >= nst) {
-      const long long c0 = clock64();
-      const uint32_t par = (uint32_t)(((u / nst) - 1) & 1);
-      for (;;) {
-        while (r_u < u && r_ready()) r_issue();
-        if (mbar_test(&ctl->empty[st], par)) break;
+      // the stage's previous occupant (chunk u - nst) must be consumable: its slice issued
+      if (r_u < r_hi && r_u <= u - nst) flush(true);
+      while (!mbar_test(&ctl->empty[st], par)) {
+        flush(false);
         __nanosleep(20);
       }
-      c_poll += clock64() - c0;
     }
-    while (u >= d_end) {
-      ++d_k;
-      d_end = S.begin[d_k + 1];
-      d_data = S.data[d_k];
-    }
-    asm volatile("cp.async.wait_group 11;" ::: "memory");
-    const uint4 dv = ctl->dq[u & 15];  // off16, bytes, rpos, rbytes (ChunkDesc)
-    q_issue();
     mbar_expect_tx(&ctl->full[st], dv.y);
-    bulk_load(stages + (size_t)st * stage_bytes, d_data + (size_t)dv.x * 16, dv.y, &ctl->full[st]);
-    if (PSLR_TRACE_BUILD && g_tma && u < 8192) g_tma[2 * u] = clock64();
-    ctl->rrec[st] = make_int2((int32_t)dv.z, (int)dv.w);
-    if (r_u == u && r_ready()) r_issue();
+    bulk_load(stages + (size_t)st * stage_bytes, data + (size_t)dv.x * 16, dv.y, &ctl->full[st]);
+    if (PSLR_TRACE_BUILD && g_tma && u < 8192) {
+      g_tma[2 * u] = clock64();
+      g_tma[2 * 8192 + u] = dv.y;
+    }
+    if (!k_ready && r_u == r_hi && phase_test(k, false)) k_ready = true;  // cheap once known
+    if (k_ready) {
+      rhs_copy(st, rhs, dv.z, dv.w);
+      r_u = r_hi = u + 1;
+    } else {
+      ctl->rrec[st] = make_int2((int32_t)dv.z, (int)dv.w);
+      r_hi = u + 1;
+    }
+    // next descriptor (its cp.async landed long ago) and the one twelve chunks ahead
+    q_issue();
+    asm volatile("cp.async.wait_group 11;" ::: "memory");
+    dv = ctl->dq[(u + 1) & 15];
+    if (++st == nst) {
+      st = 0;
+      par ^= 1u;
+    }
   }
-  for (;;) {  // the slices still deferred at the end (the last phase's first chunks)
-    while (r_u < total && r_ready()) r_issue();
-    if (r_u == total) break;
-    __nanosleep(20);
-  }
+  flush(true);  // the last phase's deferred slices
   if (g_dbg_out) {
-    atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg_out + 5), (unsigned long long)c_poll);
     atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg_out + 7), (unsigned long long)(clock64() - c_all));
     atomicAdd(reinterpret_cast<unsigned long long*>(g_dbg_out + 4), (unsigned long long)total);
   }
@@ -541,9 +570,15 @@ __device__ void tri_phase(const StepConst& K, const Streams& Sm, Ctl* ctl, uint8
   uint32_t par = (uint32_t)((u / nst) & 1);
   if (K.dbg & 16) {  // timing experiment: the stream alone (every chunk waited for and released)
     for (; u < u1; ++u) {
-      if (!(K.dbg & 256)) mbar_wait(&ctl->full[st], par);
+      if (K.dbg & 2048)
+        mbar_spin(&ctl->full[st], par);
+      else
+        mbar_wait(&ctl->full[st], par);
       if (PSLR_TRACE_BUILD && K.trace && blockIdx.x == K.trace_block && threadIdx.x == 0 && u < 8192)
         K.trace[2 + 2 * 65536 + 2 * u + 1] = clock64();
+      if (PSLR_TRACE_BUILD && K.trace && blockIdx.x == K.trace_block && (threadIdx.x & 31) == 0 && u < 8192)
+        atomicMax(reinterpret_cast<unsigned long long*>(K.trace + 2 + 2 * 65536 + 3 * 8192 + u),
+                  (unsigned long long)clock64());  // the last warp to see the chunk
       __syncwarp();
       if ((threadIdx.x & 31) == 0) mbar_arrive(&ctl->empty[st]);
       if (++st == nst) {
@@ -573,6 +608,8 @@ __device__ void tri_phase(const StepConst& K, const Streams& Sm, Ctl* ctl, uint8
         par ^= 1u;
       }
       mbar_wait(&ctl->full[st], par);
+      if (PSLR_TRACE_BUILD && K.trace && blockIdx.x == K.trace_block && threadIdx.x == 0 && u < 8192)
+        K.trace[2 + 2 * 65536 + 2 * u + 1] = clock64();  // the chunk seen by the look-ahead
       nseg = stages + (uint32_t)(st * K.stage_bytes);
       rbuf = rhsbuf + (uint32_t)(st * K.rhs_stride * 8);
       rbase = sp<int32_t>(nseg)[6];
@@ -682,6 +719,14 @@ __device__ __forceinline__ void iface_terms4(int kind, const int (&row)[4], cons
   }
 }
 
+// prepass loads in flight per thread (the prepass is latency-bound: three dependent global
+// loads per E row; more rows in flight per thread = fewer round trips)
+#ifndef PSLR_PRE_F
+#define PSLR_PRE_F 8
+#endif
+#ifndef PSLR_PRE_E
+#define PSLR_PRE_E 8
+#endif
 #ifndef PSLR_STEP_MINB
 #define PSLR_STEP_MINB 1
 #endif
@@ -765,7 +810,7 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
     if (a.fL || ey_only) {
       // fL holds f already; rhsE's non-E positions are permanently 0
     } else if (a.b1 == BT_F) {
-      constexpr int kIn = 8;  // independent loads in flight per thread
+      constexpr int kIn = PSLR_PRE_F;  // independent loads in flight per thread
       for (int row0 = r0 + tid; row0 < r1; row0 += kIn * kStepThreads) {
         vt<NV> v[kIn];
         int pos[kIn];
@@ -787,7 +832,7 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
     // csr_matvec order), kIn rows per thread in flight; one int4 record per row
     if (a.b1 == BT_EY || a.b2 == BT_EY) {
       if (!a.fL && !ey_only) consumer_sync();
-      constexpr int kIn = 4;
+      constexpr int kIn = PSLR_PRE_E;  // E rows in flight per thread (dependent chain: record, E entry, y)
       const int e0 = K.erow_off[b], e1 = K.erow_off[b + 1];
       const int4* rec = reinterpret_cast<const int4*>(K.erows);
       for (int i0 = e0 + tid; i0 < e1; i0 += kIn * kStepThreads) {

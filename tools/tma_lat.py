@@ -25,5 +25,12 @@ t = buf[2 * 65536: 2 * 65536 + 2 * 8192].reshape(-1, 2)
 ok = (t[:, 0] > 0) & (t[:, 1] > 0)
 lat = (t[ok, 1] - t[ok, 0])
 iss = np.diff(t[ok, 0])
+by = buf[2 * 65536 + 2 * 8192: 2 * 65536 + 3 * 8192][:ok.size]
+if os.environ.get("TMA_DUMP"):
+    t0 = t[ok, 0].min()
+    for u in range(min(120, ok.sum())):
+        lw = buf[2 * 65536 + 3 * 8192 + u]
+        print(f"{u:4d} issue {t[u,0]-t0:8d} land {t[u,1]-t0:8d} lastwarp {lw - t0 if lw else -1:8d} lat {t[u,1]-t[u,0]:6d} bytes {by[u]:6d}")
+print(f"bytes {by[ok].sum()} mean {by[ok].mean():.0f} min {by[ok].min()} max {by[ok].max()}")
 print(f"chunks {ok.sum()}: issue->land cycles mean {lat.mean():.0f} median {np.median(lat):.0f} p90 {np.percentile(lat, 90):.0f}; "
       f"issue interval mean {iss.mean():.0f}; total {(t[ok,1].max() - t[ok,0].min()) / 1.965e3:.1f} us")
