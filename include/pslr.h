@@ -114,6 +114,15 @@ int pslr_row_norms(int64_t n, const int64_t* indptr, const double* data, double*
 /* Uploads the system, level-schedules every triangular factor per block, packs the
  * device formats. Replaces the state build() hands to the apply (preconditioner.py:120-141). */
 int pslr_ctx_create(pslr_ctx** out, int device, const pslr_system* sys);
+/* pslr_ctx_create with the packed device format as a reusable artefact:
+ * the level schedules and streamed factor chunks are host work (pack.cpp).  blob_in (may be
+ * NULL): a blob from an earlier call for the same system; it is used when it matches the
+ * system, this library build and the device's shared-memory plan (*reused = 1), else the
+ * system is packed again (*reused = 0).  blob_out (may be NULL): receives a malloc'd blob of
+ * the packed format in use, to store next to a setup cache; free it with pslr_blob_free. */
+int pslr_ctx_create_packed(pslr_ctx** out, int device, const pslr_system* sys, const void* blob_in,
+                           int64_t blob_len, void** blob_out, int64_t* blob_out_len, int* reused);
+void pslr_blob_free(void* blob);
 void pslr_ctx_destroy(pslr_ctx* ctx);
 int pslr_ctx_info(const pslr_ctx* ctx, pslr_ctx_info_t* info);
 /* LowRankCorrection (lowrank.py:26-36): V q x r row-major, G r x r row-major, host pointers. */

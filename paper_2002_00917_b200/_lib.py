@@ -76,6 +76,9 @@ EXPORTS = {
     "pslr_factors_free": (None, P),
     "pslr_row_norms": (c_int, c_i64, P, P, P),
     "pslr_ctx_create": (c_int, ctypes.POINTER(P), c_int, ctypes.POINTER(System)),
+    "pslr_ctx_create_packed": (c_int, ctypes.POINTER(P), c_int, ctypes.POINTER(System), P, c_i64,
+                               ctypes.POINTER(P), ctypes.POINTER(c_i64), ctypes.POINTER(c_int)),
+    "pslr_blob_free": (None, P),
     "pslr_ctx_destroy": (None, P),
     "pslr_ctx_info": (c_int, P, ctypes.POINTER(CtxInfo)),
     "pslr_ctx_set_correction": (c_int, P, c_i64, P, P),

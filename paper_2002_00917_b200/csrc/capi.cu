@@ -95,35 +95,172 @@ static int upload_csr(pslr_ctx* ctx, const pslr_csr& M, DevCsr* out) {
   return PSLR_OK;
 }
 
-static int upload_tri(pslr_ctx* ctx, const TriHost& H, const TriAnalysis* AL, DevTri* out) {
-  out->nblocks = (int32_t)H.blk_chunk.size() - 1;
-  out->nchunks = (int32_t)H.chunks.size();
-  RET(upload(ctx, H.data, &out->data));
-  RET(upload(ctx, H.chunks, &out->chunks));
-  RET(upload(ctx, H.blk_chunk, &out->blk_chunk));
-  if (AL) {
-    RET(upload(ctx, AL->pos_of_row, &out->lpos));
-    RET(upload(ctx, AL->row_at_pos, &out->lrow));
+// ---------------------------------------------------------------- the packed format
+// Everything pslr_ctx_create derives on the host before uploading (level analysis +
+// streamed factor chunks): serialisable, so a setup cache can skip it.
+struct PackedFactor {
+  TriHost H;
+  std::vector<int32_t> pos_of_row, row_at_pos;  // L factors: the rhs placement (lpos / lrow)
+};
+struct PackedSystem {
+  int64_t n = 0, p = 0, q = 0, s = 0;
+  int64_t W = 0, SB = 0, reach = 0, far = 0;
+  int64_t levels[4] = {0, 0, 0, 0}, depth[4] = {0, 0, 0, 0}, nnz[4] = {0, 0, 0, 0};
+  PackedFactor F[4];                 // LB, UB, LC, UC
+  std::vector<int32_t> ub_pos;       // U_B: row -> U-position (x order, Fpos columns)
+  std::vector<int32_t> lb_pos;       // L_B: row -> L-position (E rows' rhs placement)
+};
+
+constexpr uint64_t kPackMagic = 0x31764b4150524c53ull;  // "SLRPAKv1"
+
+// Level analysis of the four factors, the ring size W (from the reach and the device's
+// shared memory) and the streamed chunks of every block (pack.cpp).
+static int pack_system(const pslr_system* sys, const std::vector<int64_t>& ioff, const std::vector<int64_t>& foff,
+                       int64_t smem_optin, int64_t SB, int64_t wmax, PackedSystem& P) {
+  P.n = sys->n;
+  P.p = sys->p;
+  P.q = sys->q;
+  P.s = sys->s;
+  P.SB = SB;
+  TriAnalysis aLB, aUB, aLC, aUC;
+  RET(analyze_factor(sys->LB, ioff, false, aLB, "L_B"));
+  RET(analyze_factor(sys->UB, ioff, true, aUB, "U_B"));
+  RET(analyze_factor(sys->LC, foff, false, aLC, "L_C0"));
+  RET(analyze_factor(sys->UC, foff, true, aUC, "U_C0"));
+  P.reach = std::max({aLB.reach, aUB.reach, aLC.reach, aUC.reach, (int64_t)1});
+  const int64_t RB = ((8 * (kChunkRows + 2)) + 127) / 128 * 128;
+  int64_t W = 2048;  // >= 2048: the ring doubles as the V^T y reduction scratch
+  while (W < P.reach && W < wmax) W *= 2;
+  while (W > 2048 && (smem_optin - 1024 - kCtlBytes - W * 8 - 128) / (SB + RB) < 2) W /= 2;
+  P.W = W;
+  const TriAnalysis* an[4] = {&aLB, &aUB, &aLC, &aUC};
+  const pslr_csr* M[4] = {&sys->LB, &sys->UB, &sys->LC, &sys->UC};
+  const char* nm[4] = {"L_B", "U_B", "L_C0", "U_C0"};
+  for (int f = 0; f < 4; ++f) {
+    P.levels[f] = an[f]->levels;
+    P.depth[f] = an[f]->depth_max;
+    P.nnz[f] = M[f]->nnz;
   }
+  // U first: L's output lands at the U-positions, where every value lives globally
+  for (int pair = 0; pair < 2; ++pair) {
+    const TriAnalysis& AL = *an[2 * pair];
+    const TriAnalysis& AU = *an[2 * pair + 1];
+    const int64_t nr = M[2 * pair]->nrows;
+    std::vector<int32_t> row_id(nr);
+    for (int64_t i = 0; i < nr; ++i) row_id[i] = (int32_t)i;
+    const auto& off = pair == 0 ? ioff : foff;
+    RET(emit_factor(*M[2 * pair + 1], off, AU, W, SB, kStepThreads, AU.pos_of_row, row_id, P.F[2 * pair + 1].H,
+                    nm[2 * pair + 1]));
+    RET(emit_factor(*M[2 * pair], off, AL, W, SB, kStepThreads, AU.pos_of_row, AU.pos_of_row, P.F[2 * pair].H,
+                    nm[2 * pair]));
+    P.F[2 * pair].pos_of_row = AL.pos_of_row;
+    P.F[2 * pair].row_at_pos = AL.row_at_pos;
+    P.far += P.F[2 * pair].H.far + P.F[2 * pair + 1].H.far;
+  }
+  P.ub_pos = aUB.pos_of_row;
+  P.lb_pos = aLB.pos_of_row;
   return PSLR_OK;
 }
 
-// Pack one block ILU pair (L, U) for the streamed solve.  The U-positions are where
-// every value lives globally (L writes its output there, U its intermediate).
-static int build_pair(pslr_ctx* ctx, const pslr_csr& L, const pslr_csr& U,
-                      const std::vector<int64_t>& off, const TriAnalysis& AL,
-                      const TriAnalysis& AU, int64_t W, int64_t SB, DevTri* dL, DevTri* dU,
-                      const char* nameL, const char* nameU, int64_t* far) {
-  const int64_t n = L.nrows;
-  std::vector<int32_t> row_id(n);
-  for (int64_t i = 0; i < n; ++i) row_id[i] = (int32_t)i;
-  TriHost HL, HU;
-  RET(emit_factor(U, off, AU, W, SB, kStepThreads, AU.pos_of_row, row_id, HU, nameU));
-  RET(emit_factor(L, off, AL, W, SB, kStepThreads, AU.pos_of_row, AU.pos_of_row, HL, nameL));
-  RET(upload_tri(ctx, HL, &AL, dL));
-  RET(upload_tri(ctx, HU, nullptr, dU));
-  *far = HL.far + HU.far;
-  return PSLR_OK;
+namespace {
+struct Writer {
+  std::vector<uint8_t> b;
+  template <class T> void put(const T& v) {
+    const uint8_t* p = reinterpret_cast<const uint8_t*>(&v);
+    b.insert(b.end(), p, p + sizeof(T));
+  }
+  template <class T> void vec(const std::vector<T>& v) {
+    put<int64_t>((int64_t)v.size());
+    const uint8_t* p = reinterpret_cast<const uint8_t*>(v.data());
+    b.insert(b.end(), p, p + v.size() * sizeof(T));
+  }
+};
+struct Reader {
+  const uint8_t* p;
+  int64_t left;
+  bool ok = true;
+  template <class T> T get() {
+    T v{};
+    if (left < (int64_t)sizeof(T)) {
+      ok = false;
+      return v;
+    }
+    std::memcpy(&v, p, sizeof(T));
+    p += sizeof(T);
+    left -= sizeof(T);
+    return v;
+  }
+  template <class T> void vec(std::vector<T>& v) {
+    const int64_t cnt = get<int64_t>();
+    if (!ok || cnt < 0 || cnt * (int64_t)sizeof(T) > left) {
+      ok = false;
+      return;
+    }
+    v.resize(cnt);
+    std::memcpy(v.data(), p, cnt * sizeof(T));
+    p += cnt * sizeof(T);
+    left -= cnt * sizeof(T);
+  }
+};
+}  // namespace
+
+static void serialize(const PackedSystem& P, std::vector<uint8_t>& out) {
+  Writer w;
+  w.put(kPackMagic);
+  w.put<int64_t>(kStepThreads);
+  w.put<int64_t>(kChunkRows);
+  for (int64_t v : {P.n, P.p, P.q, P.s, P.W, P.SB, P.reach, P.far}) w.put(v);
+  for (int f = 0; f < 4; ++f) {
+    w.put(P.levels[f]);
+    w.put(P.depth[f]);
+    w.put(P.nnz[f]);
+    w.vec(P.F[f].H.data);
+    w.vec(P.F[f].H.chunks);
+    w.vec(P.F[f].H.blk_chunk);
+    w.put(P.F[f].H.far);
+    w.vec(P.F[f].pos_of_row);
+    w.vec(P.F[f].row_at_pos);
+  }
+  w.vec(P.ub_pos);
+  w.vec(P.lb_pos);
+  out.swap(w.b);
+}
+
+// a blob packed for this system, this build of the kernel and a ring / stage plan the
+// device can hold; anything else is rejected (the caller repacks)
+static bool deserialize(const void* blob, int64_t len, const pslr_system* sys, int64_t smem_optin, int64_t SB,
+                        PackedSystem& P) {
+  Reader r{static_cast<const uint8_t*>(blob), len};
+  if (r.get<uint64_t>() != kPackMagic || r.get<int64_t>() != kStepThreads || r.get<int64_t>() != kChunkRows)
+    return false;
+  P.n = r.get<int64_t>();
+  P.p = r.get<int64_t>();
+  P.q = r.get<int64_t>();
+  P.s = r.get<int64_t>();
+  P.W = r.get<int64_t>();
+  P.SB = r.get<int64_t>();
+  P.reach = r.get<int64_t>();
+  P.far = r.get<int64_t>();
+  if (!r.ok || P.n != sys->n || P.p != sys->p || P.q != sys->q || P.s != sys->s || P.SB != SB) return false;
+  const pslr_csr* M[4] = {&sys->LB, &sys->UB, &sys->LC, &sys->UC};
+  for (int f = 0; f < 4; ++f) {
+    P.levels[f] = r.get<int64_t>();
+    P.depth[f] = r.get<int64_t>();
+    P.nnz[f] = r.get<int64_t>();
+    if (P.nnz[f] != M[f]->nnz) return false;
+    r.vec(P.F[f].H.data);
+    r.vec(P.F[f].H.chunks);
+    r.vec(P.F[f].H.blk_chunk);
+    P.F[f].H.far = r.get<int64_t>();
+    r.vec(P.F[f].pos_of_row);
+    r.vec(P.F[f].row_at_pos);
+    if ((int64_t)P.F[f].H.blk_chunk.size() != P.s + 1) return false;
+  }
+  r.vec(P.ub_pos);
+  r.vec(P.lb_pos);
+  const int64_t RB = ((8 * (kChunkRows + 2)) + 127) / 128 * 128;
+  return r.ok && r.left == 0 && (int64_t)P.ub_pos.size() == P.p && (int64_t)P.lb_pos.size() == P.p &&
+         (smem_optin - 1024 - kCtlBytes - P.W * 8 - 128) / (SB + RB) >= 2;
 }
 
 static cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
@@ -415,7 +552,16 @@ const char* pslr_last_error(void) { return g_last_error.c_str(); }
 int pslr_abi_version(void) { return 2; }
 
 int pslr_ctx_create(pslr_ctx** out, int device, const pslr_system* sys) {
+  return pslr_ctx_create_packed(out, device, sys, nullptr, 0, nullptr, nullptr, nullptr);
+}
+
+void pslr_blob_free(void* blob) { std::free(blob); }
+
+int pslr_ctx_create_packed(pslr_ctx** out, int device, const pslr_system* sys, const void* blob_in,
+                           int64_t blob_len, void** blob_out, int64_t* blob_out_len, int* reused) {
   *out = nullptr;
+  if (blob_out) *blob_out = nullptr;
+  if (blob_out_len) *blob_out_len = 0;
   if (!sys) return fail(PSLR_EINVAL, "null system");
   const int64_t n = sys->n, p = sys->p, q = sys->q, s = sys->s;
   if (p + q != n || s < 1) return fail(PSLR_EDIM, "inconsistent system dimensions");
@@ -458,28 +604,32 @@ int pslr_ctx_create(pslr_ctx** out, int device, const pslr_system* sys) {
   smem_optin = (int)std::min<int64_t>(smem_optin, env_int("PSLR_SMEM_CAP", smem_optin));
   pslr_ctx_info_t& I = ctx->info;
 
-  // ---- level analysis of the four factors, then the ring size W and the stage plan
-  TriAnalysis aLB, aUB, aLC, aUC;
-  if ((rc = analyze_factor(sys->LB, ctx->interior_off, false, aLB, "L_B"))) return bail(rc);
-  if ((rc = analyze_factor(sys->UB, ctx->interior_off, true, aUB, "U_B"))) return bail(rc);
-  if ((rc = analyze_factor(sys->LC, ctx->interface_off, false, aLC, "L_C0"))) return bail(rc);
-  if ((rc = analyze_factor(sys->UC, ctx->interface_off, true, aUC, "U_C0"))) return bail(rc);
-  const int64_t reach = std::max({aLB.reach, aUB.reach, aLC.reach, aUC.reach, (int64_t)1});
+  // ---- the packed format: from the caller's blob when it fits this system and device,
+  // else level analysis + ring plan + streamed chunks (pack_system)
   // Shared-memory plan: nst stages of (chunk bytes SB + rhs slice RB) and a W-slot ring.
-  // In-flight bytes set the per-SM stream rate (~1 us TMA latency), the ring size sets
-  // how many dependencies must come from global memory; W = 8192 balances the two
-  // for the 3D configs (tools/micro/tma_stream.cu).
   const int64_t SB = env_int("PSLR_STAGE_BYTES", 32 * 1024);
   const int64_t RB = ((8 * (kChunkRows + 2)) + 127) / 128 * 128;
-  int64_t wmax = env_int("PSLR_RING", 4096);
-  int64_t W = 2048;  // >= 2048: the ring doubles as the V^T y reduction scratch
-  while (W < reach && W < wmax) W *= 2;
+  PackedSystem P;
+  const bool reuse = blob_in && blob_len > 0 && deserialize(blob_in, blob_len, sys, smem_optin, SB, P);
+  if (reused) *reused = reuse ? 1 : 0;
+  if (!reuse) {
+    P = PackedSystem();
+    if ((rc = pack_system(sys, ctx->interior_off, ctx->interface_off, smem_optin, SB,
+                          env_int("PSLR_RING", 4096), P)))
+      return bail(rc);
+  }
+  if (blob_out) {
+    std::vector<uint8_t> bytes;
+    serialize(P, bytes);
+    void* mem = std::malloc(bytes.size());
+    if (!mem) return bail(fail(PSLR_ENOMEM, "packed-format blob"));
+    std::memcpy(mem, bytes.data(), bytes.size());
+    *blob_out = mem;
+    *blob_out_len = (int64_t)bytes.size();
+  }
+  const int64_t W = P.W, reach = P.reach;
   const int64_t CTL = kCtlBytes;  // mbarriers + descriptor queue
   int64_t nst = (smem_optin - 1024 - CTL - W * 8 - 128) / (SB + RB);
-  while (nst < 2 && W > 2048) {
-    W /= 2;
-    nst = (smem_optin - 1024 - CTL - W * 8 - 128) / (SB + RB);
-  }
   nst = std::min<int64_t>(nst, std::min<int64_t>(8, env_int("PSLR_MAX_STAGES", 8)));
   if (nst < 2) return bail(fail(PSLR_EINVAL, "not enough shared memory for the streamed solve"));
   ctx->K.ring_mask = (int)(W - 1);
@@ -504,24 +654,32 @@ int pslr_ctx_create(pslr_ctx** out, int device, const pslr_system* sys) {
     ctx->K.trace_cap = cap;
     ctx->K.trace_block = env_int("PSLR_TRACE_CTA", 0);
   }
-  int64_t farB = 0, farC = 0;
-  if ((rc = build_pair(ctx, sys->LB, sys->UB, ctx->interior_off, aLB, aUB, W, SB, &ctx->K.LB,
-                       &ctx->K.UB, "L_B", "U_B", &farB)))
-    return bail(rc);
-  if ((rc = build_pair(ctx, sys->LC, sys->UC, ctx->interface_off, aLC, aUC, W, SB, &ctx->K.LC,
-                       &ctx->K.UC, "L_C0", "U_C0", &farC)))
-    return bail(rc);
-  I.levels_LB = aLB.levels;
-  I.levels_UB = aUB.levels;
-  I.levels_LC = aLC.levels;
-  I.levels_UC = aUC.levels;
-  I.maxdepth_LB = aLB.depth_max;
-  I.maxdepth_UB = aUB.depth_max;
-  I.maxdepth_LC = aLC.depth_max;
-  I.maxdepth_UC = aUC.depth_max;
+  {
+    DevTri* dt[4] = {&ctx->K.LB, &ctx->K.UB, &ctx->K.LC, &ctx->K.UC};
+    for (int f = 0; f < 4; ++f) {
+      const PackedFactor& F = P.F[f];
+      dt[f]->nblocks = (int32_t)F.H.blk_chunk.size() - 1;
+      dt[f]->nchunks = (int32_t)F.H.chunks.size();
+      if ((rc = upload(ctx, F.H.data, &dt[f]->data))) return bail(rc);
+      if ((rc = upload(ctx, F.H.chunks, &dt[f]->chunks))) return bail(rc);
+      if ((rc = upload(ctx, F.H.blk_chunk, &dt[f]->blk_chunk))) return bail(rc);
+      if (!(f & 1)) {  // L factors: rhs placement
+        if ((rc = upload(ctx, F.pos_of_row, &dt[f]->lpos))) return bail(rc);
+        if ((rc = upload(ctx, F.row_at_pos, &dt[f]->lrow))) return bail(rc);
+      }
+    }
+  }
+  I.levels_LB = P.levels[0];
+  I.levels_UB = P.levels[1];
+  I.levels_LC = P.levels[2];
+  I.levels_UC = P.levels[3];
+  I.maxdepth_LB = P.depth[0];
+  I.maxdepth_UB = P.depth[1];
+  I.maxdepth_LC = P.depth[2];
+  I.maxdepth_UC = P.depth[3];
   I.ring_slots = W;
   I.stages = nst;
-  I.far_deps = farB + farC;
+  I.far_deps = P.far;
   I.reach = reach;
 
   if ((rc = upload_csr(ctx, sys->E, &ctx->K.E))) return bail(rc);
@@ -544,7 +702,7 @@ int pslr_ctx_create(pslr_ctx** out, int device, const pslr_system* sys) {
     for (int64_t b = 0; b < s; ++b) {
       for (int64_t i = ctx->interior_off[b]; i < ctx->interior_off[b + 1]; ++i)
         if (sys->E.indptr[i + 1] > sys->E.indptr[i]) {
-          er.push_back(aLB.pos_of_row[i]);
+          er.push_back(P.lb_pos[i]);
           er.push_back((int32_t)i);
           er.push_back((int32_t)sys->E.indptr[i]);
           er.push_back((int32_t)sys->E.indptr[i + 1]);
@@ -599,7 +757,7 @@ int pslr_ctx_create(pslr_ctx** out, int device, const pslr_system* sys) {
      // last: the other arrays keep the placement they were tuned with)
     pslr_csr Fp = sys->F;
     std::vector<int32_t> pcol(sys->F.indices, sys->F.indices + sys->F.nnz);
-    for (auto& j : pcol) j = aUB.pos_of_row[j];
+    for (auto& j : pcol) j = P.ub_pos[j];
     Fp.indices = pcol.data();
     if ((rc = upload_csr(ctx, Fp, &ctx->K.Fpos))) return bail(rc);
   }

@@ -36,7 +36,10 @@ def require_cuda():
 class DeviceContext:
     """A `pslr_ctx` built from the host system + factors (pslr_ctx_create)."""
 
-    def __init__(self, ps, b_ilu, c0_ilu, C0, Cg, device=None):
+    def __init__(self, ps, b_ilu, c0_ilu, C0, Cg, device=None, packed=None, want_packed=False):
+        """packed: a packed-format blob from an earlier context of the same system (the
+        setup cache's pack_*.bin) — pslr_ctx_create_packed skips the level analysis and
+        chunk packing when it fits; want_packed: keep the blob in use as self.packed."""
         t = require_cuda()
         if device is None:
             device = t.cuda.current_device()
@@ -62,9 +65,19 @@ class DeviceContext:
         sysd.Cg = _lib.csr_struct(Cg if ps.q else empty(0, 0), keep)
         sysd.A = _lib.csr_struct(ps.matrix, keep)
         h = ctypes.c_void_p()
+        blob_out, blob_len, reused = ctypes.c_void_p(), ctypes.c_int64(), ctypes.c_int()
+        pin = packed if packed is not None else b""
         with t.cuda.device(self.device):
-            _lib.check(_lib.fns["pslr_ctx_create"](ctypes.byref(h), self.device, ctypes.byref(sysd)))
+            _lib.check(_lib.fns["pslr_ctx_create_packed"](
+                ctypes.byref(h), self.device, ctypes.byref(sysd), pin if pin else None, len(pin),
+                ctypes.byref(blob_out) if want_packed else None, ctypes.byref(blob_len) if want_packed else None,
+                ctypes.byref(reused)))
         self.handle = h
+        self.packed_reused = bool(reused.value)
+        self.packed = None
+        if want_packed and blob_out.value:
+            self.packed = ctypes.string_at(blob_out.value, blob_len.value)
+            _lib.fns["pslr_blob_free"](blob_out)
         self.n, self.p, self.q, self.s = ps.n, ps.p, ps.q, ps.num_parts
 
     # ------------------------------------------------------------------ plumbing

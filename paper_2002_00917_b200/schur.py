@@ -47,10 +47,11 @@ def _block_diag_part(C, sizes) -> sp.csr_matrix:
 
 
 def build_schur_context(ps: PartitionedSystem, droptol: float = 1e-2, fill_cap: int | None = None,
-                        device=None, factors=None) -> SchurContext:
+                        device=None, factors=None, packed=None, want_packed=False) -> SchurContext:
     """Factor the B_i and C_i diagonal blocks (host, native C++) and upload everything
     to the device (schur.py:52-59).  `factors` = (b_ilu, c0_ilu) from the setup cache
-    skips the factorisation."""
+    skips the factorisation; `packed` (the cache's packed device format) skips the level
+    analysis and chunk packing of the context."""
     C0 = _block_diag_part(ps.C, ps.interface_sizes)
     if factors is not None:
         b_ilu, c0_ilu = factors
@@ -58,7 +59,7 @@ def build_schur_context(ps: PartitionedSystem, droptol: float = 1e-2, fill_cap: 
         b_ilu = factor_blocks(ps.B, ps.interior_sizes, droptol=droptol, fill_cap=fill_cap)
         c0_ilu = factor_blocks(C0, ps.interface_sizes, droptol=droptol, fill_cap=fill_cap)
     Cg = canonical(ps.C - C0)
-    dev = DeviceContext(ps, b_ilu, c0_ilu, C0, Cg, device=device)
+    dev = DeviceContext(ps, b_ilu, c0_ilu, C0, Cg, device=device, packed=packed, want_packed=want_packed)
     return SchurContext(system=ps, b_ilu=b_ilu, c0_ilu=c0_ilu, C0=C0, Cg=Cg, device=dev)
 
 

@@ -9,7 +9,11 @@ per matrix + configuration, everything build() derives before the device context
       the reordering (perm.forward, interior/interface sizes) and both assembled block
       factors (L, U, offsets, per-block nnz and pivot repairs);
   correction  (key: setup key + series degree m + rank):
-      V, H, G and the achieved rank.
+      V, H, G and the achieved rank;
+  packed  (key: setup key; pack_<key>.bin):
+      the device context's packed format — per-block level schedules and the TMA-streamed
+      factor chunks (csrc/pack.cpp), the host work of pslr_ctx_create.  The blob carries
+      its own build / shared-memory-plan header; a stale one is re-packed, never used.
 
 A hit rebuilds the PartitionedSystem by one symmetric permutation (no adjacency, no
 BFS), skips ILUT and Arnoldi, and yields the same factors and correction bit for bit
@@ -149,3 +153,22 @@ def load_correction(path):
         if int(d["format"][0]) != FORMAT:
             return None
         return d["V"], d["H"], d["G"], int(d["rank"][0])
+
+
+def save_packed(path, blob: bytes) -> None:
+    """The packed device format (pslr_ctx_create_packed's blob), written atomically."""
+    if not path or not blob:
+        return
+    d = os.path.dirname(path)
+    os.makedirs(d, exist_ok=True)
+    fd, tmp = tempfile.mkstemp(dir=d, suffix=".tmp.bin")
+    with os.fdopen(fd, "wb") as fh:
+        fh.write(blob)
+    os.replace(tmp, path)
+
+
+def load_packed(path):
+    if not path or not os.path.exists(path):
+        return None
+    with open(path, "rb") as fh:
+        return fh.read()

@@ -59,14 +59,28 @@ def test_build_from_cache_bitexact(tmp_path):
     cfg = pg.PslrConfig(num_subdomains=8, series_degree=3, rank=12)
     P1 = pg.build(A, cfg, cache_dir=str(tmp_path))
     files = sorted(p.name for p in tmp_path.iterdir())
-    assert len(files) == 2 and files[0].startswith("corr_") and files[1].startswith("setup_")
-    P2 = pg.build(A, cfg, cache_dir=str(tmp_path))  # hit: no partition / ILUT / Arnoldi
+    assert len(files) == 3 and files[0].startswith("corr_") and files[1].startswith("pack_") \
+        and files[2].startswith("setup_")
+    assert not P1.device.packed_reused
+    P2 = pg.build(A, cfg, cache_dir=str(tmp_path))  # hit: no partition / ILUT / Arnoldi / packing
+    assert P2.device.packed_reused
     P0 = pg.build(A, cfg)                           # no cache
     assert np.array_equal(P2.correction.V, P1.correction.V) and np.array_equal(P2.correction.G, P1.correction.G)
+    assert P2.device.info() == {**P0.device.info(), "device_bytes": P2.device.info()["device_bytes"]}
     b = np.random.default_rng(3).standard_normal(A.shape[0])
     z0, z1, z2 = P0.apply(b), P1.apply(b), P2.apply(b)
     np.testing.assert_array_equal(z1, z0)
     np.testing.assert_array_equal(z2, z0)
-    # a different series degree reuses the setup file and adds one correction file
+    f = np.random.default_rng(4).standard_normal(P0.system.p)
+    np.testing.assert_array_equal(pg.solve_B(P2.ctx, f), pg.solve_B(P0.ctx, f))
+    # a different series degree reuses the setup and packed files and adds one correction file
     pg.build(A, pg.PslrConfig(num_subdomains=8, series_degree=2, rank=12), cache_dir=str(tmp_path))
-    assert len(list(tmp_path.iterdir())) == 3
+    assert len(list(tmp_path.iterdir())) == 4
+    # a corrupted or foreign blob is never used: the context re-packs and stays bit-exact
+    pack = next(p for p in tmp_path.iterdir() if p.name.startswith("pack_"))
+    pack.write_bytes(pack.read_bytes()[:-8])
+    P3 = pg.build(A, cfg, cache_dir=str(tmp_path))
+    assert not P3.device.packed_reused
+    np.testing.assert_array_equal(P3.apply(b), z0)
+    P4 = pg.build(A, cfg, cache_dir=str(tmp_path))  # P3 rewrote a good blob
+    assert P4.device.packed_reused

@@ -27,7 +27,8 @@ if nv > 1:
         _lib.check(_lib.fns["pslr_apply_multi"](P.device.handle, wl.m, nv, B.data_ptr(), Z.data_ptr(),
                                                 P.device.stream()))
     z = Z
-for _ in range(napply):
-    z = P.apply(b)
+else:
+    for _ in range(napply):
+        z = P.apply(b)
 torch.cuda.synchronize()
 print("done", float(z.norm()))
