@@ -255,3 +255,40 @@ def test_native_comm_world1_apply_err_arnoldi_gmres_cg():
     x1, r1 = cg_device(Q, bq, tol=1e-8)
     x2, r2 = cg_device(QView, bq, tol=1e-8)
     assert r1.converged and r1.iterations == r2.iterations and r1.history == r2.history
+
+
+def test_native_comm_world1_pipelines_two_vectors():
+    """The bench's N>1 data plane on one rank: clones of the rank-local context, each with
+    its OWN one-rank communicator (pslr_comm_init on a clone), run pslr_apply_multi with two
+    right-hand sides (op_apply2_sharded: paired halos, one allreduce of 2r) concurrently on
+    their own streams; every vector equals the fused single-vector apply bit for bit."""
+    import torch
+    import paper_2002_00917_b200 as pg
+    from paper_2002_00917_b200 import _lib, shard, workloads
+    A = workloads.laplacian3d(14, 12, 10, 0.3)
+    m, r = 3, 8
+    P = pg.build(A, pg.PslrConfig(num_subdomains=6, series_degree=m, rank=r))
+    ps = P.system
+    plan = shard.plan_shard(ps, 1, 0)
+    ops = shard.DeviceShardOps(plan)
+    ops.set_correction(torch.as_tensor(np.ascontiguousarray(P.correction.V), device="cuda"), P.correction.G)
+    ctxs = [ops.dev] + [ops.dev.clone() for _ in range(2)]
+    for c in ctxs:
+        shard.attach_nccl_ctx(c, plan, shard.nccl_unique_id())
+    streams = [torch.cuda.Stream() for _ in ctxs]
+    B = torch.as_tensor(np.random.default_rng(5).standard_normal((6, ps.n)), device="cuda")
+    Z = torch.empty_like(B)
+    torch.cuda.synchronize()
+    for j, c in enumerate(ctxs):
+        _lib.check(_lib.fns["pslr_apply_multi"](c.handle, m, 2, B[2 * j].data_ptr(), Z[2 * j].data_ptr(),
+                                                streams[j].cuda_stream))
+    torch.cuda.synchronize()
+    for v in range(6):
+        assert torch.equal(Z[v], P.apply(B[v]))
+    # an odd count: the pair through the two-vector path, the last vector alone
+    Z3 = torch.empty((3, ps.n), dtype=torch.float64, device="cuda")
+    _lib.check(_lib.fns["pslr_apply_multi"](ctxs[1].handle, m, 3, B[:3].contiguous().data_ptr(), Z3.data_ptr(),
+                                            streams[1].cuda_stream))
+    torch.cuda.synchronize()
+    for v in range(3):
+        assert torch.equal(Z3[v], P.apply(B[v]))
