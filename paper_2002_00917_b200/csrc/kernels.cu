@@ -315,16 +315,27 @@ cgs_pass_kernel(const double* __restrict__ X, int64_t ld, int k, double* __restr
     if (MODE != kDot) {
       double s = 0.0;
       if (i < n) {
+        // w_i - sum_c X[c,i] h0[c] in column order, the next 8 columns' loads in flight
+        // while the current 8 fold (two register buffers: a batch's load latency hides
+        // behind the previous batch's dependent DADD chain)
         const double* xi = X + i;
-        int c = 0;
-        for (; c + 8 <= k; c += 8) {
-          double v[8];
+        double va[8], vb[8];
+        auto load8 = [&](double (&v)[8], int c0) {
 #pragma unroll
-          for (int u = 0; u < 8; ++u) v[u] = xi[(int64_t)(c + u) * ld];
+          for (int u = 0; u < 8; ++u) v[u] = (c0 + u < k) ? xi[(int64_t)(c0 + u) * ld] : 0.0;
+        };
+        auto fold8 = [&](const double (&v)[8], int c0) {
 #pragma unroll
-          for (int u = 0; u < 8; ++u) s = s + v[u] * hs[c + u];
+          for (int u = 0; u < 8; ++u)
+            if (c0 + u < k) s = s + v[u] * hs[c0 + u];
+        };
+        load8(va, 0);
+        for (int c = 0; c < k; c += 16) {
+          if (c + 8 < k) load8(vb, c + 8);
+          fold8(va, c);
+          if (c + 16 < k) load8(va, c + 16);
+          if (c + 8 < k) fold8(vb, c + 8);
         }
-        for (; c < k; ++c) s = s + xi[(int64_t)c * ld] * hs[c];
         wi = wi - s;
         w[i] = wi;
       }
