@@ -630,7 +630,7 @@ __device__ void tri_phase(const StepConst& K, const Streams& Sm, Ctl* ctl, uint8
   }
   if (UPPER && actA) ra.cadd = (cadd && ra.active) ? vldg<NV>(cadd, ra.info & 0x3fffffff) : vzero<NV>();
   for (;;) {
-    trace_clk(K, 50, hA.y & 0xff);
+    trace_clk(K, 50, (hA.x & 0xffff) | ((hA.y & 0xf) << 16) | (min(hdr_w(hA), 15) << 20) | ((int)UPPER << 24));
     if (actA && !(K.dbg & 1)) compute_row<UPPER, NV, XPOS>(K, segA, hA, ra, ring, base, z, xout, cadd);
     trace_clk(K, 52, 0);
     if (hA.y & kChunkEnd) {  // this warp no longer reads A's stage

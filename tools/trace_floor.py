@@ -41,8 +41,11 @@ args = ev[:, 0] & 0xffffffff
 clk = ev[:, 1]
 # steps: 50 (top, after barrier) -> 52 (row computed) -> 53 (next ops loaded) -> 54 (header) -> 50
 i50 = np.flatnonzero(codes == 50)
+want_upper = int(os.environ.get("UPPER", "-1"))
 d = {"compute": [], "load_ops": [], "next_hdr": [], "barrier_to_top": []}
 for a, b in zip(i50[:-1], i50[1:]):
+    if want_upper >= 0 and ((args[a] >> 24) & 1) != want_upper:
+        continue
     seg = codes[a:b + 1]
     t = clk[a:b + 1]
     try:
@@ -55,4 +58,6 @@ for k, v in d.items():
     v = np.array(v)
     print(f"{k:>15}: mean {v.mean():7.1f} median {np.median(v):7.1f} p90 {np.percentile(v, 90):7.1f} (n={v.size})")
 tot = np.diff(clk[i50])
+if want_upper >= 0:
+    tot = tot[((args[i50[:-1]] >> 24) & 1) == want_upper]
 print(f"step total: mean {tot.mean():.1f} median {np.median(tot):.1f}")
