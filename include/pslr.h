@@ -241,15 +241,15 @@ int pslr_workspace_create(pslr_ctx** out, int device);
  * order (bit-identical to A @ x): the generic drivers' operator for a scipy matrix. */
 int pslr_csr_spmv(int64_t nrows, int64_t ncols, const int32_t* indptr, const int32_t* indices, const double* data,
                   const double* x, double* y, void* stream);
-/* krylov.py:35-129 on (A = reordered matrix, M = PSLR apply (precond!=0) or identity).
- * flexible!=0: FGMRES (Z_j = M v_j stored, x += Z y) — config 3's accelerator.
- * b, x: device n-vectors. history: host buffer of maxit+1 doubles. */
 /* krylov.py:35-129 for any operator pair on device n-vectors: A_fn NULL -> the context's
  * reordered matrix; M_fn NULL -> the context's PSLR apply (precond != 0) or the identity. */
 int pslr_gmres_op(pslr_ctx* ctx, int64_t m, int64_t n, pslr_vec_fn A_fn, void* A_user, pslr_vec_fn M_fn,
                   void* M_user, int precond, const double* b, double* x, double tol, int64_t maxit,
                   int64_t restart, int flexible, int64_t* iterations, int* converged, double* final_relres,
                   double* history, int64_t* history_len, void* stream);
+/* krylov.py:35-129 on (A = reordered matrix, M = PSLR apply (precond!=0) or identity).
+ * flexible!=0: FGMRES (Z_j = M v_j stored, x += Z y) — config 3's accelerator.
+ * b, x: device n-vectors. history: host buffer of maxit+1 doubles. */
 int pslr_gmres(pslr_ctx* ctx, int64_t m, const double* b, double* x, double tol, int64_t maxit,
                int64_t restart, int precond, int flexible, int64_t* iterations, int* converged,
                double* final_relres, double* history, int64_t* history_len, void* stream);
