@@ -559,6 +559,7 @@ void pslr_blob_free(void* blob) { std::free(blob); }
 
 int pslr_ctx_create_packed(pslr_ctx** out, int device, const pslr_system* sys, const void* blob_in,
                            int64_t blob_len, void** blob_out, int64_t* blob_out_len, int* reused) {
+  pslr::NvtxRange nvtx_("pslr_ctx_create");
   *out = nullptr;
   if (blob_out) *blob_out = nullptr;
   if (blob_out_len) *blob_out_len = 0;
@@ -847,11 +848,13 @@ int pslr_ctx_set_correction_device(pslr_ctx* ctx, int64_t r, const double* V_dev
 }
 
 int pslr_solve_B(pslr_ctx* ctx, const double* f, double* x, void* stream) {
+  pslr::NvtxRange nvtx_("pslr_solve_B");
   RET(set_device(ctx));
   return op_solve_B(ctx, f, x, S(stream));
 }
 
 int pslr_solve_C0(pslr_ctx* ctx, const double* g, double* y, void* stream) {
+  pslr::NvtxRange nvtx_("pslr_solve_C0");
   RET(set_device(ctx));
   return op_solve_C0(ctx, g, y, S(stream));
 }
@@ -886,6 +889,7 @@ int pslr_apply_neumann(pslr_ctx* ctx, int64_t m, const double* v, double* out, v
 }
 
 int pslr_apply_Err(pslr_ctx* ctx, int64_t m, const double* v, double* out, void* stream) {
+  pslr::NvtxRange nvtx_("pslr_apply_Err");
   if (!ctx->comm) RET(unsharded(ctx));
   if (m < 0) return fail(PSLR_EDIM, "series degree m must be >= 0");
   RET(set_device(ctx));
@@ -905,6 +909,7 @@ int pslr_apply_correction(pslr_ctx* ctx, const double* y, double* out, void* str
 }
 
 int pslr_apply(pslr_ctx* ctx, int64_t m, const double* b, double* z, void* stream) {
+  pslr::NvtxRange nvtx_("pslr_apply");
   if (!ctx->comm) RET(unsharded(ctx));  // with a communicator: the sharded apply (comm.cu)
   if (m < 0) return fail(PSLR_EDIM, "series degree m must be >= 0");
   RET(set_device(ctx));
@@ -1132,6 +1137,7 @@ int pslr_debug_trace(pslr_ctx* ctx, int64_t* out, int64_t cap, int64_t* count) {
 }
 
 int pslr_apply_multi(pslr_ctx* ctx, int64_t m, int64_t nv, const double* b, double* z, void* stream) {
+  pslr::NvtxRange nvtx_("pslr_apply_multi");
   if (m < 0) return fail(PSLR_EDIM, "series degree m must be >= 0");
   if (nv < 0) return fail(PSLR_EDIM, "number of vectors must be >= 0");
   if (!ctx->comm) RET(unsharded(ctx));
@@ -1230,6 +1236,7 @@ int pslr_ctx_clone(const pslr_ctx* src, pslr_ctx** out) {
 }
 
 int pslr_apply_host_async(pslr_ctx* ctx, int64_t m, const double* b_host, double* z_host, void* stream) {
+  pslr::NvtxRange nvtx_("pslr_apply_host_async");
   if (m < 0) return fail(PSLR_EDIM, "series degree m must be >= 0");
   RET(unsharded(ctx));
   RET(set_device(ctx));
@@ -1242,6 +1249,7 @@ int pslr_apply_host_async(pslr_ctx* ctx, int64_t m, const double* b_host, double
 
 int pslr_apply_multi_host_async(pslr_ctx* ctx, int64_t m, int64_t nv, const double* b_host,
                                 double* z_host, void* stream) {
+  pslr::NvtxRange nvtx_("pslr_apply_multi_host_async");
   if (m < 0) return fail(PSLR_EDIM, "series degree m must be >= 0");
   if (nv < 0) return fail(PSLR_EDIM, "number of vectors must be >= 0");
   RET(unsharded(ctx));
@@ -1266,6 +1274,7 @@ int pslr_apply_multi_host_async(pslr_ctx* ctx, int64_t m, int64_t nv, const doub
 }
 
 int pslr_apply_host(pslr_ctx* ctx, int64_t m, const double* b_host, double* z_host, void* stream) {
+  pslr::NvtxRange nvtx_("pslr_apply_host");
   RET(set_device(ctx));
   cudaStream_t st = S(stream);
   CK(cudaMemcpyAsync(ctx->io_b, b_host, ctx->n * sizeof(double), cudaMemcpyHostToDevice, st));

@@ -145,6 +145,7 @@ extern "C" {
 
 int pslr_arnoldi(pslr_ctx* ctx, int64_t m, int64_t rank, const double* v0, double* V_dev, double* H,
                  int64_t* r_out, void* stream) {
+  pslr::NvtxRange nvtx_("pslr_arnoldi");
   RET(set_device(ctx));
   if (ctx->nghost && !ctx->comm)
     return fail(PSLR_EINVAL, "sharded context: pslr_comm_init + pslr_ctx_set_halo first (or shard.py)");
@@ -174,6 +175,7 @@ int pslr_arnoldi(pslr_ctx* ctx, int64_t m, int64_t rank, const double* v0, doubl
 
 int pslr_arnoldi_op(pslr_ctx* ctx, int64_t dim, pslr_vec_fn op_fn, void* user, int64_t rank, const double* v0,
                     double* V_dev, double* H, int64_t* r_out, void* stream) {
+  pslr::NvtxRange nvtx_("pslr_arnoldi_op");
   RET(set_device(ctx));
   if (!op_fn) return fail(PSLR_EINVAL, "operator callback missing");
   if (dim < 0 || rank < 0) return fail(PSLR_EDIM, "dim and rank must be >= 0");
@@ -357,6 +359,7 @@ static int gmres_core(pslr_ctx* ctx, int64_t n, const VecOp& A, const VecOp& app
 int pslr_gmres(pslr_ctx* ctx, int64_t m, const double* b, double* x, double tol, int64_t maxit,
                int64_t restart, int precond, int flexible, int64_t* iterations, int* converged,
                double* final_relres, double* history, int64_t* history_len, void* stream) {
+  pslr::NvtxRange nvtx_("pslr_gmres");
   RET(set_device(ctx));
   if (ctx->nghost && !ctx->comm)
     return fail(PSLR_EINVAL, "sharded context: pslr_comm_init + pslr_ctx_set_halo first (or shard.py)");
@@ -397,6 +400,7 @@ int pslr_gmres_op(pslr_ctx* ctx, int64_t m, int64_t n, pslr_vec_fn A_fn, void* A
                   void* M_user, int precond, const double* b, double* x, double tol, int64_t maxit,
                   int64_t restart, int flexible, int64_t* iterations, int* converged, double* final_relres,
                   double* history, int64_t* history_len, void* stream) {
+  pslr::NvtxRange nvtx_("pslr_gmres_op");
   RET(set_device(ctx));
   if (n < 0) return fail(PSLR_EDIM, "negative dimension");
   cudaStream_t st = S(stream);
@@ -503,6 +507,7 @@ static int cg_core(pslr_ctx* ctx, int64_t n, const VecOp& A, const VecOp& apply_
 int pslr_cg(pslr_ctx* ctx, int64_t m, const double* b, double* x, double tol, int64_t maxit, int precond,
             int64_t* iterations, int* converged, double* final_relres, double* history,
             int64_t* history_len, void* stream) {
+  pslr::NvtxRange nvtx_("pslr_cg");
   RET(set_device(ctx));
   if (ctx->nghost && !ctx->comm)
     return fail(PSLR_EINVAL, "sharded context: pslr_comm_init + pslr_ctx_set_halo first (or shard.py)");
@@ -517,6 +522,7 @@ int pslr_cg_op(pslr_ctx* ctx, int64_t m, int64_t n, pslr_vec_fn A_fn, void* A_us
                void* M_user, int precond, const double* b, double* x, double tol, int64_t maxit,
                int64_t* iterations, int* converged, double* final_relres, double* history, int64_t* history_len,
                void* stream) {
+  pslr::NvtxRange nvtx_("pslr_cg_op");
   RET(set_device(ctx));
   if (n < 0) return fail(PSLR_EDIM, "negative dimension");
   cudaStream_t st = S(stream);

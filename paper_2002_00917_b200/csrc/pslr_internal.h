@@ -7,6 +7,9 @@
 #include <vector>
 
 #include "../../include/pslr.h"
+#ifdef __CUDACC__
+#include <nvtx3/nvToolsExt.h>
+#endif
 
 #ifndef __CUDACC__
 typedef struct CUevent_st* cudaEvent_t;
@@ -17,6 +20,17 @@ typedef struct CUevent_st* cudaEvent_t;
 namespace pslr {
 
 int fail(int code, const std::string& msg);  // records the thread-local message, returns code
+
+// NVTX range over one C-ABI call (ranges per apply / solve for nsys/ncu
+// --nvtx filtering; header-only NVTX3, a no-op without an attached tool)
+#ifdef __CUDACC__
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#endif
 double numpy_sum(const double* a, int64_t n);
 
 // CSR on the device, int32 row pointers (every matrix here has < 2^31 entries).
