@@ -9,10 +9,42 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
+#include <utility>
 
 #include "pslr_internal.h"
 
 namespace pslr {
+
+// Programmatic dependent launch for the vector kernels (Krylov passes, correction, SpMV,
+// permutes): a kernel may be launched while the previous kernel of its stream drains;
+// pdl_wait() at the top of every kernel orders all its memory accesses after that kernel
+// (a no-op for an ordinary launch).  PSLR_PDL=0 turns the attribute off.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+static bool pdl_enabled() {
+  static const bool on = [] {
+    const char* v = std::getenv("PSLR_PDL");
+    return !(v && v[0] == '0');
+  }();
+  return on;
+}
+
+template <class... KArgs, class... Args>
+static cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 __device__ __forceinline__ double csr_row(const DevCsr& M, int row, const double* __restrict__ x) {
   double s = 0.0;
@@ -24,6 +56,7 @@ __device__ __forceinline__ double csr_row(const DevCsr& M, int row, const double
 // u = G (sum_b partials[b]) ; one CTA. h lives in u[r..2r).
 __global__ void correction_core_kernel(const double* __restrict__ partials, int s, int r,
                                        const double* __restrict__ G, double* u) {
+  pdl_wait();
   double* h = u + r;
   for (int c = threadIdx.x; c < r; c += blockDim.x) {
     double acc = 0.0;
@@ -49,6 +82,7 @@ __global__ void __launch_bounds__(kVtThreads)
 vt_dot_kernel(const double* __restrict__ V, const double* __restrict__ y, int64_t ys, int64_t q, int r,
               const double* __restrict__ G, double* __restrict__ partials, double* hu,
               unsigned int* counter) {
+  pdl_wait();
   __shared__ double red[kVtThreads / 32][128];
   __shared__ bool last;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = kVtThreads / 32;
@@ -149,6 +183,7 @@ vt_dot_kernel(const double* __restrict__ V, const double* __restrict__ y, int64_
 
 // u = G s (one CTA): the correction core after the ranks' V^T y partial sums are reduced
 __global__ void gs_kernel(const double* __restrict__ G, const double* __restrict__ s, double* u, int r) {
+  pdl_wait();
   for (int i = threadIdx.x; i < r; i += blockDim.x) {
     double acc = 0.0;
     const double* gi = G + (int64_t)i * r;
@@ -161,6 +196,7 @@ __global__ void gs_kernel(const double* __restrict__ G, const double* __restrict
 __global__ void vu_add_kernel(const double* __restrict__ V, const double* __restrict__ u,
                               const double* __restrict__ y, int64_t ys, double* __restrict__ out,
                               int64_t os, int64_t q, int r) {
+  pdl_wait();
   const int lane = threadIdx.x & 31;
   const int64_t nwarps = (int64_t)gridDim.x * (blockDim.x >> 5);
   int64_t row = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
@@ -204,6 +240,7 @@ __global__ void vu_add_kernel(const double* __restrict__ V, const double* __rest
 // fL[pos] = f[row at pos]: the L solve's right-hand side in position order, on all SMs
 __global__ void permute_f_kernel(const int32_t* __restrict__ lrow, const double* __restrict__ f,
                                  double* __restrict__ fL, int64_t p) {
+  pdl_wait();
   // gather form: coalesced stores, the random reads of f (15 MB at cfg5) hit L2
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p; i += (int64_t)gridDim.x * blockDim.x)
     fL[i] = __ldg(f + __ldg(lrow + i));
@@ -212,7 +249,7 @@ __global__ void permute_f_kernel(const int32_t* __restrict__ lrow, const double*
 int launch_permute_f(const pslr_ctx* ctx, const double* f, cudaStream_t st) {
   if (ctx->p == 0) return 0;
   const int blocks = 4 * ctx->sm_count;
-  permute_f_kernel<<<blocks, 512, 0, st>>>(ctx->K.LB.lrow, f, ctx->fL, ctx->p);
+  launch_pdl(permute_f_kernel, dim3(blocks), dim3(512), 0, st, ctx->K.LB.lrow, f, ctx->fL, ctx->p);
   return (int)cudaGetLastError();
 }
 
@@ -220,6 +257,7 @@ int launch_permute_f(const pslr_ctx* ctx, const double* f, cudaStream_t st) {
 // caller's two vectors of n, vector-major.  fL2[pos][v] = f_v[row at pos], g2[i][v] = g_v[i].
 __global__ void permute2_kernel(const int32_t* __restrict__ lrow, const double* __restrict__ b, int64_t n,
                                 int64_t p, int64_t q, double* __restrict__ fL2, double* __restrict__ g2) {
+  pdl_wait();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p + q; i += (int64_t)gridDim.x * blockDim.x) {
     if (i < p) {
       const int64_t row = __ldg(lrow + i);
@@ -233,6 +271,7 @@ __global__ void permute2_kernel(const int32_t* __restrict__ lrow, const double* 
 
 __global__ void deinterleave2_kernel(const double* __restrict__ x2, const double* __restrict__ y2, int64_t n,
                                      int64_t p, double* __restrict__ z) {
+  pdl_wait();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const double2 v = (i < p) ? reinterpret_cast<const double2*>(x2)[i] : reinterpret_cast<const double2*>(y2)[i - p];
     z[i] = v.x;
@@ -243,18 +282,18 @@ __global__ void deinterleave2_kernel(const double* __restrict__ x2, const double
 int vt_grid(int64_t q, int sm_count);
 
 int launch_permute2(const pslr_ctx* ctx, const double* b, cudaStream_t st) {
-  permute2_kernel<<<4 * ctx->sm_count, 512, 0, st>>>(ctx->K.LB.lrow, b, ctx->n, ctx->p, ctx->q, ctx->fL2, ctx->g2);
+  launch_pdl(permute2_kernel, dim3(4 * ctx->sm_count), dim3(512), 0, st, ctx->K.LB.lrow, b, ctx->n, ctx->p, ctx->q, ctx->fL2, ctx->g2);
   return (int)cudaGetLastError();
 }
 
 int launch_deinterleave2(const pslr_ctx* ctx, const double* y2, double* z, cudaStream_t st) {
-  deinterleave2_kernel<<<4 * ctx->sm_count, 512, 0, st>>>(ctx->xF2, y2, ctx->n, ctx->p, z);
+  launch_pdl(deinterleave2_kernel, dim3(4 * ctx->sm_count), dim3(512), 0, st, ctx->xF2, y2, ctx->n, ctx->p, z);
   return (int)cudaGetLastError();
 }
 
 int launch_vt_dot_strided(pslr_ctx* ctx, const double* y, int64_t ys, cudaStream_t st) {
   const int g = vt_grid(ctx->q, ctx->sm_count);
-  vt_dot_kernel<<<g, kVtThreads, 0, st>>>(ctx->V, y, ys, ctx->q, (int)ctx->r, ctx->G, ctx->red, ctx->u,
+  launch_pdl(vt_dot_kernel, dim3(g), dim3(kVtThreads), 0, st, ctx->V, y, ys, ctx->q, (int)ctx->r, ctx->G, ctx->red, ctx->u,
                                           ctx->counter);
   return (int)cudaGetLastError();
 }
@@ -262,13 +301,14 @@ int launch_vt_dot_strided(pslr_ctx* ctx, const double* y, int64_t ys, cudaStream
 int launch_vu_add_strided(const pslr_ctx* ctx, const double* y, int64_t ys, double* out, int64_t os,
                           cudaStream_t st) {
   const int64_t blocks = std::min<int64_t>((ctx->q + 7) / 8, 8 * (int64_t)ctx->sm_count);
-  vu_add_kernel<<<(unsigned)std::max<int64_t>(blocks, 1), 256, 0, st>>>(ctx->V, ctx->u, y, ys, out, os, ctx->q,
+  launch_pdl(vu_add_kernel, dim3((unsigned)std::max<int64_t>(blocks, 1)), dim3(256), 0, st, ctx->V, ctx->u, y, ys, out, os, ctx->q,
                                                                         (int)ctx->r);
   return (int)cudaGetLastError();
 }
 
 // y = M x, one thread per row (scipy csr_matvec order).
 __global__ void spmv_kernel(DevCsr M, const double* __restrict__ x, double* __restrict__ y) {
+  pdl_wait();
   const int row = blockIdx.x * blockDim.x + threadIdx.x;
   if (row < M.nrows) y[row] = csr_row(M, row, x);
 }
@@ -295,6 +335,7 @@ __global__ void __launch_bounds__(kCgsThreads, 2)
 cgs_pass_kernel(const double* __restrict__ X, int64_t ld, int k, double* __restrict__ w, int64_t n,
                 const double* __restrict__ h0, double* __restrict__ partials, double* __restrict__ out,
                 unsigned int* counter) {
+  pdl_wait();
   __shared__ double hs[kCgsMaxCols];
   __shared__ double ws[kCgsThreads];
   __shared__ double nred[kCgsWarps];
@@ -409,6 +450,7 @@ __global__ void __launch_bounds__(256)
 cg_update_kernel(double* __restrict__ x, double* __restrict__ r, const double* __restrict__ p,
                  const double* __restrict__ Ap, double alpha, int64_t n, double* __restrict__ partials,
                  double* __restrict__ out, unsigned int* counter) {
+  pdl_wait();
   __shared__ double red[8];
   __shared__ bool last;
   double acc = 0.0;
@@ -466,6 +508,7 @@ __global__ void sqrt_kernel(const double* __restrict__ in, double* __restrict__ 
 
 // p = z + beta p (krylov.py:163)
 __global__ void xpby_kernel(const double* __restrict__ z, double beta, double* __restrict__ p, int64_t n) {
+  pdl_wait();
   for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
     p[i] = z[i] + beta * p[i];
 }
@@ -473,6 +516,7 @@ __global__ void xpby_kernel(const double* __restrict__ z, double beta, double* _
 // w[i] = w[i] - sum_c X[c*ld + i] * h[c]   (w - V h, numpy order: V@h first; k > 128 passes)
 __global__ void gemv_sub_kernel(const double* __restrict__ X, int64_t ld, int k,
                                 const double* __restrict__ h, double* __restrict__ w, int64_t n) {
+  pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double s = 0.0;
@@ -483,6 +527,7 @@ __global__ void gemv_sub_kernel(const double* __restrict__ X, int64_t ld, int k,
 // y[i] = sum_c X[c*ld + i] * h[c]   (V y)
 __global__ void gemv_kernel(const double* __restrict__ X, int64_t ld, int k,
                             const double* __restrict__ h, double* __restrict__ y, int64_t n) {
+  pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double s = 0.0;
@@ -493,12 +538,14 @@ __global__ void gemv_kernel(const double* __restrict__ X, int64_t ld, int k,
 // y = a - b
 __global__ void sub_kernel(const double* __restrict__ a, const double* __restrict__ b,
                            double* __restrict__ y, int64_t n) {
+  pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) y[i] = a[i] - b[i];
 }
 
 // y = y + a
 __global__ void add_inplace_kernel(double* __restrict__ y, const double* __restrict__ a, int64_t n) {
+  pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) y[i] = y[i] + a[i];
 }
@@ -506,6 +553,7 @@ __global__ void add_inplace_kernel(double* __restrict__ y, const double* __restr
 // y = x / s (numpy: w / hnext)
 __global__ void div_scalar_kernel(const double* __restrict__ x, const double* __restrict__ s,
                                   double* __restrict__ y, int64_t n) {
+  pdl_wait();
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) y[i] = x[i] / *s;
 }
@@ -513,6 +561,7 @@ __global__ void div_scalar_kernel(const double* __restrict__ x, const double* __
 // row-major (q x r) <- column-major (ld = q) transpose for the Arnoldi basis
 __global__ void colmajor_to_rowmajor_kernel(const double* __restrict__ X, int64_t ld, int64_t q, int r,
                                             double* __restrict__ Y) {
+  pdl_wait();
   const int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= q * r) return;
   const int64_t i = idx / r;
@@ -522,7 +571,7 @@ __global__ void colmajor_to_rowmajor_kernel(const double* __restrict__ X, int64_
 
 // ---------------------------------------------------------------- host-side launchers
 int launch_correction_core(const pslr_ctx* ctx, cudaStream_t st) {
-  correction_core_kernel<<<1, 256, 0, st>>>(ctx->partials, (int)ctx->s, (int)ctx->r, ctx->G, ctx->u);
+  launch_pdl(correction_core_kernel, dim3(1), dim3(256), 0, st, ctx->partials, (int)ctx->s, (int)ctx->r, ctx->G, ctx->u);
   return (int)cudaGetLastError();
 }
 
@@ -537,7 +586,7 @@ int vt_grid(int64_t q, int sm_count) {
 // s = V^T y over this context's rows (sharded contexts; h lands in ctx->u[r..2r) first)
 int launch_vt_local(pslr_ctx* ctx, const double* y, double* s, cudaStream_t st) {
   const int g = vt_grid(ctx->q, ctx->sm_count);
-  vt_dot_kernel<<<g, kVtThreads, 0, st>>>(ctx->V, y, 1, ctx->q, (int)ctx->r, nullptr, ctx->red, ctx->u,
+  launch_pdl(vt_dot_kernel, dim3(g), dim3(kVtThreads), 0, st, ctx->V, y, 1, ctx->q, (int)ctx->r, nullptr, ctx->red, ctx->u,
                                           ctx->counter);
   if (cudaGetLastError() != cudaSuccess) return 1;
   return (int)cudaMemcpyAsync(s, ctx->u + ctx->r, ctx->r * sizeof(double), cudaMemcpyDeviceToDevice, st);
@@ -546,21 +595,21 @@ int launch_vt_local(pslr_ctx* ctx, const double* y, double* s, cudaStream_t st) 
 // s = V^T y for a strided y (rank-local partial sums; no G)
 int launch_vt_local_strided(pslr_ctx* ctx, const double* y, int64_t ys, double* s, cudaStream_t st) {
   const int g = vt_grid(ctx->q, ctx->sm_count);
-  vt_dot_kernel<<<g, kVtThreads, 0, st>>>(ctx->V, y, ys, ctx->q, (int)ctx->r, nullptr, ctx->red, ctx->u,
+  launch_pdl(vt_dot_kernel, dim3(g), dim3(kVtThreads), 0, st, ctx->V, y, ys, ctx->q, (int)ctx->r, nullptr, ctx->red, ctx->u,
                                           ctx->counter);
   if (cudaGetLastError() != cudaSuccess) return 1;
   return (int)cudaMemcpyAsync(s, ctx->u + ctx->r, ctx->r * sizeof(double), cudaMemcpyDeviceToDevice, st);
 }
 
 int launch_gs(pslr_ctx* ctx, const double* s, cudaStream_t st) {
-  gs_kernel<<<1, 128, 0, st>>>(ctx->G, s, ctx->u, (int)ctx->r);
+  launch_pdl(gs_kernel, dim3(1), dim3(128), 0, st, ctx->G, s, ctx->u, (int)ctx->r);
   return (int)cudaGetLastError();
 }
 
 // u = G V^T y  (writes ctx->u[0..r), h in ctx->u[r..2r))
 int launch_vt_dot(pslr_ctx* ctx, const double* y, cudaStream_t st) {
   const int g = vt_grid(ctx->q, ctx->sm_count);
-  vt_dot_kernel<<<g, kVtThreads, 0, st>>>(ctx->V, y, 1, ctx->q, (int)ctx->r, ctx->G, ctx->red,
+  launch_pdl(vt_dot_kernel, dim3(g), dim3(kVtThreads), 0, st, ctx->V, y, 1, ctx->q, (int)ctx->r, ctx->G, ctx->red,
                                           ctx->u, ctx->counter);
   return (int)cudaGetLastError();
 }
@@ -571,13 +620,13 @@ int launch_vu_add(const pslr_ctx* ctx, const double* y, double* out, cudaStream_
   const int64_t cap = 8 * (int64_t)ctx->sm_count;
   if (blocks > cap) blocks = cap;
   if (blocks < 1) blocks = 1;
-  vu_add_kernel<<<(unsigned)blocks, 256, 0, st>>>(ctx->V, ctx->u, y, 1, out, 1, ctx->q, (int)ctx->r);
+  launch_pdl(vu_add_kernel, dim3((unsigned)blocks), dim3(256), 0, st, ctx->V, ctx->u, y, 1, out, 1, ctx->q, (int)ctx->r);
   return (int)cudaGetLastError();
 }
 
 int launch_spmv(const DevCsr& M, const double* x, double* y, cudaStream_t st) {
   if (M.nrows == 0) return 0;
-  spmv_kernel<<<(M.nrows + 255) / 256, 256, 0, st>>>(M, x, y);
+  launch_pdl(spmv_kernel, dim3((M.nrows + 255) / 256), dim3(256), 0, st, M, x, y);
   return (int)cudaGetLastError();
 }
 
@@ -602,7 +651,7 @@ static int launch_cgs_w(pslr_ctx* ctx, const double* X, int64_t ld, int k, doubl
     resident = std::min(b, 4);
   }
   const int g = (int)std::min<int64_t>(dot_grid(n, ctx->sm_count), (int64_t)resident * ctx->sm_count);
-  cgs_pass_kernel<MODE, CPW><<<g, kCgsThreads, 0, st>>>(X, ld, k, w, n, h0, ctx->red, out, ctx->counter);
+  launch_pdl(cgs_pass_kernel<MODE, CPW>, dim3(g), dim3(kCgsThreads), 0, st, X, ld, k, w, n, h0, ctx->red, out, ctx->counter);
   return (int)cudaGetLastError();
 }
 
@@ -620,7 +669,7 @@ static int launch_cgs(pslr_ctx* ctx, const double* X, int64_t ld, int k, double*
 static int launch_gemv_sub(const double* X, int64_t ld, int k, const double* h, double* w, int64_t n,
                            cudaStream_t st) {
   if (n == 0) return 0;
-  gemv_sub_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(X, ld, k, h, w, n);
+  launch_pdl(gemv_sub_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, X, ld, k, h, w, n);
   return (int)cudaGetLastError();
 }
 
@@ -651,49 +700,49 @@ int launch_sub_norm(pslr_ctx* ctx, const double* X, int64_t ld, int k, const dou
 int launch_cg_update(pslr_ctx* ctx, double* x, double* r, const double* p, const double* Ap, double alpha,
                      int64_t n, double* out, cudaStream_t st) {
   const int g = dot_grid(n, ctx->sm_count);
-  cg_update_kernel<<<g, 256, 0, st>>>(x, r, p, Ap, alpha, n, ctx->red, out, ctx->counter);
+  launch_pdl(cg_update_kernel, dim3(g), dim3(256), 0, st, x, r, p, Ap, alpha, n, ctx->red, out, ctx->counter);
   return (int)cudaGetLastError();
 }
 
 int launch_sqrt(const double* in, double* out, cudaStream_t st) {
-  sqrt_kernel<<<1, 1, 0, st>>>(in, out);
+  launch_pdl(sqrt_kernel, dim3(1), dim3(1), 0, st, in, out);
   return (int)cudaGetLastError();
 }
 
 int launch_xpby(const double* z, double beta, double* p, int64_t n, cudaStream_t st) {
   if (n == 0) return 0;
-  xpby_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 4096), 256, 0, st>>>(z, beta, p, n);
+  launch_pdl(xpby_kernel, dim3((unsigned)std::min<int64_t>((n + 255) / 256, 4096)), dim3(256), 0, st, z, beta, p, n);
   return (int)cudaGetLastError();
 }
 
 int launch_gemv(const double* X, int64_t ld, int k, const double* h, double* y, int64_t n,
                 cudaStream_t st) {
   if (n == 0) return 0;
-  gemv_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(X, ld, k, h, y, n);
+  launch_pdl(gemv_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, X, ld, k, h, y, n);
   return (int)cudaGetLastError();
 }
 
 int launch_sub(const double* a, const double* b, double* y, int64_t n, cudaStream_t st) {
   if (n == 0) return 0;
-  sub_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(a, b, y, n);
+  launch_pdl(sub_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, a, b, y, n);
   return (int)cudaGetLastError();
 }
 
 int launch_add_inplace(double* y, const double* a, int64_t n, cudaStream_t st) {
   if (n == 0) return 0;
-  add_inplace_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(y, a, n);
+  launch_pdl(add_inplace_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, y, a, n);
   return (int)cudaGetLastError();
 }
 
 int launch_div_scalar(const double* x, const double* s, double* y, int64_t n, cudaStream_t st) {
   if (n == 0) return 0;
-  div_scalar_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(x, s, y, n);
+  launch_pdl(div_scalar_kernel, dim3((unsigned)((n + 255) / 256)), dim3(256), 0, st, x, s, y, n);
   return (int)cudaGetLastError();
 }
 
 int launch_transpose_basis(const double* X, int64_t ld, int64_t q, int r, double* Y, cudaStream_t st) {
   if (q * r == 0) return 0;
-  colmajor_to_rowmajor_kernel<<<(unsigned)((q * r + 255) / 256), 256, 0, st>>>(X, ld, q, r, Y);
+  launch_pdl(colmajor_to_rowmajor_kernel, dim3((unsigned)((q * r + 255) / 256)), dim3(256), 0, st, X, ld, q, r, Y);
   return (int)cudaGetLastError();
 }
 
