@@ -447,7 +447,10 @@ def run_single(args):
                 "d2h_bytes_per_step": 8 * n, "ms_per_step": ms_e2e / args.e2e_steps,
                 "single_call": {"api": "PslrPreconditioner.apply(numpy)", "ms": sc_s * 1e3,
                                 "value": bytes_apply / sc_s / 1e9}},
-        "gpu_launches": (launches_per_apply + (0 if NV == 1 else (3 if r > 0 else 1))) * calls,
+        # per call: the profiled launch groups (+ the two-vector permute/deinterleave, the
+        # correction's second kernel) + one all-SM E y kernel per Horner and last step
+        "gpu_launches": (launches_per_apply + (0 if NV == 1 else (3 if r > 0 else 1))
+                         + ((m + 1) if os.environ.get("PSLR_EY_ALLSM", "1") != "0" else 0)) * calls,
         "solves": solves,
         "clocks": clk,
         "levels": {k: info[k] for k in ("maxdepth_LB", "maxdepth_UB", "maxdepth_LC", "maxdepth_UC")},

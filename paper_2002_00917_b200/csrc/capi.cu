@@ -642,6 +642,7 @@ int pslr_ctx_create_packed(pslr_ctx** out, int device, const pslr_system* sys, c
   if (configure_step_kernel(1, ctx->K.smem_bytes) != 0)
     return bail(fail(PSLR_ECUDA, "cannot configure the step kernel's shared memory"));
   ctx->pdl = env_int("PSLR_PDL", 1) != 0;
+  ctx->ey_all_sm = env_int("PSLR_EY_ALLSM", 1) != 0;
   ctx->K.dbg = (int)env_int("PSLR_DBG", 0);
   ctx->K.l2ahead = env_int("PSLR_L2AHEAD", 0);
   if (env_int("PSLR_TRACE", 0)) {  // diagnostics: timeline of CTA 0 (pslr_debug_trace)
@@ -710,6 +711,7 @@ int pslr_ctx_create_packed(pslr_ctx** out, int device, const pslr_system* sys, c
         }
       eo[b + 1] = (int32_t)(er.size() / 4);
     }
+    ctx->K.nerows = eo[s];
     if (er.empty()) er.assign(4, 0);
     if ((rc = upload(ctx, er, &ctx->K.erows))) return bail(rc);
     if ((rc = upload(ctx, eo, &ctx->K.erow_off))) return bail(rc);

@@ -131,6 +131,8 @@ struct StepArgs {
   double* yout = nullptr;      // q output
   double* partials = nullptr;  // [s][r] V^T yout partial sums (nullable)
   int tag = 0;                 // launch kind, for pslr_apply_profiled
+  int ey_done = 0;             // set by launch_step: the E y rows of the L right-hand side were
+                               // written by the all-SM ey_rhs_kernel (no in-kernel prepass)
   int xpos = 0;                // set by launch_step: xb in U-position order (F read via Fpos)
 };
 
@@ -144,6 +146,7 @@ struct StepConst {
   const int32_t* erows = nullptr;     // int4 per interior row with E entries, grouped by block:
                                       // {L-position, row, E.ptr[row], E.ptr[row+1]}
   const int32_t* erow_off = nullptr;  // s+1
+  int nerows = 0;                     // erow_off[s]
   const double* V = nullptr;
   int r = 0;
   double* rhsB = nullptr;  // p: L_B right-hand side in L-position order
@@ -173,6 +176,7 @@ struct pslr_ctx {
   int64_t n = 0, p = 0, q = 0, s = 0, r = 0;
   int64_t nghost = 0;  // sharded contexts: ghost interface columns of C, Cg and A
   bool pdl = true;     // programmatic dependent launch of the step kernel (PSLR_PDL=0: off)
+  bool ey_all_sm = true;  // E y rows of the L right-hand side by the all-SM kernel (PSLR_EY_ALLSM=0: prepass)
   const pslr_ctx* parent = nullptr;  // clones: the context whose read-only data they share
   // shared by a context and its clones: use_count() - 1 = live clones of the parent
   std::shared_ptr<int> family = std::make_shared<int>(0);

@@ -830,7 +830,7 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
     }
     // pass 2: rows with E entries get the E y term: f - E y, or E y alone (scipy
     // csr_matvec order), kIn rows per thread in flight; one int4 record per row
-    if (a.b1 == BT_EY || a.b2 == BT_EY) {
+    if ((a.b1 == BT_EY || a.b2 == BT_EY) && !a.ey_done) {
       if (!a.fL && !ey_only) consumer_sync();
       constexpr int kIn = PSLR_PRE_E;  // E rows in flight per thread (dependent chain: record, E entry, y)
       const int e0 = K.erow_off[b], e1 = K.erow_off[b + 1];
@@ -918,6 +918,27 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
   trace_cta(K, 6);
 }
 
+// The E y rows of an L_B right-hand side for every block at once (all SMs; the in-kernel
+// prepass runs them on the one SM per block, ~15 us of dependent global loads before the
+// L phase can start): rhs[pos] = E_row y (ey_only) or rhs[pos] = rhs[pos] - E_row y (the
+// last step, rhs = f in L-position order), the E row summed in CSR order (scipy
+// csr_matvec) exactly as the prepass does.
+template <int NV>
+__global__ void __launch_bounds__(256) ey_rhs_kernel(const int4* __restrict__ erows, int ne, DevCsr E,
+                                                     const double* __restrict__ yE, double* rhs, int sub) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= ne) return;
+  const int4 r = __ldg(erows + i);
+  vt<NV> sum = vzero<NV>();
+  for (int e = r.z; e < r.w; ++e) sum = vmadd(sum, __ldg(E.val + e), vldg<NV>(yE, __ldg(E.col + e)));
+  if (sub) {
+    vst(rhs, r.x, vsub(vld<NV>(rhs, r.x), sum));
+  } else {
+    vst(rhs, r.x, sum);
+  }
+}
+
 int configure_step_kernel(int nv, int smem_bytes) {
   auto set = [&](auto kern) {
     return (int)cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
@@ -938,6 +959,28 @@ int launch_step(const pslr_ctx* ctx, const StepArgs& a_in, cudaStream_t st, int 
   StepArgs a = a_in;
   a.xpos = (a.b1 != BT_NONE && (a.i1 == IT_FX || a.i2 == IT_FX)) ? 1 : 0;
   const StepConst& K = (nv == 2) ? ctx->K2 : ctx->K;
+  // E y rows of the L right-hand side by the all-SM kernel when the rhs array is one the
+  // prepass would only patch at the E rows (E y alone into rhsE, or f - E y into fL)
+  const bool ey_only = a.b1 == BT_EY && a.b2 == BT_NONE;
+  const bool f_ey = a.fL && a.b1 == BT_F && a.b2 == BT_EY;
+  if ((ey_only || f_ey) && K.nerows > 0 && ctx->ey_all_sm) {
+    cudaLaunchConfig_t ec = {};
+    ec.gridDim = dim3((unsigned)((K.nerows + 255) / 256));
+    ec.blockDim = dim3(256);
+    ec.stream = st;
+    cudaLaunchAttribute eat[1];
+    eat[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    eat[0].val.programmaticStreamSerializationAllowed = ctx->pdl ? 1 : 0;
+    ec.attrs = eat;
+    ec.numAttrs = 1;
+    double* rhs = ey_only ? K.rhsE : a.fL;
+    const int sub = f_ey ? 1 : 0;
+    const int4* er = reinterpret_cast<const int4*>(K.erows);
+    const cudaError_t e = (nv == 2) ? cudaLaunchKernelEx(&ec, ey_rhs_kernel<2>, er, K.nerows, K.E, a.yE, rhs, sub)
+                                    : cudaLaunchKernelEx(&ec, ey_rhs_kernel<1>, er, K.nerows, K.E, a.yE, rhs, sub);
+    if (e != cudaSuccess) return (int)e;
+    a.ey_done = 1;
+  }
   // programmatic stream serialization: the step kernel's CTAs (one per subdomain, far
   // fewer than the 148 SMs) launch and stage their first factor chunks while the
   // previous kernel drains; griddepcontrol.wait orders the data accesses
