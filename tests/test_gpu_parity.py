@@ -349,6 +349,38 @@ def test_explicit_sd_layout_bitexact(monkeypatch):
     np.testing.assert_array_equal(pg.apply_neumann(P.ctx, meta["m"], d["v"]), d["apply_neumann"])
 
 
+def test_ey_prepass_and_all_sm_kernel_bitexact(monkeypatch):
+    """The E y rows of the L right-hand sides: the all-SM ey_rhs_kernel (default) and the
+    step kernel's own prepass (PSLR_EY_ALLSM=0) give the same bits — apply_Es, the Horner
+    series, E_rr and the full apply (one and two vectors per call)."""
+    import torch
+    import paper_2002_00917_b200 as pg
+    from paper_2002_00917_b200 import _lib
+    name = "lap3d6_s4_dt1e-2"
+    meta = G["apply"][name]
+    d = load_npz(f"apply_{name}.npz")
+    A = csr_from(d, "A")
+    cfg = pg.PslrConfig(num_subdomains=meta["s"], series_degree=meta["m"], rank=meta["rank"],
+                        droptol=meta["droptol"], seed=meta["seed"])
+    out = []
+    for env in ("1", "0"):
+        monkeypatch.setenv("PSLR_EY_ALLSM", env)
+        P = pg.build(A, cfg)
+        n = P.system.n
+        B2 = torch.from_numpy(np.random.default_rng(3).standard_normal((2, n))).cuda()
+        Z2 = torch.empty_like(B2)
+        P.device.ensure_correction(P.correction)
+        _lib.check(_lib.fns["pslr_apply_multi"](P.device.handle, meta["m"], 2, B2.data_ptr(), Z2.data_ptr(),
+                                                P.device.stream()))
+        torch.cuda.synchronize()
+        out.append((pg.apply_Es(P.ctx, d["v"]), pg.apply_neumann(P.ctx, meta["m"], d["v"]),
+                    pg.apply_Err(P.ctx, meta["m"], d["v"]), P.apply(d["b"]), Z2.cpu().numpy()))
+    for a, b in zip(*out):
+        np.testing.assert_array_equal(a, b)
+    np.testing.assert_array_equal(out[0][0], d["apply_Es"])
+    np.testing.assert_array_equal(out[0][1], d["apply_neumann"])
+
+
 def _oracle_ctx(P):
     from oracle import pslr_oracle as O
     ps = P.system
