@@ -431,6 +431,7 @@ static int ensure_nv2(pslr_ctx* ctx) {
   RET(alloc_scratch(ctx, &K2.rhsB, 2 * (p + 2)));
   RET(alloc_scratch(ctx, &K2.rhsE, 2 * (p + 2)));  // zeroed: only E rows are ever written
   RET(alloc_scratch(ctx, &K2.zB, 2 * (p + 2)));
+  RET(alloc_scratch(ctx, &K2.cgy, 2 * (q + 1)));
   RET(alloc_scratch(ctx, &K2.rhsC, 2 * (q + 2)));
   RET(alloc_scratch(ctx, &K2.zC, 2 * (q + 2)));
   RET(alloc_scratch(ctx, &ctx->fL2, 2 * (p + 2)));
@@ -720,6 +721,7 @@ int pslr_ctx_create_packed(pslr_ctx** out, int device, const pslr_system* sys, c
   if ((rc = alloc_scratch(ctx, &ctx->K.rhsB, p + 2))) return bail(rc);
   if ((rc = alloc_scratch(ctx, &ctx->K.rhsE, p + 2))) return bail(rc);  // zeroed
   if ((rc = alloc_scratch(ctx, &ctx->K.zB, p + 2))) return bail(rc);
+  if ((rc = alloc_scratch(ctx, &ctx->K.cgy, q + 1))) return bail(rc);
   if ((rc = alloc_scratch(ctx, &ctx->K.rhsC, q + 2))) return bail(rc);
   if ((rc = alloc_scratch(ctx, &ctx->K.zC, q + 2))) return bail(rc);
   if ((rc = alloc_scratch(ctx, &ctx->xb, p))) return bail(rc);
@@ -1205,6 +1207,7 @@ int pslr_ctx_clone(const pslr_ctx* src, pslr_ctx** out) {
   if ((rc = alloc_scratch(ctx, &ctx->K.rhsB, p + 2))) return bail(rc);
   if ((rc = alloc_scratch(ctx, &ctx->K.rhsE, p + 2))) return bail(rc);  // zeroed
   if ((rc = alloc_scratch(ctx, &ctx->K.zB, p + 2))) return bail(rc);
+  if ((rc = alloc_scratch(ctx, &ctx->K.cgy, q + 1))) return bail(rc);
   if ((rc = alloc_scratch(ctx, &ctx->K.rhsC, q + 2))) return bail(rc);
   if ((rc = alloc_scratch(ctx, &ctx->K.zC, q + 2))) return bail(rc);
   if ((rc = alloc_scratch(ctx, &ctx->xb, p))) return bail(rc);

@@ -110,7 +110,7 @@ int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAna
 
 // Terms of the per-subdomain fused step (see kernels.cu: subdomain_step_kernel).
 enum BTerm : int { BT_NONE = 0, BT_F = 1, BT_EY = 2 };
-enum ITerm : int { IT_NONE = 0, IT_G = 1, IT_FX = 2, IT_CY = 3, IT_CGY = 4, IT_VU = 5 };
+enum ITerm : int { IT_NONE = 0, IT_G = 1, IT_FX = 2, IT_CY = 3, IT_CGY = 4, IT_VU = 5, IT_PRE = 6 };
 
 struct StepArgs {
   // ---- interior (B) phase:  rhs = b1 [(-) b2];  xb = B^{-1} rhs
@@ -126,6 +126,7 @@ struct StepArgs {
   const double* g = nullptr;   // q-vector for IT_G
   const double* yC = nullptr;  // q-vector for IT_CY / IT_CGY
   const double* u = nullptr;   // r-vector for IT_VU
+  const double* pre = nullptr; // q-vector for IT_PRE (C_g y by the all-SM pre-kernel)
   int do_c0 = 0;
   const double* cadd = nullptr;
   double* yout = nullptr;      // q output
@@ -155,6 +156,7 @@ struct StepConst {
   double* zB = nullptr;    // p: L_B output / U_B intermediate in U-position order
   double* rhsC = nullptr;  // q
   double* zC = nullptr;    // q
+  double* cgy = nullptr;   // q: C_g y of the step, by the all-SM pre-kernel (launch_step)
   int ring_mask = 0;       // W - 1
   int nst = 0;             // pipeline stages
   int stage_bytes = 0;

@@ -713,6 +713,10 @@ __device__ __forceinline__ void iface_terms4(int kind, const int (&row)[4], cons
     case IT_FX: spmv4<false, NV>(XPOS ? K.Fpos : K.F, row, ok, a.xb, t); break;
     case IT_CY: spmv4<true, NV>(K.C, row, ok, a.yC, t); break;
     case IT_CGY: spmv4<true, NV>(K.Cg, row, ok, a.yC, t); break;
+    case IT_PRE:
+#pragma unroll
+      for (int j = 0; j < 4; ++j) t[j] = ok[j] ? vldg<NV>(a.pre, row[j]) : vzero<NV>();
+      break;
     default:
 #pragma unroll
       for (int j = 0; j < 4; ++j) t[j] = vzero<NV>();
@@ -918,24 +922,35 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
   trace_cta(K, 6);
 }
 
-// The E y rows of an L_B right-hand side for every block at once (all SMs; the in-kernel
-// prepass runs them on the one SM per block, ~15 us of dependent global loads before the
-// L phase can start): rhs[pos] = E_row y (ey_only) or rhs[pos] = rhs[pos] - E_row y (the
-// last step, rhs = f in L-position order), the E row summed in CSR order (scipy
-// csr_matvec) exactly as the prepass does.
+// The parts of a step that only need vectors of earlier launches, for every block at once
+// on all SMs (in the step kernel they run on the one SM per block, as dependent global
+// loads on the critical path — the E y prepass alone took 13-17 us before the L phase):
+//   threads [0, ne): the E y rows of the L_B right-hand side, rhs[pos] = E_row y (ey_only)
+//                    or rhs[pos] = rhs[pos] - E_row y (the last step, rhs = f in L order);
+//   threads [ne, ne + nq): cgy[i] = C_g row i . y, the interface phase's C_g term.
+// Every row is summed in CSR order from 0 (scipy csr_matvec), exactly as the step kernel.
 template <int NV>
-__global__ void __launch_bounds__(256) ey_rhs_kernel(const int4* __restrict__ erows, int ne, DevCsr E,
-                                                     const double* __restrict__ yE, double* rhs, int sub) {
+__global__ void __launch_bounds__(256) pre_step_kernel(const int4* __restrict__ erows, int ne, DevCsr E,
+                                                       const double* __restrict__ yE, double* rhs, int sub,
+                                                       DevCsr Cg, const double* __restrict__ yC, double* cgy,
+                                                       int nq) {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= ne) return;
-  const int4 r = __ldg(erows + i);
-  vt<NV> sum = vzero<NV>();
-  for (int e = r.z; e < r.w; ++e) sum = vmadd(sum, __ldg(E.val + e), vldg<NV>(yE, __ldg(E.col + e)));
-  if (sub) {
-    vst(rhs, r.x, vsub(vld<NV>(rhs, r.x), sum));
-  } else {
-    vst(rhs, r.x, sum);
+  if (i < ne) {
+    const int4 r = __ldg(erows + i);
+    vt<NV> sum = vzero<NV>();
+    for (int e = r.z; e < r.w; ++e) sum = vmadd(sum, __ldg(E.val + e), vldg<NV>(yE, __ldg(E.col + e)));
+    if (sub) {
+      vst(rhs, r.x, vsub(vld<NV>(rhs, r.x), sum));
+    } else {
+      vst(rhs, r.x, sum);
+    }
+  } else if (i - ne < nq) {
+    const int row = i - ne;
+    vt<NV> sum = vzero<NV>();
+    const int e1 = __ldg(Cg.ptr + row + 1);
+    for (int e = __ldg(Cg.ptr + row); e < e1; ++e) sum = vmadd(sum, __ldg(Cg.val + e), vldg<NV>(yC, __ldg(Cg.col + e)));
+    vst(cgy, row, sum);
   }
 }
 
@@ -959,13 +974,16 @@ int launch_step(const pslr_ctx* ctx, const StepArgs& a_in, cudaStream_t st, int 
   StepArgs a = a_in;
   a.xpos = (a.b1 != BT_NONE && (a.i1 == IT_FX || a.i2 == IT_FX)) ? 1 : 0;
   const StepConst& K = (nv == 2) ? ctx->K2 : ctx->K;
-  // E y rows of the L right-hand side by the all-SM kernel when the rhs array is one the
-  // prepass would only patch at the E rows (E y alone into rhsE, or f - E y into fL)
+  // E y rows of the L right-hand side (when the rhs array is one the prepass would only
+  // patch at the E rows: E y alone into rhsE, or f - E y into fL) and the C_g y term of the
+  // interface phase, by the all-SM pre-kernel
   const bool ey_only = a.b1 == BT_EY && a.b2 == BT_NONE;
   const bool f_ey = a.fL && a.b1 == BT_F && a.b2 == BT_EY;
-  if ((ey_only || f_ey) && K.nerows > 0 && ctx->ey_all_sm) {
+  const int ne = ((ey_only || f_ey) && ctx->ey_all_sm) ? K.nerows : 0;
+  const int nq = (a.i2 == IT_CGY && K.cgy && ctx->ey_all_sm) ? (int)K.Cg.nrows : 0;
+  if (ne > 0 || nq > 0) {
     cudaLaunchConfig_t ec = {};
-    ec.gridDim = dim3((unsigned)((K.nerows + 255) / 256));
+    ec.gridDim = dim3((unsigned)((ne + nq + 255) / 256));
     ec.blockDim = dim3(256);
     ec.stream = st;
     cudaLaunchAttribute eat[1];
@@ -976,10 +994,15 @@ int launch_step(const pslr_ctx* ctx, const StepArgs& a_in, cudaStream_t st, int 
     double* rhs = ey_only ? K.rhsE : a.fL;
     const int sub = f_ey ? 1 : 0;
     const int4* er = reinterpret_cast<const int4*>(K.erows);
-    const cudaError_t e = (nv == 2) ? cudaLaunchKernelEx(&ec, ey_rhs_kernel<2>, er, K.nerows, K.E, a.yE, rhs, sub)
-                                    : cudaLaunchKernelEx(&ec, ey_rhs_kernel<1>, er, K.nerows, K.E, a.yE, rhs, sub);
+    const cudaError_t e =
+        (nv == 2) ? cudaLaunchKernelEx(&ec, pre_step_kernel<2>, er, ne, K.E, a.yE, rhs, sub, K.Cg, a.yC, K.cgy, nq)
+                  : cudaLaunchKernelEx(&ec, pre_step_kernel<1>, er, ne, K.E, a.yE, rhs, sub, K.Cg, a.yC, K.cgy, nq);
     if (e != cudaSuccess) return (int)e;
-    a.ey_done = 1;
+    if (ne > 0) a.ey_done = 1;
+    if (nq > 0) {
+      a.i2 = IT_PRE;
+      a.pre = K.cgy;
+    }
   }
   // programmatic stream serialization: the step kernel's CTAs (one per subdomain, far
   // fewer than the 148 SMs) launch and stage their first factor chunks while the
