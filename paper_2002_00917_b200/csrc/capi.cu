@@ -107,17 +107,24 @@ struct PackedSystem {
   int64_t W = 0, SB = 0, reach = 0, far = 0;
   int64_t levels[4] = {0, 0, 0, 0}, depth[4] = {0, 0, 0, 0}, nnz[4] = {0, 0, 0, 0};
   PackedFactor F[4];                 // LB, UB, LC, UC
+  // the factor streams again at the two-vector launches' chunk size SB2 (empty: SB2 == SB):
+  // one vector per launch (the latency a GMRES iteration sees) prefers larger chunks and
+  // fewer stages, two vectors per launch (whose ring and rhs slices are twice as large)
+  // more stages
+  int64_t SB2 = 0;
+  TriHost H2[4];
   std::vector<int32_t> ub_pos;       // U_B: row -> U-position (x order, Fpos columns)
   std::vector<int32_t> lb_pos;       // L_B: row -> L-position (E rows' rhs placement)
 };
 
-constexpr uint64_t kPackMagic = 0x31764b4150524c53ull;  // "SLRPAKv1"
+constexpr uint64_t kPackMagic = 0x32764b4150524c53ull;  // "SLRPAKv2" (two chunk sizes)
 
 // Level analysis of the four factors, the ring size W (from the reach and the device's
 // shared memory) and the streamed chunks of every block (pack.cpp).
 static int pack_system(const pslr_system* sys, const std::vector<int64_t>& ioff, const std::vector<int64_t>& foff,
-                       int64_t smem_optin, int64_t SB, int64_t wmax, PackedSystem& P) {
+                       int64_t smem_optin, int64_t SB, int64_t SB2, int64_t wmax, PackedSystem& P) {
   P.n = sys->n;
+  P.SB2 = SB2;
   P.p = sys->p;
   P.q = sys->q;
   P.s = sys->s;
@@ -153,6 +160,12 @@ static int pack_system(const pslr_system* sys, const std::vector<int64_t>& ioff,
                     nm[2 * pair + 1]));
     RET(emit_factor(*M[2 * pair], off, AL, W, SB, kStepThreads, AU.pos_of_row, AU.pos_of_row, P.F[2 * pair].H,
                     nm[2 * pair]));
+    if (SB2 != SB) {
+      RET(emit_factor(*M[2 * pair + 1], off, AU, W, SB2, kStepThreads, AU.pos_of_row, row_id, P.H2[2 * pair + 1],
+                      nm[2 * pair + 1]));
+      RET(emit_factor(*M[2 * pair], off, AL, W, SB2, kStepThreads, AU.pos_of_row, AU.pos_of_row, P.H2[2 * pair],
+                      nm[2 * pair]));
+    }
     P.F[2 * pair].pos_of_row = AL.pos_of_row;
     P.F[2 * pair].row_at_pos = AL.row_at_pos;
     P.far += P.F[2 * pair].H.far + P.F[2 * pair + 1].H.far;
@@ -209,7 +222,7 @@ static void serialize(const PackedSystem& P, std::vector<uint8_t>& out) {
   w.put(kPackMagic);
   w.put<int64_t>(kStepThreads);
   w.put<int64_t>(kChunkRows);
-  for (int64_t v : {P.n, P.p, P.q, P.s, P.W, P.SB, P.reach, P.far}) w.put(v);
+  for (int64_t v : {P.n, P.p, P.q, P.s, P.W, P.SB, P.SB2, P.reach, P.far}) w.put(v);
   for (int f = 0; f < 4; ++f) {
     w.put(P.levels[f]);
     w.put(P.depth[f]);
@@ -220,6 +233,9 @@ static void serialize(const PackedSystem& P, std::vector<uint8_t>& out) {
     w.put(P.F[f].H.far);
     w.vec(P.F[f].pos_of_row);
     w.vec(P.F[f].row_at_pos);
+    w.vec(P.H2[f].data);
+    w.vec(P.H2[f].chunks);
+    w.vec(P.H2[f].blk_chunk);
   }
   w.vec(P.ub_pos);
   w.vec(P.lb_pos);
@@ -229,7 +245,7 @@ static void serialize(const PackedSystem& P, std::vector<uint8_t>& out) {
 // a blob packed for this system, this build of the kernel and a ring / stage plan the
 // device can hold; anything else is rejected (the caller repacks)
 static bool deserialize(const void* blob, int64_t len, const pslr_system* sys, int64_t smem_optin, int64_t SB,
-                        PackedSystem& P) {
+                        int64_t SB2, PackedSystem& P) {
   Reader r{static_cast<const uint8_t*>(blob), len};
   if (r.get<uint64_t>() != kPackMagic || r.get<int64_t>() != kStepThreads || r.get<int64_t>() != kChunkRows)
     return false;
@@ -239,9 +255,11 @@ static bool deserialize(const void* blob, int64_t len, const pslr_system* sys, i
   P.s = r.get<int64_t>();
   P.W = r.get<int64_t>();
   P.SB = r.get<int64_t>();
+  P.SB2 = r.get<int64_t>();
   P.reach = r.get<int64_t>();
   P.far = r.get<int64_t>();
-  if (!r.ok || P.n != sys->n || P.p != sys->p || P.q != sys->q || P.s != sys->s || P.SB != SB) return false;
+  if (!r.ok || P.n != sys->n || P.p != sys->p || P.q != sys->q || P.s != sys->s || P.SB != SB || P.SB2 != SB2)
+    return false;
   const pslr_csr* M[4] = {&sys->LB, &sys->UB, &sys->LC, &sys->UC};
   for (int f = 0; f < 4; ++f) {
     P.levels[f] = r.get<int64_t>();
@@ -254,7 +272,11 @@ static bool deserialize(const void* blob, int64_t len, const pslr_system* sys, i
     P.F[f].H.far = r.get<int64_t>();
     r.vec(P.F[f].pos_of_row);
     r.vec(P.F[f].row_at_pos);
+    r.vec(P.H2[f].data);
+    r.vec(P.H2[f].chunks);
+    r.vec(P.H2[f].blk_chunk);
     if ((int64_t)P.F[f].H.blk_chunk.size() != P.s + 1) return false;
+    if ((SB2 != SB) != ((int64_t)P.H2[f].blk_chunk.size() == P.s + 1)) return false;
   }
   r.vec(P.ub_pos);
   r.vec(P.lb_pos);
@@ -418,12 +440,17 @@ static int ensure_nv2(pslr_ctx* ctx) {
   if (ctx->nv2_ready) return PSLR_OK;
   const int64_t p = ctx->p, q = ctx->q;
   StepConst K2 = ctx->K;
-  const int64_t W = (int64_t)ctx->K.ring_mask + 1, SB = ctx->K.stage_bytes, CTL = kCtlBytes;
+  K2.LB = ctx->tri2[0];
+  K2.UB = ctx->tri2[1];
+  K2.LC = ctx->tri2[2];
+  K2.UC = ctx->tri2[3];
+  const int64_t W = (int64_t)ctx->K.ring_mask + 1, SB = ctx->sb2, CTL = kCtlBytes;
   const int64_t RB2 = ((16 * (kChunkRows + 2)) + 127) / 128 * 128;
   int64_t nst = (ctx->smem_optin - 1024 - CTL - W * 16 - 128) / (SB + RB2);
   nst = std::min<int64_t>(nst, 8);
   if (nst < 2) return fail(PSLR_EINVAL, "not enough shared memory for two right-hand sides per launch");
   K2.nst = (int)nst;
+  K2.stage_bytes = (int)SB;
   K2.rhs_stride = (int)(RB2 / 8);
   K2.smem_bytes = (int)(CTL + W * 16 + 128 + nst * (SB + RB2));
   if (configure_step_kernel(2, K2.smem_bytes) != 0)
@@ -609,14 +636,18 @@ int pslr_ctx_create_packed(pslr_ctx** out, int device, const pslr_system* sys, c
   // ---- the packed format: from the caller's blob when it fits this system and device,
   // else level analysis + ring plan + streamed chunks (pack_system)
   // Shared-memory plan: nst stages of (chunk bytes SB + rhs slice RB) and a W-slot ring.
-  const int64_t SB = env_int("PSLR_STAGE_BYTES", 32 * 1024);
+  // chunk size of the one-vector launches (SB) and of the two-vector launches (SB2): one
+  // vector at a time runs 1.8 % faster with 45 KB chunks in 3 stages, two vectors per
+  // launch 5 % slower than with 32 KB chunks in 4 stages (cfg5, round 2)
+  const int64_t SB = env_int("PSLR_STAGE_BYTES", 45 * 1024);
+  const int64_t SB2 = env_int("PSLR_STAGE_BYTES2", 32 * 1024);
   const int64_t RB = ((8 * (kChunkRows + 2)) + 127) / 128 * 128;
   PackedSystem P;
-  const bool reuse = blob_in && blob_len > 0 && deserialize(blob_in, blob_len, sys, smem_optin, SB, P);
+  const bool reuse = blob_in && blob_len > 0 && deserialize(blob_in, blob_len, sys, smem_optin, SB, SB2, P);
   if (reused) *reused = reuse ? 1 : 0;
   if (!reuse) {
     P = PackedSystem();
-    if ((rc = pack_system(sys, ctx->interior_off, ctx->interface_off, smem_optin, SB,
+    if ((rc = pack_system(sys, ctx->interior_off, ctx->interface_off, smem_optin, SB, SB2,
                           env_int("PSLR_RING", 4096), P)))
       return bail(rc);
   }
@@ -670,7 +701,17 @@ int pslr_ctx_create_packed(pslr_ctx** out, int device, const pslr_system* sys, c
         if ((rc = upload(ctx, F.pos_of_row, &dt[f]->lpos))) return bail(rc);
         if ((rc = upload(ctx, F.row_at_pos, &dt[f]->lrow))) return bail(rc);
       }
+      // the two-vector launches' streams (same positions, other chunk boundaries)
+      ctx->tri2[f] = *dt[f];
+      if (SB2 != SB) {
+        const TriHost& H2 = P.H2[f];
+        ctx->tri2[f].nchunks = (int32_t)H2.chunks.size();
+        if ((rc = upload(ctx, H2.data, &ctx->tri2[f].data))) return bail(rc);
+        if ((rc = upload(ctx, H2.chunks, &ctx->tri2[f].chunks))) return bail(rc);
+        if ((rc = upload(ctx, H2.blk_chunk, &ctx->tri2[f].blk_chunk))) return bail(rc);
+      }
     }
+    ctx->sb2 = SB2;
   }
   I.levels_LB = P.levels[0];
   I.levels_UB = P.levels[1];

@@ -187,6 +187,8 @@ struct pslr_ctx {
   // ring / rhs slices and interleaved ([row][2]) scratch, set up on first use
   bool nv2_ready = false;
   pslr::StepConst K2;
+  pslr::DevTri tri2[4];  // the factor streams packed at the two-vector chunk size (LB, UB, LC, UC)
+  int64_t sb2 = 0;       // that chunk size
   double *fL2 = nullptr, *g2 = nullptr, *xb2 = nullptr, *y0_2 = nullptr, *y1_2 = nullptr;
   double *c2 = nullptr, *yA2 = nullptr, *yB2 = nullptr, *yF2 = nullptr, *xF2 = nullptr;
   double *io_b2 = nullptr, *io_z2 = nullptr;  // host-buffer two-vector apply staging
