@@ -448,9 +448,12 @@ def run_single(args):
                 "single_call": {"api": "PslrPreconditioner.apply(numpy)", "ms": sc_s * 1e3,
                                 "value": bytes_apply / sc_s / 1e9}},
         # per call: the profiled launch groups (+ the two-vector permute/deinterleave, the
-        # correction's second kernel) + one all-SM E y kernel per Horner and last step
+        # correction's second kernel) + one all-SM pre-step kernel per Horner and last step
+        # + the split interface phase (an iface kernel per first/correction/Horner step and
+        # a second step launch per correction/Horner step)
         "gpu_launches": (launches_per_apply + (0 if NV == 1 else (3 if r > 0 else 1))
-                         + ((m + 1) if os.environ.get("PSLR_EY_ALLSM", "1") != "0" else 0)) * calls,
+                         + ((m + 1) if os.environ.get("PSLR_EY_ALLSM", "1") != "0" else 0)
+                         + ((2 + 2 * m + 1) if os.environ.get("PSLR_SPLIT_IFACE", "1") != "0" else 0)) * calls,
         "solves": solves,
         "clocks": clk,
         "levels": {k: info[k] for k in ("maxdepth_LB", "maxdepth_UB", "maxdepth_LC", "maxdepth_UC")},

@@ -117,7 +117,7 @@ struct PackedSystem {
   std::vector<int32_t> lb_pos;       // L_B: row -> L-position (E rows' rhs placement)
 };
 
-constexpr uint64_t kPackMagic = 0x32764b4150524c53ull;  // "SLRPAKv2" (two chunk sizes)
+constexpr uint64_t kPackMagic = 0x33764b4150524c53ull;  // "SLRPAKv3" (two chunk sizes, far-ring)
 
 // Level analysis of the four factors, the ring size W (from the reach and the device's
 // shared memory) and the streamed chunks of every block (pack.cpp).
@@ -148,6 +148,16 @@ static int pack_system(const pslr_system* sys, const std::vector<int64_t>& ioff,
     P.depth[f] = an[f]->depth_max;
     P.nnz[f] = M[f]->nnz;
   }
+  // far-ring capacity of each launch width: the shared memory a launch's stage plan leaves
+  // beside the ring (PSLR_FAR_SLOTS caps it; 0 = every far dependency read from global)
+  auto far_cap = [&](int64_t sb, int64_t rb, int64_t nv) -> int64_t {
+    const int64_t nst = std::min<int64_t>(8, (smem_optin - 1024 - kCtlBytes - W * 8 * nv - 128) / (sb + rb));
+    const int64_t left = smem_optin - 1024 - kCtlBytes - nst * (sb + rb);
+    return std::max<int64_t>(0, std::min<int64_t>(left / (8 * nv) - W - 17, env_int("PSLR_FAR_SLOTS", 1 << 14)));
+  };
+  const int64_t RB2 = ((16 * (kChunkRows + 2)) + 127) / 128 * 128;
+  const int64_t fr1 = (SB2 != SB) ? far_cap(SB, RB, 1) : std::min(far_cap(SB, RB, 1), far_cap(SB, RB2, 2));
+  const int64_t fr2 = far_cap(SB2, RB2, 2);
   // U first: L's output lands at the U-positions, where every value lives globally
   for (int pair = 0; pair < 2; ++pair) {
     const TriAnalysis& AL = *an[2 * pair];
@@ -156,15 +166,15 @@ static int pack_system(const pslr_system* sys, const std::vector<int64_t>& ioff,
     std::vector<int32_t> row_id(nr);
     for (int64_t i = 0; i < nr; ++i) row_id[i] = (int32_t)i;
     const auto& off = pair == 0 ? ioff : foff;
-    RET(emit_factor(*M[2 * pair + 1], off, AU, W, SB, kStepThreads, AU.pos_of_row, row_id, P.F[2 * pair + 1].H,
-                    nm[2 * pair + 1]));
-    RET(emit_factor(*M[2 * pair], off, AL, W, SB, kStepThreads, AU.pos_of_row, AU.pos_of_row, P.F[2 * pair].H,
-                    nm[2 * pair]));
+    RET(emit_factor(*M[2 * pair + 1], off, AU, W, SB, kStepThreads, AU.pos_of_row, row_id, fr1,
+                    P.F[2 * pair + 1].H, nm[2 * pair + 1]));
+    RET(emit_factor(*M[2 * pair], off, AL, W, SB, kStepThreads, AU.pos_of_row, AU.pos_of_row, fr1,
+                    P.F[2 * pair].H, nm[2 * pair]));
     if (SB2 != SB) {
-      RET(emit_factor(*M[2 * pair + 1], off, AU, W, SB2, kStepThreads, AU.pos_of_row, row_id, P.H2[2 * pair + 1],
-                      nm[2 * pair + 1]));
-      RET(emit_factor(*M[2 * pair], off, AL, W, SB2, kStepThreads, AU.pos_of_row, AU.pos_of_row, P.H2[2 * pair],
-                      nm[2 * pair]));
+      RET(emit_factor(*M[2 * pair + 1], off, AU, W, SB2, kStepThreads, AU.pos_of_row, row_id, fr2,
+                      P.H2[2 * pair + 1], nm[2 * pair + 1]));
+      RET(emit_factor(*M[2 * pair], off, AL, W, SB2, kStepThreads, AU.pos_of_row, AU.pos_of_row, fr2,
+                      P.H2[2 * pair], nm[2 * pair]));
     }
     P.F[2 * pair].pos_of_row = AL.pos_of_row;
     P.F[2 * pair].row_at_pos = AL.row_at_pos;
@@ -231,6 +241,8 @@ static void serialize(const PackedSystem& P, std::vector<uint8_t>& out) {
     w.vec(P.F[f].H.chunks);
     w.vec(P.F[f].H.blk_chunk);
     w.put(P.F[f].H.far);
+    w.put(P.F[f].H.far_slots);
+    w.put(P.H2[f].far_slots);
     w.vec(P.F[f].pos_of_row);
     w.vec(P.F[f].row_at_pos);
     w.vec(P.H2[f].data);
@@ -270,6 +282,8 @@ static bool deserialize(const void* blob, int64_t len, const pslr_system* sys, i
     r.vec(P.F[f].H.chunks);
     r.vec(P.F[f].H.blk_chunk);
     P.F[f].H.far = r.get<int64_t>();
+    P.F[f].H.far_slots = r.get<int64_t>();
+    P.H2[f].far_slots = r.get<int64_t>();
     r.vec(P.F[f].pos_of_row);
     r.vec(P.F[f].row_at_pos);
     r.vec(P.H2[f].data);
@@ -452,7 +466,8 @@ static int ensure_nv2(pslr_ctx* ctx) {
   K2.nst = (int)nst;
   K2.stage_bytes = (int)SB;
   K2.rhs_stride = (int)(RB2 / 8);
-  K2.smem_bytes = (int)(CTL + W * 16 + 128 + nst * (SB + RB2));
+  K2.far_slots = (int)ctx->far2;
+  K2.smem_bytes = (int)(CTL + (((W + 1 + ctx->far2) * 16 + 127) / 128) * 128 + nst * (SB + RB2));
   if (configure_step_kernel(2, K2.smem_bytes) != 0)
     return fail(PSLR_ECUDA, "cannot configure the two-vector step kernel's shared memory");
   RET(alloc_scratch(ctx, &K2.rhsB, 2 * (p + 2)));
@@ -665,16 +680,25 @@ int pslr_ctx_create_packed(pslr_ctx** out, int device, const pslr_system* sys, c
   int64_t nst = (smem_optin - 1024 - CTL - W * 8 - 128) / (SB + RB);
   nst = std::min<int64_t>(nst, std::min<int64_t>(8, env_int("PSLR_MAX_STAGES", 8)));
   if (nst < 2) return bail(fail(PSLR_EINVAL, "not enough shared memory for the streamed solve"));
+  int64_t fr1 = 0, fr2 = 0;  // far-ring slots of the one- and two-vector packings
+  for (int f = 0; f < 4; ++f) {
+    fr1 = std::max(fr1, P.F[f].H.far_slots);
+    fr2 = std::max(fr2, SB2 != SB ? P.H2[f].far_slots : P.F[f].H.far_slots);
+  }
   ctx->K.ring_mask = (int)(W - 1);
+  ctx->K.far_slots = (int)fr1;
   ctx->K.nst = (int)nst;
   ctx->K.stage_bytes = (int)SB;
   ctx->K.rhs_stride = (int)(RB / 8);
-  ctx->K.smem_bytes = (int)(CTL + W * 8 + 128 + nst * (SB + RB));  // ring + zero slot (padded)
+  // ring + zero slot + far-ring (padded to 128 B), then the stages
+  ctx->K.smem_bytes = (int)(CTL + (((W + 1 + fr1) * 8 + 127) / 128) * 128 + nst * (SB + RB));
+  ctx->far2 = fr2;
   ctx->smem_optin = smem_optin;
   if (configure_step_kernel(1, ctx->K.smem_bytes) != 0)
     return bail(fail(PSLR_ECUDA, "cannot configure the step kernel's shared memory"));
   ctx->pdl = env_int("PSLR_PDL", 1) != 0;
   ctx->ey_all_sm = env_int("PSLR_EY_ALLSM", 1) != 0;
+  ctx->split_iface = env_int("PSLR_SPLIT_IFACE", 1) != 0;
   ctx->K.dbg = (int)env_int("PSLR_DBG", 0);
   ctx->K.l2ahead = env_int("PSLR_L2AHEAD", 0);
   if (env_int("PSLR_TRACE", 0)) {  // diagnostics: timeline of CTA 0 (pslr_debug_trace)

@@ -19,6 +19,9 @@
 #include <cstdlib>
 #include <cstring>
 #include <numeric>
+#include <queue>
+#include <set>
+#include <tuple>
 
 namespace pslr {
 
@@ -111,7 +114,7 @@ int analyze_factor(const pslr_csr& M, const std::vector<int64_t>& off, bool uppe
 // info_of_row[row]: the per-row int the kernel needs (L: U-position, U: row id).
 int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAnalysis& A, int64_t W,
                 int64_t stage_bytes, int64_t seg_rows, const std::vector<int32_t>& far_index,
-                const std::vector<int32_t>& info_of_row, TriHost& out, const char* name) {
+                const std::vector<int32_t>& info_of_row, int64_t far_slots_max, TriHost& out, const char* name) {
   const int64_t nb = (int64_t)off.size() - 1;
   const bool upper = A.upper;
   out.data.clear();
@@ -133,9 +136,10 @@ int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAna
   // carries it (rcp = RN(1/sd) is then a constant), other values switch the segment to
   // explicit sd / rcp arrays.
   constexpr double kSdLow = 0x1.fffffffffffffp-1;  // 1 - 2^-53
-  auto seg_bytes = [&](int64_t nrows, int64_t w, int64_t nfar, bool explicit_sd) {
+  auto seg_bytes = [&](int64_t nrows, int64_t w, int64_t nfar, bool explicit_sd, bool has_fr) {
     const int64_t S = a4(nrows), G = std::max<int64_t>(1, (w + 3) / 4);
     int64_t b = 48 + 4 * S;
+    if (has_fr) b += (2 * S + 15) & ~int64_t(15);
     if (upper) b += (explicit_sd ? 24 : 8) * S;
     b += 40 * G * S;
     b += 4 * a4(nfar);
@@ -147,17 +151,71 @@ int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAna
     const double v = sd_of(r);
     return !force_explicit && (v == 1.0 || (v == kSdLow && 1.0 / v == 0x1.0000000000001p+0));
   };
-  // far dependencies of the row at position s1 within a level ending at lend
+  // Far-ring: a row read as a far dependency (more than W positions behind the end of the
+  // reading row's level) keeps its value in a shared-memory slot beside the ring (ring index
+  // W + 1 + slot) from its level to the level of its last far reader, instead of being read
+  // back from global memory inside the reader's dependent chain (round 2: those L2 reads cost
+  // ~8 % of the single-vector apply).  Slots are reused greedily per block: a target whose
+  // last far reader is at level L frees its slot for targets written at levels > L (the level
+  // barrier orders the read before the overwrite).  Targets beyond far_slots_max stay global.
+  std::vector<int32_t> tend(M.nrows, -1), fslot(M.nrows, -1);
+  for (int64_t r = 0; r < M.nrows; ++r) {
+    const int64_t lend_r = A.level_end[r];
+    for (int64_t e = M.indptr[r]; e < M.indptr[r + 1]; ++e) {
+      const int64_t j = M.indices[e];
+      if (j != r && lend_r - A.pos_of_row[j] > W) tend[j] = std::max(tend[j], A.level_of_row[r]);
+    }
+  }
+  out.far_slots = 0;
+  if (far_slots_max > 0) {
+    // When the ring is full, the live target whose last reader comes latest gives up its
+    // slot to a new target with an earlier last reader (earliest-end-first keeps the most
+    // intervals in a capacity-C interval set); the demoted target is read from global.
+    for (int64_t b = 0; b < nb; ++b) {
+      std::set<std::tuple<int32_t, int32_t, int32_t>> busy;  // (last reader level, slot, row)
+      std::vector<int32_t> freed;
+      int32_t next_new = 0, cur = -1;
+      for (int64_t k = off[b]; k < off[b + 1]; ++k) {
+        const int32_t j = A.row_at_pos[k], lv = A.level_of_row[j];
+        if (lv != cur) {
+          cur = lv;
+          while (!busy.empty() && std::get<0>(*busy.begin()) < lv) {
+            freed.push_back(std::get<1>(*busy.begin()));
+            busy.erase(busy.begin());
+          }
+        }
+        if (tend[j] < 0) continue;
+        int32_t sl = -1;
+        if (!freed.empty()) {
+          sl = freed.back();
+          freed.pop_back();
+        } else if (next_new < far_slots_max) {
+          sl = next_new++;
+        } else if (!busy.empty() && std::get<0>(*busy.rbegin()) > tend[j]) {
+          const auto victim = *busy.rbegin();
+          busy.erase(std::prev(busy.end()));
+          fslot[std::get<2>(victim)] = -1;  // its readers go to global memory
+          sl = std::get<1>(victim);
+        }
+        if (sl < 0) continue;  // the far-ring is full of earlier-ending targets: global
+        fslot[j] = sl;
+        busy.insert({tend[j], sl, j});
+      }
+      out.far_slots = std::max<int64_t>(out.far_slots, next_new);
+    }
+  }
+  // far dependencies of the row at position s1 within a level ending at lend that are read
+  // from global memory (the segment's far list)
   auto row_far = [&](int64_t s1, int64_t lend) {
     const int64_t r = A.row_at_pos[s1];
     int64_t f = 0;
     for (int64_t e = M.indptr[r]; e < M.indptr[r + 1]; ++e) {
       const int64_t j = M.indices[e];
-      if (j != r && lend - A.pos_of_row[j] > W) ++f;
+      if (j != r && lend - A.pos_of_row[j] > W && fslot[j] < 0) ++f;
     }
     return f;
   };
-  if (W >= 0x8000) return fail(PSLR_EINVAL, std::string(name) + ": ring too large for 16-bit slots");
+  if (W + 1 + out.far_slots >= 0x8000) return fail(PSLR_EINVAL, std::string(name) + ": ring too large for 16-bit slots");
   // U rows whose value some later row reads as a far dependency: only they need their
   // value in the global position-ordered array (info bit 30); the others stay in the ring
   std::vector<uint8_t> far_target;
@@ -167,7 +225,7 @@ int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAna
       const int64_t lend_r = A.level_end[r];
       for (int64_t e = M.indptr[r]; e < M.indptr[r + 1]; ++e) {
         const int64_t j = M.indices[e];
-        if (j != r && lend_r - A.pos_of_row[j] > W) far_target[j] = 1;
+        if (j != r && lend_r - A.pos_of_row[j] > W && fslot[j] < 0) far_target[j] = 1;
       }
     }
   }
@@ -206,20 +264,23 @@ int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAna
         const int64_t tb = (s0 - k) % seg_rows;
         // grow a segment while it fits a stage
         int64_t s1 = s0, nnz = 0, w = 0, nfar = 0;
-        bool expl = false;
+        bool expl = false, hfr = false;
         auto grow = [&](int64_t cap) {
           s1 = s0, nnz = 0, w = 0, nfar = 0;
           expl = false;
+          hfr = false;
           while (s1 < lend && s1 - s0 < cap) {
             const int64_t len = A.len[A.row_at_pos[s1]];
             const int64_t w2 = std::max(w, len);
             const int64_t f2 = nfar + row_far(s1, lend);
             const bool e2 = expl || (upper && !sd_plain(A.row_at_pos[s1]));
-            if (seg_bytes(s1 - s0 + 1, w2, f2, e2) > stage_bytes || f2 >= 0x8000) break;
+            const bool h2 = hfr || fslot[A.row_at_pos[s1]] >= 0;
+            if (seg_bytes(s1 - s0 + 1, w2, f2, e2, h2) > stage_bytes || f2 >= 0x8000) break;
             w = w2;
             nnz += len;
             nfar = f2;
             expl = e2;
+            hfr = h2;
             ++s1;
           }
         };
@@ -235,7 +296,7 @@ int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAna
           if (end_t > tb && end_t - tb < s1 - s0) grow(end_t - tb);
         }
         const int64_t nrows = s1 - s0;
-        const int64_t bytes = seg_bytes(nrows, w, nfar, expl);
+        const int64_t bytes = seg_bytes(nrows, w, nfar, expl, hfr);
         if ((int64_t)out.data.size() - chunk_start + bytes > stage_bytes ||
             chunk_rows + nrows > kChunkRows)
           close_chunk();
@@ -245,7 +306,8 @@ int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAna
         int32_t* h = reinterpret_cast<int32_t*>(seg.data());
         if (w > 0xffff) return fail(PSLR_EINVAL, std::string(name) + ": a row is too long for the streaming format");
         h[0] = (int32_t)(nrows | (w << 16));
-        h[1] = ((s1 == lend) ? 1 : 0) | (expl ? 4 : 0) | (int32_t)(tb << 8);  // bit0 level end, bit2 explicit sd
+        h[1] = ((s1 == lend) ? 1 : 0) | (expl ? 4 : 0) | (hfr ? 16 : 0) |
+               (int32_t)(tb << 8);  // bit0 level end, bit2 explicit sd, bit4 far-ring targets
         const int64_t S = a4(nrows);
         const int64_t G = std::max<int64_t>(1, (w + 3) / 4);
         h[2] = (int32_t)s0;
@@ -254,6 +316,11 @@ int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAna
         last_seg = (int64_t)out.data.size();
         int32_t* info = h + 12;
         uint8_t* p = reinterpret_cast<uint8_t*>(info + S);
+        uint16_t* fsl = nullptr;  // far-ring slot + 1 of each row (0: not a far-ring target)
+        if (hfr) {
+          fsl = reinterpret_cast<uint16_t*>(p);
+          p += (2 * S + 15) & ~int64_t(15);
+        }
         double* invd = nullptr;
         double* sd = nullptr;
         double* rcp = nullptr;
@@ -282,6 +349,7 @@ int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAna
         for (int64_t t = 0; t < nrows; ++t) {
           const int64_t r = A.row_at_pos[s0 + t];
           info[t] = info_of_row[r];
+          if (fsl) fsl[t] = (uint16_t)(fslot[r] + 1);
           if (upper) {
             const double dinv = 1.0 / A.diag[r];
             const double sdv = A.diag[r] * dinv;  // scipy: (U @ diags(1/diag)) diagonal
@@ -306,7 +374,9 @@ int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAna
             if (upper) v = v * (1.0 / A.diag[j]);  // scipy pre-scales U's columns by 1/diag
             val_at(t, kk) = v;
             const int64_t pj = A.pos_of_row[j];
-            if (lend - pj <= W) {
+            if (lend - pj > W && fslot[j] >= 0) {
+              slot_at(t, kk) = (uint16_t)(W + 1 + fslot[j]);  // far-ring: a shared-memory read
+            } else if (lend - pj <= W) {
               slot_at(t, kk) = (uint16_t)((pj - lo) & (W - 1));
             } else {
               far[nf] = far_index[j];

@@ -93,6 +93,7 @@ struct TriHost {
   std::vector<ChunkDesc> chunks;
   std::vector<int32_t> blk_chunk;
   int64_t far = 0, nnz_offdiag = 0, segments = 0;
+  int64_t far_slots = 0;  // far-ring slots used (shared memory beside the ring)
 };
 
 int analyze_factor(const pslr_csr& M, const std::vector<int64_t>& off, bool upper, TriAnalysis& A,
@@ -106,7 +107,7 @@ constexpr int kStepThreads = PSLR_STEP_THREADS;
 
 int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAnalysis& A, int64_t W,
                 int64_t stage_bytes, int64_t seg_rows, const std::vector<int32_t>& far_index,
-                const std::vector<int32_t>& info_of_row, TriHost& out, const char* name);
+                const std::vector<int32_t>& info_of_row, int64_t far_slots_max, TriHost& out, const char* name);
 
 // Terms of the per-subdomain fused step (see kernels.cu: subdomain_step_kernel).
 enum BTerm : int { BT_NONE = 0, BT_F = 1, BT_EY = 2 };
@@ -132,6 +133,8 @@ struct StepArgs {
   double* yout = nullptr;      // q output
   double* partials = nullptr;  // [s][r] V^T yout partial sums (nullable)
   int tag = 0;                 // launch kind, for pslr_apply_profiled
+  int ifc_done = 0;            // set by launch_step: the interface phase's result (rhsC) was
+                               // written by the all-SM iface_kernel (split launch)
   int ey_done = 0;             // set by launch_step: the E y rows of the L right-hand side were
                                // written by the all-SM ey_rhs_kernel (no in-kernel prepass)
   int xpos = 0;                // set by launch_step: xb in U-position order (F read via Fpos)
@@ -158,6 +161,7 @@ struct StepConst {
   double* zC = nullptr;    // q
   double* cgy = nullptr;   // q: C_g y of the step, by the all-SM pre-kernel (launch_step)
   int ring_mask = 0;       // W - 1
+  int far_slots = 0;       // far-ring slots after the ring's zero slot (ring index W + 1 + slot)
   int nst = 0;             // pipeline stages
   int stage_bytes = 0;
   int rhs_stride = 0;      // doubles per stage right-hand-side buffer
@@ -179,6 +183,8 @@ struct pslr_ctx {
   int64_t nghost = 0;  // sharded contexts: ghost interface columns of C, Cg and A
   bool pdl = true;     // programmatic dependent launch of the step kernel (PSLR_PDL=0: off)
   bool ey_all_sm = true;  // E y rows of the L right-hand side by the all-SM kernel (PSLR_EY_ALLSM=0: prepass)
+  bool split_iface = true;  // interface phase by the all-SM iface_kernel between a B-phase and a
+                            // C0-phase launch (PSLR_SPLIT_IFACE=0: inside the step kernel)
   const pslr_ctx* parent = nullptr;  // clones: the context whose read-only data they share
   // shared by a context and its clones: use_count() - 1 = live clones of the parent
   std::shared_ptr<int> family = std::make_shared<int>(0);
@@ -189,6 +195,7 @@ struct pslr_ctx {
   pslr::StepConst K2;
   pslr::DevTri tri2[4];  // the factor streams packed at the two-vector chunk size (LB, UB, LC, UC)
   int64_t sb2 = 0;       // that chunk size
+  int64_t far2 = 0;      // far-ring slots of the two-vector packing
   double *fL2 = nullptr, *g2 = nullptr, *xb2 = nullptr, *y0_2 = nullptr, *y1_2 = nullptr;
   double *c2 = nullptr, *yA2 = nullptr, *yB2 = nullptr, *yF2 = nullptr, *xF2 = nullptr;
   double *io_b2 = nullptr, *io_z2 = nullptr;  // host-buffer two-vector apply staging

@@ -401,7 +401,7 @@ __device__ __forceinline__ double2 vmul(double2 a, double s) { return make_doubl
 // Inactive lanes of an active warp compute on row 0 of the segment and skip the stores.
 //
 // Segment layout (pack.cpp, pslr_internal.h); consumer thread tb + t owns row t.
-constexpr int kLevelEnd = 1, kFar = 2, kExplicitSd = 4, kChunkEnd = 8;
+constexpr int kLevelEnd = 1, kFar = 2, kExplicitSd = 4, kChunkEnd = 8, kFarRing = 16;
 
 // one row's operands, loaded before the barrier of the level that precedes it
 template <int NV>
@@ -415,13 +415,18 @@ struct RowOps {
   vt<NV> rhs;     // raw right-hand side(s)
   uint2 s0, s1;   // slot groups 0 and 1 (zero slot when absent)
   vt<NV> cadd;    // U epilogue addend
+  int fsl;        // far-ring slot + 1 (0: the row is not a far-ring target)
 };
 
 __device__ __forceinline__ int hdr_rows(int4 h) { return h.x & 0xffff; }
 __device__ __forceinline__ int hdr_w(int4 h) { return h.x >> 16; }
 __device__ __forceinline__ int hdr_S(int4 h) { return ((h.x & 0xffff) + 3) & ~3; }
+// bytes of a segment's per-row far-ring slots (uint16, present when flag bit 4 is set)
+__device__ __forceinline__ uint32_t fsl_bytes(int S, int flags) {
+  return (flags & kFarRing) ? (uint32_t)((2 * S + 15) & ~15) : 0u;
+}
 __device__ __forceinline__ uint32_t pre_bytes(bool upper, int S, int flags) {
-  return 48 + 4 * S + (upper ? ((flags & kExplicitSd) ? 24 : 8) * S : 0);
+  return 48 + 4 * S + fsl_bytes(S, flags) + (upper ? ((flags & kExplicitSd) ? 24 : 8) * S : 0);
 }
 // does this warp own rows of the segment?
 __device__ __forceinline__ bool warp_owns(int4 h) {
@@ -445,7 +450,8 @@ __device__ __forceinline__ void load_ops(uint32_t seg, int4 h, uint32_t rbuf, in
   const unsigned z2 = (unsigned)zslot | ((unsigned)zslot << 16);
   r.s1 = (hdr_w(h) > 4) ? *sp<uint2>(slots + 8 * S) : make_uint2(z2, z2);
   r.vals = slots + 8 * G * S + 8 * t;  // val[0][0][t] = pre + 8GS + 16t
-  r.invd = seg + 48 + 4 * S + 8 * t;
+  r.invd = seg + 48 + 4 * S + fsl_bytes(S, h.y) + 8 * t;
+  r.fsl = (h.y & kFarRing) ? (int)sp<uint16_t>(seg + 48 + 4 * S)[t] : 0;
 }
 
 // U rows start from rhs / sd.  rcp = RN(1/sd): q0 = RN(x rcp) is within an ulp of x/sd
@@ -540,6 +546,7 @@ __device__ __forceinline__ void compute_row(const StepConst& K, uint32_t seg, in
   if (r.active) {
     const int gp = h.z + r.t;
     vst(ring, (gp - base) & K.ring_mask, acc);
+    if (r.fsl) vst(ring, K.ring_mask + 1 + r.fsl, acc);  // kept for its far readers
     if (UPPER) {
       if (r.info & 0x40000000) vst(z, gp, acc);  // only far-dependency targets go to global z
       vt<NV> x = vmul(acc, invd);
@@ -746,7 +753,8 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
   // [Ctl 256 B][ring: (W + zero slot) x NV, padded to 128 B][nst stages][nst rhs slices]
   // The ring sits at a constant offset, so a gather is one address op on its slot.
   double* ring = reinterpret_cast<double*>(smem + kCtlBytes);
-  uint8_t* stages = smem + kCtlBytes + (size_t)(K.ring_mask + 1) * 8 * NV + 128;
+  // [ring W | zero slot | far-ring] padded to 128 B, then the stages
+  uint8_t* stages = smem + kCtlBytes + (((size_t)(K.ring_mask + 2 + K.far_slots) * 8 * NV + 127) / 128) * 128;
   double* rhsbuf = reinterpret_cast<double*>(stages + (size_t)K.nst * K.stage_bytes);
 
   // The stream table lives in shared memory: dynamically indexed per-thread arrays would
@@ -883,8 +891,9 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
     tri_phase<true, NV, XPOS>(K, S, ctl, stages, rhsbuf, ph_UB, ring, r0, K.zB, a.xb, nullptr);
   }
   if (do_i) {
+    trace_cta(K, 7);
     const int r0 = K.ifc_off[b], r1 = K.ifc_off[b + 1];
-    for (int row0 = r0 + tid; row0 < r1; row0 += 4 * kStepThreads) {
+    for (int row0 = r0 + tid; row0 < r1 && !a.ifc_done; row0 += 4 * kStepThreads) {
       int row[4];
       bool ok[4];
 #pragma unroll
@@ -954,6 +963,50 @@ __global__ void __launch_bounds__(256) pre_step_kernel(const int4* __restrict__ 
   }
 }
 
+// One term of the interface phase for one row (the step kernel's iface_terms4, one row):
+// an SpMV row is summed in CSR order from 0 (scipy csr_matvec) exactly as there.
+template <int NV>
+__device__ __forceinline__ vt<NV> spmv_row1(const DevCsr& M, int row, const double* __restrict__ x) {
+  vt<NV> s = vzero<NV>();
+  const int e1 = __ldg(M.ptr + row + 1);
+  for (int e = __ldg(M.ptr + row); e < e1; ++e) s = vmadd(s, __ldg(M.val + e), vldg<NV>(x, __ldg(M.col + e)));
+  return s;
+}
+template <int NV, bool XPOS>
+__device__ __forceinline__ vt<NV> iface_term1(int kind, int row, const StepArgs& a, const StepConst& K) {
+  switch (kind) {
+    case IT_G: return vldg<NV>(a.g, row);
+    case IT_FX: return spmv_row1<NV>(XPOS ? K.Fpos : K.F, row, a.xb);
+    case IT_CY: return spmv_row1<NV>(K.C, row, a.yC);
+    case IT_CGY: return spmv_row1<NV>(K.Cg, row, a.yC);
+    case IT_PRE: return vldg<NV>(a.pre, row);
+    default: return vzero<NV>();
+  }
+}
+
+// The interface phase of a step for every block at once (all SMs, one interface row per
+// thread), between the launch of the B phases (x_B written) and the launch of the C0 phases:
+// on the one SM per block it was 40-50 us of dependent gathers (F x_B, C_g y) on the
+// critical block.  w = i1 (-|+) i2 ; do_c0: rhsC[L_C0 position] = w, else yout = w [+ cadd].
+template <int NV, bool XPOS>
+__global__ void __launch_bounds__(256) iface_kernel(const __grid_constant__ StepArgs a,
+                                                    const __grid_constant__ StepConst K, int q) {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  const int row = blockIdx.x * blockDim.x + threadIdx.x;
+  if (row >= q) return;
+  vt<NV> w = iface_term1<NV, XPOS>(a.i1, row, a, K);
+  if (a.i2 != IT_NONE) {
+    const vt<NV> t2 = iface_term1<NV, XPOS>(a.i2, row, a, K);
+    w = a.i2_sub ? vsub(w, t2) : vadd(w, t2);
+  }
+  if (a.do_c0) {
+    vst(K.rhsC, __ldg(K.LC.lpos + row), w);
+  } else {
+    if (a.cadd) w = vadd(w, vldg<NV>(a.cadd, row));
+    vst(a.yout, row, w);
+  }
+}
+
 int configure_step_kernel(int nv, int smem_bytes) {
   auto set = [&](auto kern) {
     return (int)cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
@@ -965,6 +1018,8 @@ int configure_step_kernel(int nv, int smem_bytes) {
   const int e = set(subdomain_step_kernel<1, false>);
   return e ? e : set(subdomain_step_kernel<1, true>);
 }
+
+int launch_step_kernel(const pslr_ctx* ctx, const StepArgs& a, const StepConst& K, cudaStream_t st, int nv);
 
 int launch_step(const pslr_ctx* ctx, const StepArgs& a_in, cudaStream_t st, int nv) {
   if (ctx->s == 0) return 0;
@@ -1007,6 +1062,47 @@ int launch_step(const pslr_ctx* ctx, const StepArgs& a_in, cudaStream_t st, int 
   // programmatic stream serialization: the step kernel's CTAs (one per subdomain, far
   // fewer than the 148 SMs) launch and stage their first factor chunks while the
   // previous kernel drains; griddepcontrol.wait orders the data accesses
+  // The interface phase of a launch that also has a B phase (or a C0 phase) runs as its own
+  // all-SM kernel: [B phases] -> iface_kernel -> [C0 phases], the two step launches being
+  // the same kernel with the other phases switched off (bit for bit the same results).
+  if (ctx->split_iface && a.i1 != IT_NONE && (a.b1 != BT_NONE || a.do_c0) && !a.ifc_done) {
+    if (a.b1 != BT_NONE) {
+      StepArgs ab = a;
+      ab.i1 = ab.i2 = IT_NONE;
+      ab.do_c0 = 0;
+      ab.yout = nullptr;
+      const int e = launch_step_kernel(ctx, ab, K, st, nv);
+      if (e) return e;
+    }
+    cudaLaunchConfig_t ic = {};
+    ic.gridDim = dim3((unsigned)((ctx->q + 255) / 256));
+    ic.blockDim = dim3(256);
+    ic.stream = st;
+    cudaLaunchAttribute iat[1];
+    iat[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    iat[0].val.programmaticStreamSerializationAllowed = ctx->pdl ? 1 : 0;
+    ic.attrs = iat;
+    ic.numAttrs = 1;
+    const int q = (int)ctx->q;
+    cudaError_t e;
+    if (nv == 2)
+      e = a.xpos ? cudaLaunchKernelEx(&ic, iface_kernel<2, true>, a, K, q)
+                 : cudaLaunchKernelEx(&ic, iface_kernel<2, false>, a, K, q);
+    else
+      e = a.xpos ? cudaLaunchKernelEx(&ic, iface_kernel<1, true>, a, K, q)
+                 : cudaLaunchKernelEx(&ic, iface_kernel<1, false>, a, K, q);
+    if (e != cudaSuccess) return (int)e;
+    if (!a.do_c0) return 0;
+    StepArgs ac = a;
+    ac.b1 = ac.b2 = BT_NONE;
+    ac.ifc_done = 1;
+    ac.xpos = 0;
+    return launch_step_kernel(ctx, ac, K, st, nv);
+  }
+  return launch_step_kernel(ctx, a, K, st, nv);
+}
+
+int launch_step_kernel(const pslr_ctx* ctx, const StepArgs& a, const StepConst& K, cudaStream_t st, int nv) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)ctx->s);
   cfg.blockDim = dim3(kBlockThreads);

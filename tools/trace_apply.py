@@ -134,7 +134,7 @@ if i51.size:
         print(f"   phase {k}: n={sel.sum()}, mean {w[sel].mean():.0f}, sum {w[sel].sum() / 1.965e3:.1f} us")
 # per-CTA phase stamps, the last launch of each kind (trace builds): which block is critical
 kinds = {2: "first_step", 3: "correction_c0", 4: "horner_step", 5: "last_step"}
-names_s = ["start", "prepass", "L_B", "U_B", "L_C0", "U_C0", "end"]
+names_s = ["start", "prepass", "L_B", "U_B", "L_C0", "U_C0", "end", "iface"]
 area = buf[2 * (1 << 20) - 8 * 4096:].reshape(4096, 8)
 dump = {}
 for tag, kname in kinds.items():
@@ -150,7 +150,7 @@ for tag, kname in kinds.items():
     for b in order:
         row = cs[b]
         seg = []
-        marks = [(i, row[i]) for i in range(7) if row[i] >= row[0] > 0]
+        marks = sorted([(i, row[i]) for i in range(8) if row[i] >= row[0] > 0], key=lambda m: m[1])
         for (i, tv), (j, tn) in zip(marks, marks[1:]):
             seg.append(f"{names_s[i]} {(tn - tv) / 1e3:.1f}")
         print(f"   CTA {b:3d}: start {(row[0] - t0) / 1e3:6.1f} end {(row[6] - t0) / 1e3:6.1f}  |  " + ", ".join(seg))
