@@ -350,9 +350,10 @@ def test_explicit_sd_layout_bitexact(monkeypatch):
 
 
 def test_ey_prepass_and_all_sm_kernel_bitexact(monkeypatch):
-    """The E y rows of the L right-hand sides: the all-SM ey_rhs_kernel (default) and the
-    step kernel's own prepass (PSLR_EY_ALLSM=0) give the same bits — apply_Es, the Horner
-    series, E_rr and the full apply (one and two vectors per call)."""
+    """The work moved off the step kernel's critical blocks gives the same bits as doing it
+    inside: the E y / C_g y pre-step kernel (vs PSLR_EY_ALLSM=0), the split interface phase
+    (vs PSLR_SPLIT_IFACE=0) and the shared-memory far-ring (vs PSLR_FAR_SLOTS=0) — apply_Es,
+    the Horner series, E_rr and the full apply (one and two vectors per call)."""
     import torch
     import paper_2002_00917_b200 as pg
     from paper_2002_00917_b200 import _lib
@@ -365,6 +366,8 @@ def test_ey_prepass_and_all_sm_kernel_bitexact(monkeypatch):
     out = []
     for env in ("1", "0"):
         monkeypatch.setenv("PSLR_EY_ALLSM", env)
+        monkeypatch.setenv("PSLR_SPLIT_IFACE", env)  # the interface phase as its own all-SM kernel
+        monkeypatch.setenv("PSLR_FAR_SLOTS", "4096" if env == "1" else "0")  # far-ring vs global far reads
         P = pg.build(A, cfg)
         n = P.system.n
         B2 = torch.from_numpy(np.random.default_rng(3).standard_normal((2, n))).cuda()
