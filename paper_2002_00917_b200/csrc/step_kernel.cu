@@ -1097,6 +1097,7 @@ int launch_step(const pslr_ctx* ctx, const StepArgs& a_in, cudaStream_t st, int 
     ac.b1 = ac.b2 = BT_NONE;
     ac.ifc_done = 1;
     ac.xpos = 0;
+    ac.tag = a.tag | 8;  // trace builds: the C0 launch of a split step stamps its own row
     return launch_step_kernel(ctx, ac, K, st, nv);
   }
   return launch_step_kernel(ctx, a, K, st, nv);

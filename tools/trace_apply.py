@@ -133,7 +133,8 @@ if i51.size:
         sel = phase_of[i51] == k
         print(f"   phase {k}: n={sel.sum()}, mean {w[sel].mean():.0f}, sum {w[sel].sum() / 1.965e3:.1f} us")
 # per-CTA phase stamps, the last launch of each kind (trace builds): which block is critical
-kinds = {2: "first_step", 3: "correction_c0", 4: "horner_step", 5: "last_step"}
+kinds = {2: "first_step", 3: "correction_c0", 11: "correction_c0 (C0 launch)", 4: "horner_step (B launch)",
+         12: "horner_step (C0 launch)", 5: "last_step"}
 names_s = ["start", "prepass", "L_B", "U_B", "L_C0", "U_C0", "end", "iface"]
 area = buf[2 * (1 << 20) - 8 * 4096:].reshape(4096, 8)
 dump = {}
