@@ -43,11 +43,21 @@ def call_summary(call):
 def main(nv1, nv2, bench, tag):
     L1, L2 = load(nv1), load(nv2)
     c1, c2 = last_call(L1, "permute_f_kernel"), last_call(L2, "permute2_kernel")
-    horner = [d for d in c1 if d["kernel"].startswith("subdomain_step_kernel<1, 1>")][1:4]
-    hb = sum(d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"] for d in horner) / len(horner)
+    # a Horner step = pre_step_kernel + the B launch + iface_kernel + the C0 launch (split
+    # interface phase; one fused step launch before round 2's split)
+    groups = []
+    for i, d in enumerate(c1):
+        if d["kernel"].startswith("pre_step_kernel") and i + 3 < len(c1) and \
+                c1[i + 3]["kernel"].startswith("subdomain_step_kernel<1, 0>") and \
+                c1[i + 2]["kernel"].startswith("iface_kernel"):
+            groups.append(c1[i:i + 4])
+    if not groups:
+        groups = [[d] for d in c1 if d["kernel"].startswith("subdomain_step_kernel<1, 1>")][1:4]
+    hb = sum(sum(d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"] for d in g) for g in groups) / len(groups)
+    ht = sum(sum(d["gpu__time_duration.sum"] for d in g) for g in groups) / len(groups)
     summ = {"round": tag,
             "horner_step_dram_bytes": hb,
-            "horner_step_us_ncu": sum(d["gpu__time_duration.sum"] for d in horner) / len(horner) / 1e3,
+            "horner_step_us_ncu": ht / 1e3,
             "apply1_call_dram_bytes": sum(d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"] for d in c1),
             "apply1_call_us_ncu": sum(d["gpu__time_duration.sum"] for d in c1) / 1e3,
             "apply2_call_dram_bytes": sum(d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"] for d in c2),
