@@ -197,6 +197,7 @@ struct Streams {
   const uint8_t* data[4];
   const ChunkDesc* chunks[4];  // this block's first chunk of the phase
   const double* rhs[4];        // position-ordered right-hand-side array of each phase
+  uint32_t pf_lo[4], pf_hi[4]; // byte range of this block's chunks in data[k] (L2 prefetch)
 };
 
 __device__ __forceinline__ ChunkDesc load_desc(const ChunkDesc* p) {
@@ -227,7 +228,7 @@ static_assert(sizeof(Ctl) <= kCtlBytes, "the control block must fit the header o
 // expect_tx + bulk-copy pairs.  Phase bookkeeping only runs at phase boundaries.
 __device__ void producer(const Streams& S, Ctl* ctl, uint8_t* stages, double* rhsbuf, int nst,
                          int stage_bytes, int rhs_stride, int nv, long long* g_dbg_out, int dbg,
-                         long long* g_tma) {
+                         long long* g_tma, long long l2ahead) {
   if ((threadIdx.x & 31) != 0) return;
   const int np = S.nphase;
   const int total = S.begin[np];
@@ -290,6 +291,11 @@ __device__ void producer(const Streams& S, Ctl* ctl, uint8_t* stages, double* rh
   };
   int st = 0;
   uint32_t par = 1;  // parity of the empty-barrier phase a reused stage waits for
+  // L2 prefetch cursor: phase kp, byte offset pf; bytes copied / prefetched so far
+  int kp = 0;
+  while (kp < np && S.pf_hi[kp] == S.pf_lo[kp]) ++kp;
+  uint32_t pf = kp < np ? S.pf_lo[kp] : 0u;
+  long long issued = 0, prefetched = 0;
   const long long c_all = clock64();
   for (int u = 0; u < total; ++u) {
     if (u == k_end) {  // next phase (its slices are deferred until it is ready)
@@ -314,6 +320,16 @@ __device__ void producer(const Streams& S, Ctl* ctl, uint8_t* stages, double* rh
     }
     mbar_expect_tx(&ctl->full[st], dv.y);
     bulk_load(stages + (size_t)st * stage_bytes, data + (size_t)dv.x * 16, dv.y, &ctl->full[st]);
+    if (l2ahead > 0) {  // keep the factor stream l2ahead bytes ahead in L2 (phases in order)
+      issued += dv.y;
+      while (prefetched < issued + l2ahead && kp < np) {
+        const uint32_t n = min(32768u, S.pf_hi[kp] - pf);
+        if (n) bulk_prefetch_l2(S.data[kp] + pf, n);
+        pf += n;
+        prefetched += n;
+        if (pf >= S.pf_hi[kp] && ++kp < np) pf = S.pf_lo[kp];
+      }
+    }
     if (PSLR_TRACE_BUILD && g_tma && u < 8192) {
       g_tma[2 * u] = clock64();
       g_tma[2 * 8192 + u] = dv.y;
@@ -769,6 +785,13 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
       S.data[S.nphase] = T.data;
       S.chunks[S.nphase] = T.chunks + c0;
       S.rhs[S.nphase] = rhs;
+      if (K.l2ahead > 0 && c1 > c0) {
+        const ChunkDesc d0 = load_desc(T.chunks + c0), d1 = load_desc(T.chunks + c1 - 1);
+        S.pf_lo[S.nphase] = d0.off16 * 16u;
+        S.pf_hi[S.nphase] = d1.off16 * 16u + d1.bytes;
+      } else {
+        S.pf_lo[S.nphase] = S.pf_hi[S.nphase] = 0;
+      }
       S.begin[S.nphase + 1] = S.begin[S.nphase] + (c1 - c0);
       S.nphase++;
     };
@@ -795,7 +818,8 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
              (K.trace && K.trace_cap >= (1 << 20)) ? K.trace + 2 + 2 * K.trace_cap - 8 * 4096 + b * 8
                                                    : nullptr,
              K.dbg,
-             (PSLR_TRACE_BUILD && K.trace && b == K.trace_block) ? K.trace + 2 + 2 * 65536 : nullptr);
+             (PSLR_TRACE_BUILD && K.trace && b == K.trace_block) ? K.trace + 2 + 2 * 65536 : nullptr,
+             K.l2ahead);
     return;
   }
   // Programmatic dependent launch: this grid may start while the previous kernel of the
