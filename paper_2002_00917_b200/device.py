@@ -17,6 +17,7 @@ from . import _lib
 _torch = None
 # numpy vectors at least this large travel through pinned host memory (vec_op)
 _PIN_BYTES = 1 << 20
+_PIN_CHUNK = 1 << 20  # doubles per pipelined host-copy / DMA chunk (8 MB; tools/single_call.py)
 
 
 def torch_mod():
@@ -160,8 +161,14 @@ class DeviceContext:
         # pinned memory runs on the intra-op threads), both DMA copies are asynchronous on
         # the operator's stream, and the result lands in a pinned host array returned as is
         # (a fresh array, as the reference returns): no pageable, driver-staged transfer
-        xp = t.from_numpy(xa).pin_memory()
-        xt = xp.to(self.dev, non_blocking=True)
+        # the host copy into pinned memory and the DMA overlap chunk by chunk
+        src = t.from_numpy(xa)
+        xp = t.empty(n_in, dtype=t.float64, pin_memory=True)
+        xt = t.empty(n_in, dtype=t.float64, device=self.dev)
+        step = _PIN_CHUNK
+        for i in range(0, n_in, step):
+            xp[i:i + step].copy_(src[i:i + step])
+            xt[i:i + step].copy_(xp[i:i + step], non_blocking=True)
         out = t.empty(n_out, dtype=t.float64, device=self.dev)
         _lib.check(_lib.fns[name](self.handle, *scalars, xt.data_ptr(), out.data_ptr(), self.stream()))
         res = t.empty(n_out, dtype=t.float64, pin_memory=True)
