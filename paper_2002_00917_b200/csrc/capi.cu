@@ -117,7 +117,16 @@ struct PackedSystem {
   std::vector<int32_t> lb_pos;       // L_B: row -> L-position (E rows' rhs placement)
 };
 
-constexpr uint64_t kPackMagic = 0x33764b4150524c53ull;  // "SLRPAKv3" (two chunk sizes, far-ring)
+constexpr uint64_t kPackMagic = 0x34764b4150524c53ull;  // "SLRPAKv4" (two chunk sizes, far-ring, rhs in stage)
+
+// Stages of the step kernel's pipeline for chunk size sb and nv vectors per launch: what
+// the shared memory holds beside the control block and the (nv-wide) value ring, at most 8
+// (PSLR_MAX_STAGES caps it); a chunk's rhs slice travels inside its stage.
+static int64_t stage_count(int64_t smem_optin, int64_t W, int64_t sb, int64_t nv) {
+  const int64_t n = (smem_optin - 1024 - kCtlBytes - W * 8 * nv - 128) / sb;
+  const int64_t cap = nv == 1 ? env_int("PSLR_MAX_STAGES", 8) : env_int("PSLR_MAX_STAGES2", 8);
+  return std::min<int64_t>(n, std::min<int64_t>(8, cap));
+}
 
 // Level analysis of the four factors, the ring size W (from the reach and the device's
 // shared memory) and the streamed chunks of every block (pack.cpp).
@@ -135,10 +144,9 @@ static int pack_system(const pslr_system* sys, const std::vector<int64_t>& ioff,
   RET(analyze_factor(sys->LC, foff, false, aLC, "L_C0"));
   RET(analyze_factor(sys->UC, foff, true, aUC, "U_C0"));
   P.reach = std::max({aLB.reach, aUB.reach, aLC.reach, aUC.reach, (int64_t)1});
-  const int64_t RB = ((8 * (kChunkRows + 2)) + 127) / 128 * 128;
   int64_t W = 2048;  // >= 2048: the ring doubles as the V^T y reduction scratch
   while (W < P.reach && W < wmax) W *= 2;
-  while (W > 2048 && (smem_optin - 1024 - kCtlBytes - W * 8 - 128) / (SB + RB) < 2) W /= 2;
+  while (W > 2048 && (smem_optin - 1024 - kCtlBytes - W * 8 - 128) / SB < 2) W /= 2;
   P.W = W;
   const TriAnalysis* an[4] = {&aLB, &aUB, &aLC, &aUC};
   const pslr_csr* M[4] = {&sys->LB, &sys->UB, &sys->LC, &sys->UC};
@@ -150,14 +158,15 @@ static int pack_system(const pslr_system* sys, const std::vector<int64_t>& ioff,
   }
   // far-ring capacity of each launch width: the shared memory a launch's stage plan leaves
   // beside the ring (PSLR_FAR_SLOTS caps it; 0 = every far dependency read from global)
-  auto far_cap = [&](int64_t sb, int64_t rb, int64_t nv) -> int64_t {
-    const int64_t nst = std::min<int64_t>(8, (smem_optin - 1024 - kCtlBytes - W * 8 * nv - 128) / (sb + rb));
-    const int64_t left = smem_optin - 1024 - kCtlBytes - nst * (sb + rb);
+  auto far_cap = [&](int64_t sb, int64_t nv) -> int64_t {
+    const int64_t nst = stage_count(smem_optin, W, sb, nv);
+    const int64_t left = smem_optin - 1024 - kCtlBytes - nst * sb;
     return std::max<int64_t>(0, std::min<int64_t>(left / (8 * nv) - W - 17, env_int("PSLR_FAR_SLOTS", 1 << 14)));
   };
-  const int64_t RB2 = ((16 * (kChunkRows + 2)) + 127) / 128 * 128;
-  const int64_t fr1 = (SB2 != SB) ? far_cap(SB, RB, 1) : std::min(far_cap(SB, RB, 1), far_cap(SB, RB2, 2));
-  const int64_t fr2 = far_cap(SB2, RB2, 2);
+  const int64_t fr1 = (SB2 != SB) ? far_cap(SB, 1) : std::min(far_cap(SB, 1), far_cap(SB, 2));
+  const int64_t fr2 = far_cap(SB2, 2);
+  // a chunk's rhs slice shares its stage (8 B per row and vector)
+  const int64_t rr1 = (SB2 != SB) ? 8 : 16, rr2 = 16;
   // U first: L's output lands at the U-positions, where every value lives globally
   for (int pair = 0; pair < 2; ++pair) {
     const TriAnalysis& AL = *an[2 * pair];
@@ -166,14 +175,14 @@ static int pack_system(const pslr_system* sys, const std::vector<int64_t>& ioff,
     std::vector<int32_t> row_id(nr);
     for (int64_t i = 0; i < nr; ++i) row_id[i] = (int32_t)i;
     const auto& off = pair == 0 ? ioff : foff;
-    RET(emit_factor(*M[2 * pair + 1], off, AU, W, SB, kStepThreads, AU.pos_of_row, row_id, fr1,
+    RET(emit_factor(*M[2 * pair + 1], off, AU, W, SB, kStepThreads, AU.pos_of_row, row_id, fr1, rr1,
                     P.F[2 * pair + 1].H, nm[2 * pair + 1]));
-    RET(emit_factor(*M[2 * pair], off, AL, W, SB, kStepThreads, AU.pos_of_row, AU.pos_of_row, fr1,
+    RET(emit_factor(*M[2 * pair], off, AL, W, SB, kStepThreads, AU.pos_of_row, AU.pos_of_row, fr1, rr1,
                     P.F[2 * pair].H, nm[2 * pair]));
     if (SB2 != SB) {
-      RET(emit_factor(*M[2 * pair + 1], off, AU, W, SB2, kStepThreads, AU.pos_of_row, row_id, fr2,
+      RET(emit_factor(*M[2 * pair + 1], off, AU, W, SB2, kStepThreads, AU.pos_of_row, row_id, fr2, rr2,
                       P.H2[2 * pair + 1], nm[2 * pair + 1]));
-      RET(emit_factor(*M[2 * pair], off, AL, W, SB2, kStepThreads, AU.pos_of_row, AU.pos_of_row, fr2,
+      RET(emit_factor(*M[2 * pair], off, AL, W, SB2, kStepThreads, AU.pos_of_row, AU.pos_of_row, fr2, rr2,
                       P.H2[2 * pair], nm[2 * pair]));
     }
     P.F[2 * pair].pos_of_row = AL.pos_of_row;
@@ -294,9 +303,8 @@ static bool deserialize(const void* blob, int64_t len, const pslr_system* sys, i
   }
   r.vec(P.ub_pos);
   r.vec(P.lb_pos);
-  const int64_t RB = ((8 * (kChunkRows + 2)) + 127) / 128 * 128;
   return r.ok && r.left == 0 && (int64_t)P.ub_pos.size() == P.p && (int64_t)P.lb_pos.size() == P.p &&
-         (smem_optin - 1024 - kCtlBytes - P.W * 8 - 128) / (SB + RB) >= 2;
+         stage_count(smem_optin, P.W, SB, 1) >= 2;
 }
 
 static cudaStream_t S(void* s) { return static_cast<cudaStream_t>(s); }
@@ -459,15 +467,13 @@ static int ensure_nv2(pslr_ctx* ctx) {
   K2.LC = ctx->tri2[2];
   K2.UC = ctx->tri2[3];
   const int64_t W = (int64_t)ctx->K.ring_mask + 1, SB = ctx->sb2, CTL = kCtlBytes;
-  const int64_t RB2 = ((16 * (kChunkRows + 2)) + 127) / 128 * 128;
-  int64_t nst = (ctx->smem_optin - 1024 - CTL - W * 16 - 128) / (SB + RB2);
-  nst = std::min<int64_t>(nst, 8);
+  const int64_t nst = stage_count(ctx->smem_optin, W, SB, 2);
   if (nst < 2) return fail(PSLR_EINVAL, "not enough shared memory for two right-hand sides per launch");
   K2.nst = (int)nst;
   K2.stage_bytes = (int)SB;
-  K2.rhs_stride = (int)(RB2 / 8);
+  K2.rhs_stride = 0;  // the rhs slice follows the data inside its stage
   K2.far_slots = (int)ctx->far2;
-  K2.smem_bytes = (int)(CTL + (((W + 1 + ctx->far2) * 16 + 127) / 128) * 128 + nst * (SB + RB2));
+  K2.smem_bytes = (int)(CTL + (((W + 1 + ctx->far2) * 16 + 127) / 128) * 128 + nst * SB);
   if (configure_step_kernel(2, K2.smem_bytes) != 0)
     return fail(PSLR_ECUDA, "cannot configure the two-vector step kernel's shared memory");
   RET(alloc_scratch(ctx, &K2.rhsB, 2 * (p + 2)));
@@ -650,13 +656,14 @@ int pslr_ctx_create_packed(pslr_ctx** out, int device, const pslr_system* sys, c
 
   // ---- the packed format: from the caller's blob when it fits this system and device,
   // else level analysis + ring plan + streamed chunks (pack_system)
-  // Shared-memory plan: nst stages of (chunk bytes SB + rhs slice RB) and a W-slot ring.
-  // chunk size of the one-vector launches (SB) and of the two-vector launches (SB2): one
-  // vector at a time runs 1.8 % faster with 45 KB chunks in 3 stages, two vectors per
-  // launch 5 % slower than with 32 KB chunks in 4 stages (cfg5, round 2)
-  const int64_t SB = env_int("PSLR_STAGE_BYTES", 45 * 1024);
-  const int64_t SB2 = env_int("PSLR_STAGE_BYTES2", 32 * 1024);
-  const int64_t RB = ((8 * (kChunkRows + 2)) + 127) / 128 * 128;
+  // Shared-memory plan: a W-slot value ring, nst stages of SB bytes (a chunk's data and its
+  // rhs slice), the far-ring in what is left.
+  // stage size (a chunk's data + its rhs slice) of the one-vector launches (SB) and of the
+  // two-vector launches (SB2), cfg5 round 2 (tools/stage_plan_sweep.sh, tools/sb_bench.sh):
+  // one vector at a time prefers 3 stages of 52 KB (far-ring 4.7 k slots; 56 KB and more
+  // shrink the far-ring below the wide blocks' needs), two vectors 4 stages of 36 KB
+  const int64_t SB = env_int("PSLR_STAGE_BYTES", 52 * 1024);
+  const int64_t SB2 = env_int("PSLR_STAGE_BYTES2", 36 * 1024);
   PackedSystem P;
   const bool reuse = blob_in && blob_len > 0 && deserialize(blob_in, blob_len, sys, smem_optin, SB, SB2, P);
   if (reused) *reused = reuse ? 1 : 0;
@@ -677,8 +684,7 @@ int pslr_ctx_create_packed(pslr_ctx** out, int device, const pslr_system* sys, c
   }
   const int64_t W = P.W, reach = P.reach;
   const int64_t CTL = kCtlBytes;  // mbarriers + descriptor queue
-  int64_t nst = (smem_optin - 1024 - CTL - W * 8 - 128) / (SB + RB);
-  nst = std::min<int64_t>(nst, std::min<int64_t>(8, env_int("PSLR_MAX_STAGES", 8)));
+  const int64_t nst = stage_count(smem_optin, W, SB, 1);
   if (nst < 2) return bail(fail(PSLR_EINVAL, "not enough shared memory for the streamed solve"));
   int64_t fr1 = 0, fr2 = 0;  // far-ring slots of the one- and two-vector packings
   for (int f = 0; f < 4; ++f) {
@@ -689,9 +695,9 @@ int pslr_ctx_create_packed(pslr_ctx** out, int device, const pslr_system* sys, c
   ctx->K.far_slots = (int)fr1;
   ctx->K.nst = (int)nst;
   ctx->K.stage_bytes = (int)SB;
-  ctx->K.rhs_stride = (int)(RB / 8);
+  ctx->K.rhs_stride = 0;  // the rhs slice follows the data inside its stage
   // ring + zero slot + far-ring (padded to 128 B), then the stages
-  ctx->K.smem_bytes = (int)(CTL + (((W + 1 + fr1) * 8 + 127) / 128) * 128 + nst * (SB + RB));
+  ctx->K.smem_bytes = (int)(CTL + (((W + 1 + fr1) * 8 + 127) / 128) * 128 + nst * SB);
   ctx->far2 = fr2;
   ctx->smem_optin = smem_optin;
   if (configure_step_kernel(1, ctx->K.smem_bytes) != 0)

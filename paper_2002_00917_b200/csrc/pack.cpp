@@ -114,7 +114,8 @@ int analyze_factor(const pslr_csr& M, const std::vector<int64_t>& off, bool uppe
 // info_of_row[row]: the per-row int the kernel needs (L: U-position, U: row id).
 int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAnalysis& A, int64_t W,
                 int64_t stage_bytes, int64_t seg_rows, const std::vector<int32_t>& far_index,
-                const std::vector<int32_t>& info_of_row, int64_t far_slots_max, TriHost& out, const char* name) {
+                const std::vector<int32_t>& info_of_row, int64_t far_slots_max, int64_t rhs_row_bytes,
+                TriHost& out, const char* name) {
   const int64_t nb = (int64_t)off.size() - 1;
   const bool upper = A.upper;
   out.data.clear();
@@ -145,6 +146,9 @@ int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAna
     b += 4 * a4(nfar);
     return b;
   };
+  // a chunk's rhs slice lands in its stage right behind the data: at most (rows + 2) rows
+  // (the slice starts at an even position) of rhs_row_bytes each
+  auto rhs_bytes = [&](int64_t rows) { return (rows + 2) * rhs_row_bytes; };
   auto sd_of = [&](int64_t r) { return A.diag[r] * (1.0 / A.diag[r]); };
   const bool force_explicit = std::getenv("PSLR_EXPLICIT_SD") != nullptr;  // tests: general layout
   auto sd_plain = [&](int64_t r) {
@@ -244,6 +248,8 @@ int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAna
     chunk_rows = 0;
     // the base position of the chunk's rhs slice: first segment, word 6 (even: 16-B TMA alignment)
     reinterpret_cast<int32_t*>(out.data.data() + chunk_start)[6] = (int32_t)(chunk_pos0 & ~int64_t(1));
+    // word 7: the chunk's data bytes = where its rhs slice starts in the stage
+    reinterpret_cast<int32_t*>(out.data.data() + chunk_start)[7] = (int32_t)d.bytes;
     out.chunks.push_back(d);
     chunk_nseg = 0;
     chunk_start = (int64_t)out.data.size();
@@ -275,7 +281,7 @@ int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAna
             const int64_t f2 = nfar + row_far(s1, lend);
             const bool e2 = expl || (upper && !sd_plain(A.row_at_pos[s1]));
             const bool h2 = hfr || fslot[A.row_at_pos[s1]] >= 0;
-            if (seg_bytes(s1 - s0 + 1, w2, f2, e2, h2) > stage_bytes || f2 >= 0x8000) break;
+            if (seg_bytes(s1 - s0 + 1, w2, f2, e2, h2) + rhs_bytes(s1 - s0 + 1) > stage_bytes || f2 >= 0x8000) break;
             w = w2;
             nnz += len;
             nfar = f2;
@@ -297,7 +303,7 @@ int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAna
         }
         const int64_t nrows = s1 - s0;
         const int64_t bytes = seg_bytes(nrows, w, nfar, expl, hfr);
-        if ((int64_t)out.data.size() - chunk_start + bytes > stage_bytes ||
+        if ((int64_t)out.data.size() - chunk_start + bytes + rhs_bytes(chunk_rows + nrows) > stage_bytes ||
             chunk_rows + nrows > kChunkRows)
           close_chunk();
         if (chunk_nseg == 0) chunk_pos0 = s0;

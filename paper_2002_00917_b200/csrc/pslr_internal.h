@@ -56,7 +56,7 @@ struct alignas(16) ChunkDesc {
 #endif
 constexpr int kChunkRows = PSLR_CHUNK_ROWS;
 // bytes of the step kernel's shared-memory control block (mbarriers, descriptor queue)
-constexpr int kCtlBytes = 512;
+constexpr int kCtlBytes = 1024;
 
 // Segment layout inside a chunk (all parts 16-byte aligned; pack.cpp emit_factor):
 //   int32 hdr[12] = {nrows | w << 16, flags | tb << 8, pos0, bytes, S, far_off,
@@ -107,7 +107,8 @@ constexpr int kStepThreads = PSLR_STEP_THREADS;
 
 int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAnalysis& A, int64_t W,
                 int64_t stage_bytes, int64_t seg_rows, const std::vector<int32_t>& far_index,
-                const std::vector<int32_t>& info_of_row, int64_t far_slots_max, TriHost& out, const char* name);
+                const std::vector<int32_t>& info_of_row, int64_t far_slots_max, int64_t rhs_row_bytes,
+                TriHost& out, const char* name);
 
 // Terms of the per-subdomain fused step (see kernels.cu: subdomain_step_kernel).
 enum BTerm : int { BT_NONE = 0, BT_F = 1, BT_EY = 2 };

@@ -187,7 +187,7 @@ struct Ctl {
   uint64_t full[8];       // data + rhs landed (2 arrivals + tx bytes)
   uint64_t empty[8];      // all consumer warps done with the stage (kConsumerWarps arrivals)
   uint64_t rhs_ready[4];  // phase k's rhs array is final (1 arrival)
-  int2 rrec[8];           // per stage: rhs slice (first position, bytes) of the staged chunk
+  int4 rrec[8];           // per stage: rhs slice (first position, bytes, offset in the stage) of its chunk
 };
 
 // The chunks of up to four factor streams of this CTA's block form one sequence.
@@ -226,8 +226,8 @@ static_assert(sizeof(Ctl) <= kCtlBytes, "the control block must fit the header o
 // instructions — poll the stage, read the next descriptor (prefetched into shared
 // memory by cp.async twelve chunks ahead and into registers one chunk ahead), two
 // expect_tx + bulk-copy pairs.  Phase bookkeeping only runs at phase boundaries.
-__device__ void producer(const Streams& S, Ctl* ctl, uint8_t* stages, double* rhsbuf, int nst,
-                         int stage_bytes, int rhs_stride, int nv, long long* g_dbg_out, int dbg,
+__device__ void producer(const Streams& S, Ctl* ctl, uint8_t* stages, int nst,
+                         int stage_bytes, int nv, long long* g_dbg_out, int dbg,
                          long long* g_tma, long long l2ahead) {
   if ((threadIdx.x & 31) != 0) return;
   const int np = S.nphase;
@@ -261,12 +261,13 @@ __device__ void producer(const Streams& S, Ctl* ctl, uint8_t* stages, double* rh
   bool k_ready = false;
   // deferred slices: chunks [r_u, r_hi) of phase r_k (always the current or the next phase)
   int r_u = 0, r_hi = 0, r_k = k;
-  auto rhs_copy = [&](int st, const double* src, uint32_t rpos, uint32_t rbytes) {
+  // the rhs slice lands in the chunk's stage right behind its data (dbytes)
+  auto rhs_copy = [&](int st, const double* src, uint32_t rpos, uint32_t rbytes, uint32_t dbytes) {
     if (dbg & 64) {
       mbar_arrive(&ctl->full[st]);
     } else {
       mbar_expect_tx(&ctl->full[st], rbytes * nv);  // nv interleaved right-hand sides
-      bulk_load(rhsbuf + (size_t)st * rhs_stride, src + (size_t)rpos * nv, rbytes * nv, &ctl->full[st]);
+      bulk_load(stages + (size_t)st * stage_bytes + dbytes, src + (size_t)rpos * nv, rbytes * nv, &ctl->full[st]);
     }
   };
   auto phase_test = [&](int kk, bool block) -> bool {
@@ -284,8 +285,8 @@ __device__ void producer(const Streams& S, Ctl* ctl, uint8_t* stages, double* rh
     if (!phase_test(r_k, block)) return;
     for (; r_u < r_hi; ++r_u) {
       const int st = r_u % nst;
-      const int2 rr = ctl->rrec[st];
-      rhs_copy(st, S.rhs[r_k], (uint32_t)rr.x, (uint32_t)rr.y);
+      const int4 rr = ctl->rrec[st];
+      rhs_copy(st, S.rhs[r_k], (uint32_t)rr.x, (uint32_t)rr.y, (uint32_t)rr.z);
     }
     if (r_k == k) k_ready = true;
   };
@@ -336,10 +337,10 @@ __device__ void producer(const Streams& S, Ctl* ctl, uint8_t* stages, double* rh
     }
     if (!k_ready && r_u == r_hi && phase_test(k, false)) k_ready = true;  // cheap once known
     if (k_ready) {
-      rhs_copy(st, rhs, dv.z, dv.w);
+      rhs_copy(st, rhs, dv.z, dv.w, dv.y);
       r_u = r_hi = u + 1;
     } else {
-      ctl->rrec[st] = make_int2((int32_t)dv.z, (int)dv.w);
+      ctl->rrec[st] = make_int4((int32_t)dv.z, (int)dv.w, (int)dv.y, 0);
       r_hi = u + 1;
     }
     // next descriptor (its cp.async landed long ago) and the one twelve chunks ahead
@@ -579,7 +580,7 @@ __device__ __forceinline__ void compute_row(const StepConst& K, uint32_t seg, in
 // of its last level.  rel: the release cursor over the stages (carried across phases).
 template <bool UPPER, int NV, bool XPOS = false>
 __device__ void tri_phase(const StepConst& K, const Streams& Sm, Ctl* ctl, uint8_t* stages_p,
-                          double* rhsbuf_p, int k, double* ring, int base, double* z, double* xout,
+                          int k, double* ring, int base, double* z, double* xout,
                           const double* cadd) {
   trace_ev(K, 10 + k, 0);
   trace_cta(K, 2 + k);
@@ -587,7 +588,7 @@ __device__ void tri_phase(const StepConst& K, const Streams& Sm, Ctl* ctl, uint8
   int u = Sm.begin[k];
   const int u1 = Sm.begin[k + 1];
   if (u == u1) return;
-  const uint32_t stages = (uint32_t)(stages_p - smem), rhsbuf = (uint32_t)((uint8_t*)rhsbuf_p - smem);
+  const uint32_t stages = (uint32_t)(stages_p - smem);
   const int nst = K.nst, zslot = K.ring_mask + 1;
   int st = u % nst;
   uint32_t par = (uint32_t)((u / nst) & 1);
@@ -616,7 +617,7 @@ __device__ void tri_phase(const StepConst& K, const Streams& Sm, Ctl* ctl, uint8
   mbar_wait(&ctl->full[st], par);
   uint32_t segA = stages + (uint32_t)(st * K.stage_bytes);
   int stA = st, stB = st;  // stages holding A and B (released after their chunk's last segment)
-  uint32_t rbuf = rhsbuf + (uint32_t)(st * K.rhs_stride * 8);
+  uint32_t rbuf = segA + (uint32_t)sp<int32_t>(segA)[7];  // the rhs slice behind the chunk's data
   int rbase = sp<int32_t>(segA)[6];
   int4 hA = *sp<int4>(segA);
   bool actA = warp_owns(hA);
@@ -634,7 +635,7 @@ __device__ void tri_phase(const StepConst& K, const Streams& Sm, Ctl* ctl, uint8
       if (PSLR_TRACE_BUILD && K.trace && blockIdx.x == K.trace_block && threadIdx.x == 0 && u < 8192)
         K.trace[2 + 2 * 65536 + 2 * u + 1] = clock64();  // the chunk seen by the look-ahead
       nseg = stages + (uint32_t)(st * K.stage_bytes);
-      rbuf = rhsbuf + (uint32_t)(st * K.rhs_stride * 8);
+      rbuf = nseg + (uint32_t)sp<int32_t>(nseg)[7];
       rbase = sp<int32_t>(nseg)[6];
     } else {
       nseg = seg + (uint32_t)h.w;
@@ -766,12 +767,11 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
   const bool do_c = do_i && a.do_c0;
 
   Ctl* ctl = reinterpret_cast<Ctl*>(smem);
-  // [Ctl 256 B][ring: (W + zero slot) x NV, padded to 128 B][nst stages][nst rhs slices]
+  // [Ctl][ring: (W + zero slot + far-ring) x NV, padded to 128 B][nst stages: chunk data + its rhs slice]
   // The ring sits at a constant offset, so a gather is one address op on its slot.
   double* ring = reinterpret_cast<double*>(smem + kCtlBytes);
   // [ring W | zero slot | far-ring] padded to 128 B, then the stages
   uint8_t* stages = smem + kCtlBytes + (((size_t)(K.ring_mask + 2 + K.far_slots) * 8 * NV + 127) / 128) * 128;
-  double* rhsbuf = reinterpret_cast<double*>(stages + (size_t)K.nst * K.stage_bytes);
 
   // The stream table lives in shared memory: dynamically indexed per-thread arrays would
   // spill to local memory, which misses the small L1 left beside 229 KB of shared memory.
@@ -814,7 +814,7 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
   }
   __syncthreads();
   if (threadIdx.x >= kStepThreads) {  // producer warp (all 32 lanes)
-    producer(S, ctl, stages, rhsbuf, K.nst, K.stage_bytes, K.rhs_stride, NV,
+    producer(S, ctl, stages, K.nst, K.stage_bytes, NV,
              (K.trace && K.trace_cap >= (1 << 20)) ? K.trace + 2 + 2 * K.trace_cap - 8 * 4096 + b * 8
                                                    : nullptr,
              K.dbg,
@@ -911,8 +911,8 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
     consumer_sync();
     trace_ev(K, 3, 0);
     trace_cta(K, 1);
-    tri_phase<false, NV>(K, S, ctl, stages, rhsbuf, ph_LB, ring, r0, K.zB, nullptr, nullptr);
-    tri_phase<true, NV, XPOS>(K, S, ctl, stages, rhsbuf, ph_UB, ring, r0, K.zB, a.xb, nullptr);
+    tri_phase<false, NV>(K, S, ctl, stages, ph_LB, ring, r0, K.zB, nullptr, nullptr);
+    tri_phase<true, NV, XPOS>(K, S, ctl, stages, ph_UB, ring, r0, K.zB, a.xb, nullptr);
   }
   if (do_i) {
     trace_cta(K, 7);
@@ -948,8 +948,8 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
     consumer_sync();
     trace_ev(K, 30, 0);
     if (do_c) {
-      tri_phase<false, NV>(K, S, ctl, stages, rhsbuf, ph_LC, ring, r0, K.zC, nullptr, nullptr);
-      tri_phase<true, NV>(K, S, ctl, stages, rhsbuf, ph_UC, ring, r0, K.zC, a.yout, a.cadd);
+      tri_phase<false, NV>(K, S, ctl, stages, ph_LC, ring, r0, K.zC, nullptr, nullptr);
+      tri_phase<true, NV>(K, S, ctl, stages, ph_UC, ring, r0, K.zC, a.yout, a.cadd);
     }
   }
   trace_cta(K, 6);

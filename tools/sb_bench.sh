@@ -1,7 +1,7 @@
 #!/bin/bash
 # stage-size sweep through the bench: concurrent sweep ms/apply, single stream, Horner launch
 mkdir -p gpurun_out
-for sb in ${SBS:-32768 45056}; do
+for sb in ${SBS:-53248}; do
   PSLR_STAGE_BYTES=$sb timeout 400 python bench.py --steps 400 --warmup 3 --no-cpu-baseline --e2e-steps 8 --gmres-maxit 0 --solves "" 2>>gpurun_out/sb_bench.err | python3 -c "
 import json,sys
 for l in sys.stdin:
