@@ -122,6 +122,8 @@ __device__ __forceinline__ double spmv_row_rw(const DevCsr& M, int row, const do
 __shared__ long long* g_trace_ptr;
 __shared__ int g_trace_n;
 __shared__ int g_trace_tag;
+__shared__ long long g_wait_cyc;  // trace builds: thread 0's chunk-wait cycles / transitions
+__shared__ int g_wait_n, g_wait_big;
 
 constexpr int kTraceWindow = 1 << 15;
 
@@ -631,7 +633,15 @@ __device__ void tri_phase(const StepConst& K, const Streams& Sm, Ctl* ctl, uint8
         st = 0;
         par ^= 1u;
       }
+      long long tw0 = 0;
+      if (PSLR_TRACE_BUILD && threadIdx.x == 0) tw0 = clock64();
       mbar_wait(&ctl->full[st], par);
+      if (PSLR_TRACE_BUILD && threadIdx.x == 0) {
+        const long long dw = clock64() - tw0;
+        g_wait_cyc += dw;
+        g_wait_n += 1;
+        g_wait_big += dw > 200 ? 1 : 0;
+      }
       if (PSLR_TRACE_BUILD && K.trace && blockIdx.x == K.trace_block && threadIdx.x == 0 && u < 8192)
         K.trace[2 + 2 * 65536 + 2 * u + 1] = clock64();  // the chunk seen by the look-ahead
       nseg = stages + (uint32_t)(st * K.stage_bytes);
@@ -827,7 +837,11 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
   // consumers wait here for its completion before reading any vector it produced or
   // writing any buffer it may still read.  A no-op for ordinary launches.
   asm volatile("griddepcontrol.wait;" ::: "memory");
-  if (PSLR_TRACE_BUILD && threadIdx.x == 0) g_trace_tag = a.tag;
+  if (PSLR_TRACE_BUILD && threadIdx.x == 0) {
+    g_trace_tag = a.tag;
+    g_wait_cyc = 0;
+    g_wait_n = g_wait_big = 0;
+  }
   trace_begin(K);
   trace_ev(K, 1, S.begin[S.nphase]);
   trace_cta(K, 0);
@@ -953,6 +967,12 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
     }
   }
   trace_cta(K, 6);
+  if (PSLR_TRACE_BUILD && K.trace && threadIdx.x == 0 && K.trace_cap >= (1 << 20) && blockIdx.x < 64) {
+    long long* w = K.trace + 2 + 2 * K.trace_cap - 8 * 4096 + (3072 + 64 * (g_trace_tag & 15) + blockIdx.x) * 8;
+    w[0] = g_wait_cyc;
+    w[1] = g_wait_n;
+    w[2] = g_wait_big;
+  }
 }
 
 // The parts of a step that only need vectors of earlier launches, for every block at once

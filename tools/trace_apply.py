@@ -154,7 +154,9 @@ for tag, kname in kinds.items():
         marks = sorted([(i, row[i]) for i in range(8) if row[i] >= row[0] > 0], key=lambda m: m[1])
         for (i, tv), (j, tn) in zip(marks, marks[1:]):
             seg.append(f"{names_s[i]} {(tn - tv) / 1e3:.1f}")
-        print(f"   CTA {b:3d}: start {(row[0] - t0) / 1e3:6.1f} end {(row[6] - t0) / 1e3:6.1f}  |  " + ", ".join(seg))
+        wt = area[3072 + 64 * tag + b]
+        wtxt = f"  | chunk waits {wt[0] / 1.965e3:.1f} us over {int(wt[1])} transitions ({int(wt[2])} > 200 cyc)" if wt[1] else ""
+        print(f"   CTA {b:3d}: start {(row[0] - t0) / 1e3:6.1f} end {(row[6] - t0) / 1e3:6.1f}  |  " + ", ".join(seg) + wtxt)
 out = os.environ.get("TRACE_DUMP")
 if out:
     np.savez(out, **dump)
