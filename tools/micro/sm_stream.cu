@@ -1,5 +1,5 @@
 // Per-SM streaming bandwidth: TMA bulk ring vs plain LDG with many loads in flight,
-// 1 CTA and 32 CTAs (one per SM), 8 MB per CTA from HBM (buffer >> L2 in total).
+// 1, 32, 148 and 296 CTAs (296: two per SM), 8 MB per CTA from HBM (buffer >> L2 in total).
 #include <cstdio>
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -66,8 +66,8 @@ int main() {
   const size_t per = 8u << 20;
   uint8_t* src;
   double* sink;
-  cudaMalloc(&src, per * 148);
-  cudaMemset(src, 0, per * 148);
+  cudaMalloc(&src, per * 296);
+  cudaMemset(src, 0, per * 296);
   cudaMalloc(&sink, 8);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
@@ -82,23 +82,23 @@ int main() {
     cudaEventElapsedTime(&ms, e0, e1);
     return (double)per / (ms * 1e-3) / 1e9;
   };
-  for (int ctas : {1, 32}) {
-    for (int sb : {16384, 32768, 49152}) {
+  for (int ctas : {1, 32, 148, 296}) {
+    for (int sb : {16384, 24576, 32768, 49152}) {
       for (int nst : {4, 6}) {
         int smem = 256 + sb * nst;
-        if (smem > 227 * 1024) continue;
+        if (smem > 227 * 1024 || (ctas == 296 && smem > 113 * 1024)) continue;
         cudaFuncSetAttribute(tma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
         double g = timeit([&](int c) { tma_kernel<<<c, 512, smem>>>(src, per, nst, sb, sink); }, ctas);
-        printf("ctas %2d TMA sb %6d nst %d (%3d KB in flight): %6.1f GB/s per CTA\n", ctas, sb, nst, sb * nst / 1024, g);
+        printf("ctas %3d TMA sb %6d nst %d (%3d KB in flight): %6.1f GB/s per CTA, %7.0f GB/s total\n", ctas, sb, nst, sb * nst / 1024, g, g * ctas);
       }
     }
     double g;
     g = timeit([&](int c) { ldg_kernel<8><<<c, 512>>>(src, per, sink); }, ctas);
-    printf("ctas %2d LDG 512x8x16B (64 KB in flight): %6.1f GB/s per CTA\n", ctas, g);
+    printf("ctas %3d LDG 512x8x16B (64 KB in flight): %6.1f GB/s per CTA, %7.0f GB/s total\n", ctas, g, g * ctas);
     g = timeit([&](int c) { ldg_kernel<16><<<c, 512>>>(src, per, sink); }, ctas);
-    printf("ctas %2d LDG 512x16x16B (128 KB in flight): %6.1f GB/s per CTA\n", ctas, g);
+    printf("ctas %3d LDG 512x16x16B (128 KB in flight): %6.1f GB/s per CTA, %7.0f GB/s total\n", ctas, g, g * ctas);
     g = timeit([&](int c) { ldg_kernel<16><<<c, 1024>>>(src, per, sink); }, ctas);
-    printf("ctas %2d LDG 1024x16x16B (256 KB in flight): %6.1f GB/s per CTA\n", ctas, g);
+    printf("ctas %3d LDG 1024x16x16B (256 KB in flight): %6.1f GB/s per CTA, %7.0f GB/s total\n", ctas, g, g * ctas);
   }
   printf("err %s\n", cudaGetErrorString(cudaGetLastError()));
 }
