@@ -115,9 +115,16 @@ struct PackedSystem {
   TriHost H2[4];
   std::vector<int32_t> ub_pos;       // U_B: row -> U-position (x order, Fpos columns)
   std::vector<int32_t> lb_pos;       // L_B: row -> L-position (E rows' rhs placement)
+  // level-merged factors (PSLR_MERGE bit f/2: 1 = L_B/U_B, 2 = L_C0/U_C0; pack.cpp
+  // merge_levels): each factor's rhs transform in the position space of the array it
+  // rewrites, and L_B's again in row space (permute_f, E' = E - N E)
+  int64_t merged = 0;
+  std::vector<int32_t> blk_levels;   // per block: L_B + U_B dependency levels (L2 residency)
+  MergeXf X[4];
+  MergeXf XLBrow;
 };
 
-constexpr uint64_t kPackMagic = 0x34764b4150524c53ull;  // "SLRPAKv4" (two chunk sizes, far-ring, rhs in stage)
+constexpr uint64_t kPackMagic = 0x35764b4150524c53ull;  // "SLRPAKv5" (v4 + level-merged factors)
 
 // Stages of the step kernel's pipeline for chunk size sb and nv vectors per launch: what
 // the shared memory holds beside the control block and the (nv-wide) value ring, at most 8
@@ -130,6 +137,17 @@ static int64_t stage_count(int64_t smem_optin, int64_t W, int64_t sb, int64_t nv
 
 // Level analysis of the four factors, the ring size W (from the reach and the device's
 // shared memory) and the streamed chunks of every block (pack.cpp).
+// PSLR_MERGE: 0 = the reference's factors as they are (bit-exact), 1 = level-merged B
+// factors, 2 = level-merged C0 factors (default), 3 = both.  PSLR_MERGE_W / _WC: merge only
+// level pairs of at most that many rows (B: kStepThreads, C0: 0 = every pair)
+// The blob key: mode bits 0-1, the B width limit from bit 2, the C0 width limit from bit 32
+static int64_t merge_mode() {
+  const int64_t mode = env_int("PSLR_MERGE", 2) & 3;
+  const int64_t wB = std::min<int64_t>(std::max<int64_t>(env_int("PSLR_MERGE_W", kStepThreads), 0), (1 << 29) - 1);
+  const int64_t wC = std::min<int64_t>(std::max<int64_t>(env_int("PSLR_MERGE_WC", 0), 0), (1 << 29) - 1);
+  return mode | (wB << 2) | (wC << 32);
+}
+
 static int pack_system(const pslr_system* sys, const std::vector<int64_t>& ioff, const std::vector<int64_t>& foff,
                        int64_t smem_optin, int64_t SB, int64_t SB2, int64_t wmax, PackedSystem& P) {
   P.n = sys->n;
@@ -138,24 +156,48 @@ static int pack_system(const pslr_system* sys, const std::vector<int64_t>& ioff,
   P.q = sys->q;
   P.s = sys->s;
   P.SB = SB;
+  // level merging (depth halving, pack.cpp merge_levels): the streams carry the merged rows
+  P.merged = merge_mode();
+  HostCsr mf[4];
+  pslr_csr LB = sys->LB, UB = sys->UB, LC = sys->LC, UC = sys->UC;
+  if (P.merged & 1) {
+    const int64_t wB = (P.merged >> 2) & ((1 << 29) - 1);
+    RET(merge_levels(sys->LB, ioff, false, wB, mf[0], P.X[0], "L_B"));
+    RET(merge_levels(sys->UB, ioff, true, wB, mf[1], P.X[1], "U_B"));
+    LB = mf[0].view();
+    UB = mf[1].view();
+  }
+  if (P.merged & 2) {
+    const int64_t wC = P.merged >> 32;
+    RET(merge_levels(sys->LC, foff, false, wC, mf[2], P.X[2], "L_C0"));
+    RET(merge_levels(sys->UC, foff, true, wC, mf[3], P.X[3], "U_C0"));
+    LC = mf[2].view();
+    UC = mf[3].view();
+  }
   TriAnalysis aLB, aUB, aLC, aUC;
-  RET(analyze_factor(sys->LB, ioff, false, aLB, "L_B"));
-  RET(analyze_factor(sys->UB, ioff, true, aUB, "U_B"));
-  RET(analyze_factor(sys->LC, foff, false, aLC, "L_C0"));
-  RET(analyze_factor(sys->UC, foff, true, aUC, "U_C0"));
+  RET(analyze_factor(LB, ioff, false, aLB, "L_B"));
+  RET(analyze_factor(UB, ioff, true, aUB, "U_B"));
+  RET(analyze_factor(LC, foff, false, aLC, "L_C0"));
+  RET(analyze_factor(UC, foff, true, aUC, "U_C0"));
   P.reach = std::max({aLB.reach, aUB.reach, aLC.reach, aUC.reach, (int64_t)1});
   int64_t W = 2048;  // >= 2048: the ring doubles as the V^T y reduction scratch
   while (W < P.reach && W < wmax) W *= 2;
   while (W > 2048 && (smem_optin - 1024 - kCtlBytes - W * 8 - 128) / SB < 2) W /= 2;
   P.W = W;
   const TriAnalysis* an[4] = {&aLB, &aUB, &aLC, &aUC};
-  const pslr_csr* M[4] = {&sys->LB, &sys->UB, &sys->LC, &sys->UC};
+  const pslr_csr* M[4] = {&LB, &UB, &LC, &UC};
+  const pslr_csr* M0[4] = {&sys->LB, &sys->UB, &sys->LC, &sys->UC};
   const char* nm[4] = {"L_B", "U_B", "L_C0", "U_C0"};
   for (int f = 0; f < 4; ++f) {
     P.levels[f] = an[f]->levels;
     P.depth[f] = an[f]->depth_max;
-    P.nnz[f] = M[f]->nnz;
+    P.nnz[f] = M0[f]->nnz;  // the system's factors (blob validation)
   }
+  // the merged rows' rhs transforms: L_B's in row space too, then every record in the
+  // position space of the array it rewrites (L: L-positions, U: U-positions)
+  P.XLBrow = P.X[0];
+  for (int f = 0; f < 4; ++f)
+    for (auto& v : P.X[f].rows) v = an[f]->pos_of_row[v];
   // far-ring capacity of each launch width: the shared memory a launch's stage plan leaves
   // beside the ring (PSLR_FAR_SLOTS caps it; 0 = every far dependency read from global)
   auto far_cap = [&](int64_t sb, int64_t nv) -> int64_t {
@@ -191,6 +233,8 @@ static int pack_system(const pslr_system* sys, const std::vector<int64_t>& ioff,
   }
   P.ub_pos = aUB.pos_of_row;
   P.lb_pos = aLB.pos_of_row;
+  P.blk_levels.assign(P.s, 0);
+  for (int64_t b = 0; b < P.s; ++b) P.blk_levels[b] = aLB.blk_depth[b] + aUB.blk_depth[b];
   return PSLR_OK;
 }
 
@@ -260,6 +304,14 @@ static void serialize(const PackedSystem& P, std::vector<uint8_t>& out) {
   }
   w.vec(P.ub_pos);
   w.vec(P.lb_pos);
+  w.put(P.merged);
+  w.vec(P.blk_levels);
+  for (int f = 0; f < 5; ++f) {
+    const MergeXf& X = f < 4 ? P.X[f] : P.XLBrow;
+    w.vec(X.rows);
+    w.vec(X.c);
+    w.vec(X.blk);
+  }
   out.swap(w.b);
 }
 
@@ -303,6 +355,16 @@ static bool deserialize(const void* blob, int64_t len, const pslr_system* sys, i
   }
   r.vec(P.ub_pos);
   r.vec(P.lb_pos);
+  P.merged = r.get<int64_t>();
+  if (!r.ok || P.merged != merge_mode()) return false;
+  r.vec(P.blk_levels);
+  if ((int64_t)P.blk_levels.size() != P.s) return false;
+  for (int f = 0; f < 5; ++f) {
+    MergeXf& X = f < 4 ? P.X[f] : P.XLBrow;
+    r.vec(X.rows);
+    r.vec(X.c);
+    r.vec(X.blk);
+  }
   return r.ok && r.left == 0 && (int64_t)P.ub_pos.size() == P.p && (int64_t)P.lb_pos.size() == P.p &&
          stage_count(smem_optin, P.W, SB, 1) >= 2;
 }
@@ -707,6 +769,27 @@ int pslr_ctx_create_packed(pslr_ctx** out, int device, const pslr_system* sys, c
   ctx->split_iface = env_int("PSLR_SPLIT_IFACE", 1) != 0;
   ctx->K.dbg = (int)env_int("PSLR_DBG", 0);
   ctx->K.l2ahead = env_int("PSLR_L2AHEAD", 0);
+  {  // L2 residency of the deepest blocks' B factor streams (PSLR_L2KEEP_MB, 0 = off): blocks
+     // in decreasing dependency depth while their L_B + U_B chunks fit the budget
+    const int64_t budget = env_int("PSLR_L2KEEP_MB", 48) << 20;
+    if (budget > 0 && s > 0) {
+      std::vector<int64_t> order(s), bytes(s, 0);
+      for (int64_t b = 0; b < s; ++b) {
+        order[b] = b;
+        for (int f = 0; f < 2; ++f)
+          for (int32_t c = P.F[f].H.blk_chunk[b]; c < P.F[f].H.blk_chunk[b + 1]; ++c) bytes[b] += P.F[f].H.chunks[c].bytes;
+      }
+      std::stable_sort(order.begin(), order.end(), [&](int64_t a, int64_t c) { return P.blk_levels[a] > P.blk_levels[c]; });
+      std::vector<int8_t> keep(s, 0);
+      int64_t used = 0;
+      for (int64_t b : order) {
+        if (used + bytes[b] > budget) break;
+        used += bytes[b];
+        keep[b] = 1;
+      }
+      if (used > 0 && (rc = upload(ctx, keep, &ctx->K.l2keep))) return bail(rc);
+    }
+  }
   if (env_int("PSLR_TRACE", 0)) {  // diagnostics: timeline of CTA 0 (pslr_debug_trace)
     const int64_t cap = 1 << 20;
     void* d = nullptr;
@@ -756,7 +839,76 @@ int pslr_ctx_create_packed(pslr_ctx** out, int device, const pslr_system* sys, c
   I.far_deps = P.far;
   I.reach = reach;
 
-  if ((rc = upload_csr(ctx, sys->E, &ctx->K.E))) return bail(rc);
+  // level-merged factors: the in-place rhs transforms of the merged rows; L_B's also as
+  // the permute_f gather map (lrowx) and folded into E (E' = E - N E: the E y rows of the
+  // L_B right-hand side arrive transformed)
+  HostCsr Em;
+  pslr_csr Eu = sys->E;
+  {
+    DevXform* dx[4] = {&ctx->K.XLB, &ctx->K.XUB, &ctx->K.XLC, &ctx->K.XUC};
+    for (int f = 0; f < 4; ++f) {
+      const MergeXf& X = P.X[f];
+      if (X.blk.empty() || X.rows.empty()) continue;
+      dx[f]->nrec = (int32_t)(X.rows.size() / kXfWidth1);
+      if ((rc = upload(ctx, X.rows, &dx[f]->idx))) return bail(rc);
+      if ((rc = upload(ctx, X.c, &dx[f]->val))) return bail(rc);
+      if ((rc = upload(ctx, X.blk, &dx[f]->blk))) return bail(rc);
+    }
+    const MergeXf& XL = P.XLBrow;
+    const int64_t nrec = (int64_t)(XL.rows.size() / kXfWidth1);
+    if (nrec > 0) {
+      std::vector<int32_t> lrowx = P.F[0].row_at_pos;
+      for (int64_t k = 0; k < nrec; ++k) lrowx[P.lb_pos[XL.rows[kXfWidth1 * k]]] = (int32_t)(-(k + 1));
+      if ((rc = upload(ctx, lrowx, &ctx->K.lrowx))) return bail(rc);
+      if ((rc = upload(ctx, XL.rows, &ctx->K.xlb_rows))) return bail(rc);
+      // E'_i = E_i - sum_j c_ij E_j over the record of each merged row i
+      const pslr_csr& E = sys->E;
+      std::vector<int64_t> rec_of(p, -1);
+      for (int64_t k = 0; k < nrec; ++k) rec_of[XL.rows[kXfWidth1 * k]] = k;
+      Em.nrows = E.nrows;
+      Em.ncols = E.ncols;
+      Em.indptr.assign(p + 1, 0);
+      std::vector<double> acc(q, 0.0);
+      std::vector<uint8_t> used(q, 0);
+      std::vector<int32_t> cols;
+      for (int64_t i = 0; i < p; ++i) {
+        const int64_t k = rec_of[i];
+        if (k < 0) {
+          for (int64_t e = E.indptr[i]; e < E.indptr[i + 1]; ++e) {
+            Em.indices.push_back(E.indices[e]);
+            Em.data.push_back(E.data[e]);
+          }
+        } else {
+          cols.clear();
+          auto add = [&](int32_t j, double v) {
+            if (!used[j]) {
+              used[j] = 1;
+              acc[j] = 0.0;
+              cols.push_back(j);
+            }
+            acc[j] += v;
+          };
+          for (int64_t e = E.indptr[i]; e < E.indptr[i + 1]; ++e) add(E.indices[e], E.data[e]);
+          for (int a = 0; a < kXfWidth; ++a) {
+            const int64_t j = XL.rows[kXfWidth1 * k + 1 + a];
+            const double c = XL.c[kXfWidth1 * k + a];
+            if (c == 0.0) continue;
+            for (int64_t e = E.indptr[j]; e < E.indptr[j + 1]; ++e) add(E.indices[e], -c * E.data[e]);
+          }
+          std::sort(cols.begin(), cols.end());
+          for (int32_t j : cols) {
+            used[j] = 0;
+            Em.indices.push_back(j);
+            Em.data.push_back(acc[j]);
+          }
+        }
+        Em.indptr[i + 1] = (int64_t)Em.indices.size();
+      }
+      Em.nnz = (int64_t)Em.indices.size();
+      Eu = Em.view();
+    }
+  }
+  if ((rc = upload_csr(ctx, Eu, &ctx->K.E))) return bail(rc);
   if ((rc = upload_csr(ctx, sys->F, &ctx->K.F))) return bail(rc);
   if ((rc = upload_csr(ctx, sys->C, &ctx->K.C))) return bail(rc);
   if ((rc = upload_csr(ctx, sys->C0, &ctx->C0))) return bail(rc);
@@ -775,11 +927,11 @@ int pslr_ctx_create_packed(pslr_ctx** out, int device, const pslr_system* sys, c
     std::vector<int32_t> er, eo(s + 1, 0);
     for (int64_t b = 0; b < s; ++b) {
       for (int64_t i = ctx->interior_off[b]; i < ctx->interior_off[b + 1]; ++i)
-        if (sys->E.indptr[i + 1] > sys->E.indptr[i]) {
+        if (Eu.indptr[i + 1] > Eu.indptr[i]) {
           er.push_back(P.lb_pos[i]);
           er.push_back((int32_t)i);
-          er.push_back((int32_t)sys->E.indptr[i]);
-          er.push_back((int32_t)sys->E.indptr[i + 1]);
+          er.push_back((int32_t)Eu.indptr[i]);
+          er.push_back((int32_t)Eu.indptr[i + 1]);
         }
       eo[b + 1] = (int32_t)(er.size() / 4);
     }

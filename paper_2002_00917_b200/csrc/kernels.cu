@@ -246,10 +246,55 @@ __global__ void permute_f_kernel(const int32_t* __restrict__ lrow, const double*
     fL[i] = __ldg(f + __ldg(lrow + i));
 }
 
+// Level-merged L_B (pack.cpp merge_levels): a merged row's right-hand side is
+// f_i - (c0 f_j0 + c1 f_j1 + c2 f_j2); lrowx holds -(record + 1) at its position.
+template <int NV>
+__device__ __forceinline__ void permute_x_one(const int32_t* __restrict__ lrowx, const int4* __restrict__ xrows,
+                                              const double2* __restrict__ xval, const double* __restrict__ b,
+                                              int64_t n, double* __restrict__ fL, int64_t i) {
+  auto ld = [&](int64_t row) -> double2 {
+    return make_double2(__ldg(b + row), NV == 2 ? __ldg(b + n + row) : 0.0);
+  };
+  const int r = __ldg(lrowx + i);
+  double2 v;
+  if (r >= 0) {
+    v = ld(r);
+  } else {
+    const int k = -r - 1;
+    const int4 id = __ldg(xrows + k);
+    const double2 c01 = __ldg(xval + 2 * k), c2 = __ldg(xval + 2 * k + 1);
+    const double2 fi = ld(id.x), f0 = ld(id.y), f1 = ld(id.z), f2 = ld(id.w);
+    double tx = f0.x * c01.x;
+    tx = tx + c01.y * f1.x;
+    tx = tx + c2.x * f2.x;
+    double ty = f0.y * c01.x;
+    ty = ty + c01.y * f1.y;
+    ty = ty + c2.x * f2.y;
+    v = make_double2(fi.x - tx, fi.y - ty);
+  }
+  if (NV == 2)
+    reinterpret_cast<double2*>(fL)[i] = v;
+  else
+    fL[i] = v.x;
+}
+
+__global__ void permute_fx_kernel(const int32_t* __restrict__ lrowx, const int4* __restrict__ xrows,
+                                  const double2* __restrict__ xval, const double* __restrict__ f,
+                                  double* __restrict__ fL, int64_t p) {
+  pdl_wait();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p; i += (int64_t)gridDim.x * blockDim.x)
+    permute_x_one<1>(lrowx, xrows, xval, f, 0, fL, i);
+}
+
 int launch_permute_f(const pslr_ctx* ctx, const double* f, cudaStream_t st) {
   if (ctx->p == 0) return 0;
   const int blocks = 4 * ctx->sm_count;
-  launch_pdl(permute_f_kernel, dim3(blocks), dim3(512), 0, st, ctx->K.LB.lrow, f, ctx->fL, ctx->p);
+  if (ctx->K.lrowx)
+    launch_pdl(permute_fx_kernel, dim3(blocks), dim3(512), 0, st, ctx->K.lrowx,
+               reinterpret_cast<const int4*>(ctx->K.xlb_rows), reinterpret_cast<const double2*>(ctx->K.XLB.val), f,
+               ctx->fL, ctx->p);
+  else
+    launch_pdl(permute_f_kernel, dim3(blocks), dim3(512), 0, st, ctx->K.LB.lrow, f, ctx->fL, ctx->p);
   return (int)cudaGetLastError();
 }
 
@@ -262,6 +307,20 @@ __global__ void permute2_kernel(const int32_t* __restrict__ lrow, const double* 
     if (i < p) {
       const int64_t row = __ldg(lrow + i);
       reinterpret_cast<double2*>(fL2)[i] = make_double2(__ldg(b + row), __ldg(b + n + row));
+    } else {
+      const int64_t k = i - p;
+      reinterpret_cast<double2*>(g2)[k] = make_double2(__ldg(b + p + k), __ldg(b + n + p + k));
+    }
+  }
+}
+
+__global__ void permute2x_kernel(const int32_t* __restrict__ lrowx, const int4* __restrict__ xrows,
+                                 const double2* __restrict__ xval, const double* __restrict__ b, int64_t n,
+                                 int64_t p, int64_t q, double* __restrict__ fL2, double* __restrict__ g2) {
+  pdl_wait();
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < p + q; i += (int64_t)gridDim.x * blockDim.x) {
+    if (i < p) {
+      permute_x_one<2>(lrowx, xrows, xval, b, n, fL2, i);
     } else {
       const int64_t k = i - p;
       reinterpret_cast<double2*>(g2)[k] = make_double2(__ldg(b + p + k), __ldg(b + n + p + k));
@@ -282,7 +341,13 @@ __global__ void deinterleave2_kernel(const double* __restrict__ x2, const double
 int vt_grid(int64_t q, int sm_count);
 
 int launch_permute2(const pslr_ctx* ctx, const double* b, cudaStream_t st) {
-  launch_pdl(permute2_kernel, dim3(4 * ctx->sm_count), dim3(512), 0, st, ctx->K.LB.lrow, b, ctx->n, ctx->p, ctx->q, ctx->fL2, ctx->g2);
+  if (ctx->K.lrowx)
+    launch_pdl(permute2x_kernel, dim3(4 * ctx->sm_count), dim3(512), 0, st, ctx->K.lrowx,
+               reinterpret_cast<const int4*>(ctx->K.xlb_rows), reinterpret_cast<const double2*>(ctx->K.XLB.val), b,
+               ctx->n, ctx->p, ctx->q, ctx->fL2, ctx->g2);
+  else
+    launch_pdl(permute2_kernel, dim3(4 * ctx->sm_count), dim3(512), 0, st, ctx->K.LB.lrow, b, ctx->n, ctx->p,
+               ctx->q, ctx->fL2, ctx->g2);
   return (int)cudaGetLastError();
 }
 

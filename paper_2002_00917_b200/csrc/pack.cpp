@@ -46,6 +46,7 @@ int analyze_factor(const pslr_csr& M, const std::vector<int64_t>& off, bool uppe
   A.reach = 0;
   A.level_of_row.assign(n, 0);
   A.len.assign(n, 0);
+  A.blk_depth.assign(nb, 0);
   for (int64_t r = 0; r < n; ++r) {
     int32_t c = 0;
     for (int64_t e = M.indptr[r]; e < M.indptr[r + 1]; ++e) c += (M.indices[e] != r);
@@ -80,6 +81,7 @@ int analyze_factor(const pslr_csr& M, const std::vector<int64_t>& off, bool uppe
     int32_t depth = 0;
     for (int64_t i = 0; i < nr; ++i) depth = std::max(depth, lev[i] + 1);
     A.depth_max = std::max<int64_t>(A.depth_max, depth);
+    A.blk_depth[b] = depth;
     A.levels += depth;
     std::vector<int64_t> order(nr);
     std::iota(order.begin(), order.end(), 0);
@@ -407,6 +409,153 @@ int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAna
   out.blk_chunk[nb] = (int32_t)out.chunks.size();
   if ((uint64_t)out.data.size() / 16 > 0xffffffffull)
     return fail(PSLR_EINVAL, std::string(name) + ": packed factor exceeds 64 GiB");
+  return PSLR_OK;
+}
+
+}  // namespace pslr
+
+namespace pslr {
+
+// Level merging (depth halving) of a block-diagonal triangular factor.
+//
+// A row i at an odd dependency level l has its dependencies at level l - 1 substituted by
+// their own rows (rows at level l - 1 are at an even level and keep theirs):
+//   L (unit lower):  z_i = b_i - sum_k L_ik z_k,  z_j = b_j - sum_k L_jk z_k
+//     L'_ik = L_ik [k not adjacent] - sum_j L_ij L_jk ,   b'_i = b_i - sum_j L_ij b_j
+//   U (upper):       U_ii x_i = y_i - sum_k U_ik x_k,  c_ij = U_ij / U_jj
+//     U'_ik = U_ik [k not adjacent] - sum_j c_ij U_jk ,   y'_i = y_i - sum_j c_ij y_j
+// over the adjacent-level dependencies j of i.  Every dependency of a merged row then sits
+// at level <= l - 2, so a row at level l lands at level ceil(l / 2): the level count halves
+// at ~1.5x the off-diagonal entries (cfg5: L 156 -> 78, U 370 -> 185 levels on the deepest
+// block).  Same operator, different rounding: the solve is exact up to fp64 round-off, not
+// bit-identical with the reference's row-by-row substitution (north star: 1e-10).
+//
+// The right-hand-side transform of the merged rows is returned as records of at most
+// kXfWidth terms (i, j0..j2; c0..c2): rhs'_i = rhs_i - (c0 rhs_j0 + c1 rhs_j1 + c2 rhs_j2).
+// It reads only unmerged (even-level) rows and writes only merged ones, so it runs in place.
+// A row with more adjacent dependencies than kXfWidth keeps the rest (still correct; that
+// row's level just does not halve).  wmax > 0 merges only the level pairs of at most wmax
+// rows (the narrow, latency-bound levels): fewer levels at a few more streamed bytes.
+int merge_levels(const pslr_csr& M, const std::vector<int64_t>& off, bool upper, int64_t wmax, HostCsr& out,
+                 MergeXf& X, const char* name) {
+  const int64_t n = M.nrows, nb = (int64_t)off.size() - 1;
+  out.nrows = n;
+  out.ncols = M.ncols;
+  out.indptr.assign(n + 1, 0);
+  out.indices.clear();
+  out.data.clear();
+  out.indices.reserve((size_t)(M.nnz * 3 / 2));
+  out.data.reserve((size_t)(M.nnz * 3 / 2));
+  X.rows.clear();
+  X.c.clear();
+  X.blk.assign(nb + 1, 0);
+  std::vector<int32_t> lev;
+  std::vector<double> acc;        // dense accumulator over the block's columns
+  std::vector<uint8_t> used;
+  std::vector<int32_t> cols;
+  for (int64_t b = 0; b < nb; ++b) {
+    const int64_t lo = off[b], hi = off[b + 1], nr = hi - lo;
+    X.blk[b] = (int32_t)(X.rows.size() / kXfWidth1);
+    lev.assign(nr, 0);
+    for (int64_t t = 0; t < nr; ++t) {
+      const int64_t i = upper ? nr - 1 - t : t;
+      int32_t lv = 0;
+      for (int64_t e = M.indptr[lo + i]; e < M.indptr[lo + i + 1]; ++e) {
+        const int64_t jg = M.indices[e];
+        if (jg < lo || jg >= hi) return fail(PSLR_EINVAL, std::string(name) + " is not block diagonal");
+        const int64_t j = jg - lo;
+        if (upper ? (j < i) : (j > i))
+          return fail(PSLR_EINVAL, std::string(name) + (upper ? " is not upper" : " is not lower") + " triangular");
+        if (j != i) lv = std::max(lv, lev[j] + 1);
+      }
+      lev[i] = lv;
+    }
+    // level pair (l - 1, l), l odd, is merged when its rows fit one pass of the consumer
+    // threads (wmax > 0): wider pairs would take two row steps per level, and their merged
+    // rows reach past the ring (far dependencies) while saving no barrier on the critical path
+    int32_t depth = 0;
+    for (int64_t i = 0; i < nr; ++i) depth = std::max(depth, lev[i] + 1);
+    std::vector<int64_t> width(depth + 1, 0);
+    for (int64_t i = 0; i < nr; ++i) ++width[lev[i]];
+    auto merge_level = [&](int32_t l) { return (l & 1) && (wmax <= 0 || width[l] + width[l - 1] <= wmax); };
+    acc.assign(nr, 0.0);
+    used.assign(nr, 0);
+    auto diag_of = [&](int64_t r) -> double {  // r global
+      for (int64_t e = M.indptr[r]; e < M.indptr[r + 1]; ++e)
+        if (M.indices[e] == r) return M.data[e];
+      return 0.0;
+    };
+    for (int64_t i = 0; i < nr; ++i) {
+      const int64_t ig = lo + i;
+      const int64_t e0 = M.indptr[ig], e1 = M.indptr[ig + 1];
+      int nadj = 0;
+      int32_t adj[kXfWidth];
+      double cadj[kXfWidth];
+      if (merge_level(lev[i])) {
+        for (int64_t e = e0; e < e1 && nadj < kXfWidth; ++e) {
+          const int64_t j = M.indices[e] - lo;
+          if (j != i && lev[j] == lev[i] - 1) {
+            double c = M.data[e];
+            if (upper) {
+              const double dj = diag_of(lo + j);
+              if (dj == 0.0) return fail(PSLR_ESINGULAR, std::string(name) + ": A is singular: zero entry on diagonal.");
+              c = c / dj;
+            }
+            adj[nadj] = (int32_t)j;
+            cadj[nadj] = c;
+            ++nadj;
+          }
+        }
+      }
+      if (nadj == 0) {  // copied as is
+        for (int64_t e = e0; e < e1; ++e) {
+          out.indices.push_back(M.indices[e]);
+          out.data.push_back(M.data[e]);
+        }
+        out.indptr[ig + 1] = (int64_t)out.indices.size();
+        continue;
+      }
+      cols.clear();
+      auto add = [&](int64_t j, double v) {
+        if (!used[j]) {
+          used[j] = 1;
+          acc[j] = 0.0;
+          cols.push_back((int32_t)j);
+        }
+        acc[j] += v;
+      };
+      for (int64_t e = e0; e < e1; ++e) {
+        const int64_t j = M.indices[e] - lo;
+        bool is_adj = false;
+        for (int a = 0; a < nadj; ++a) is_adj |= (adj[a] == j);
+        if (!is_adj) add(j, M.data[e]);
+      }
+      for (int a = 0; a < nadj; ++a) {
+        const int64_t jg = lo + adj[a];
+        for (int64_t e = M.indptr[jg]; e < M.indptr[jg + 1]; ++e) {
+          const int64_t k = M.indices[e] - lo;
+          if (k == adj[a]) continue;
+          add(k, -cadj[a] * M.data[e]);
+        }
+      }
+      std::sort(cols.begin(), cols.end());
+      for (int32_t j : cols) {
+        used[j] = 0;
+        if (acc[j] == 0.0 && j != i) continue;  // exact cancellation: no entry
+        out.indices.push_back((int32_t)(lo + j));
+        out.data.push_back(acc[j]);
+      }
+      out.indptr[ig + 1] = (int64_t)out.indices.size();
+      X.rows.push_back((int32_t)ig);
+      for (int a = 0; a < kXfWidth; ++a) {
+        X.rows.push_back(a < nadj ? (int32_t)(lo + adj[a]) : (int32_t)ig);
+        X.c.push_back(a < nadj ? cadj[a] : 0.0);
+      }
+      X.c.push_back(0.0);
+    }
+  }
+  X.blk[nb] = (int32_t)(X.rows.size() / kXfWidth1);
+  out.nnz = (int64_t)out.indices.size();
   return PSLR_OK;
 }
 

@@ -84,6 +84,7 @@ struct DevTri {
 struct TriAnalysis {
   bool upper = false;
   std::vector<int32_t> pos_of_row, row_at_pos, level_end, level_of_row, len;
+  std::vector<int32_t> blk_depth;  // dependency levels of each block
   std::vector<double> diag;
   int64_t depth_max = 0, levels = 0, reach = 0;
 };
@@ -98,6 +99,37 @@ struct TriHost {
 
 int analyze_factor(const pslr_csr& M, const std::vector<int64_t>& off, bool upper, TriAnalysis& A,
                    const char* name);
+// Level-merged factors (pack.cpp merge_levels): an owned host CSR and the right-hand-side
+// transform of the merged rows, one record per row: rows[4] = {i, j0, j1, j2} (padding
+// j = i), c[4] = {c0, c1, c2, 0};  rhs'_i = rhs_i - (c0 rhs_j0 + c1 rhs_j1 + c2 rhs_j2).
+constexpr int kXfWidth = 3;   // substituted dependencies per row
+constexpr int kXfWidth1 = 4;  // ints per record
+struct HostCsr {
+  int64_t nrows = 0, ncols = 0, nnz = 0;
+  std::vector<int64_t> indptr;
+  std::vector<int32_t> indices;
+  std::vector<double> data;
+  pslr_csr view() const { return pslr_csr{nrows, ncols, nnz, indptr.data(), indices.data(), data.data()}; }
+};
+struct MergeXf {
+  std::vector<int32_t> rows;  // 4 per record, row space
+  std::vector<double> c;      // 4 per record
+  std::vector<int32_t> blk;   // nblocks + 1 record offsets
+};
+int merge_levels(const pslr_csr& M, const std::vector<int64_t>& off, bool upper, int64_t wmax, HostCsr& out,
+                 MergeXf& X, const char* name);
+
+// The transform on the device, in the position space of the array it rewrites in place
+// (L: the L-position-ordered rhs, U: the U-position-ordered L output): idx = {pos_i,
+// pos_j0, pos_j1, pos_j2}, val = {c0, c1}, {c2, 0}; blk: records of block b are
+// [blk[b], blk[b+1]).  nrec == 0: the factor is not merged.
+struct DevXform {
+  int32_t nrec = 0;
+  const int32_t* idx = nullptr;  // 4 per record (read as int4)
+  const double* val = nullptr;   // 4 per record (read as two double2)
+  const int32_t* blk = nullptr;
+};
+
 // consumer threads per CTA of the fused step kernel = max rows per packed segment
 // (PSLR_STEP_THREADS: timing-experiment builds under lib_variants/ only)
 #ifndef PSLR_STEP_THREADS
@@ -144,6 +176,10 @@ struct StepArgs {
 // Everything the fused kernel reads besides StepArgs (constant per context).
 struct StepConst {
   DevTri LB, UB, LC, UC;
+  DevXform XLB, XUB, XLC, XUC;  // level-merged factors: their in-place rhs transforms
+  const int32_t* lrowx = nullptr;   // merged L_B: L-position -> row, or -(record + 1) for a
+  const int32_t* xlb_rows = nullptr;  //   merged row whose f gets the transform (permute_f):
+                                    //   {row_i, row_j0, row_j1, row_j2} of the record
   DevCsr E, F, C, Cg;
   DevCsr Fpos;  // F with its columns mapped to the interior rows' U-positions
   const int32_t* int_off = nullptr;
@@ -173,6 +209,9 @@ struct StepConst {
   int dbg = 0;               // PSLR_DBG timing experiments (wrong results): bit0 skip rows,
                              // bit1 skip next-row loads, bit3 no producer back-off
   long long l2ahead = 0;     // bytes of the factor stream prefetched into L2 ahead (0: default)
+  const int8_t* l2keep = nullptr;  // per block: 1 = its factor chunks are copied with an L2
+                                   // evict_last policy (the deepest blocks, whose streams
+                                   // bound every step, stay L2-resident across the steps)
 };
 
 }  // namespace pslr

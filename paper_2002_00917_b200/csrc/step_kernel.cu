@@ -78,6 +78,20 @@ __device__ __forceinline__ void bulk_load(void* dst, const void* src, uint32_t b
       "l"(src), "r"(bytes), "r"(smem_addr(bar))
       : "memory");
 }
+// the same copy with an L2 cache policy (createpolicy): the kept blocks' factor streams
+__device__ __forceinline__ void bulk_load_hint(void* dst, const void* src, uint32_t bytes, uint64_t* bar,
+                                               uint64_t pol) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_addr(dst)),
+      "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(pol)
+      : "memory");
+}
+__device__ __forceinline__ uint64_t policy_evict_last() {
+  uint64_t pol;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
+}
 __device__ __forceinline__ void bulk_prefetch_l2(const void* src, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
@@ -230,8 +244,9 @@ static_assert(sizeof(Ctl) <= kCtlBytes, "the control block must fit the header o
 // expect_tx + bulk-copy pairs.  Phase bookkeeping only runs at phase boundaries.
 __device__ void producer(const Streams& S, Ctl* ctl, uint8_t* stages, int nst,
                          int stage_bytes, int nv, long long* g_dbg_out, int dbg,
-                         long long* g_tma, long long l2ahead) {
+                         long long* g_tma, long long l2ahead, int keep) {
   if ((threadIdx.x & 31) != 0) return;
+  const uint64_t pol = keep ? policy_evict_last() : 0ull;
   const int np = S.nphase;
   const int total = S.begin[np];
   if (total == 0) return;
@@ -322,7 +337,10 @@ __device__ void producer(const Streams& S, Ctl* ctl, uint8_t* stages, int nst,
       }
     }
     mbar_expect_tx(&ctl->full[st], dv.y);
-    bulk_load(stages + (size_t)st * stage_bytes, data + (size_t)dv.x * 16, dv.y, &ctl->full[st]);
+    if (keep)
+      bulk_load_hint(stages + (size_t)st * stage_bytes, data + (size_t)dv.x * 16, dv.y, &ctl->full[st], pol);
+    else
+      bulk_load(stages + (size_t)st * stage_bytes, data + (size_t)dv.x * 16, dv.y, &ctl->full[st]);
     if (l2ahead > 0) {  // keep the factor stream l2ahead bytes ahead in L2 (phases in order)
       issued += dv.y;
       while (prefetched < issued + l2ahead && kp < np) {
@@ -757,6 +775,45 @@ __device__ __forceinline__ void iface_terms4(int kind, const int (&row)[4], cons
   }
 }
 
+// Right-hand-side transform of a level-merged factor (pack.cpp merge_levels), for this
+// CTA's block, in place: arr[pos_i] -= c0 arr[pos_j0] + c1 arr[pos_j1] + c2 arr[pos_j2].
+// The records read only unmerged rows and write only merged ones (no ordering among them).
+// Callers fence and barrier before the phase that reads arr.
+template <int NV>
+__device__ __forceinline__ void xform_block(const DevXform& X, int b, double* arr) {
+  const int r0 = __ldg(X.blk + b), r1 = __ldg(X.blk + b + 1);
+  constexpr int kIn = 4;  // records in flight per thread (two dependent global round trips)
+  const int4* idx = reinterpret_cast<const int4*>(X.idx);
+  const double2* val = reinterpret_cast<const double2*>(X.val);
+  for (int i0 = r0 + (int)threadIdx.x; i0 < r1; i0 += kIn * kStepThreads) {
+    int4 id[kIn];
+    double2 c01[kIn], c2[kIn];
+#pragma unroll
+    for (int j = 0; j < kIn; ++j) {
+      const int i = i0 + j * kStepThreads;
+      const bool ok = i < r1;
+      id[j] = ok ? __ldg(idx + i) : make_int4(0, 0, 0, 0);
+      c01[j] = ok ? __ldg(val + 2 * i) : make_double2(0.0, 0.0);
+      c2[j] = ok ? __ldg(val + 2 * i + 1) : make_double2(0.0, 0.0);
+    }
+    vt<NV> a[kIn], z0[kIn], z1[kIn], z2[kIn];
+#pragma unroll
+    for (int j = 0; j < kIn; ++j) {
+      a[j] = vld<NV>(arr, id[j].x);
+      z0[j] = vld<NV>(arr, id[j].y);
+      z1[j] = vld<NV>(arr, id[j].z);
+      z2[j] = vld<NV>(arr, id[j].w);
+    }
+#pragma unroll
+    for (int j = 0; j < kIn; ++j) {
+      vt<NV> t = vmul(z0[j], c01[j].x);
+      t = vmadd(t, c01[j].y, z1[j]);
+      t = vmadd(t, c2[j].x, z2[j]);
+      if (i0 + j * kStepThreads < r1) vst(arr, id[j].x, vsub(a[j], t));
+    }
+  }
+}
+
 // prepass loads in flight per thread (the prepass is latency-bound: three dependent global
 // loads per E row; more rows in flight per thread = fewer round trips)
 #ifndef PSLR_PRE_F
@@ -829,7 +886,7 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
                                                    : nullptr,
              K.dbg,
              (PSLR_TRACE_BUILD && K.trace && b == K.trace_block) ? K.trace + 2 + 2 * 65536 : nullptr,
-             K.l2ahead);
+             K.l2ahead, K.l2keep ? (int)K.l2keep[b] : 0);
     return;
   }
   // Programmatic dependent launch: this grid may start while the previous kernel of the
@@ -875,6 +932,10 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
         for (int j = 0; j < kIn; ++j)
           if (row0 + j * kStepThreads < r1) vst(K.rhsB, pos[j], v[j]);
       }
+      if (K.XLB.nrec) {  // level-merged L_B: f' = (I - N) f in place
+        consumer_sync();
+        xform_block<NV>(K.XLB, b, K.rhsB);
+      }
     } else {
       for (int p = r0 + tid; p < r1; p += kStepThreads) vst(K.rhsB, p, vzero<NV>());
     }
@@ -898,8 +959,7 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
         }
 #pragma unroll
         for (int j = 0; j < kIn; ++j)
-          fv[j] = (a.b1 == BT_F && r[j].w > r[j].z) ? (a.fL ? vld<NV>(a.fL, r[j].x) : vldg<NV>(a.f, r[j].y))
-                                                    : vzero<NV>();
+          fv[j] = (a.b1 == BT_F && r[j].w > r[j].z) ? vld<NV>(rhs, r[j].x) : vzero<NV>();  // f (pass 1)
         for (int k = 0; k < len; ++k) {
           int c[kIn];
           double v[kIn];
@@ -926,6 +986,11 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
     trace_ev(K, 3, 0);
     trace_cta(K, 1);
     tri_phase<false, NV>(K, S, ctl, stages, ph_LB, ring, r0, K.zB, nullptr, nullptr);
+    if (K.XUB.nrec) {  // level-merged U_B: y' = (I - M) y in place (y: L_B's output)
+      xform_block<NV>(K.XUB, b, K.zB);
+      fence_rhs_written();
+      consumer_sync();
+    }
     tri_phase<true, NV, XPOS>(K, S, ctl, stages, ph_UB, ring, r0, K.zB, a.xb, nullptr);
   }
   if (do_i) {
@@ -962,7 +1027,17 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
     consumer_sync();
     trace_ev(K, 30, 0);
     if (do_c) {
+      if (K.XLC.nrec) {  // level-merged L_C0: w' = (I - N) w in place
+        xform_block<NV>(K.XLC, b, K.rhsC);
+        fence_rhs_written();
+        consumer_sync();
+      }
       tri_phase<false, NV>(K, S, ctl, stages, ph_LC, ring, r0, K.zC, nullptr, nullptr);
+      if (K.XUC.nrec) {  // level-merged U_C0
+        xform_block<NV>(K.XUC, b, K.zC);
+        fence_rhs_written();
+        consumer_sync();
+      }
       tri_phase<true, NV>(K, S, ctl, stages, ph_UC, ring, r0, K.zC, a.yout, a.cadd);
     }
   }
