@@ -201,6 +201,16 @@ int pslr_apply2_last(pslr_ctx* ctx, const double* b, const double* y, double* z,
 /* out = C0^{-1}? (F B^{-1} E v - Cg v) with v extended: one E_rr / Arnoldi operator step
  * (schur.py:83-86, 104-112); do_c0 selects the C0 solve. */
 int pslr_apply_es_step(pslr_ctx* ctx, const double* v, double* out, int do_c0, void* stream);
+/* Halo overlapped with the interior phase.  Of a horner / es_step call only the C_g y term
+ * of the interface phase reads ghost columns; the E y rows and the B solves (most of the
+ * step) read local values.  A caller whose ghost refresh of y runs on ANOTHER stream
+ * registers the cudaEvent_t that completes it: the next horner / es_step (one- or
+ * two-vector) on this context launches the E y kernel and the B phases at once and makes
+ * its stream wait for the event only before the C_g y kernel.  The exchange itself must be
+ * ordered after the producer of y by the caller (an event on the compute stream).  The
+ * registration is consumed by that one call; event NULL clears it.  The in-library NCCL
+ * route (pslr_comm_init) does the same internally on a communication stream of its own. */
+int pslr_halo_pending(pslr_ctx* ctx, void* event);
 
 /* ---------------------------------------------------------------- multi-GPU (NCCL) */
 /* One process per GPU; each rank holds a rank-local context (pslr_ctx_create on its

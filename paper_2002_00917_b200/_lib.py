@@ -100,6 +100,7 @@ EXPORTS = {
     "pslr_apply_first": (c_int, P, P, P, P, P),
     "pslr_apply_mid": (c_int, P, P, P, P, P),
     "pslr_apply_horner": (c_int, P, P, P, P, P),
+    "pslr_halo_pending": (c_int, P, P),
     "pslr_apply_last": (c_int, P, P, P, P, P),
     "pslr_apply2_first": (c_int, P, P, P, P, P),
     "pslr_apply2_mid": (c_int, P, P, P, P, P),

@@ -769,9 +769,9 @@ int pslr_ctx_create_packed(pslr_ctx** out, int device, const pslr_system* sys, c
   ctx->split_iface = env_int("PSLR_SPLIT_IFACE", 1) != 0;
   ctx->K.dbg = (int)env_int("PSLR_DBG", 0);
   ctx->K.l2ahead = env_int("PSLR_L2AHEAD", 0);
-  {  // L2 residency of the deepest blocks' B factor streams (PSLR_L2KEEP_MB, 0 = off): blocks
+  {  // L2 residency of the deepest blocks' B factor streams (PSLR_L2KEEP_MB, default 0 = off: measured no gain on cfg5): blocks
      // in decreasing dependency depth while their L_B + U_B chunks fit the budget
-    const int64_t budget = env_int("PSLR_L2KEEP_MB", 48) << 20;
+    const int64_t budget = env_int("PSLR_L2KEEP_MB", 0) << 20;
     if (budget > 0 && s > 0) {
       std::vector<int64_t> order(s), bytes(s, 0);
       for (int64_t b = 0; b < s; ++b) {
@@ -1196,6 +1196,12 @@ int pslr_apply_es_step(pslr_ctx* ctx, const double* v, double* out, int do_c0, v
   return op_es_step(ctx, v, out, do_c0 ? 1 : 0, nullptr, S(stream));
 }
 
+int pslr_halo_pending(pslr_ctx* ctx, void* event) {
+  if (!ctx) return fail(PSLR_EINVAL, "null context");
+  ctx->pending_halo = static_cast<cudaEvent_t>(event);
+  return PSLR_OK;
+}
+
 int pslr_apply_last(pslr_ctx* ctx, const double* b, const double* y, double* z, void* stream) {
   RET(set_device(ctx));
   cudaStream_t st = S(stream);
@@ -1405,6 +1411,9 @@ int pslr_ctx_clone(const pslr_ctx* src, pslr_ctx** out) {
   ctx->red = nullptr;  // reduction partials are per context (Krylov / dnorm on a clone)
   ctx->red_len = 0;
   ctx->comm = nullptr;  // a clone has no communicator of its own
+  ctx->comm_stream = nullptr;
+  ctx->ev_y = ctx->ev_halo = nullptr;
+  ctx->pending_halo = nullptr;
   ctx->world = 1;
   ctx->rank = 0;
   ctx->halo_idx = nullptr;

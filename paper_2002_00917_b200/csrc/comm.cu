@@ -17,6 +17,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -155,9 +156,42 @@ int comm_halo2(pslr_ctx* ctx, double* v2_ext, cudaStream_t st) {
   return PSLR_OK;
 }
 
+// The halo of v_ext (nv = 1) or of an interleaved pair (nv = 2) overlapped with the next
+// step's interior phase: the exchange is ordered after the caller's stream (ev_y: v is
+// final), runs on the context's communication stream and leaves ev_halo in
+// ctx->pending_halo; launch_step (step_kernel.cu) makes the caller's stream wait for it only
+// before the C_g y term, the one reader of ghost columns (E y and the B solves of the step
+// run meanwhile).  PSLR_HALO_OVERLAP=0, or a context without a communicator: the plain
+// stream-ordered exchange.
+int comm_halo_async(pslr_ctx* ctx, double* v_ext, int nv, cudaStream_t st) {
+  if (!ctx->comm) return PSLR_OK;
+  if (!ctx->halo_overlap || !ctx->comm_stream) return nv == 2 ? comm_halo2(ctx, v_ext, st) : comm_halo(ctx, v_ext, st);
+  CK(cudaEventRecord(ctx->ev_y, st));
+  CK(cudaStreamWaitEvent(ctx->comm_stream, ctx->ev_y, 0));
+  RET(nv == 2 ? comm_halo2(ctx, v_ext, ctx->comm_stream) : comm_halo(ctx, v_ext, ctx->comm_stream));
+  CK(cudaEventRecord(ctx->ev_halo, ctx->comm_stream));
+  ctx->pending_halo = ctx->ev_halo;
+  return PSLR_OK;
+}
+
+// a pending halo nobody consumed (no launch_step followed): order the stream after it
+int comm_halo_join(pslr_ctx* ctx, cudaStream_t st) {
+  if (ctx->pending_halo) {
+    CK(cudaStreamWaitEvent(st, ctx->pending_halo, 0));
+    ctx->pending_halo = nullptr;
+  }
+  return PSLR_OK;
+}
+
 int comm_destroy(pslr_ctx* ctx) {
   if (ctx->comm && nccl().commDestroy) nccl().commDestroy(static_cast<ncclComm_t>(ctx->comm));
   ctx->comm = nullptr;
+  ctx->pending_halo = nullptr;
+  if (ctx->comm_stream) cudaStreamDestroy(ctx->comm_stream);
+  if (ctx->ev_y) cudaEventDestroy(ctx->ev_y);
+  if (ctx->ev_halo) cudaEventDestroy(ctx->ev_halo);
+  ctx->comm_stream = nullptr;
+  ctx->ev_y = ctx->ev_halo = nullptr;
   return PSLR_OK;
 }
 
@@ -184,14 +218,16 @@ int op_apply_sharded(pslr_ctx* ctx, int64_t m, const double* b, double* z, cudaS
   RET(pslr_apply_mid(ctx, ctx->y0, ctx->sh_s, ctx->sh_c, sv));  // c = C0^{-1}(y0 + V G s)
   const double* y = ctx->sh_c;
   if (m > 0) {
-    RET(comm_halo(ctx, ctx->sh_c, st));
+    // each halo overlaps the E y rows and the B solves of the step that consumes it
+    RET(comm_halo_async(ctx, ctx->sh_c, 1, st));
     double* outs[2] = {ctx->sh_a, ctx->sh_b};
     for (int64_t k = 0; k < m; ++k) {
       double* out = outs[k & 1];
       RET(pslr_apply_horner(ctx, y, ctx->sh_c, out, sv));
-      if (k < m - 1) RET(comm_halo(ctx, out, st));
+      if (k < m - 1) RET(comm_halo_async(ctx, out, 1, st));
       y = out;
     }
+    RET(comm_halo_join(ctx, st));  // (q == 0 ranks launch no step)
   }
   return pslr_apply_last(ctx, b, y, z, sv);
 }
@@ -220,14 +256,15 @@ int op_apply2_sharded(pslr_ctx* ctx, int64_t m, const double* b2, double* z2, cu
   RET(pslr_apply2_mid(ctx, ctx->sh2_y0, ctx->sh_s, ctx->sh2_c, sv));
   const double* y = ctx->sh2_c;
   if (m > 0) {
-    RET(comm_halo2(ctx, ctx->sh2_c, st));
+    RET(comm_halo_async(ctx, ctx->sh2_c, 2, st));
     double* outs[2] = {ctx->sh2_a, ctx->sh2_b};
     for (int64_t k = 0; k < m; ++k) {
       double* out = outs[k & 1];
       RET(pslr_apply2_horner(ctx, y, ctx->sh2_c, out, sv));
-      if (k < m - 1) RET(comm_halo2(ctx, out, st));
+      if (k < m - 1) RET(comm_halo_async(ctx, out, 2, st));
       y = out;
     }
+    RET(comm_halo_join(ctx, st));
   }
   return pslr_apply2_last(ctx, b2, y, z2, sv);
 }
@@ -244,8 +281,9 @@ int op_apply_err_sharded(pslr_ctx* ctx, int64_t m, const double* v, double* out,
   double* src = ctx->sh_a;
   double* dst = ctx->sh_b;
   for (int64_t k = 1; k <= m + 1; ++k) {
-    RET(comm_halo(ctx, src, st));
+    RET(comm_halo_async(ctx, src, 1, st));
     RET(pslr_apply_es_step(ctx, src, dst, k != m + 1 ? 1 : 0, sv));
+    RET(comm_halo_join(ctx, st));
     std::swap(src, dst);
   }
   if (q) CK(cudaMemcpyAsync(out, src, q * sizeof(double), cudaMemcpyDeviceToDevice, st));
@@ -293,6 +331,13 @@ int pslr_comm_init(pslr_ctx* ctx, const void* nccl_unique_id, int nranks, int ra
   ctx->comm = comm;
   ctx->world = nranks;
   ctx->rank = rank;
+  const char* ov = std::getenv("PSLR_HALO_OVERLAP");
+  ctx->halo_overlap = !(ov && ov[0] == '0');
+  if (ctx->halo_overlap) {
+    CK(cudaStreamCreateWithFlags(&ctx->comm_stream, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&ctx->ev_y, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ctx->ev_halo, cudaEventDisableTiming));
+  }
   ctx->halo_send_cnt.assign(nranks, 0);
   ctx->halo_send_off.assign(nranks, 0);
   ctx->halo_recv_cnt.assign(nranks, 0);

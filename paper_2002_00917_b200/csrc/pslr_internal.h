@@ -13,6 +13,7 @@
 
 #ifndef __CUDACC__
 typedef struct CUevent_st* cudaEvent_t;
+typedef struct CUstream_st* cudaStream_t;
 #else
 #include <cuda_runtime.h>
 #endif
@@ -279,6 +280,14 @@ struct pslr_ctx {
   int32_t* halo_idx = nullptr;   // local interface indices to send, peers in rank order
   double* halo_buf = nullptr;    // their gathered values
   int64_t halo_nsend = 0;
+  // halo overlapped with the interior phase (comm.cu comm_halo_async; PSLR_HALO_OVERLAP=0: off):
+  // the exchange runs on comm_stream after ev_y (the sent vector is final on the caller's
+  // stream) and records ev_halo; the next launch_step runs its E y rows and B phases first and
+  // waits for pending_halo only before the C_g y term of its interface phase
+  bool halo_overlap = true;
+  cudaStream_t comm_stream = nullptr;
+  cudaEvent_t ev_y = nullptr, ev_halo = nullptr;
+  mutable cudaEvent_t pending_halo = nullptr;
   double *sh_a = nullptr, *sh_b = nullptr, *sh_c = nullptr, *sh_s = nullptr, *sh_x = nullptr;
   int64_t sh_a_len = 0, sh_b_len = 0, sh_c_len = 0, sh_s_len = 0, sh_x_len = 0;
   double *sh2_y0 = nullptr, *sh2_a = nullptr, *sh2_b = nullptr, *sh2_c = nullptr, *halo_buf2 = nullptr;

@@ -80,6 +80,9 @@ int comm_destroy(pslr_ctx* ctx);
 int op_apply_sharded(pslr_ctx* ctx, int64_t m, const double* b, double* z, cudaStream_t st);
 int op_apply2_sharded(pslr_ctx* ctx, int64_t m, const double* b2, double* z2, cudaStream_t st);
 int comm_halo2(pslr_ctx* ctx, double* v2_ext, cudaStream_t st);
+// the exchange on the communication stream, consumed by the next launch_step (comm.cu)
+int comm_halo_async(pslr_ctx* ctx, double* v_ext, int nv, cudaStream_t st);
+int comm_halo_join(pslr_ctx* ctx, cudaStream_t st);
 int op_apply_err_sharded(pslr_ctx* ctx, int64_t m, const double* v, double* out, cudaStream_t st);
 int op_spmv_A_sharded(pslr_ctx* ctx, const double* x, double* w, cudaStream_t st);
 

@@ -1155,9 +1155,22 @@ int launch_step(const pslr_ctx* ctx, const StepArgs& a_in, cudaStream_t st, int 
   const bool f_ey = a.fL && a.b1 == BT_F && a.b2 == BT_EY;
   const int ne = ((ey_only || f_ey) && ctx->ey_all_sm) ? K.nerows : 0;
   const int nq = (a.i2 == IT_CGY && K.cgy && ctx->ey_all_sm) ? (int)K.Cg.nrows : 0;
-  if (ne > 0 || nq > 0) {
+  // A halo exchange of yC's ghost columns may still be in flight on the communication stream
+  // (comm.cu comm_halo_async).  Only C_g reads ghosts: with the split interface phase the E y
+  // rows and the B phases run first and the stream waits for the halo between the B launch
+  // and the C_g y kernel; every other launch shape waits here.
+  cudaEvent_t halo_ev = ctx->pending_halo;
+  ctx->pending_halo = nullptr;
+  const bool split = ctx->split_iface && a.i1 != IT_NONE && (a.b1 != BT_NONE || a.do_c0) && !a.ifc_done;
+  const bool defer_cgy = halo_ev && nq > 0 && split && a.b1 != BT_NONE;
+  if (halo_ev && !defer_cgy) {
+    const cudaError_t e = cudaStreamWaitEvent(st, halo_ev, 0);
+    if (e != cudaSuccess) return (int)e;
+    halo_ev = nullptr;
+  }
+  auto pre_launch = [&](int ne_, int nq_) -> int {
     cudaLaunchConfig_t ec = {};
-    ec.gridDim = dim3((unsigned)((ne + nq + 255) / 256));
+    ec.gridDim = dim3((unsigned)((ne_ + nq_ + 255) / 256));
     ec.blockDim = dim3(256);
     ec.stream = st;
     cudaLaunchAttribute eat[1];
@@ -1168,15 +1181,18 @@ int launch_step(const pslr_ctx* ctx, const StepArgs& a_in, cudaStream_t st, int 
     double* rhs = ey_only ? K.rhsE : a.fL;
     const int sub = f_ey ? 1 : 0;
     const int4* er = reinterpret_cast<const int4*>(K.erows);
-    const cudaError_t e =
-        (nv == 2) ? cudaLaunchKernelEx(&ec, pre_step_kernel<2>, er, ne, K.E, a.yE, rhs, sub, K.Cg, a.yC, K.cgy, nq)
-                  : cudaLaunchKernelEx(&ec, pre_step_kernel<1>, er, ne, K.E, a.yE, rhs, sub, K.Cg, a.yC, K.cgy, nq);
-    if (e != cudaSuccess) return (int)e;
-    if (ne > 0) a.ey_done = 1;
-    if (nq > 0) {
-      a.i2 = IT_PRE;
-      a.pre = K.cgy;
-    }
+    return (int)((nv == 2)
+                     ? cudaLaunchKernelEx(&ec, pre_step_kernel<2>, er, ne_, K.E, a.yE, rhs, sub, K.Cg, a.yC, K.cgy, nq_)
+                     : cudaLaunchKernelEx(&ec, pre_step_kernel<1>, er, ne_, K.E, a.yE, rhs, sub, K.Cg, a.yC, K.cgy, nq_));
+  };
+  if (ne > 0 || (nq > 0 && !defer_cgy)) {
+    const int e = pre_launch(ne, defer_cgy ? 0 : nq);
+    if (e) return e;
+  }
+  if (ne > 0) a.ey_done = 1;
+  if (nq > 0) {
+    a.i2 = IT_PRE;
+    a.pre = K.cgy;
   }
   // programmatic stream serialization: the step kernel's CTAs (one per subdomain, far
   // fewer than the 148 SMs) launch and stage their first factor chunks while the
@@ -1184,7 +1200,7 @@ int launch_step(const pslr_ctx* ctx, const StepArgs& a_in, cudaStream_t st, int 
   // The interface phase of a launch that also has a B phase (or a C0 phase) runs as its own
   // all-SM kernel: [B phases] -> iface_kernel -> [C0 phases], the two step launches being
   // the same kernel with the other phases switched off (bit for bit the same results).
-  if (ctx->split_iface && a.i1 != IT_NONE && (a.b1 != BT_NONE || a.do_c0) && !a.ifc_done) {
+  if (split) {
     if (a.b1 != BT_NONE) {
       StepArgs ab = a;
       ab.i1 = ab.i2 = IT_NONE;
@@ -1192,6 +1208,12 @@ int launch_step(const pslr_ctx* ctx, const StepArgs& a_in, cudaStream_t st, int 
       ab.yout = nullptr;
       const int e = launch_step_kernel(ctx, ab, K, st, nv);
       if (e) return e;
+    }
+    if (defer_cgy) {  // the ghosts of yC have landed: C_g y, then the interface phase
+      cudaError_t e = cudaStreamWaitEvent(st, halo_ev, 0);
+      if (e != cudaSuccess) return (int)e;
+      const int e2 = pre_launch(0, nq);
+      if (e2) return e2;
     }
     cudaLaunchConfig_t ic = {};
     ic.gridDim = dim3((unsigned)((ctx->q + 255) / 256));

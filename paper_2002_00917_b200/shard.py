@@ -26,6 +26,7 @@ which plug in an oracle backend).
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -226,6 +227,29 @@ class Halo:
             w.wait()
         return v_ext
 
+    def exchange_for_step(self, v_ext, ops):
+        """exchange(v_ext) for the horner / es_step call that follows on `ops`, overlapped
+        with that step's interior phase when the rank-local operators are the device ones:
+        the exchange runs on a side stream ordered after v_ext's producer and its completion
+        event is registered with the context (pslr_halo_pending), so the step's E y kernel
+        and B solves start at once and only the C_g y term waits for the ghosts.  Any other
+        backend (or PSLR_HALO_OVERLAP=0): the plain exchange."""
+        t = self.t
+        if (not (self.peers_send or self.peers_recv) or not getattr(v_ext, "is_cuda", False)
+                or not hasattr(ops, "halo_pending") or os.environ.get("PSLR_HALO_OVERLAP", "1") == "0"):
+            return self.exchange(v_ext)
+        if getattr(self, "_side", None) is None:
+            self._side = t.cuda.Stream(device=v_ext.device)
+            self._event = t.cuda.Event()
+        main = t.cuda.current_stream(v_ext.device)
+        self._side.wait_stream(main)
+        v_ext.record_stream(self._side)
+        with t.cuda.stream(self._side):
+            self.exchange(v_ext)
+            self._event.record(self._side)
+        ops.halo_pending(self._event)
+        return v_ext
+
     def allreduce(self, x):
         if self.plan.world > 1:
             self.dist.all_reduce(x, group=self.group)
@@ -326,6 +350,12 @@ class DeviceShardOps:
         self._call("pslr_solve_C0", g.data_ptr(), out.data_ptr())
         return out
 
+    def halo_pending(self, event):
+        """The ghosts of the vector the next horner / es_step reads land when `event` (a
+        torch.cuda.Event recorded on the exchanging stream) completes (pslr_halo_pending)."""
+        from . import _lib
+        _lib.check(_lib.fns["pslr_halo_pending"](self.dev.handle, event.cuda_event if event is not None else None))
+
     def es_step(self, v_ext, do_c0):
         out = self.zeros(self.q + self.ng)
         from . import _lib
@@ -422,8 +452,9 @@ def sharded_arnoldi(ops, halo: Halo, q_global: int, ifc_lo: int, m: int, rank: i
 
     def op(v):
         src = ops.solve_C0(v)
+        xch = getattr(halo, "exchange_for_step", None)
         for k in range(1, m + 2):
-            halo.exchange(src)
+            xch(src, ops) if xch else halo.exchange(src)
             src = ops.es_step(src, do_c0=(k != m + 1))
         return src[:q]
 
@@ -460,11 +491,12 @@ class ShardedPreconditioner:
         c = ops.mid(y0, s)
         y = c
         if m > 0:
-            halo.exchange(c)
+            xch = getattr(halo, "exchange_for_step", None) or (lambda v, _o: halo.exchange(v))
+            xch(c, ops)
             for k in range(m):
                 out = ops.horner(y, c)
                 if k < m - 1:
-                    halo.exchange(out)
+                    xch(out, ops)
                 y = out
         return ops.last(b, y[:ops.q].contiguous())
 
@@ -493,7 +525,9 @@ class ShardedPreconditioner:
         c = ops.mid2(y0, s) if native else t.stack([ops.mid(yv, s[v].clone()) for v, yv in enumerate(cols(y0))], 1)
         y = c
         if m > 0:
-            halo.exchange(c)
+            # (the per-vector fallback reads copies of y: no overlap there)
+            xch = (getattr(halo, "exchange_for_step", None) if native else None) or (lambda v, _o: halo.exchange(v))
+            xch(c, ops)
             cc = None if native else cols(c)
             for k in range(m):
                 if native:
@@ -501,7 +535,7 @@ class ShardedPreconditioner:
                 else:
                     out = t.stack([ops.horner(yv, cc[v]) for v, yv in enumerate(cols(y))], 1)
                 if k < m - 1:
-                    halo.exchange(out)
+                    xch(out, ops)
                 y = out
         if native:
             return ops.last2(b2, y[:ops.q].contiguous())

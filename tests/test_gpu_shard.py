@@ -35,6 +35,32 @@ class LocalHalo:
                 vecs[h][ph.q_loc + a:ph.q_loc + b] = vals
 
 
+class LocalHaloAsync(LocalHalo):
+    """The same ghost refresh on a side stream, registered with every rank's context
+    (pslr_halo_pending): the horner calls that follow start their E y kernel and B solves
+    while the copies run and wait for them only before the C_g y term."""
+
+    def __init__(self, plans, device, ops):
+        super().__init__(plans, device)
+        self.ops = ops
+        self.side = self.t.cuda.Stream()
+        self.event = self.t.cuda.Event()
+
+    def exchange(self, vecs):
+        t = self.t
+        self.side.wait_stream(t.cuda.current_stream())
+        for v in vecs:
+            v.record_stream(self.side)
+        with t.cuda.stream(self.side):
+            super().exchange(vecs)
+            # delay the event well past the launch of the step's first kernels, so a step
+            # that did not wait before C_g y would read stale ghosts
+            t.cuda._sleep(2_000_000)
+            self.event.record(self.side)
+        for o in self.ops:
+            o.halo_pending(self.event)
+
+
 def _lockstep_apply(plans, ops, halo, b, p_global, m):
     import torch
     from paper_2002_00917_b200 import shard
@@ -83,6 +109,33 @@ def test_split_apply_matches_fused(world, with_corr):
         np.testing.assert_array_equal(z, z_ref)
     if world > 1:
         assert sum(pl.nghost for pl in plans) > 0  # the halo was exercised
+
+
+@pytest.mark.parametrize("world", [2, 4])
+def test_split_apply_halo_overlapped_with_interior_phase(world):
+    """pslr_halo_pending: the ghosts of y arrive on a side stream (late: the exchange is
+    followed by a device sleep) while the Horner step's E y kernel and B solves already run;
+    only the C_g y term waits.  Bit-exact against the fused apply (correction off), so a
+    step that read the ghosts early would fail."""
+    import torch
+    import paper_2002_00917_b200 as pg
+    from paper_2002_00917_b200 import shard, workloads
+    A = workloads.laplacian3d(14, 14, 14, 0.5)
+    m = 3
+    P = pg.build(A, pg.PslrConfig(num_subdomains=8, series_degree=m, rank=0, droptol=1e-2, seed=0))
+    ps = P.system
+    plans = [shard.plan_shard(ps, world, r) for r in range(world)]
+    ops = [shard.DeviceShardOps(pl) for pl in plans]
+    assert sum(pl.nghost for pl in plans) > 0
+    b = torch.as_tensor(np.random.default_rng(5).standard_normal(ps.n), device="cuda")
+    z_ref = P.apply(b)
+    for _ in range(3):  # repeated: buffers of the previous apply are reused
+        z = _lockstep_apply(plans, ops, LocalHaloAsync(plans, "cuda", ops), b, ps.p, m)
+        assert torch.equal(z, z_ref)
+    # a registration is consumed by one call; clearing it is allowed
+    ops[0].halo_pending(None)
+    z = _lockstep_apply(plans, ops, LocalHalo(plans, "cuda"), b, ps.p, m)
+    assert torch.equal(z, z_ref)
 
 
 def test_sharded_arnoldi_matches_build():
@@ -257,8 +310,11 @@ def test_native_comm_world1_apply_err_arnoldi_gmres_cg():
     assert r1.converged and r1.iterations == r2.iterations and r1.history == r2.history
 
 
-def test_native_comm_world1_pipelines_two_vectors():
-    """The bench's N>1 data plane on one rank: clones of the rank-local context, each with
+@pytest.mark.parametrize("overlap", ["1", "0"])
+def test_native_comm_world1_pipelines_two_vectors(overlap, monkeypatch):
+    """(overlap: PSLR_HALO_OVERLAP, read by pslr_comm_init — the halo on the context's
+    communication stream, consumed before the C_g y term, or stream-ordered.)
+    The bench's N>1 data plane on one rank: clones of the rank-local context, each with
     its OWN one-rank communicator (pslr_comm_init on a clone), run pslr_apply_multi with two
     right-hand sides (op_apply2_sharded: paired halos, one allreduce of 2r) concurrently on
     their own streams; every vector equals the fused single-vector apply bit for bit."""
@@ -273,6 +329,7 @@ def test_native_comm_world1_pipelines_two_vectors():
     ops = shard.DeviceShardOps(plan)
     ops.set_correction(torch.as_tensor(np.ascontiguousarray(P.correction.V), device="cuda"), P.correction.G)
     ctxs = [ops.dev] + [ops.dev.clone() for _ in range(2)]
+    monkeypatch.setenv("PSLR_HALO_OVERLAP", overlap)
     for c in ctxs:
         shard.attach_nccl_ctx(c, plan, shard.nccl_unique_id())
     streams = [torch.cuda.Stream() for _ in ctxs]
