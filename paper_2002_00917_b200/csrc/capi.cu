@@ -140,12 +140,14 @@ static int64_t stage_count(int64_t smem_optin, int64_t W, int64_t sb, int64_t nv
 // PSLR_MERGE: 0 = the reference's factors as they are (bit-exact), 1 = level-merged B
 // factors, 2 = level-merged C0 factors (default), 3 = both.  PSLR_MERGE_W / _WC: merge only
 // level pairs of at most that many rows (B: kStepThreads, C0: 0 = every pair)
-// The blob key: mode bits 0-1, the B width limit from bit 2, the C0 width limit from bit 32
+// The blob key: mode bits 0-1, the B width limit from bit 2, the C0 width limit from bit 32,
+// PSLR_ALT_GROUPS (alternating warp groups, pack.cpp) in bits 61-62
 static int64_t merge_mode() {
   const int64_t mode = env_int("PSLR_MERGE", 2) & 3;
   const int64_t wB = std::min<int64_t>(std::max<int64_t>(env_int("PSLR_MERGE_W", kStepThreads), 0), (1 << 29) - 1);
   const int64_t wC = std::min<int64_t>(std::max<int64_t>(env_int("PSLR_MERGE_WC", 0), 0), (1 << 29) - 1);
-  return mode | (wB << 2) | (wC << 32);
+  const int64_t alt = env_int("PSLR_ALT_GROUPS", 1) & 3;
+  return mode | (wB << 2) | (wC << 32) | (alt << 61);
 }
 
 static int pack_system(const pslr_system* sys, const std::vector<int64_t>& ioff, const std::vector<int64_t>& foff,
@@ -168,7 +170,7 @@ static int pack_system(const pslr_system* sys, const std::vector<int64_t>& ioff,
     UB = mf[1].view();
   }
   if (P.merged & 2) {
-    const int64_t wC = P.merged >> 32;
+    const int64_t wC = (P.merged >> 32) & ((1 << 29) - 1);
     RET(merge_levels(sys->LC, foff, false, wC, mf[2], P.X[2], "L_C0"));
     RET(merge_levels(sys->UC, foff, true, wC, mf[3], P.X[3], "U_C0"));
     LC = mf[2].view();
@@ -213,19 +215,22 @@ static int pack_system(const pslr_system* sys, const std::vector<int64_t>& ioff,
   for (int pair = 0; pair < 2; ++pair) {
     const TriAnalysis& AL = *an[2 * pair];
     const TriAnalysis& AU = *an[2 * pair + 1];
+    // narrow levels on alternating consumer warp groups (pack.cpp emit_factor): bit 0 the
+    // one-vector packing, bit 1 the two-vector packing
+    const bool alt1 = (P.merged >> 61) & 1, alt2 = (P.merged >> 62) & 1;
     const int64_t nr = M[2 * pair]->nrows;
     std::vector<int32_t> row_id(nr);
     for (int64_t i = 0; i < nr; ++i) row_id[i] = (int32_t)i;
     const auto& off = pair == 0 ? ioff : foff;
     RET(emit_factor(*M[2 * pair + 1], off, AU, W, SB, kStepThreads, AU.pos_of_row, row_id, fr1, rr1,
-                    P.F[2 * pair + 1].H, nm[2 * pair + 1]));
+                    P.F[2 * pair + 1].H, nm[2 * pair + 1], alt1));
     RET(emit_factor(*M[2 * pair], off, AL, W, SB, kStepThreads, AU.pos_of_row, AU.pos_of_row, fr1, rr1,
-                    P.F[2 * pair].H, nm[2 * pair]));
+                    P.F[2 * pair].H, nm[2 * pair], alt1));
     if (SB2 != SB) {
       RET(emit_factor(*M[2 * pair + 1], off, AU, W, SB2, kStepThreads, AU.pos_of_row, row_id, fr2, rr2,
-                      P.H2[2 * pair + 1], nm[2 * pair + 1]));
+                      P.H2[2 * pair + 1], nm[2 * pair + 1], alt2));
       RET(emit_factor(*M[2 * pair], off, AL, W, SB2, kStepThreads, AU.pos_of_row, AU.pos_of_row, fr2, rr2,
-                      P.H2[2 * pair], nm[2 * pair]));
+                      P.H2[2 * pair], nm[2 * pair], alt2));
     }
     P.F[2 * pair].pos_of_row = AL.pos_of_row;
     P.F[2 * pair].row_at_pos = AL.row_at_pos;

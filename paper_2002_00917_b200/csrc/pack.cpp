@@ -117,7 +117,7 @@ int analyze_factor(const pslr_csr& M, const std::vector<int64_t>& off, bool uppe
 int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAnalysis& A, int64_t W,
                 int64_t stage_bytes, int64_t seg_rows, const std::vector<int32_t>& far_index,
                 const std::vector<int32_t>& info_of_row, int64_t far_slots_max, int64_t rhs_row_bytes,
-                TriHost& out, const char* name) {
+                TriHost& out, const char* name, bool alt_groups) {
   const int64_t nb = (int64_t)off.size() - 1;
   const bool upper = A.upper;
   out.data.clear();
@@ -256,20 +256,31 @@ int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAna
     chunk_nseg = 0;
     chunk_start = (int64_t)out.data.size();
   };
+  // Alternating warp groups (PSLR_ALT_GROUPS, capi.cu): a level that fits the upper consumer
+  // warps (threads [hi_tb, seg_rows)) goes there when the previous level did not, so
+  // consecutive narrow levels belong to different warps.  A warp loads its row operands one
+  // segment ahead, in program order behind its current row's chain; with the levels
+  // alternating, the group that idles through level l loads its operands for level l + 1
+  // meanwhile, and the level's critical path is barrier -> gathers -> chain -> publish.
+  const int64_t hi_tb = ((seg_rows / 2 + 31) / 32) * 32;  // 480 rows: 256 (8 + 7 warps)
   for (int64_t b = 0; b < nb; ++b) {
     const int64_t lo = off[b], hi = off[b + 1];
     close_chunk();
     out.blk_chunk[b] = (int32_t)out.chunks.size();
     int64_t k = lo;
+    bool prev_upper = true;
     while (k < hi) {
       // one level: positions [k, level_end)
       const int64_t row0 = A.row_at_pos[k];
       const int64_t lend = A.level_end[row0];
+      const bool to_upper = alt_groups && !prev_upper && lend - k <= seg_rows - hi_tb;
+      const int64_t tb0 = to_upper ? hi_tb : 0;
+      prev_upper = to_upper || lend - k > hi_tb;  // (a wide level occupies both groups)
       int64_t s0 = k;
       while (s0 < lend) {
         // Segments of one level run side by side: the segment's rows go to consumer
         // threads [tb, tb + nrows), tb = rows of the level emitted before, mod seg_rows.
-        const int64_t tb = (s0 - k) % seg_rows;
+        const int64_t tb = (tb0 + s0 - k) % seg_rows;
         // grow a segment while it fits a stage
         int64_t s1 = s0, nnz = 0, w = 0, nfar = 0;
         bool expl = false, hfr = false;

@@ -141,7 +141,7 @@ constexpr int kStepThreads = PSLR_STEP_THREADS;
 int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAnalysis& A, int64_t W,
                 int64_t stage_bytes, int64_t seg_rows, const std::vector<int32_t>& far_index,
                 const std::vector<int32_t>& info_of_row, int64_t far_slots_max, int64_t rhs_row_bytes,
-                TriHost& out, const char* name);
+                TriHost& out, const char* name, bool alt_groups = false);
 
 // Terms of the per-subdomain fused step (see kernels.cu: subdomain_step_kernel).
 enum BTerm : int { BT_NONE = 0, BT_F = 1, BT_EY = 2 };
