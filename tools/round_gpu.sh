@@ -8,5 +8,5 @@ timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; ech
 timeout 300 python tools/prof_apply.py cfg5 3 > gpurun_out/plain.log 2>&1 && \
   timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches.csv python tools/prof_apply.py cfg5 3 > gpurun_out/ncu_launch.log 2>&1
 timeout 300 python tools/prof_apply.py cfg5 1 > gpurun_out/plain1.log 2>&1 && \
-  timeout 900 ncu --set full --import-source on --clock-control none -k regex:subdomain_step -s 322 -c 1 -o gpurun_out/prof_horner python tools/prof_apply.py cfg5 1 > gpurun_out/ncu_full.log 2>&1
+  timeout 900 ncu --set full --import-source on --clock-control none --nvtx --nvtx-include "pslr_apply/" -k regex:subdomain_step -s 2 -c 1 -o gpurun_out/prof_horner python tools/prof_apply.py cfg5 1 > gpurun_out/ncu_full.log 2>&1
 echo done
