@@ -105,6 +105,7 @@ struct PackedFactor {
 struct PackedSystem {
   int64_t n = 0, p = 0, q = 0, s = 0;
   int64_t W = 0, SB = 0, reach = 0, far = 0;
+  int64_t nthr = kStepThreads;       // consumer threads per step CTA = rows per segment
   int64_t levels[4] = {0, 0, 0, 0}, depth[4] = {0, 0, 0, 0}, nnz[4] = {0, 0, 0, 0};
   PackedFactor F[4];                 // LB, UB, LC, UC
   // the factor streams again at the two-vector launches' chunk size SB2 (empty: SB2 == SB):
@@ -124,7 +125,7 @@ struct PackedSystem {
   MergeXf XLBrow;
 };
 
-constexpr uint64_t kPackMagic = 0x35764b4150524c53ull;  // "SLRPAKv5" (v4 + level-merged factors)
+constexpr uint64_t kPackMagic = 0x36764b4150524c53ull;  // "SLRPAKv6" (v5 + per-system consumer-thread count)
 
 // Stages of the step kernel's pipeline for chunk size sb and nv vectors per launch: what
 // the shared memory holds beside the control block and the (nv-wide) value ring, at most 8
@@ -148,6 +149,15 @@ static int64_t merge_mode() {
   const int64_t wC = std::min<int64_t>(std::max<int64_t>(env_int("PSLR_MERGE_WC", 0), 0), (1 << 29) - 1);
   const int64_t alt = env_int("PSLR_ALT_GROUPS", 1) & 3;
   return mode | (wB << 2) | (wC << 32) | (alt << 61);
+}
+
+static int64_t step_threads_for(int64_t levels_LB, int64_t levels_UB, int64_t p) {
+  int64_t t = env_int("PSLR_STEP_THREADS_RT", 0);
+  if (t <= 0) {
+    const int64_t lv = std::max<int64_t>(1, std::min(levels_LB, levels_UB));
+    t = (p / lv < 40) ? kNarrowThreads : kStepThreads;  // rows per level of the shallower B factor
+  }
+  return t <= kNarrowThreads ? kNarrowThreads : kStepThreads;  // the kernel's two instantiations
 }
 
 static int pack_system(const pslr_system* sys, const std::vector<int64_t>& ioff, const std::vector<int64_t>& foff,
@@ -186,6 +196,12 @@ static int pack_system(const pslr_system* sys, const std::vector<int64_t>& ioff,
   while (W < P.reach && W < wmax) W *= 2;
   while (W > 2048 && (smem_optin - 1024 - kCtlBytes - W * 8 - 128) / SB < 2) W /= 2;
   P.W = W;
+  // Consumer threads per step CTA (= rows per segment).  Systems whose B levels are narrow
+  // (2D grids: cfg4 averages 18 rows per level, cfg1 2) run with 4 consumer warps instead of
+  // 15: the level barrier and the idle warps' header walks are most of such a level (cfg4
+  // solve_B 1,083 -> 937 us, cfg1 445 -> 377 us; the 3D configs, 50-500 rows per level, are
+  // 15-30 % slower with 128 threads and keep 480).  PSLR_STEP_THREADS_RT overrides.
+  P.nthr = step_threads_for(aLB.levels, aUB.levels, sys->p);
   const TriAnalysis* an[4] = {&aLB, &aUB, &aLC, &aUC};
   const pslr_csr* M[4] = {&LB, &UB, &LC, &UC};
   const pslr_csr* M0[4] = {&sys->LB, &sys->UB, &sys->LC, &sys->UC};
@@ -222,14 +238,14 @@ static int pack_system(const pslr_system* sys, const std::vector<int64_t>& ioff,
     std::vector<int32_t> row_id(nr);
     for (int64_t i = 0; i < nr; ++i) row_id[i] = (int32_t)i;
     const auto& off = pair == 0 ? ioff : foff;
-    RET(emit_factor(*M[2 * pair + 1], off, AU, W, SB, kStepThreads, AU.pos_of_row, row_id, fr1, rr1,
+    RET(emit_factor(*M[2 * pair + 1], off, AU, W, SB, P.nthr, AU.pos_of_row, row_id, fr1, rr1,
                     P.F[2 * pair + 1].H, nm[2 * pair + 1], alt1));
-    RET(emit_factor(*M[2 * pair], off, AL, W, SB, kStepThreads, AU.pos_of_row, AU.pos_of_row, fr1, rr1,
+    RET(emit_factor(*M[2 * pair], off, AL, W, SB, P.nthr, AU.pos_of_row, AU.pos_of_row, fr1, rr1,
                     P.F[2 * pair].H, nm[2 * pair], alt1));
     if (SB2 != SB) {
-      RET(emit_factor(*M[2 * pair + 1], off, AU, W, SB2, kStepThreads, AU.pos_of_row, row_id, fr2, rr2,
+      RET(emit_factor(*M[2 * pair + 1], off, AU, W, SB2, P.nthr, AU.pos_of_row, row_id, fr2, rr2,
                       P.H2[2 * pair + 1], nm[2 * pair + 1], alt2));
-      RET(emit_factor(*M[2 * pair], off, AL, W, SB2, kStepThreads, AU.pos_of_row, AU.pos_of_row, fr2, rr2,
+      RET(emit_factor(*M[2 * pair], off, AL, W, SB2, P.nthr, AU.pos_of_row, AU.pos_of_row, fr2, rr2,
                       P.H2[2 * pair], nm[2 * pair], alt2));
     }
     P.F[2 * pair].pos_of_row = AL.pos_of_row;
@@ -288,7 +304,7 @@ struct Reader {
 static void serialize(const PackedSystem& P, std::vector<uint8_t>& out) {
   Writer w;
   w.put(kPackMagic);
-  w.put<int64_t>(kStepThreads);
+  w.put<int64_t>(P.nthr);
   w.put<int64_t>(kChunkRows);
   for (int64_t v : {P.n, P.p, P.q, P.s, P.W, P.SB, P.SB2, P.reach, P.far}) w.put(v);
   for (int f = 0; f < 4; ++f) {
@@ -325,8 +341,11 @@ static void serialize(const PackedSystem& P, std::vector<uint8_t>& out) {
 static bool deserialize(const void* blob, int64_t len, const pslr_system* sys, int64_t smem_optin, int64_t SB,
                         int64_t SB2, PackedSystem& P) {
   Reader r{static_cast<const uint8_t*>(blob), len};
-  if (r.get<uint64_t>() != kPackMagic || r.get<int64_t>() != kStepThreads || r.get<int64_t>() != kChunkRows)
-    return false;
+  if (r.get<uint64_t>() != kPackMagic) return false;
+  P.nthr = r.get<int64_t>();  // the packing's consumer-thread count (step_threads_for)
+  if ((P.nthr != kNarrowThreads && P.nthr != kStepThreads) || r.get<int64_t>() != kChunkRows) return false;
+  const int64_t want_thr = env_int("PSLR_STEP_THREADS_RT", 0);
+  if (want_thr > 0 && P.nthr != (want_thr <= kNarrowThreads ? kNarrowThreads : kStepThreads)) return false;
   P.n = r.get<int64_t>();
   P.p = r.get<int64_t>();
   P.q = r.get<int64_t>();
@@ -759,6 +778,7 @@ int pslr_ctx_create_packed(pslr_ctx** out, int device, const pslr_system* sys, c
     fr2 = std::max(fr2, SB2 != SB ? P.H2[f].far_slots : P.F[f].H.far_slots);
   }
   ctx->K.ring_mask = (int)(W - 1);
+  ctx->K.nthr = (int)P.nthr;
   ctx->K.far_slots = (int)fr1;
   ctx->K.nst = (int)nst;
   ctx->K.stage_bytes = (int)SB;

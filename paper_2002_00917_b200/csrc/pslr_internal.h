@@ -137,6 +137,8 @@ struct DevXform {
 #define PSLR_STEP_THREADS 480
 #endif
 constexpr int kStepThreads = PSLR_STEP_THREADS;
+// consumer threads of the step kernel's second instantiation (systems of narrow levels)
+constexpr int kNarrowThreads = kStepThreads < 128 ? kStepThreads : 128;
 
 int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAnalysis& A, int64_t W,
                 int64_t stage_bytes, int64_t seg_rows, const std::vector<int32_t>& far_index,
@@ -210,6 +212,7 @@ struct StepConst {
   int dbg = 0;               // PSLR_DBG timing experiments (wrong results): bit0 skip rows,
                              // bit1 skip next-row loads, bit3 no producer back-off
   long long l2ahead = 0;     // bytes of the factor stream prefetched into L2 ahead (0: default)
+  int nthr = kStepThreads;  // consumer threads per step CTA (the packing's segment rows)
   const int8_t* l2keep = nullptr;  // per block: 1 = its factor chunks are copied with an L2
                                    // evict_last policy (the deepest blocks, whose streams
                                    // bound every step, stay L2-resident across the steps)

@@ -23,8 +23,12 @@
 
 namespace pslr {
 
-constexpr int kConsumerWarps = kStepThreads / 32;
-constexpr int kBlockThreads = kStepThreads + 32;  // + one producer warp
+constexpr int kBlockThreads = kStepThreads + 32;  // + one producer warp (the launch bound)
+// Consumer threads of a launch: a template parameter NT of the kernel (kStepThreads, or
+// kNarrowThreads for systems of narrow levels: a cheaper level barrier, fewer idle warps
+// walking the segment headers; StepConst::nthr, chosen per context by capi.cu); the block is
+// launched with NT + 32 threads.  A compile-time count keeps the barrier's operand immediate
+// (a runtime count cost the cfg5 apply 1.2 %).
 constexpr int kBatch = 8;                          // entries gathered per batch in the row loop
 
 __device__ __forceinline__ uint32_t smem_addr(const void* p) {
@@ -104,8 +108,9 @@ __device__ __forceinline__ void fence_mbar_init() {
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 // barrier among the consumer warps only (the producer warp never joins)
+template <int NT>
 __device__ __forceinline__ void consumer_sync() {
-  asm volatile("bar.sync 1, %0;" ::"n"(kStepThreads) : "memory");
+  asm volatile("bar.sync 1, %0;" ::"n"(NT) : "memory");
 }
 
 __device__ __forceinline__ int A4(int x) { return (x + 3) & ~3; }
@@ -598,8 +603,8 @@ __device__ __forceinline__ void compute_row(const StepConst& K, uint32_t seg, in
 // Consumer side of one triangular phase.  Callers arrive right after a consumer barrier
 // that follows the last write of the phase's rhs array; the phase ends with the barrier
 // of its last level.  rel: the release cursor over the stages (carried across phases).
-template <bool UPPER, int NV, bool XPOS = false>
-__device__ void tri_phase(const StepConst& K, const Streams& Sm, Ctl* ctl, uint8_t* stages_p,
+template <int NT, bool UPPER, int NV, bool XPOS = false>
+__device__ __forceinline__ void tri_phase(const StepConst& K, const Streams& Sm, Ctl* ctl, uint8_t* stages_p,
                           int k, double* ring, int base, double* z, double* xout,
                           const double* cadd) {
   trace_ev(K, 10 + k, 0);
@@ -630,7 +635,7 @@ __device__ void tri_phase(const StepConst& K, const Streams& Sm, Ctl* ctl, uint8
         par ^= 1u;
       }
     }
-    consumer_sync();
+    consumer_sync<NT>();
     return;
   }
   // segment A (computed this step), B (its operands loaded this step), C (header read)
@@ -692,7 +697,7 @@ __device__ void tri_phase(const StepConst& K, const Streams& Sm, Ctl* ctl, uint8
     const int flagsA = hA.y;
     if (!validB) {
       fence_rhs_written();  // z (an L phase's output) is the next phase's right-hand side
-      if (flagsA & kLevelEnd) consumer_sync();
+      if (flagsA & kLevelEnd) consumer_sync<NT>();
       break;
     }
     // B: this warp's row operands (before the barrier; consumed after it)
@@ -704,7 +709,7 @@ __device__ void tri_phase(const StepConst& K, const Streams& Sm, Ctl* ctl, uint8
     const bool validC = next(segB, hB, segC);
     const int4 hC = validC ? *sp<int4>(segC) : make_int4(0, 0, 0, 0);
     trace_clk(K, 54, 0);
-    if (flagsA & kLevelEnd) consumer_sync();
+    if (flagsA & kLevelEnd) consumer_sync<NT>();
     if (UPPER && actB)  // the epilogue addend: a global load a level ahead of its use
       ra.cadd = (cadd && ra.active) ? vldg<NV>(cadd, ra.info & 0x3fffffff) : vzero<NV>();
     segA = segB;
@@ -779,18 +784,18 @@ __device__ __forceinline__ void iface_terms4(int kind, const int (&row)[4], cons
 // CTA's block, in place: arr[pos_i] -= c0 arr[pos_j0] + c1 arr[pos_j1] + c2 arr[pos_j2].
 // The records read only unmerged rows and write only merged ones (no ordering among them).
 // Callers fence and barrier before the phase that reads arr.
-template <int NV>
+template <int NV, int NT>
 __device__ __forceinline__ void xform_block(const DevXform& X, int b, double* arr) {
   const int r0 = __ldg(X.blk + b), r1 = __ldg(X.blk + b + 1);
   constexpr int kIn = 4;  // records in flight per thread (two dependent global round trips)
   const int4* idx = reinterpret_cast<const int4*>(X.idx);
   const double2* val = reinterpret_cast<const double2*>(X.val);
-  for (int i0 = r0 + (int)threadIdx.x; i0 < r1; i0 += kIn * kStepThreads) {
+  for (int i0 = r0 + (int)threadIdx.x; i0 < r1; i0 += kIn * NT) {
     int4 id[kIn];
     double2 c01[kIn], c2[kIn];
 #pragma unroll
     for (int j = 0; j < kIn; ++j) {
-      const int i = i0 + j * kStepThreads;
+      const int i = i0 + j * NT;
       const bool ok = i < r1;
       id[j] = ok ? __ldg(idx + i) : make_int4(0, 0, 0, 0);
       c01[j] = ok ? __ldg(val + 2 * i) : make_double2(0.0, 0.0);
@@ -809,7 +814,7 @@ __device__ __forceinline__ void xform_block(const DevXform& X, int b, double* ar
       vt<NV> t = vmul(z0[j], c01[j].x);
       t = vmadd(t, c01[j].y, z1[j]);
       t = vmadd(t, c2[j].x, z2[j]);
-      if (i0 + j * kStepThreads < r1) vst(arr, id[j].x, vsub(a[j], t));
+      if (i0 + j * NT < r1) vst(arr, id[j].x, vsub(a[j], t));
     }
   }
 }
@@ -825,7 +830,7 @@ __device__ __forceinline__ void xform_block(const DevXform& X, int b, double* ar
 #ifndef PSLR_STEP_MINB
 #define PSLR_STEP_MINB 1
 #endif
-template <int NV, bool XPOS>
+template <int NV, bool XPOS, int NT>
 __global__ void __launch_bounds__(kBlockThreads, PSLR_STEP_MINB)
 subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant__ StepConst K) {
   const int b = blockIdx.x;
@@ -874,13 +879,13 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
   if (threadIdx.x == 0) {
     for (int s = 0; s < K.nst; ++s) {
       mbar_init(&ctl->full[s], 2);
-      mbar_init(&ctl->empty[s], kConsumerWarps);
+      mbar_init(&ctl->empty[s], NT / 32);
     }
     for (int k = 0; k < 4; ++k) mbar_init(&ctl->rhs_ready[k], 1);
     fence_mbar_init();
   }
   __syncthreads();
-  if (threadIdx.x >= kStepThreads) {  // producer warp (all 32 lanes)
+  if (threadIdx.x >= NT) {  // producer warp (all 32 lanes)
     producer(S, ctl, stages, K.nst, K.stage_bytes, NV,
              (K.trace && K.trace_cap >= (1 << 20)) ? K.trace + 2 + 2 * K.trace_cap - 8 * 4096 + b * 8
                                                    : nullptr,
@@ -918,41 +923,41 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
       // fL holds f already; rhsE's non-E positions are permanently 0
     } else if (a.b1 == BT_F) {
       constexpr int kIn = PSLR_PRE_F;  // independent loads in flight per thread
-      for (int row0 = r0 + tid; row0 < r1; row0 += kIn * kStepThreads) {
+      for (int row0 = r0 + tid; row0 < r1; row0 += kIn * NT) {
         vt<NV> v[kIn];
         int pos[kIn];
 #pragma unroll
         for (int j = 0; j < kIn; ++j) {
-          const int row = row0 + j * kStepThreads;
+          const int row = row0 + j * NT;
           const bool ok = row < r1;
           v[j] = ok ? vldg<NV>(a.f, row) : vzero<NV>();
           pos[j] = ok ? __ldg(K.LB.lpos + row) : 0;
         }
 #pragma unroll
         for (int j = 0; j < kIn; ++j)
-          if (row0 + j * kStepThreads < r1) vst(K.rhsB, pos[j], v[j]);
+          if (row0 + j * NT < r1) vst(K.rhsB, pos[j], v[j]);
       }
       if (K.XLB.nrec) {  // level-merged L_B: f' = (I - N) f in place
-        consumer_sync();
-        xform_block<NV>(K.XLB, b, K.rhsB);
+        consumer_sync<NT>();
+        xform_block<NV, NT>(K.XLB, b, K.rhsB);
       }
     } else {
-      for (int p = r0 + tid; p < r1; p += kStepThreads) vst(K.rhsB, p, vzero<NV>());
+      for (int p = r0 + tid; p < r1; p += NT) vst(K.rhsB, p, vzero<NV>());
     }
     // pass 2: rows with E entries get the E y term: f - E y, or E y alone (scipy
     // csr_matvec order), kIn rows per thread in flight; one int4 record per row
     if ((a.b1 == BT_EY || a.b2 == BT_EY) && !a.ey_done) {
-      if (!a.fL && !ey_only) consumer_sync();
+      if (!a.fL && !ey_only) consumer_sync<NT>();
       constexpr int kIn = PSLR_PRE_E;  // E rows in flight per thread (dependent chain: record, E entry, y)
       const int e0 = K.erow_off[b], e1 = K.erow_off[b + 1];
       const int4* rec = reinterpret_cast<const int4*>(K.erows);
-      for (int i0 = e0 + tid; i0 < e1; i0 += kIn * kStepThreads) {
+      for (int i0 = e0 + tid; i0 < e1; i0 += kIn * NT) {
         int4 r[kIn];
         vt<NV> fv[kIn], sum[kIn];
         int len = 0;
 #pragma unroll
         for (int j = 0; j < kIn; ++j) {
-          const int i = i0 + j * kStepThreads;
+          const int i = i0 + j * NT;
           r[j] = i < e1 ? __ldg(rec + i) : make_int4(0, 0, 0, 0);
           len = max(len, r[j].w - r[j].z);
           sum[j] = vzero<NV>();
@@ -978,30 +983,30 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
         }
 #pragma unroll
         for (int j = 0; j < kIn; ++j)
-          if (i0 + j * kStepThreads < e1) vst(rhs, r[j].x, (a.b1 == BT_F) ? vsub(fv[j], sum[j]) : sum[j]);
+          if (i0 + j * NT < e1) vst(rhs, r[j].x, (a.b1 == BT_F) ? vsub(fv[j], sum[j]) : sum[j]);
       }
     }
     fence_rhs_written();  // the L_B right-hand side (f / E y rows) is read by TMA next
-    consumer_sync();
+    consumer_sync<NT>();
     trace_ev(K, 3, 0);
     trace_cta(K, 1);
-    tri_phase<false, NV>(K, S, ctl, stages, ph_LB, ring, r0, K.zB, nullptr, nullptr);
+    tri_phase<NT, false, NV>(K, S, ctl, stages, ph_LB, ring, r0, K.zB, nullptr, nullptr);
     if (K.XUB.nrec) {  // level-merged U_B: y' = (I - M) y in place (y: L_B's output)
-      xform_block<NV>(K.XUB, b, K.zB);
+      xform_block<NV, NT>(K.XUB, b, K.zB);
       fence_rhs_written();
-      consumer_sync();
+      consumer_sync<NT>();
     }
-    tri_phase<true, NV, XPOS>(K, S, ctl, stages, ph_UB, ring, r0, K.zB, a.xb, nullptr);
+    tri_phase<NT, true, NV, XPOS>(K, S, ctl, stages, ph_UB, ring, r0, K.zB, a.xb, nullptr);
   }
   if (do_i) {
     trace_cta(K, 7);
     const int r0 = K.ifc_off[b], r1 = K.ifc_off[b + 1];
-    for (int row0 = r0 + tid; row0 < r1 && !a.ifc_done; row0 += 4 * kStepThreads) {
+    for (int row0 = r0 + tid; row0 < r1 && !a.ifc_done; row0 += 4 * NT) {
       int row[4];
       bool ok[4];
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        row[j] = row0 + j * kStepThreads;
+        row[j] = row0 + j * NT;
         ok[j] = row[j] < r1;
       }
       vt<NV> w[4], t2[4];
@@ -1024,21 +1029,21 @@ subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant_
       }
     }
     fence_rhs_written();  // rhsC is the L_C0 right-hand side
-    consumer_sync();
+    consumer_sync<NT>();
     trace_ev(K, 30, 0);
     if (do_c) {
       if (K.XLC.nrec) {  // level-merged L_C0: w' = (I - N) w in place
-        xform_block<NV>(K.XLC, b, K.rhsC);
+        xform_block<NV, NT>(K.XLC, b, K.rhsC);
         fence_rhs_written();
-        consumer_sync();
+        consumer_sync<NT>();
       }
-      tri_phase<false, NV>(K, S, ctl, stages, ph_LC, ring, r0, K.zC, nullptr, nullptr);
+      tri_phase<NT, false, NV>(K, S, ctl, stages, ph_LC, ring, r0, K.zC, nullptr, nullptr);
       if (K.XUC.nrec) {  // level-merged U_C0
-        xform_block<NV>(K.XUC, b, K.zC);
+        xform_block<NV, NT>(K.XUC, b, K.zC);
         fence_rhs_written();
-        consumer_sync();
+        consumer_sync<NT>();
       }
-      tri_phase<true, NV>(K, S, ctl, stages, ph_UC, ring, r0, K.zC, a.yout, a.cadd);
+      tri_phase<NT, true, NV>(K, S, ctl, stages, ph_UC, ring, r0, K.zC, a.yout, a.cadd);
     }
   }
   trace_cta(K, 6);
@@ -1130,12 +1135,17 @@ int configure_step_kernel(int nv, int smem_bytes) {
   auto set = [&](auto kern) {
     return (int)cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_bytes);
   };
+  int e;
   if (nv == 2) {
-    const int e = set(subdomain_step_kernel<2, false>);
-    return e ? e : set(subdomain_step_kernel<2, true>);
+    if ((e = set(subdomain_step_kernel<2, false, kStepThreads>))) return e;
+    if ((e = set(subdomain_step_kernel<2, true, kStepThreads>))) return e;
+    if ((e = set(subdomain_step_kernel<2, false, kNarrowThreads>))) return e;
+    return set(subdomain_step_kernel<2, true, kNarrowThreads>);
   }
-  const int e = set(subdomain_step_kernel<1, false>);
-  return e ? e : set(subdomain_step_kernel<1, true>);
+  if ((e = set(subdomain_step_kernel<1, false, kStepThreads>))) return e;
+  if ((e = set(subdomain_step_kernel<1, true, kStepThreads>))) return e;
+  if ((e = set(subdomain_step_kernel<1, false, kNarrowThreads>))) return e;
+  return set(subdomain_step_kernel<1, true, kNarrowThreads>);
 }
 
 int launch_step_kernel(const pslr_ctx* ctx, const StepArgs& a, const StepConst& K, cudaStream_t st, int nv);
@@ -1247,7 +1257,7 @@ int launch_step(const pslr_ctx* ctx, const StepArgs& a_in, cudaStream_t st, int 
 int launch_step_kernel(const pslr_ctx* ctx, const StepArgs& a, const StepConst& K, cudaStream_t st, int nv) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3((unsigned)ctx->s);
-  cfg.blockDim = dim3(kBlockThreads);
+  cfg.blockDim = dim3((unsigned)(K.nthr + 32));
   cfg.dynamicSmemBytes = (size_t)K.smem_bytes;
   cfg.stream = st;
   cudaLaunchAttribute attr[1];
@@ -1255,11 +1265,16 @@ int launch_step_kernel(const pslr_ctx* ctx, const StepArgs& a, const StepConst& 
   attr[0].val.programmaticStreamSerializationAllowed = ctx->pdl ? 1 : 0;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  if (nv == 2)
-    return (int)(a.xpos ? cudaLaunchKernelEx(&cfg, subdomain_step_kernel<2, true>, a, K)
-                        : cudaLaunchKernelEx(&cfg, subdomain_step_kernel<2, false>, a, K));
-  return (int)(a.xpos ? cudaLaunchKernelEx(&cfg, subdomain_step_kernel<1, true>, a, K)
-                      : cudaLaunchKernelEx(&cfg, subdomain_step_kernel<1, false>, a, K));
+  auto go = [&](auto kern) { return (int)cudaLaunchKernelEx(&cfg, kern, a, K); };
+  const bool narrow = K.nthr == kNarrowThreads && kNarrowThreads != kStepThreads;
+  if (nv == 2) {
+    if (narrow)
+      return a.xpos ? go(subdomain_step_kernel<2, true, kNarrowThreads>) : go(subdomain_step_kernel<2, false, kNarrowThreads>);
+    return a.xpos ? go(subdomain_step_kernel<2, true, kStepThreads>) : go(subdomain_step_kernel<2, false, kStepThreads>);
+  }
+  if (narrow)
+    return a.xpos ? go(subdomain_step_kernel<1, true, kNarrowThreads>) : go(subdomain_step_kernel<1, false, kNarrowThreads>);
+  return a.xpos ? go(subdomain_step_kernel<1, true, kStepThreads>) : go(subdomain_step_kernel<1, false, kStepThreads>);
 }
 
 }  // namespace pslr

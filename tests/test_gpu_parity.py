@@ -384,6 +384,43 @@ def test_ey_prepass_and_all_sm_kernel_bitexact(monkeypatch):
     np.testing.assert_array_equal(out[0][1], d["apply_neumann"])
 
 
+@pytest.mark.parametrize("threads", ["128", "480"])
+@pytest.mark.parametrize("alt", ["0", "3"])
+def test_consumer_thread_count_and_warp_groups_bitexact(threads, alt, monkeypatch):
+    """The step kernel's two instantiations (480 and 128 consumer threads, chosen per system
+    from the rows per level; PSLR_STEP_THREADS_RT forces one) and the packer's alternating
+    warp groups (PSLR_ALT_GROUPS) only change which thread owns a row: every operator is
+    the reference's output bit for bit in each combination, one and two vectors per call."""
+    import torch
+    import paper_2002_00917_b200 as pg
+    from paper_2002_00917_b200 import _lib
+    name = "lap3d6_s4_dt1e-2"
+    meta = G["apply"][name]
+    d = load_npz(f"apply_{name}.npz")
+    A = csr_from(d, "A")
+    cfg = pg.PslrConfig(num_subdomains=meta["s"], series_degree=meta["m"], rank=meta["rank"],
+                        droptol=meta["droptol"], seed=meta["seed"])
+    ref = pg.build(A, cfg)
+    monkeypatch.setenv("PSLR_STEP_THREADS_RT", threads)
+    monkeypatch.setenv("PSLR_ALT_GROUPS", alt)
+    P = pg.build(A, cfg)
+    np.testing.assert_array_equal(pg.solve_B(P.ctx, d["f"]), d["solve_B"])
+    np.testing.assert_array_equal(pg.solve_C0(P.ctx, d["v"]), d["solve_C0"])
+    np.testing.assert_array_equal(pg.apply_Es(P.ctx, d["v"]), d["apply_Es"])
+    np.testing.assert_array_equal(pg.apply_neumann(P.ctx, meta["m"], d["v"]), d["apply_neumann"])
+    np.testing.assert_array_equal(pg.apply_Err(P.ctx, meta["m"], d["v"]), d["apply_Err"])
+    np.testing.assert_array_equal(P.apply(d["b"]), ref.apply(d["b"]))
+    n = P.system.n
+    B2 = torch.from_numpy(np.random.default_rng(3).standard_normal((2, n))).cuda()
+    Z2 = torch.empty_like(B2)
+    P.device.ensure_correction(P.correction)
+    _lib.check(_lib.fns["pslr_apply_multi"](P.device.handle, meta["m"], 2, B2.data_ptr(), Z2.data_ptr(),
+                                            P.device.stream()))
+    torch.cuda.synchronize()
+    for v in range(2):
+        assert torch.equal(Z2[v], ref.apply(B2[v].contiguous()))
+
+
 def _oracle_ctx(P):
     from oracle import pslr_oracle as O
     ps = P.system
