@@ -125,7 +125,7 @@ struct PackedSystem {
   MergeXf XLBrow;
 };
 
-constexpr uint64_t kPackMagic = 0x36764b4150524c53ull;  // "SLRPAKv6" (v5 + per-system consumer-thread count)
+constexpr uint64_t kPackMagic = 0x37764b4150524c53ull;  // "SLRPAKv7" (v6 + the two-vector packing's own segment height)
 
 // Stages of the step kernel's pipeline for chunk size sb and nv vectors per launch: what
 // the shared memory holds beside the control block and the (nv-wide) value ring, at most 8
@@ -159,6 +159,11 @@ static int64_t step_threads_for(int64_t levels_LB, int64_t levels_UB, int64_t p)
   }
   return t <= kNarrowThreads ? kNarrowThreads : kStepThreads;  // the kernel's two instantiations
 }
+
+// the two-vector packing's consumer threads (pslr_internal.h kWide2Threads), and whether the
+// two-vector launches need a packing of their own (another chunk size or segment height)
+static int64_t nthr2_for(int64_t nthr) { return nthr == kStepThreads ? kWide2Threads : nthr; }
+static bool separate2(int64_t SB, int64_t SB2, int64_t nthr) { return SB2 != SB || nthr2_for(nthr) != nthr; }
 
 static int pack_system(const pslr_system* sys, const std::vector<int64_t>& ioff, const std::vector<int64_t>& foff,
                        int64_t smem_optin, int64_t SB, int64_t SB2, int64_t wmax, PackedSystem& P) {
@@ -223,10 +228,11 @@ static int pack_system(const pslr_system* sys, const std::vector<int64_t>& ioff,
     const int64_t left = smem_optin - 1024 - kCtlBytes - nst * sb;
     return std::max<int64_t>(0, std::min<int64_t>(left / (8 * nv) - W - 17, env_int("PSLR_FAR_SLOTS", 1 << 14)));
   };
-  const int64_t fr1 = (SB2 != SB) ? far_cap(SB, 1) : std::min(far_cap(SB, 1), far_cap(SB, 2));
+  const bool sep2 = separate2(SB, SB2, P.nthr);
+  const int64_t fr1 = sep2 ? far_cap(SB, 1) : std::min(far_cap(SB, 1), far_cap(SB, 2));
   const int64_t fr2 = far_cap(SB2, 2);
   // a chunk's rhs slice shares its stage (8 B per row and vector)
-  const int64_t rr1 = (SB2 != SB) ? 8 : 16, rr2 = 16;
+  const int64_t rr1 = sep2 ? 8 : 16, rr2 = 16;
   // U first: L's output lands at the U-positions, where every value lives globally
   for (int pair = 0; pair < 2; ++pair) {
     const TriAnalysis& AL = *an[2 * pair];
@@ -242,10 +248,10 @@ static int pack_system(const pslr_system* sys, const std::vector<int64_t>& ioff,
                     P.F[2 * pair + 1].H, nm[2 * pair + 1], alt1));
     RET(emit_factor(*M[2 * pair], off, AL, W, SB, P.nthr, AU.pos_of_row, AU.pos_of_row, fr1, rr1,
                     P.F[2 * pair].H, nm[2 * pair], alt1));
-    if (SB2 != SB) {
-      RET(emit_factor(*M[2 * pair + 1], off, AU, W, SB2, P.nthr, AU.pos_of_row, row_id, fr2, rr2,
+    if (sep2) {
+      RET(emit_factor(*M[2 * pair + 1], off, AU, W, SB2, nthr2_for(P.nthr), AU.pos_of_row, row_id, fr2, rr2,
                       P.H2[2 * pair + 1], nm[2 * pair + 1], alt2));
-      RET(emit_factor(*M[2 * pair], off, AL, W, SB2, P.nthr, AU.pos_of_row, AU.pos_of_row, fr2, rr2,
+      RET(emit_factor(*M[2 * pair], off, AL, W, SB2, nthr2_for(P.nthr), AU.pos_of_row, AU.pos_of_row, fr2, rr2,
                       P.H2[2 * pair], nm[2 * pair], alt2));
     }
     P.F[2 * pair].pos_of_row = AL.pos_of_row;
@@ -375,7 +381,7 @@ static bool deserialize(const void* blob, int64_t len, const pslr_system* sys, i
     r.vec(P.H2[f].chunks);
     r.vec(P.H2[f].blk_chunk);
     if ((int64_t)P.F[f].H.blk_chunk.size() != P.s + 1) return false;
-    if ((SB2 != SB) != ((int64_t)P.H2[f].blk_chunk.size() == P.s + 1)) return false;
+    if (separate2(SB, SB2, P.nthr) != ((int64_t)P.H2[f].blk_chunk.size() == P.s + 1)) return false;
   }
   r.vec(P.ub_pos);
   r.vec(P.lb_pos);
@@ -556,6 +562,7 @@ static int ensure_nv2(pslr_ctx* ctx) {
   const int64_t nst = stage_count(ctx->smem_optin, W, SB, 2);
   if (nst < 2) return fail(PSLR_EINVAL, "not enough shared memory for two right-hand sides per launch");
   K2.nst = (int)nst;
+  K2.nthr = (int)nthr2_for(ctx->K.nthr);
   K2.stage_bytes = (int)SB;
   K2.rhs_stride = 0;  // the rhs slice follows the data inside its stage
   K2.far_slots = (int)ctx->far2;
@@ -775,7 +782,7 @@ int pslr_ctx_create_packed(pslr_ctx** out, int device, const pslr_system* sys, c
   int64_t fr1 = 0, fr2 = 0;  // far-ring slots of the one- and two-vector packings
   for (int f = 0; f < 4; ++f) {
     fr1 = std::max(fr1, P.F[f].H.far_slots);
-    fr2 = std::max(fr2, SB2 != SB ? P.H2[f].far_slots : P.F[f].H.far_slots);
+    fr2 = std::max(fr2, separate2(SB, SB2, P.nthr) ? P.H2[f].far_slots : P.F[f].H.far_slots);
   }
   ctx->K.ring_mask = (int)(W - 1);
   ctx->K.nthr = (int)P.nthr;
@@ -841,7 +848,7 @@ int pslr_ctx_create_packed(pslr_ctx** out, int device, const pslr_system* sys, c
       }
       // the two-vector launches' streams (same positions, other chunk boundaries)
       ctx->tri2[f] = *dt[f];
-      if (SB2 != SB) {
+      if (separate2(SB, SB2, P.nthr)) {
         const TriHost& H2 = P.H2[f];
         ctx->tri2[f].nchunks = (int32_t)H2.chunks.size();
         if ((rc = upload(ctx, H2.data, &ctx->tri2[f].data))) return bail(rc);

@@ -139,6 +139,12 @@ struct DevXform {
 constexpr int kStepThreads = PSLR_STEP_THREADS;
 // consumer threads of the step kernel's second instantiation (systems of narrow levels)
 constexpr int kNarrowThreads = kStepThreads < 128 ? kStepThreads : 128;
+// consumer threads of the two-vector launches of a wide system: a row's two interleaved
+// chains need ~167 registers per thread; under the 512-thread launch bound the compiler
+// caps them at 128 and spills, under 352 + 32 threads it does not, and the two-vector sweep
+// gains 6 % (cfg5: 0.315 -> 0.295 ms per apply; 224-352 consumer threads measure alike).
+// The one-vector kernel fits 128 registers and keeps 480 threads (1.63 vs 1.67 ms at 352).
+constexpr int kWide2Threads = kStepThreads < 352 ? kStepThreads : 352;
 
 int emit_factor(const pslr_csr& M, const std::vector<int64_t>& off, const TriAnalysis& A, int64_t W,
                 int64_t stage_bytes, int64_t seg_rows, const std::vector<int32_t>& far_index,

@@ -831,7 +831,7 @@ __device__ __forceinline__ void xform_block(const DevXform& X, int b, double* ar
 #define PSLR_STEP_MINB 1
 #endif
 template <int NV, bool XPOS, int NT>
-__global__ void __launch_bounds__(kBlockThreads, PSLR_STEP_MINB)
+__global__ void __launch_bounds__(NT + 32, PSLR_STEP_MINB)
 subdomain_step_kernel(const __grid_constant__ StepArgs a, const __grid_constant__ StepConst K) {
   const int b = blockIdx.x;
   const bool do_b = a.b1 != BT_NONE;
@@ -1137,8 +1137,8 @@ int configure_step_kernel(int nv, int smem_bytes) {
   };
   int e;
   if (nv == 2) {
-    if ((e = set(subdomain_step_kernel<2, false, kStepThreads>))) return e;
-    if ((e = set(subdomain_step_kernel<2, true, kStepThreads>))) return e;
+    if ((e = set(subdomain_step_kernel<2, false, kWide2Threads>))) return e;
+    if ((e = set(subdomain_step_kernel<2, true, kWide2Threads>))) return e;
     if ((e = set(subdomain_step_kernel<2, false, kNarrowThreads>))) return e;
     return set(subdomain_step_kernel<2, true, kNarrowThreads>);
   }
@@ -1266,11 +1266,12 @@ int launch_step_kernel(const pslr_ctx* ctx, const StepArgs& a, const StepConst& 
   cfg.attrs = attr;
   cfg.numAttrs = 1;
   auto go = [&](auto kern) { return (int)cudaLaunchKernelEx(&cfg, kern, a, K); };
-  const bool narrow = K.nthr == kNarrowThreads && kNarrowThreads != kStepThreads;
+  const bool narrow = K.nthr == kNarrowThreads && kNarrowThreads != (nv == 2 ? kWide2Threads : kStepThreads);
+  if (!narrow && K.nthr != (nv == 2 ? kWide2Threads : kStepThreads)) return (int)cudaErrorInvalidValue;
   if (nv == 2) {
     if (narrow)
       return a.xpos ? go(subdomain_step_kernel<2, true, kNarrowThreads>) : go(subdomain_step_kernel<2, false, kNarrowThreads>);
-    return a.xpos ? go(subdomain_step_kernel<2, true, kStepThreads>) : go(subdomain_step_kernel<2, false, kStepThreads>);
+    return a.xpos ? go(subdomain_step_kernel<2, true, kWide2Threads>) : go(subdomain_step_kernel<2, false, kWide2Threads>);
   }
   if (narrow)
     return a.xpos ? go(subdomain_step_kernel<1, true, kNarrowThreads>) : go(subdomain_step_kernel<1, false, kNarrowThreads>);
