@@ -48,11 +48,11 @@ def main(nv1, nv2, bench, tag):
     groups = []
     for i, d in enumerate(c1):
         if d["kernel"].startswith("pre_step_kernel") and i + 3 < len(c1) and \
-                c1[i + 3]["kernel"].startswith("subdomain_step_kernel<1, 0>") and \
+                c1[i + 3]["kernel"].startswith("subdomain_step_kernel<1, 0") and \
                 c1[i + 2]["kernel"].startswith("iface_kernel"):
             groups.append(c1[i:i + 4])
     if not groups:
-        groups = [[d] for d in c1 if d["kernel"].startswith("subdomain_step_kernel<1, 1>")][1:4]
+        groups = [[d] for d in c1 if d["kernel"].startswith("subdomain_step_kernel<1, 1")][1:4]
     hb = sum(sum(d["dram__bytes_read.sum"] + d["dram__bytes_write.sum"] for d in g) for g in groups) / len(groups)
     ht = sum(sum(d["gpu__time_duration.sum"] for d in g) for g in groups) / len(groups)
     summ = {"round": tag,
