@@ -395,8 +395,14 @@ constexpr int kCgsWarps = kCgsThreads / 32;
 constexpr int kCgsMaxCols = 128;
 enum CgsMode : int { kDot = 0, kSubDot = 1, kSubNorm = 2 };
 
+// resident CTAs per SM the register budget is set for: the fused mode-1 pass (two dependent
+// phases per tile) gains from occupancy (3 CTAs at 80 registers: k = 10 / 25 / 50 columns
+// 69 -> 56 / 116 -> 99 / 203 -> 190 us), the one-phase passes from registers (2 CTAs at 128)
+#ifndef PSLR_CGS_MINB1
+#define PSLR_CGS_MINB1 3
+#endif
 template <int MODE, int CPW>  // CPW: columns per warp (k <= 8 * CPW)
-__global__ void __launch_bounds__(kCgsThreads, 2)
+__global__ void __launch_bounds__(kCgsThreads, MODE == 1 ? PSLR_CGS_MINB1 : 2)
 cgs_pass_kernel(const double* __restrict__ X, int64_t ld, int k, double* __restrict__ w, int64_t n,
                 const double* __restrict__ h0, double* __restrict__ partials, double* __restrict__ out,
                 unsigned int* counter) {
