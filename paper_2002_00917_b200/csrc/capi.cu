@@ -142,13 +142,15 @@ static int64_t stage_count(int64_t smem_optin, int64_t W, int64_t sb, int64_t nv
 // factors, 2 = level-merged C0 factors (default), 3 = both.  PSLR_MERGE_W / _WC: merge only
 // level pairs of at most that many rows (B: kStepThreads, C0: 0 = every pair)
 // The blob key: mode bits 0-1, the B width limit from bit 2, the C0 width limit from bit 32,
-// PSLR_ALT_GROUPS (alternating warp groups, pack.cpp) in bits 61-62
+// PSLR_LIST_SCHED (list-scheduled steps, pack.cpp) in bit 31, PSLR_ALT_GROUPS (alternating
+// warp groups, pack.cpp) in bits 61-62
 static int64_t merge_mode() {
   const int64_t mode = env_int("PSLR_MERGE", 2) & 3;
   const int64_t wB = std::min<int64_t>(std::max<int64_t>(env_int("PSLR_MERGE_W", kStepThreads), 0), (1 << 29) - 1);
   const int64_t wC = std::min<int64_t>(std::max<int64_t>(env_int("PSLR_MERGE_WC", 0), 0), (1 << 29) - 1);
   const int64_t alt = env_int("PSLR_ALT_GROUPS", 1) & 3;
-  return mode | (wB << 2) | (wC << 32) | (alt << 61);
+  const int64_t sched = env_int("PSLR_LIST_SCHED", 1) ? 1 : 0;
+  return mode | (wB << 2) | (sched << 31) | (wC << 32) | (alt << 61);
 }
 
 static int64_t step_threads_for(int64_t levels_LB, int64_t levels_UB, int64_t p) {
@@ -178,7 +180,7 @@ static int pack_system(const pslr_system* sys, const std::vector<int64_t>& ioff,
   HostCsr mf[4];
   pslr_csr LB = sys->LB, UB = sys->UB, LC = sys->LC, UC = sys->UC;
   if (P.merged & 1) {
-    const int64_t wB = (P.merged >> 2) & ((1 << 29) - 1);
+    const int64_t wB = (P.merged >> 2) & ((1 << 29) - 1);  // (bit 31: list scheduling)
     RET(merge_levels(sys->LB, ioff, false, wB, mf[0], P.X[0], "L_B"));
     RET(merge_levels(sys->UB, ioff, true, wB, mf[1], P.X[1], "U_B"));
     LB = mf[0].view();
@@ -192,10 +194,14 @@ static int pack_system(const pslr_system* sys, const std::vector<int64_t>& ioff,
     UC = mf[3].view();
   }
   TriAnalysis aLB, aUB, aLC, aUC;
-  RET(analyze_factor(LB, ioff, false, aLB, "L_B"));
-  RET(analyze_factor(UB, ioff, true, aUB, "U_B"));
-  RET(analyze_factor(LC, foff, false, aLC, "L_C0"));
-  RET(analyze_factor(UC, foff, true, aUC, "U_C0"));
+  // rows of levels wider than a launch's consumer threads are list-scheduled into full steps
+  // (pack.cpp list_schedule; PSLR_LIST_SCHED=0: the ASAP dependency levels as they are)
+  const int64_t scap = ((P.merged >> 31) & 1) ? kStepThreads : 0;
+  const int64_t sdel = std::max<int64_t>(0, env_int("PSLR_SCHED_DELAY", 16));
+  RET(analyze_factor(LB, ioff, false, aLB, "L_B", scap, sdel));
+  RET(analyze_factor(UB, ioff, true, aUB, "U_B", scap, sdel));
+  RET(analyze_factor(LC, foff, false, aLC, "L_C0", scap, sdel));
+  RET(analyze_factor(UC, foff, true, aUC, "U_C0", scap, sdel));
   P.reach = std::max({aLB.reach, aUB.reach, aLC.reach, aUC.reach, (int64_t)1});
   int64_t W = 2048;  // >= 2048: the ring doubles as the V^T y reduction scratch
   while (W < P.reach && W < wmax) W *= 2;

@@ -32,8 +32,88 @@ inline int64_t a2(int64_t x) { return (x + 1) & ~int64_t(1); }
 
 }  // namespace
 
+// List scheduling of a block's rows into steps of at most `cap` rows (cap = the consumer
+// threads of a launch).  The ASAP dependency levels cost ceil(width / cap) steps each: cfg5's
+// L_B levels are ~500 rows wide, i.e. two steps per level, the second one nearly empty
+// (block 19: 118 levels, 215 steps).  Any schedule that keeps a row after its dependencies
+// computes the same bits, so rows with slack move to later steps: each step takes up to cap
+// ready rows, most urgent first (deadline = min(latest start that keeps the critical path,
+// ASAP level + max_delay): the bound keeps a delayed row's dependencies within reach of the
+// solution ring).  lev (ASAP levels on entry) is replaced by the step of each row when that
+// takes fewer steps; returns the number of levels of the result.
+static int32_t list_schedule(const pslr_csr& M, int64_t lo, int64_t nr, bool upper, int64_t cap, int64_t max_delay,
+                             std::vector<int32_t>& lev) {
+  int32_t depth = 0;
+  for (int64_t i = 0; i < nr; ++i) depth = std::max(depth, lev[i] + 1);
+  if (cap <= 0 || nr == 0) return depth;
+  std::vector<int64_t> width(depth, 0);
+  for (int64_t i = 0; i < nr; ++i) ++width[lev[i]];
+  int64_t steps_asap = 0;
+  for (int64_t w : width) steps_asap += (w + cap - 1) / cap;
+  if (steps_asap == depth) return depth;  // every level fits one step already
+  // successors (the transpose pattern) and the unscheduled-dependency count of each row
+  std::vector<int64_t> sptr(nr + 1, 0);
+  std::vector<int32_t> indeg(nr, 0);
+  for (int64_t i = 0; i < nr; ++i)
+    for (int64_t e = M.indptr[lo + i]; e < M.indptr[lo + i + 1]; ++e) {
+      const int64_t j = M.indices[e] - lo;
+      if (j != i) {
+        ++sptr[j + 1];
+        ++indeg[i];
+      }
+    }
+  for (int64_t i = 0; i < nr; ++i) sptr[i + 1] += sptr[i];
+  std::vector<int32_t> succ(sptr[nr]);
+  {
+    std::vector<int64_t> fill(sptr.begin(), sptr.end() - 1);
+    for (int64_t i = 0; i < nr; ++i)
+      for (int64_t e = M.indptr[lo + i]; e < M.indptr[lo + i + 1]; ++e) {
+        const int64_t j = M.indices[e] - lo;
+        if (j != i) succ[fill[j]++] = (int32_t)i;
+      }
+  }
+  // height: the longest chain of dependents below a row (reverse topological order)
+  std::vector<int32_t> height(nr, 0);
+  for (int64_t t = 0; t < nr; ++t) {
+    const int64_t i = upper ? t : nr - 1 - t;
+    int32_t h = 0;
+    for (int64_t e = sptr[i]; e < sptr[i + 1]; ++e) h = std::max(h, height[succ[e]] + 1);
+    height[i] = h;
+  }
+  auto deadline = [&](int64_t i) {
+    return std::min<int64_t>((int64_t)depth - 1 - height[i], (int64_t)lev[i] + max_delay);
+  };
+  using Key = std::pair<int64_t, int32_t>;  // (deadline, row): most urgent first, then row order
+  std::priority_queue<Key, std::vector<Key>, std::greater<Key>> ready;
+  for (int64_t i = 0; i < nr; ++i)
+    if (indeg[i] == 0) ready.push({deadline(i), (int32_t)i});
+  std::vector<int32_t> step(nr, 0), batch, freed;
+  int64_t done = 0;
+  int32_t t = 0;
+  while (done < nr) {
+    batch.clear();
+    freed.clear();
+    while (!ready.empty() && (int64_t)batch.size() < cap) {
+      batch.push_back(ready.top().second);
+      ready.pop();
+    }
+    if (batch.empty()) return depth;  // (a cycle: cannot happen for a triangular factor)
+    for (int32_t i : batch) {
+      step[i] = t;
+      for (int64_t e = sptr[i]; e < sptr[i + 1]; ++e)
+        if (--indeg[succ[e]] == 0) freed.push_back(succ[e]);
+    }
+    for (int32_t i : freed) ready.push({deadline(i), i});
+    done += (int64_t)batch.size();
+    ++t;
+  }
+  if ((int64_t)t >= steps_asap) return depth;  // no gain: keep the ASAP levels
+  lev.swap(step);
+  return t;
+}
+
 int analyze_factor(const pslr_csr& M, const std::vector<int64_t>& off, bool upper, TriAnalysis& A,
-                   const char* name) {
+                   const char* name, int64_t sched_cap, int64_t sched_delay) {
   const int64_t n = M.nrows;
   const int64_t nb = (int64_t)off.size() - 1;
   A.upper = upper;
@@ -78,8 +158,7 @@ int analyze_factor(const pslr_csr& M, const std::vector<int64_t>& off, bool uppe
         return fail(PSLR_ESINGULAR, std::string(name) + ": A is singular: zero entry on diagonal.");
       lev[i] = lv;
     }
-    int32_t depth = 0;
-    for (int64_t i = 0; i < nr; ++i) depth = std::max(depth, lev[i] + 1);
+    const int32_t depth = list_schedule(M, lo, nr, upper, sched_cap, sched_delay, lev);
     A.depth_max = std::max<int64_t>(A.depth_max, depth);
     A.blk_depth[b] = depth;
     A.levels += depth;

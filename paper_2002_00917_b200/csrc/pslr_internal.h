@@ -99,7 +99,7 @@ struct TriHost {
 };
 
 int analyze_factor(const pslr_csr& M, const std::vector<int64_t>& off, bool upper, TriAnalysis& A,
-                   const char* name);
+                   const char* name, int64_t sched_cap = 0, int64_t sched_delay = 0);
 // Level-merged factors (pack.cpp merge_levels): an owned host CSR and the right-hand-side
 // transform of the merged rows, one record per row: rows[4] = {i, j0, j1, j2} (padding
 // j = i), c[4] = {c0, c1, c2, 0};  rhs'_i = rhs_i - (c0 rhs_j0 + c1 rhs_j1 + c2 rhs_j2).
