@@ -196,7 +196,7 @@ static int pack_system(const pslr_system* sys, const std::vector<int64_t>& ioff,
   TriAnalysis aLB, aUB, aLC, aUC;
   // rows of levels wider than a launch's consumer threads are list-scheduled into full steps
   // (pack.cpp list_schedule; PSLR_LIST_SCHED=0: the ASAP dependency levels as they are)
-  const int64_t scap = ((P.merged >> 31) & 1) ? kStepThreads : 0;
+  const int64_t scap = ((P.merged >> 31) & 1) ? std::max<int64_t>(32, env_int("PSLR_SCHED_CAP", kStepThreads)) : 0;
   const int64_t sdel = std::max<int64_t>(0, env_int("PSLR_SCHED_DELAY", 16));
   RET(analyze_factor(LB, ioff, false, aLB, "L_B", scap, sdel));
   RET(analyze_factor(UB, ioff, true, aUB, "U_B", scap, sdel));
